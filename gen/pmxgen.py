@@ -1,0 +1,354 @@
+"""Deterministic synthetic inputs for the BASELINE configs (bench/test infra).
+
+Thin numpy wrapper over gen/libpmx_gen.so (counter-based splitmix64 RNG +
+explicit Box-Muller, FP64 ray casting).  The BASELINE configs name synthetic
+512x384 pointmaps; there is no dataset.  Resolved ambiguities (SURVEY.md
+Appendix B) are recorded in DESIGN.md §3 and in the docstrings below.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libpmx_gen.so")
+_lib = None
+
+H, W, F, CX, CY, DIM = 384, 512, 400.0, 256.0, 192.0, 24
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            subprocess.check_call(["make", "-s", "-C", _HERE])
+        _lib = C.CDLL(_LIB_PATH)
+        _lib.gen_image.restype = C.c_int
+        _lib.gen_gt_matches.restype = C.c_int
+    return _lib
+
+
+def _threads():
+    return max(1, min(32, os.cpu_count() or 1))
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+class Pose:
+    """Sim(3) x -> s R x + t (FP64), the reference's Sim3Pose (lie.hpp:36-70)."""
+
+    def __init__(self, R=None, t=None, s=1.0):
+        self.R = np.eye(3) if R is None else np.asarray(R, dtype=np.float64).reshape(3, 3)
+        self.t = np.zeros(3) if t is None else np.asarray(t, dtype=np.float64).reshape(3)
+        self.s = float(s)
+
+    def __mul__(self, o: "Pose") -> "Pose":  # lie.cpp:131-140
+        return Pose(self.R @ o.R, self.s * (self.R @ o.t) + self.t, self.s * o.s)
+
+    def inverse(self) -> "Pose":  # lie.cpp:121-129
+        Ri = self.R.T
+        si = 1.0 / self.s
+        return Pose(Ri, -si * (Ri @ self.t), si)
+
+    def act(self, x):
+        return self.s * (np.asarray(x) @ self.R.T) + self.t
+
+    def to_struct(self, struct_cls):
+        T = struct_cls()
+        for i, v in enumerate(self.R.reshape(-1)):
+            T.R[i] = float(v)
+        for i in range(3):
+            T.t[i] = float(self.t[i])
+        T.s = self.s
+        return T
+
+    @staticmethod
+    def from_struct(T) -> "Pose":
+        return Pose(np.array(T.R[:]).reshape(3, 3), np.array(T.t[:]), T.s)
+
+    def __repr__(self):
+        return f"Pose(R={self.R.tolist()}, t={self.t.tolist()}, s={self.s})"
+
+
+def rodrigues(omega) -> np.ndarray:
+    omega = np.asarray(omega, dtype=np.float64)
+    th = float(np.linalg.norm(omega))
+    K = np.array([[0, -omega[2], omega[1]], [omega[2], 0, -omega[0]], [-omega[1], omega[0], 0]])
+    if th < 1e-12:
+        return np.eye(3) + K
+    return np.eye(3) + math.sin(th) / th * K + (1 - math.cos(th)) / th ** 2 * (K @ K)
+
+
+def uniform(seed, stream, n):
+    out = np.empty(n, dtype=np.float64)
+    _load().gen_uniform(C.c_uint64(seed), C.c_uint64(stream), C.c_int64(n), _p(out))
+    return out
+
+
+def gauss(seed, stream, n):
+    out = np.empty(n, dtype=np.float64)
+    _load().gen_gauss(C.c_uint64(seed), C.c_uint64(stream), C.c_int64(n), _p(out))
+    return out
+
+
+def unit_vector(seed, stream):
+    g = gauss(seed, stream, 3)
+    return g / np.linalg.norm(g)
+
+
+def random_pose(seed, stream, max_rot_deg, max_trans, scale_lo, scale_hi) -> Pose:
+    """Axis uniform on S^2, angle U[0, max]; translation direction uniform,
+    magnitude U[0, max]; scale U[lo, hi] (BASELINE configs 0/1)."""
+    u = uniform(seed, stream, 3)
+    axis = unit_vector(seed, stream + 1)
+    tdir = unit_vector(seed, stream + 2)
+    R = rodrigues(axis * math.radians(max_rot_deg) * u[0])
+    return Pose(R, tdir * max_trans * u[1], scale_lo + (scale_hi - scale_lo) * u[2])
+
+
+def perturb_pose(T: Pose, seed, stream, rot_deg, trans, scale_frac) -> Pose:
+    """Fixed-magnitude perturbation along random directions (configs 3/4):
+    rotation rot_deg about a random axis, translation `trans` in a random
+    direction, scale x exp(+-scale_frac)."""
+    axis = unit_vector(seed, stream)
+    tdir = unit_vector(seed, stream + 1)
+    sign = 1.0 if uniform(seed, stream + 2, 1)[0] < 0.5 else -1.0
+    dR = rodrigues(axis * math.radians(rot_deg))
+    return Pose(dR @ T.R, T.t + tdir * trans, T.s * math.exp(sign * scale_frac))
+
+
+class Scene:
+    """The config-0 surface z = 2 + 0.3 sin(3x) cos(2y) + a x + b y over the
+    reference camera's normalised coordinates; tilt a, b ~ U[-0.2, 0.2].
+
+    Point noise N(0, point_sigma^2): ``noise="radial"`` (default) perturbs
+    the distance along each view's own viewing ray, the reference's noise
+    model (src/synth.cpp:221-226); ``noise="isotropic"`` adds it per
+    coordinate (a rough ray field; an adversarial parity case)."""
+
+    def __init__(self, seed: int, height=H, width=W, f=F, cx=CX, cy=CY, dim=DIM,
+                 point_sigma=0.005, desc_sigma=0.05, noise="radial"):
+        ab = uniform(seed, 7, 2) * 0.4 - 0.2
+        self.seed, self.height, self.width, self.dim = seed, height, width, dim
+        self.f, self.cx, self.cy = f, cx, cy
+        self.params = np.array([seed, ab[0], ab[1], f, cx, cy, height, width, dim,
+                                point_sigma, desc_sigma, 0 if noise == "radial" else 1],
+                               dtype=np.float64)
+
+    def image(self, image_id: int, T_wk: Pose, T_frame: Pose, salt: int = 0,
+              want=("X", "valid", "Q", "D")):
+        from paper_2412_12392_b200.abi import pmx_sim3
+        n = self.height * self.width
+        X = np.empty((n, 3), np.float32) if "X" in want else None
+        valid = np.empty(n, np.uint8) if "valid" in want else None
+        Q = np.empty(n, np.float32) if "Q" in want else None
+        D = np.empty((n, self.dim), np.uint16) if "D" in want else None
+        a, b = T_wk.to_struct(pmx_sim3), T_frame.to_struct(pmx_sim3)
+        _load().gen_image(_p(self.params), C.c_int64(image_id), C.byref(a), C.byref(b),
+                          C.c_uint64(salt), _p(X), _p(valid), _p(Q), _p(D), None,
+                          C.c_int(_threads()))
+        return {"X": X, "valid": valid, "Q": Q, "D": D}
+
+    def pair(self, ia: int, T_wa: Pose, ib: int, T_wb: Pose, salt: int = 0):
+        """Pair prediction of edge (a, b) in frame a (what MASt3R predicts):
+        X_a = camera a's points in frame a, X_b_in_a = camera b's points in
+        frame a, per-image Q and fp16 descriptors."""
+        A = self.image(ia, T_wa, T_wa, salt)
+        B = self.image(ib, T_wb, T_wa, salt + 1)
+        return {"X_a": A["X"], "valid_a": A["valid"], "Q_a": A["Q"], "D_a": A["D"],
+                "X_b": B["X"], "valid_b": B["valid"], "Q_b": B["Q"], "D_b": B["D"],
+                "height": self.height, "width": self.width}
+
+    def gt_matches(self, ia, T_wa, ib, T_wb, subpixel=False):
+        from paper_2412_12392_b200.abi import pmx_sim3
+        n = self.height * self.width
+        pa = np.empty(n, np.int32)
+        q = np.empty(n, np.float32)
+        v = np.empty(n, np.uint8)
+        sp = np.empty((n, 2), np.float64) if subpixel else None
+        a, b = T_wa.to_struct(pmx_sim3), T_wb.to_struct(pmx_sim3)
+        _load().gen_gt_matches(_p(self.params), C.c_int64(ia), C.byref(a), C.c_int64(ib),
+                               C.byref(b), _p(pa), _p(q), _p(v), _p(sp), C.c_int(_threads()))
+        out = {"pixel_a": pa, "confidence": q, "valid": v}
+        if subpixel:
+            out["subpixel"] = sp
+        return out
+
+
+# ------------------------------------------------------------------ configs
+
+def config0(seed: int = 0, height=H, width=W, noise="radial"):
+    """BASELINE config 0: one pair, camera j under a random relative Sim(3)
+    (rotation <= 5 deg, translation <= 0.1, scale in [0.9, 1.1])."""
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H, noise=noise)
+    T_ij = random_pose(seed, 100, 5.0, 0.1, 0.9, 1.1)
+    pair = sc.pair(0, Pose(), 1, T_ij)
+    pair["T_ij"] = T_ij
+    pair["scene"] = sc
+    return pair
+
+
+def config1(seed: int = 1, height=H, width=W):
+    """BASELINE config 1: keyframe (reference camera) + frame under T_kf
+    (rotation <= 3 deg, translation <= 0.05, scale in [0.95, 1.05]).
+    Returns canonical (keyframe own view, noisy), C~, the frame prediction
+    (X_f_f, X_k_f, C_f, C_k, F_f, F_k) and the true T_kf."""
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
+    T_kf = random_pose(seed, 200, 3.0, 0.05, 0.95, 1.05)
+    kf = sc.image(0, Pose(), Pose(), salt=10)
+    pred = sc.pair(1, T_kf, 0, Pose(), salt=20)  # a = frame, b = keyframe image
+    return {"scene": sc, "T_kf": T_kf,
+            "canonical": kf["X"], "canonical_valid": kf["valid"], "canonical_conf": kf["Q"],
+            "X_f_f": pred["X_a"], "valid_f": pred["valid_a"], "C_f": pred["Q_a"], "D_f": pred["D_a"],
+            "X_k_f": pred["X_b"], "valid_k": pred["valid_b"], "C_k": pred["Q_b"], "D_k": pred["D_b"],
+            "height": height, "width": width}
+
+
+def inject_outliers(pixel_a: np.ndarray, valid: np.ndarray, frac: float, seed: int, hw: int):
+    """Config 1: `frac` of entries get a uniform-random pixel_a and are flagged valid."""
+    n = pixel_a.shape[0]
+    u = uniform(seed, 300, n)
+    r = uniform(seed, 301, n)
+    pa = pixel_a.copy()
+    v = valid.copy()
+    sel = u < frac
+    pa[sel] = np.minimum((r[sel] * hw).astype(np.int64), hw - 1).astype(np.int32)
+    v[sel] = 1
+    return pa, v
+
+
+def trajectory_config2(seed: int = 2, n_kf: int = 32):
+    """32 keyframes on a smooth lateral arc over the surface (small yaw/pitch
+    wobble).  Returns camera->world poses (the reference camera = world)."""
+    poses = []
+    for k in range(n_kf):
+        s = k / (n_kf - 1)
+        t = np.array([1.2 * (s - 0.5), 0.25 * math.sin(math.pi * s), 0.05 * math.sin(2 * math.pi * s)])
+        w = np.array([0.03 * math.sin(2 * math.pi * s), -0.04 * (s - 0.5), 0.02 * math.cos(math.pi * s)])
+        poses.append(Pose(rodrigues(w), t, 1.0))
+    return poses
+
+
+def edges_config2(seed: int = 2, n_kf: int = 32, n_consecutive: int = 28, n_long: int = 8,
+                  min_overlap: float = 0.4, poses=None, scene=None):
+    """64 directed edges: 28 consecutive pairs x both directions + 8 long-range
+    pairs (|i-j| >= 3) with GT overlap >= 40%, chosen deterministically."""
+    edges = []
+    for k in range(n_consecutive):
+        edges.append((k, k + 1))
+        edges.append((k + 1, k))
+    poses = poses or trajectory_config2(seed, n_kf)
+    sc = scene or Scene(seed, 48, 64, f=F * 64 / W, cx=CX * 64 / W, cy=CY * 48 / H)
+    u = uniform(seed, 400, 4096)
+    k = 0
+    longs = []
+    while len(longs) < n_long and k + 1 < len(u):
+        i = int(u[k] * n_kf) % n_kf
+        j = int(u[k + 1] * n_kf) % n_kf
+        k += 2
+        if abs(i - j) < 3 or (i, j) in longs:
+            continue
+        gt = sc.gt_matches(i, poses[i], j, poses[j])
+        if gt["valid"].mean() >= min_overlap:
+            longs.append((i, j))
+    return edges + longs
+
+
+def loop_trajectory(n_kf: int, radius: float = 5.0, loops: int = 1, seed: int = 3):
+    """Keyframes on `loops` turns of a circle of radius `radius` (m) in the
+    reference camera's XY plane, looking down +Z at the surface; the radius
+    shrinks by 4% per extra loop (multi-loop, config 4)."""
+    poses = []
+    for k in range(n_kf):
+        a = 2 * math.pi * loops * k / n_kf
+        r = radius * (1.0 - 0.04 * (loops * k // n_kf))
+        t = np.array([r * math.cos(a), r * math.sin(a), 0.02 * math.sin(3 * a)])
+        R = rodrigues(np.array([0.0, 0.0, a]))
+        poses.append(Pose(R, t, 1.0))
+    return poses
+
+
+def loop_edges(n_kf: int, reach: int):
+    """Cyclic neighbours k <-> k+1 .. k+reach (the wrap-around edges are the
+    loop closures): n_kf * reach bidirectional edges."""
+    return [(k, (k + d) % n_kf) for k in range(n_kf) for d in range(1, reach + 1)]
+
+
+def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: int = 1,
+                  radius: float = 5.0, rot_deg=2.0, trans=0.05, scale_frac=0.03,
+                  edges=None):
+    """Configs 3/4: GT loop poses, canonical pointmaps (own view + noise),
+    edges with ground-truth matches (pixel_a in i, pixel_b in j, dense), and
+    perturbed initial poses (anchor = keyframe 0, unperturbed)."""
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
+    gt = loop_trajectory(n_kf, radius, loops, seed)
+    canon = []
+    for k in range(n_kf):
+        im = sc.image(k, gt[k], gt[k], salt=1000 + k, want=("X", "valid"))
+        canon.append((im["X"], im["valid"]))
+    edges = edges if edges is not None else loop_edges(n_kf, reach)
+    matches = []
+    for (i, j) in edges:
+        m = sc.gt_matches(i, gt[i], j, gt[j])
+        matches.append(m)
+    init = [gt[0]] + [perturb_pose(gt[k], seed, 5000 + 3 * k, rot_deg, trans, scale_frac)
+                      for k in range(1, n_kf)]
+    return {"scene": sc, "gt": gt, "init": init, "canonicals": canon, "edges": edges,
+            "matches": matches, "height": height, "width": width}
+
+
+class Camera:
+    """A ray-cast camera (world points cached) for many-edge configs."""
+
+    def __init__(self, scene: Scene, image_id: int, T_wk: Pose):
+        from paper_2412_12392_b200.abi import pmx_sim3
+        n = scene.height * scene.width
+        self.scene, self.image_id, self.T = scene, image_id, T_wk
+        self.P = np.empty((n, 3), np.float64)
+        self.valid = np.empty(n, np.uint8)
+        self.Q = np.empty(n, np.float32)
+        self.D = np.empty((n, scene.dim), np.uint16)
+        a = T_wk.to_struct(pmx_sim3)
+        _load().gen_camera(_p(scene.params), C.c_int64(image_id), C.byref(a), _p(self.P), _p(self.valid),
+                           _p(self.Q), _p(self.D), C.c_int(_threads()))
+
+    def express(self, T_frame: Pose, salt: int) -> np.ndarray:
+        from paper_2412_12392_b200.abi import pmx_sim3
+        X = np.empty(self.P.shape, np.float32)
+        a, b = self.T.to_struct(pmx_sim3), T_frame.to_struct(pmx_sim3)
+        _load().gen_express(_p(self.scene.params), C.c_int64(self.image_id), C.byref(a), C.byref(b),
+                            C.c_uint64(salt), _p(self.P), _p(self.valid), _p(X), C.c_int(_threads()))
+        return X
+
+
+def pair_from_cameras(ca: Camera, cb: Camera, salt: int):
+    """Pair prediction of edge (a, b) in frame a from cached cameras."""
+    return {"X_a": ca.express(ca.T, salt), "valid_a": ca.valid, "Q_a": ca.Q, "D_a": ca.D,
+            "X_b": cb.express(ca.T, salt + 1), "valid_b": cb.valid, "Q_b": cb.Q, "D_b": cb.D,
+            "height": ca.scene.height, "width": ca.scene.width}
+
+
+def config2(seed: int = 2, height=H, width=W, n_kf: int = 32, edges=None):
+    """BASELINE config 2: 32 keyframes on a smooth trajectory, 64 directed edges.
+    Returns (scene, cameras, edges, make_pair(e))."""
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
+    poses = trajectory_config2(seed, n_kf)
+    edges = edges if edges is not None else edges_config2(seed, n_kf, poses=poses)
+    cams = {}
+
+    def cam(k):
+        if k not in cams:
+            cams[k] = Camera(sc, k, poses[k])
+        return cams[k]
+
+    def make_pair(e):
+        a, b = edges[e]
+        return pair_from_cameras(cam(a), cam(b), salt=2 * e)
+
+    return sc, poses, edges, make_pair

@@ -1,0 +1,478 @@
+"""Python mirror of the reference's matching / tracking / optimiser API.
+
+Same names, argument meaning and error behaviour as the CPU reference
+``pmslam`` (/root/reference/proj/include/pmslam/{camera,tracking,backend}.hpp),
+executed by ``libpmx_cuda.so`` through the C ABI of ``include/pmx.h``:
+
+=====================  ==================================================
+reference              here
+=====================  ==================================================
+normalize_rays         Context.normalize_rays        (camera.hpp:100)
+iterative_project      Context.iterative_project     (camera.hpp:123)
+match_pointmaps        Context.match_pointmaps       (camera.hpp:135)
+feature_refine         Context.feature_refine        (camera.hpp:147)
+(loop-edge matching)   Context.match_batch           (retrieval.cpp:232)
+residual_blocks        Context.residual_blocks       (tracking.hpp:56)
+(GN normal equations)  Context.normal_equations      (tracking.cpp:188)
+solve_pose             Context.solve_pose            (tracking.hpp:105)
+(GN on given matches)  Context.track_given_matches   (tracking.cpp:165)
+fuse_canonical         Context.fuse_canonical        (tracking.hpp:112)
+keyframe_decision      Context.keyframe_decision     (tracking.hpp:117)
+assemble_system        Context.assemble_system       (backend.hpp:57)
+backend_cost           Context.backend_cost          (backend.hpp:72)
+global_optimize        Context.global_optimize       (backend.hpp:69)
+=====================  ==================================================
+
+Arrays are numpy (host memory: the call stages them H2D and returns host
+results) or torch CUDA tensors (device memory: results stay on the device).
+The reference's std::invalid_argument / std::domain_error surface as
+``ValueError`` / ``ArithmeticError`` (``PmxError`` subclasses).  There is no
+CPU fallback: a missing extension or device raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Any, List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .abi import ptr
+
+
+class PmxError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"pmx status {code}: {msg}")
+        self.code = code
+
+
+class PmxInvalidArgument(PmxError, ValueError):
+    pass
+
+
+class PmxDomainError(PmxError, ArithmeticError):
+    pass
+
+
+def _is_dev(a) -> bool:
+    return a is not None and hasattr(a, "is_cuda") and a.is_cuda
+
+
+@dataclass
+class Pointmap:
+    """H x W grid of points, row-major (camera.hpp:17-31): xyz (HW, 3) fp32, valid (HW,) u8 or None."""
+    xyz: Any
+    valid: Any
+    height: int
+    width: int
+
+    def struct(self):
+        return abi.pointmap(self.xyz, self.valid, self.height, self.width)
+
+
+@dataclass
+class FeatureMap:
+    """Per-pixel fp16 descriptors (HW, dim) + match confidence Q (HW,) (camera.hpp:55-71)."""
+    descriptors: Any
+    match_confidence: Any
+    height: int
+    width: int
+
+    @property
+    def dim(self) -> int:
+        return int(self.descriptors.shape[-1])
+
+    def struct(self):
+        return abi.featuremap(self.descriptors, self.match_confidence, self.height, self.width, self.dim)
+
+
+@dataclass
+class MatchSet:
+    """SoA MatchSet (camera.hpp:73-89); pixel_b None = dense (pixel_b[k] == k)."""
+    pixel_a: Any
+    confidence: Any
+    valid: Any
+    pixel_b: Any = None
+
+    def __len__(self):
+        return int(self.pixel_a.shape[0])
+
+    def struct(self):
+        return abi.matchset(self.pixel_a, self.pixel_b, self.confidence, self.valid)
+
+    @staticmethod
+    def empty(n: int, device=None, dense: bool = True) -> "MatchSet":
+        if device is not None:
+            import torch
+            pb = None if dense else torch.empty(n, dtype=torch.int32, device=device)
+            return MatchSet(torch.empty(n, dtype=torch.int32, device=device),
+                            torch.empty(n, dtype=torch.float32, device=device),
+                            torch.empty(n, dtype=torch.uint8, device=device), pb)
+        pb = None if dense else np.empty(n, np.int32)
+        return MatchSet(np.empty(n, np.int32), np.empty(n, np.float32), np.empty(n, np.uint8), pb)
+
+    def valid_count(self) -> int:  # camera.cpp:10-14
+        v = self.valid
+        return int(v.sum().item() if hasattr(v, "sum") and _is_dev(v) else np.count_nonzero(v))
+
+
+@dataclass
+class TrackResult:  # tracking.hpp:93-99
+    T_kf: Any
+    iterations: int
+    lost: bool
+    cost_trace: List[float]
+    matches: Optional[MatchSet] = None
+
+
+@dataclass
+class OptimizeResult:  # backend.hpp:59-63
+    iterations: int
+    converged: bool
+    cost_trace: List[float]
+    pose_trace: List[list] = field(default_factory=list)
+
+
+@dataclass
+class Graph:
+    """Keyframe graph (backend.hpp:18-32) by index: canonicals[k] = Pointmap,
+    poses[k] = pmx_sim3 (T_WC, updated in place by global_optimize), edges
+    [(i, j)], matches[e] = MatchSet (pixel_a in i, pixel_b in j)."""
+    canonicals: Sequence[Pointmap]
+    poses: list
+    edges: Sequence[tuple]
+    matches: Sequence[MatchSet]
+    anchor: int = 0
+
+    def struct(self, keep: list):
+        n = len(self.canonicals)
+        cans = (abi.pmx_pointmap * max(1, n))(*[c.struct() for c in self.canonicals])
+        poses = (abi.pmx_sim3 * max(1, n))(*self.poses)
+        ei = np.ascontiguousarray([e[0] for e in self.edges], np.int32)
+        ej = np.ascontiguousarray([e[1] for e in self.edges], np.int32)
+        ms = (abi.pmx_matchset * max(1, len(self.edges)))(*[m.struct() for m in self.matches])
+        keep.extend([cans, poses, ei, ej, ms])
+        return abi.pmx_graph(n, cans, poses, self.anchor, len(self.edges), ptr(ei), ptr(ej), ms)
+
+
+class Context:
+    """One pmx context (device + stream).  ``stream`` may be a torch.cuda.Stream
+    (or raw cudaStream_t int) the library enqueues on."""
+
+    def __init__(self, device: int = 0, stream=None):
+        self.lib = abi.load_library()
+        h = C.c_void_p()
+        code = self.lib.pmx_create(int(device), C.byref(h))
+        if code != abi.PMX_OK:
+            raise PmxError(code, f"pmx_create(device={device}) failed (no sm_100 device?)")
+        self.h = h
+        self.device = device
+        if stream is not None:
+            self.set_stream(stream)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.pmx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream):
+        raw = getattr(stream, "cuda_stream", stream)
+        self._check(self.lib.pmx_set_stream(self.h, C.c_void_p(raw)))
+
+    def synchronize(self):
+        self._check(self.lib.pmx_synchronize(self.h))
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.pmx_kernel_launch_count(self.h))
+
+    def profile_enable(self, on: bool = True):
+        self._check(self.lib.pmx_profile_enable(self.h, int(on)))
+
+    def profile_reset(self):
+        self._check(self.lib.pmx_profile_reset(self.h))
+
+    def profile_get(self, kernel: str):
+        """(total ms, launches) of a bracketed hot kernel since the last reset."""
+        t, n = C.c_double(), C.c_int64()
+        self._check(self.lib.pmx_profile_get(self.h, kernel.encode(), C.byref(t), C.byref(n)))
+        return t.value, n.value
+
+    def _check(self, code):
+        if code == abi.PMX_OK:
+            return
+        msg = self.lib.pmx_last_error(self.h).decode()
+        if code == abi.PMX_ERR_INVALID_ARGUMENT:
+            raise PmxInvalidArgument(code, msg)
+        if code == abi.PMX_ERR_DOMAIN:
+            raise PmxDomainError(code, msg)
+        raise PmxError(code, msg)
+
+    @staticmethod
+    def _mem(*arrays):
+        dev = [_is_dev(a) for a in arrays if a is not None]
+        if any(dev) and not all(dev):
+            raise PmxInvalidArgument(abi.PMX_ERR_INVALID_ARGUMENT, "mixed host and device arrays")
+        return abi.PMX_MEM_DEVICE if dev and all(dev) else abi.PMX_MEM_HOST
+
+    # ---------------------------------------------------------- matching
+    def normalize_rays(self, pm: Pointmap):
+        n = pm.height * pm.width
+        mem = self._mem(pm.xyz, pm.valid)
+        if mem == abi.PMX_MEM_DEVICE:
+            import torch
+            dv = pm.xyz.device
+            rays = torch.empty((n, 3), dtype=torch.float64, device=dv)
+            dist = torch.empty(n, dtype=torch.float64, device=dv)
+            valid = torch.empty(n, dtype=torch.uint8, device=dv)
+        else:
+            rays, dist, valid = np.empty((n, 3)), np.empty(n), np.empty(n, np.uint8)
+        s = pm.struct()
+        self._check(self.lib.pmx_normalize_rays(self.h, mem, C.byref(s), ptr(rays), ptr(dist), ptr(valid)))
+        return rays, dist, valid
+
+    def iterative_project(self, pm: Pointmap, x, p0, params=None):
+        x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)
+        p0 = np.ascontiguousarray(p0, np.float64).reshape(-1, 2)
+        n = x.shape[0]
+        pix, conv, it = np.empty((n, 2)), np.empty(n, np.uint8), np.empty(n, np.int32)
+        params = params or abi.default_match_params().projection
+        s = pm.struct()
+        self._check(self.lib.pmx_iterative_project(self.h, abi.PMX_MEM_HOST, C.byref(s), C.c_int64(n), ptr(x),
+                                                   ptr(p0), C.byref(params), ptr(pix), ptr(conv), ptr(it)))
+        return pix, conv, it
+
+    def match_pointmaps(self, X_a: Pointmap, X_b_in_a: Pointmap, F_a: FeatureMap, F_b: FeatureMap,
+                        init: Optional[MatchSet] = None, params=None) -> MatchSet:
+        return self.match_batch([(X_a, X_b_in_a, F_a, F_b, init)], params=params, refine=None)[0]
+
+    def feature_refine(self, matches: MatchSet, F_a: FeatureMap, F_b: FeatureMap, params=None) -> MatchSet:
+        mem = self._mem(matches.pixel_a, F_a.descriptors)
+        n = len(matches)
+        dev = matches.pixel_a.device if mem == abi.PMX_MEM_DEVICE else None
+        out = MatchSet.empty(n, dev, dense=matches.pixel_b is None)
+        params = params or abi.default_refine_params()
+        i, o, fa, fb = matches.struct(), out.struct(), F_a.struct(), F_b.struct()
+        self._check(self.lib.pmx_feature_refine(self.h, mem, C.byref(i), C.byref(fa), C.byref(fb), C.byref(params),
+                                                C.byref(o)))
+        if matches.pixel_b is not None and out.pixel_b is None:
+            out.pixel_b = matches.pixel_b
+        return out
+
+    def match_batch(self, pairs, params=None, refine=None, outs: Optional[List[MatchSet]] = None) -> List[MatchSet]:
+        """Fused match_pointmaps (+ feature_refine when ``refine`` is given)
+        over independent pairs (X_a, X_b_in_a, F_a, F_b[, init])."""
+        keep = []
+        structs = []
+        mem = None
+        for p in pairs:
+            X_a, X_b, F_a, F_b = p[:4]
+            init = p[4] if len(p) > 4 else None
+            m = self._mem(X_a.xyz, X_b.xyz, F_a.descriptors, F_b.descriptors)
+            if mem is not None and m != mem:
+                raise PmxInvalidArgument(abi.PMX_ERR_INVALID_ARGUMENT, "mixed host and device pairs")
+            mem = m
+            ip = None
+            if init is not None:
+                ist = init.struct()
+                keep.append(ist)
+                ip = C.pointer(ist)
+            structs.append(abi.pmx_pair(X_a.struct(), X_b.struct(), F_a.struct(), F_b.struct(), ip))
+        n = len(structs)
+        if outs is None:
+            outs = []
+            for p in pairs:
+                dev = p[1].xyz.device if mem == abi.PMX_MEM_DEVICE else None
+                outs.append(MatchSet.empty(p[1].height * p[1].width, dev))
+        arr = (abi.pmx_pair * max(1, n))(*structs)
+        oarr = (abi.pmx_matchset * max(1, n))(*[o.struct() for o in outs])
+        params = params or abi.default_match_params()
+        self._check(self.lib.pmx_match_batch(self.h, mem if mem is not None else abi.PMX_MEM_HOST, C.c_int32(n), arr,
+                                             C.byref(params), C.byref(refine) if refine is not None else None, oarr))
+        return outs
+
+    def match_stats(self, m: MatchSet, num_pixels_a: int):
+        vc, uf = C.c_int64(), C.c_double()
+        s = m.struct()
+        self._check(self.lib.pmx_match_stats(self.h, self._mem(m.pixel_a), C.byref(s), C.c_int32(num_pixels_a),
+                                             C.byref(vc), C.byref(uf)))
+        return vc.value, uf.value
+
+    def keyframe_decision(self, m: MatchSet, height: int, width: int, omega_k: float) -> bool:
+        out = C.c_int32()
+        s = m.struct()
+        self._check(self.lib.pmx_keyframe_decision(self.h, self._mem(m.pixel_a), C.byref(s), C.c_int32(height),
+                                                   C.c_int32(width), C.c_double(omega_k), C.byref(out)))
+        return bool(out.value)
+
+    # ---------------------------------------------------------- tracking
+    def residual_blocks(self, T, matches: MatchSet, X_ref: Pointmap, X_src: Pointmap, mode=abi.PMX_TRACK_RAY,
+                        params=None, K=None):
+        n = len(matches)
+        res, jac, wt, info, used = (np.zeros((n, 4)), np.zeros((n, 4, 7)), np.zeros((n, 4)), np.zeros(n),
+                                    np.zeros(n, np.uint8))
+        s, r, x = matches.struct(), X_ref.struct(), X_src.struct()
+        params = params or abi.default_robust_weight_params()
+        self._check(self.lib.pmx_residual_blocks(self.h, abi.PMX_MEM_HOST, C.byref(T), C.byref(s), C.byref(r),
+                                                 C.byref(x), C.c_int(mode), C.byref(params),
+                                                 C.byref(K) if K is not None else None, ptr(res), ptr(jac), ptr(wt),
+                                                 ptr(info), ptr(used)))
+        return res, jac, wt, info, used
+
+    def normal_equations(self, T, matches: MatchSet, X_ref: Pointmap, X_src: Pointmap, mode=abi.PMX_TRACK_RAY,
+                         params=None, K=None):
+        H, g, cost, used = np.zeros((7, 7)), np.zeros(7), C.c_double(), C.c_int64()
+        s, r, x = matches.struct(), X_ref.struct(), X_src.struct()
+        params = params or abi.default_robust_weight_params()
+        mem = self._mem(matches.pixel_a, X_ref.xyz, X_src.xyz)
+        self._check(self.lib.pmx_normal_equations(self.h, mem, C.byref(T), C.byref(s), C.byref(r), C.byref(x),
+                                                  C.c_int(mode), C.byref(params),
+                                                  C.byref(K) if K is not None else None, ptr(H), ptr(g),
+                                                  C.byref(cost), C.byref(used)))
+        return H, g, cost.value, used.value
+
+    def track_given_matches(self, canonical: Pointmap, X_f_f: Pointmap, matches: MatchSet, init,
+                            mode=abi.PMX_TRACK_RAY, params=None) -> TrackResult:
+        res = abi.pmx_track_result()
+        c, f, m = canonical.struct(), X_f_f.struct(), matches.struct()
+        params = params or abi.default_solve_pose_params()
+        mem = self._mem(canonical.xyz, X_f_f.xyz, matches.pixel_a)
+        self._check(self.lib.pmx_track_given_matches(self.h, mem, C.byref(c), C.byref(f), C.byref(m),
+                                                     C.byref(init), C.c_int(mode), C.byref(params), C.byref(res)))
+        return TrackResult(abi.pmx_sim3.from_buffer_copy(res.T_kf), res.iterations, bool(res.lost),
+                           list(res.cost_trace[:res.cost_trace_len]), matches)
+
+    def solve_pose(self, canonical: Pointmap, X_f_f: Pointmap, X_k_f: Pointmap, F_f: FeatureMap,
+                   F_k: FeatureMap, init, mode=abi.PMX_TRACK_RAY, params=None,
+                   match_seed: Optional[MatchSet] = None) -> TrackResult:
+        res = abi.pmx_track_result()
+        params = params or abi.default_solve_pose_params()
+        mem = self._mem(canonical.xyz, X_f_f.xyz, X_k_f.xyz)
+        dev = X_k_f.xyz.device if mem == abi.PMX_MEM_DEVICE else None
+        out = MatchSet.empty(X_k_f.height * X_k_f.width, dev)
+        c, f, k, ff, fk, o = (canonical.struct(), X_f_f.struct(), X_k_f.struct(), F_f.struct(), F_k.struct(),
+                              out.struct())
+        seed = match_seed.struct() if match_seed is not None else None
+        self._check(self.lib.pmx_solve_pose(self.h, mem, C.byref(c), C.byref(f), C.byref(k), C.byref(ff), C.byref(fk),
+                                            C.byref(init), C.c_int(mode), C.byref(params),
+                                            C.byref(seed) if seed is not None else None, C.byref(res), C.byref(o)))
+        return TrackResult(abi.pmx_sim3.from_buffer_copy(res.T_kf), res.iterations, bool(res.lost),
+                           list(res.cost_trace[:res.cost_trace_len]), out)
+
+    def fuse_canonical(self, canonical_xyz, canonical_valid, canonical_conf, X_k_f: Pointmap, confidence, T_kf,
+                       height: int, width: int):
+        """In place on (canonical_xyz, canonical_valid, canonical_conf)."""
+        mem = self._mem(canonical_xyz, X_k_f.xyz)
+        k = X_k_f.struct()
+        self._check(self.lib.pmx_fuse_canonical(self.h, mem, C.c_int32(height), C.c_int32(width), ptr(canonical_xyz),
+                                                ptr(canonical_valid), ptr(canonical_conf), C.byref(k),
+                                                ptr(confidence), C.byref(T_kf)))
+
+    # ----------------------------------------------------------- backend
+    def _graph_mem(self, g: Graph):
+        arrays = [c.xyz for c in g.canonicals] + [m.pixel_a for m in g.matches]
+        return self._mem(*arrays) if arrays else abi.PMX_MEM_HOST
+
+    def assemble_system(self, g: Graph, params=None):
+        keep = []
+        gs = g.struct(keep)
+        dim = 7 * len(g.canonicals)
+        H, grad = np.zeros((dim, dim)), np.zeros(dim)
+        params = params or abi.default_backend_params()
+        mem = self._graph_mem(g)
+        if mem == abi.PMX_MEM_DEVICE:
+            import torch
+            dev = g.canonicals[0].xyz.device
+            Hd = torch.empty((dim, dim), dtype=torch.float64, device=dev)
+            gd = torch.empty(dim, dtype=torch.float64, device=dev)
+            self._check(self.lib.pmx_assemble_system(self.h, mem, C.byref(gs), C.byref(params), ptr(Hd), ptr(gd)))
+            return Hd, gd
+        self._check(self.lib.pmx_assemble_system(self.h, mem, C.byref(gs), C.byref(params), ptr(H), ptr(grad)))
+        return H, grad
+
+    def backend_cost(self, g: Graph, params=None) -> float:
+        keep = []
+        gs = g.struct(keep)
+        out = C.c_double()
+        params = params or abi.default_backend_params()
+        self._check(self.lib.pmx_backend_cost(self.h, self._graph_mem(g), C.byref(gs), C.byref(params), C.byref(out)))
+        return out.value
+
+    def backend_edge_terms(self, g: Graph, params=None, begin: int = 0, end: Optional[int] = None):
+        keep = []
+        gs = g.struct(keep)
+        end = len(g.edges) if end is None else end
+        out = np.zeros((end - begin, abi.PMX_EDGE_TERMS))
+        params = params or abi.default_backend_params()
+        mem = self._graph_mem(g)
+        if mem == abi.PMX_MEM_DEVICE:
+            import torch
+            outd = torch.zeros((end - begin, abi.PMX_EDGE_TERMS), dtype=torch.float64,
+                               device=g.canonicals[0].xyz.device)
+            self._check(self.lib.pmx_backend_edge_terms(self.h, mem, C.byref(gs), C.byref(params), C.c_int32(begin),
+                                                        C.c_int32(end), ptr(outd)))
+            return outd
+        self._check(self.lib.pmx_backend_edge_terms(self.h, mem, C.byref(gs), C.byref(params), C.c_int32(begin),
+                                                    C.c_int32(end), ptr(out)))
+        return out
+
+    def backend_solve_terms(self, g: Graph, terms, params=None):
+        keep = []
+        gs = g.struct(keep)
+        dim = 7 * len(g.canonicals)
+        params = params or abi.default_backend_params()
+        cost, solved = C.c_double(), C.c_int32()
+        if _is_dev(terms):
+            import torch
+            tau = torch.zeros(dim, dtype=torch.float64, device=terms.device)
+            self._check(self.lib.pmx_backend_solve_terms(self.h, abi.PMX_MEM_DEVICE, C.byref(gs), C.byref(params),
+                                                         ptr(terms), ptr(tau), C.byref(cost), C.byref(solved)))
+        else:
+            terms = np.ascontiguousarray(terms, np.float64)
+            tau = np.zeros(dim)
+            self._check(self.lib.pmx_backend_solve_terms(self.h, abi.PMX_MEM_HOST, C.byref(gs), C.byref(params),
+                                                         ptr(terms), ptr(tau), C.byref(cost), C.byref(solved)))
+        return tau, cost.value, bool(solved.value)
+
+    def global_optimize(self, g: Graph, params=None, trace: bool = False) -> OptimizeResult:
+        keep = []
+        gs = g.struct(keep)
+        params = params or abi.default_backend_params()
+        res = abi.pmx_optimize_result()
+        n = len(g.canonicals)
+        tr = (abi.pmx_sim3 * max(1, params.max_iterations * n))() if trace else None
+        self._check(self.lib.pmx_global_optimize(self.h, self._graph_mem(g), C.byref(gs), C.byref(params),
+                                                 C.byref(res), tr))
+        g.poses = [abi.pmx_sim3.from_buffer_copy(gs.poses[k]) for k in range(n)]
+        pt = []
+        if trace:
+            pt = [[abi.pmx_sim3.from_buffer_copy(tr[it * n + k]) for k in range(n)] for it in range(res.iterations)]
+        return OptimizeResult(res.iterations, bool(res.converged), list(res.cost_trace[:res.cost_trace_len]), pt)
+
+    def ldlt_solve(self, A, b):
+        A = np.ascontiguousarray(A, np.float64)
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.zeros(b.shape[0])
+        ok = C.c_int32()
+        self._check(self.lib.pmx_ldlt_solve(self.h, abi.PMX_MEM_HOST, C.c_int32(b.shape[0]), ptr(A), ptr(b), ptr(x),
+                                            C.byref(ok)))
+        return x, bool(ok.value)
+
+
+def sim3(R=None, t=None, s=1.0) -> abi.pmx_sim3:
+    T = abi.pmx_sim3()
+    R = np.eye(3) if R is None else np.asarray(R, np.float64)
+    for i, v in enumerate(R.reshape(-1)):
+        T.R[i] = float(v)
+    t = np.zeros(3) if t is None else np.asarray(t, np.float64)
+    for i in range(3):
+        T.t[i] = float(t[i])
+    T.s = float(s)
+    return T

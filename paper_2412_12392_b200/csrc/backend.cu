@@ -1,0 +1,783 @@
+// Backend global optimisation (BASELINE path 3).
+//
+// Reference: /root/reference/proj/src/backend.cpp:29-256 (directed_constraints
+// 55-69, assemble_system 91-173, backend_cost 175-190, global_optimize
+// 192-256).
+//
+//   K7 k_edge_terms  per bidirectional edge, both directed constraints from ONE
+//                    pass over the edge's matches: relative-frame normal
+//                    equations H_d (28), g_d (7), cost_d of each direction,
+//                    fp32 per thread -> FP64 block partials (no per-match
+//                    Jacobians in HBM).
+//   K8 k_edge_blocks adjoint sandwich once per edge.  With A_k = Ad(T_wk^-1)
+//                    (backend.cpp:114) and j_ref = -j adj, j_src = j adj
+//                    (126-128), the 14x14 edge block is [[S, -S], [-S, S]] with
+//                    S = A_i^T H_1 A_i + A_j^T H_2 A_j, and the gradient is
+//                    [g, -g] with g = -A_i^T g_1 + A_j^T g_2.
+//      k_assemble    deterministic scatter (edge order, as the reference's
+//                    std::map accumulation) into the dense FP64 7N x 7N system
+//                    with the anchor gauge of backend.cpp:144-155.
+//   K9 k_ldlt        cooperative blocked right-looking LDL^T (FP64, natural
+//                    order, no pivoting; fails iff a pivot is exactly 0 — the
+//                    SimplicialLDLT factorisation semantics) + blocked
+//                    triangular solves, with the damping-retry schedule of
+//                    backend.cpp:208-230 driven from the host.
+//   K10              Sim(3) retract of the non-anchor poses (FP64, host: N poses).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "residual.cuh"
+#include "select.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace pmx {
+
+struct EdgeArgs {
+  const CloudDev* clouds;     // [N]
+  const MatchesDev* matches;  // [E]  (pixel_a in i, pixel_b in j)
+  const int2* edges;          // [E]
+  const PoseR<float>* rel;    // [E][2]: dir1 = T_i^-1 T_j (ref i), dir2 = T_j^-1 T_i (ref j)
+  const double* qmin;         // [E]
+  WeightsDev wp;
+  IntrDev K;
+  int mode;
+  int N;
+  int bpe;           // blocks per edge
+  double* partials;  // [E][bpe][2][kAcc]
+};
+
+__global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
+  const int e = e0 + blockIdx.y;
+  const int b = blockIdx.x;
+  const int2 ij = A.edges[e];
+  const MatchesDev M = A.matches[e];
+  WeightsDev wp = A.wp;
+  wp.q_min = A.qmin[e];
+  const bool ok = ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N;  // backend.cpp:61
+  for (int dir = 0; dir < 2; ++dir) {
+    float acc[kAcc];
+#pragma unroll
+    for (int i = 0; i < kAcc; ++i) acc[i] = 0.0f;
+    if (ok) {
+      // dir 0: ref = i, src = j, swapped matches (backend.cpp:65)
+      // dir 1: ref = j, src = i, original matches (backend.cpp:66)
+      MatchesDev Md = M;
+      if (dir == 0) {
+        Md.pa = M.pb;
+        Md.pb = M.pa;
+      }
+      const CloudDev Xref = A.clouds[dir == 0 ? ij.x : ij.y];
+      const CloudDev Xsrc = A.clouds[dir == 0 ? ij.y : ij.x];
+      const PoseR<float> T = A.rel[2 * e + dir];
+      const int64_t stride = (int64_t)A.bpe * blockDim.x;
+      for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < Md.count; k += stride) {
+        MatchEval<float> m;
+        eval_match<float>(T, Md, Xref, Xsrc, A.mode, wp, A.K, k, m);
+        accumulate<float>(m, A.mode, wp, acc);
+      }
+    }
+    block_reduce_to(acc, A.partials + (((size_t)e * A.bpe + b) * 2 + dir) * kAcc);
+  }
+}
+
+// terms[e] = {H1 (28), g1 (7), cost1, H2 (28), g2 (7), cost2}
+__global__ void k_edge_sum(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ terms) {
+  const int e = e0 + blockIdx.x;
+  for (int t = threadIdx.x; t < 2 * 36; t += blockDim.x) {
+    const int dir = t / 36, i = t % 36;
+    double s = 0.0;
+    for (int b = 0; b < bpe; ++b) s += partials[(((size_t)e * bpe + b) * 2 + dir) * kAcc + i];
+    terms[(size_t)e * PMX_EDGE_TERMS + t] = s;
+  }
+}
+
+__device__ __forceinline__ double tri(const double* h28, int a, int b) {  // upper-tri (row-major) entry
+  if (a > b) {
+    const int t = a;
+    a = b;
+    b = t;
+  }
+  return h28[a * 7 - a * (a - 1) / 2 + (b - a)];
+}
+
+// K8: per edge S (49) and g (7) in the global frame.  adj[k] = Ad(T_wk^-1).
+__global__ void k_edge_blocks(const double* __restrict__ terms, const int2* __restrict__ edges,
+                              const double* __restrict__ adj, int N, int E, double* __restrict__ S,
+                              double* __restrict__ G) {
+  const int e = blockIdx.x;
+  if (e >= E) return;
+  const int2 ij = edges[e];
+  __shared__ double Ai[49], Aj[49], T1[49], T2[49];
+  const bool ok = ij.x >= 0 && ij.y >= 0 && ij.x < N && ij.y < N;
+  const double* t = terms + (size_t)e * PMX_EDGE_TERMS;
+  const int tid = threadIdx.x;
+  if (tid < 49) {
+    Ai[tid] = ok ? adj[(size_t)ij.x * 49 + tid] : 0.0;
+    Aj[tid] = ok ? adj[(size_t)ij.y * 49 + tid] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 49) {  // T1 = H1 A_i, T2 = H2 A_j
+    const int r = tid / 7, c = tid % 7;
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < 7; ++k) {
+      s1 += tri(t, r, k) * Ai[k * 7 + c];
+      s2 += tri(t + 36, r, k) * Aj[k * 7 + c];
+    }
+    T1[tid] = s1;
+    T2[tid] = s2;
+  }
+  __syncthreads();
+  if (tid < 49) {
+    const int r = tid / 7, c = tid % 7;
+    double s = 0.0;
+    for (int k = 0; k < 7; ++k) s += Ai[k * 7 + r] * T1[k * 7 + c];
+    double s2 = 0.0;
+    for (int k = 0; k < 7; ++k) s2 += Aj[k * 7 + r] * T2[k * 7 + c];
+    S[(size_t)e * 49 + tid] = ok ? s + s2 : 0.0;
+  } else if (tid < 56) {
+    const int r = tid - 49;
+    double s = 0.0;
+    for (int k = 0; k < 7; ++k) s += -Ai[k * 7 + r] * t[28 + k] + Aj[k * 7 + r] * t[36 + 28 + k];
+    G[(size_t)e * 7 + r] = ok ? s : 0.0;
+  }
+}
+
+// Dense assembly: one CTA per non-zero 7x7 block (contribution lists in edge order).
+__global__ void k_assemble(const int* __restrict__ blk_rc, const int* __restrict__ blk_ptr,
+                           const int* __restrict__ contrib, const double* __restrict__ S, int dim,
+                           double* __restrict__ H) {
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid >= 49) return;
+  const int k = blk_rc[2 * b], l = blk_rc[2 * b + 1];
+  double s = 0.0;
+  for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; ++q) {
+    const int c = contrib[q];
+    const int e = c >> 1;
+    const double v = S[(size_t)e * 49 + tid];
+    s += (c & 1) ? -v : v;
+  }
+  H[(size_t)(7 * k + tid / 7) * dim + 7 * l + tid % 7] = s;
+}
+
+__global__ void k_assemble_grad(const int* __restrict__ g_ptr, const int* __restrict__ g_contrib,
+                                const double* __restrict__ G, int N, int anchor, double* __restrict__ grad,
+                                double* __restrict__ H, int dim) {
+  const int k = blockIdx.x;
+  const int r = threadIdx.x;
+  if (k >= N || r >= 7) return;
+  double s = 0.0;
+  for (int q = g_ptr[k]; q < g_ptr[k + 1]; ++q) {
+    const int c = g_contrib[q];
+    const double v = G[(size_t)(c >> 1) * 7 + r];
+    s += (c & 1) ? -v : v;
+  }
+  if (k == anchor) {  // backend.cpp:153-154
+    s = 0.0;
+    for (int c = 0; c < 7; ++c) H[(size_t)(7 * k + r) * dim + 7 * k + c] = (c == r) ? 1.0 : 0.0;
+  }
+  grad[7 * k + r] = s;
+}
+
+// Sum of directed-constraint costs in the reference's order (backend.cpp:179-188).
+__global__ void k_cost_sum(const double* __restrict__ terms, int E, double* out) {
+  if (threadIdx.x != 0) return;
+  double c = 0.0;
+  for (int e = 0; e < E; ++e) {
+    c += terms[(size_t)e * PMX_EDGE_TERMS + 35];
+    c += terms[(size_t)e * PMX_EDGE_TERMS + 71];
+  }
+  *out = c;
+}
+
+// ------------------------------------------------------------------- K9
+constexpr int NB = 32;
+
+struct LdltArgs {
+  double* A;        // n x n row-major (lower triangle used / overwritten by L, D on diag)
+  const double* H;  // source (copied into A with + lambda on the diagonal)
+  double lambda;
+  const double* b;  // rhs
+  double* x;        // solution
+  double* W;        // scratch n x NB
+  int n;
+  int* status;      // [0] = ok (1) / zero pivot (0)
+};
+
+__global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
+  cg::grid_group grid = cg::this_grid();
+  const int n = P.n;
+  double* A = P.A;
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t gsz = (size_t)gridDim.x * blockDim.x;
+  // copy + damping (backend.cpp:212-215: lambda added to every diagonal)
+  for (size_t i = gtid; i < (size_t)n * n; i += gsz) {
+    const size_t r = i / n, c = i % n;
+    A[i] = P.H[i] + ((r == c) ? P.lambda : 0.0);
+  }
+  if (gtid == 0) P.status[0] = 1;
+  grid.sync();
+  __shared__ double sh[NB][NB + 1];
+  __shared__ double tileW[64][NB + 1];
+  __shared__ double tileL[64][NB + 1];
+  for (int p = 0; p < n; p += NB) {
+    const int nb = min(NB, n - p);
+    // (a) diagonal block, unblocked LDL^T (block 0)
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) {
+        const int r = i / nb, c = i % nb;
+        sh[r][c] = (c <= r) ? A[(size_t)(p + r) * n + p + c] : 0.0;
+      }
+      __syncthreads();
+      for (int c = 0; c < nb; ++c) {
+        const double d = sh[c][c];
+        if (threadIdx.x == 0 && d == 0.0) P.status[0] = 0;
+        __syncthreads();
+        // L[r][c] = A[r][c] / d ; trailing A[r][s] -= L[r][c] * A[s][c] (s <= r), using unscaled A[s][c]
+        for (int i = threadIdx.x; i < (nb - c - 1) * (nb - c - 1); i += blockDim.x) {
+          const int r = c + 1 + i / (nb - c - 1), s = c + 1 + i % (nb - c - 1);
+          if (s <= r) sh[r][s] -= sh[r][c] * sh[s][c] / d;
+        }
+        __syncthreads();
+        for (int r = c + 1 + threadIdx.x; r < nb; r += blockDim.x) sh[r][c] /= d;
+        __syncthreads();
+      }
+      for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) {
+        const int r = i / nb, c = i % nb;
+        if (c <= r) A[(size_t)(p + r) * n + p + c] = sh[r][c];
+      }
+    }
+    grid.sync();
+    // (b) panel rows below: W[r][k] = A[r][p+k] - sum_{m<k} W[r][m] L11[k][m];  L21 = W / D
+    for (int r = p + nb + (int)gtid; r < n; r += (int)gsz) {
+      double w[NB];
+      for (int k = 0; k < nb; ++k) {
+        double s = A[(size_t)r * n + p + k];
+        for (int m = 0; m < k; ++m) s -= w[m] * A[(size_t)(p + k) * n + p + m];
+        w[k] = s;
+      }
+      for (int k = 0; k < nb; ++k) {
+        P.W[(size_t)r * NB + k] = w[k];
+        A[(size_t)r * n + p + k] = w[k] / A[(size_t)(p + k) * n + p + k];
+      }
+    }
+    grid.sync();
+    // (c) trailing update of the lower triangle: A[r][c] -= sum_k W[r][k] L[c][k]
+    const int m0 = p + nb;
+    const int mt = (n - m0 + 63) / 64;
+    const int ntiles = mt * (mt + 1) / 2;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int ti = 0, acc = 0;
+      while (acc + ti + 1 <= t) {
+        acc += ti + 1;
+        ++ti;
+      }
+      const int tj = t - acc;  // tile (ti, tj), tj <= ti
+      const int r0 = m0 + ti * 64, c0 = m0 + tj * 64;
+      for (int i = threadIdx.x; i < 64 * nb; i += blockDim.x) {
+        const int rr = i / nb, k = i % nb;
+        tileW[rr][k] = (r0 + rr < n) ? P.W[(size_t)(r0 + rr) * NB + k] : 0.0;
+        tileL[rr][k] = (c0 + rr < n) ? A[(size_t)(c0 + rr) * n + p + k] : 0.0;
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+        const int rr = i / 64, cc = i % 64;
+        const int r = r0 + rr, c = c0 + cc;
+        if (r < n && c <= r) {
+          double s = 0.0;
+          for (int k = 0; k < nb; ++k) s += tileW[rr][k] * tileL[cc][k];
+          A[(size_t)r * n + c] -= s;
+        }
+      }
+      __syncthreads();
+    }
+    grid.sync();
+  }
+  // forward: L y = b (unit lower), blocked by NB; x holds y
+  for (size_t i = gtid; i < (size_t)n; i += gsz) P.x[i] = P.b[i];
+  grid.sync();
+  for (int p = 0; p < n; p += NB) {
+    const int nb = min(NB, n - p);
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      for (int i = 0; i < nb; ++i) {
+        double part = 0.0;
+        if ((int)threadIdx.x < i) part = A[(size_t)(p + i) * n + p + threadIdx.x] * P.x[p + threadIdx.x];
+        part = warp_sum(part);
+        if (threadIdx.x == 0) P.x[p + i] -= part;
+        __syncwarp();
+      }
+    }
+    grid.sync();
+    for (int r = p + nb + (int)gtid; r < n; r += (int)gsz) {
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += A[(size_t)r * n + p + k] * P.x[p + k];
+      P.x[r] -= s;
+    }
+    grid.sync();
+  }
+  for (size_t i = gtid; i < (size_t)n; i += gsz) P.x[i] /= A[i * n + i];
+  grid.sync();
+  // backward: L^T x = z
+  for (int p1 = n; p1 > 0; p1 -= NB) {
+    const int p0 = max(0, p1 - NB);
+    const int nb = p1 - p0;
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      for (int i = nb - 1; i >= 0; --i) {
+        double part = 0.0;
+        const int k = threadIdx.x;
+        if (k > i && k < nb) part = A[(size_t)(p0 + k) * n + p0 + i] * P.x[p0 + k];
+        part = warp_sum(part);
+        if (threadIdx.x == 0) P.x[p0 + i] -= part;
+        __syncwarp();
+      }
+    }
+    grid.sync();
+    for (int r = (int)gtid; r < p0; r += (int)gsz) {
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += A[(size_t)(p0 + k) * n + r] * P.x[p0 + k];
+      P.x[r] -= s;
+    }
+    grid.sync();
+  }
+}
+
+// ------------------------------------------------------------------ host
+struct DevGraph {
+  int N = 0, E = 0, anchor = -1;
+  std::vector<int2> edges;
+  DevBuf clouds, matches, edges_dev, qmin, segs, selscratch;
+  std::vector<CloudDev> hclouds;
+  std::vector<MatchesDev> hmatches;
+  int64_t max_count = 0;
+};
+
+static WeightsDev backend_weights(const pmx_backend_params& p) {
+  WeightsDev w;
+  w.sigma2 = p.mode == PMX_TRACK_RAY ? p.weights.sigma2_ray
+             : p.mode == PMX_TRACK_POINT ? p.weights.sigma2_point
+                                         : p.weights.sigma2_pixel;
+  w.q_min = 0.0;
+  w.huber_delta = p.weights.huber_delta;
+  w.distance_weight = p.weights.distance_weight;
+  return w;
+}
+
+static void stage_graph(Context& ctx, Stager& st, const pmx_graph* g, const pmx_backend_params& p, DevGraph& G) {
+  require(g && g->num_keyframes >= 0 && g->num_edges >= 0, "graph: null");
+  require(g->num_keyframes == 0 || (g->canonicals && g->poses), "graph: null keyframe arrays");
+  require(g->num_edges == 0 || (g->edge_i && g->edge_j && g->edge_matches), "graph: null edge arrays");
+  if (p.mode == PMX_TRACK_PIXEL && !p.has_intrinsics && g->num_edges > 0)
+    throw Error(PMX_ERR_INVALID_ARGUMENT, "residual_blocks: pixel mode requires intrinsics");
+  G.N = g->num_keyframes;
+  G.E = g->num_edges;
+  G.anchor = g->anchor_index;
+  G.hclouds.resize(G.N);
+  for (int k = 0; k < G.N; ++k) {
+    const pmx_pointmap& c = g->canonicals[k];
+    require(c.xyz && c.height > 0 && c.width > 0, "graph: empty canonical");
+    const size_t hw = (size_t)c.height * c.width;
+    G.hclouds[k] = CloudDev{st.in(c.xyz, 3 * hw), st.in(c.valid, hw), c.height, c.width};
+  }
+  G.edges.resize(G.E);
+  G.hmatches.resize(G.E);
+  for (int e = 0; e < G.E; ++e) {
+    G.edges[e] = make_int2(g->edge_i[e], g->edge_j[e]);
+    const pmx_matchset& m = g->edge_matches[e];
+    require(m.count >= 0 && (m.count == 0 || (m.pixel_a && m.confidence)), "graph: null edge matches");
+    MatchesDev d;
+    d.count = m.count;
+    d.pa = st.in(m.pixel_a, (size_t)m.count);
+    d.pb = st.in(m.pixel_b, (size_t)m.count);
+    d.q = st.in(m.confidence, (size_t)m.count);
+    d.valid = st.in(m.valid, (size_t)m.count);
+    G.hmatches[e] = d;
+    G.max_count = std::max(G.max_count, m.count);
+  }
+  G.clouds = DevBuf(sizeof(CloudDev) * std::max(G.N, 1), ctx.stream);
+  G.matches = DevBuf(sizeof(MatchesDev) * std::max(G.E, 1), ctx.stream);
+  G.edges_dev = DevBuf(sizeof(int2) * std::max(G.E, 1), ctx.stream);
+  G.qmin = DevBuf(sizeof(double) * std::max(G.E, 1), ctx.stream);
+  if (G.N) PMX_CUDA(cudaMemcpyAsync(G.clouds.p, G.hclouds.data(), sizeof(CloudDev) * G.N, cudaMemcpyHostToDevice, ctx.stream));
+  if (G.E) {
+    PMX_CUDA(cudaMemcpyAsync(G.matches.p, G.hmatches.data(), sizeof(MatchesDev) * G.E, cudaMemcpyHostToDevice, ctx.stream));
+    PMX_CUDA(cudaMemcpyAsync(G.edges_dev.p, G.edges.data(), sizeof(int2) * G.E, cudaMemcpyHostToDevice, ctx.stream));
+    // per-edge q_min = q_min_fraction * median valid confidence (backend.cpp:62-63)
+    std::vector<SelSeg> segs(G.E);
+    for (int e = 0; e < G.E; ++e)
+      segs[e] = SelSeg{G.hmatches[e].q, G.hmatches[e].valid, G.hmatches[e].count, G.qmin.as<double>() + e,
+                       p.weights.q_min_fraction};
+    G.segs = DevBuf(sizeof(SelSeg) * G.E, ctx.stream);
+    PMX_CUDA(cudaMemcpyAsync(G.segs.p, segs.data(), sizeof(SelSeg) * G.E, cudaMemcpyHostToDevice, ctx.stream));
+    segmented_median(ctx, G.segs.as<SelSeg>(), G.E, G.max_count, G.selscratch);
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // segs host vector goes out of scope
+  }
+}
+
+static std::vector<DSim3> host_poses(const pmx_graph* g) {
+  std::vector<DSim3> P(g->num_keyframes);
+  for (int k = 0; k < g->num_keyframes; ++k) {
+    require(g->poses[k].s > 0.0, "Sim3Pose: scale must be positive");
+    P[k] = to_dsim3(g->poses[k]);
+  }
+  return P;
+}
+
+// Edge terms for edges [e0, e1) at poses P -> terms (device, indexed by absolute edge).
+static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, const std::vector<DSim3>& P, int e0,
+                       int e1, double* terms) {
+  if (e1 <= e0) return;
+  std::vector<PoseR<float>> rel(2 * (size_t)G.E);
+  for (int e = e0; e < e1; ++e) {
+    const int i = G.edges[e].x, j = G.edges[e].y;
+    if (i < 0 || j < 0 || i >= G.N || j >= G.N) continue;
+    rel[2 * e] = make_pose<float>(sim3_mul(sim3_inv(P[i]), P[j]));      // relative_pose(ref=i, src=j)
+    rel[2 * e + 1] = make_pose<float>(sim3_mul(sim3_inv(P[j]), P[i]));  // relative_pose(ref=j, src=i)
+  }
+  DevBuf drel(sizeof(PoseR<float>) * rel.size(), ctx.stream);
+  PMX_CUDA(cudaMemcpyAsync(drel.p, rel.data(), drel.bytes, cudaMemcpyHostToDevice, ctx.stream));
+  const int bpe = (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 4095) / 4096));
+  DevBuf partials(sizeof(double) * (size_t)G.E * bpe * 2 * kAcc, ctx.stream);
+  EdgeArgs A;
+  A.clouds = G.clouds.as<CloudDev>();
+  A.matches = G.matches.as<MatchesDev>();
+  A.edges = G.edges_dev.as<int2>();
+  A.rel = drel.as<PoseR<float>>();
+  A.qmin = G.qmin.as<double>();
+  A.wp = backend_weights(p);
+  A.K = p.has_intrinsics ? IntrDev{p.intrinsics.fx, p.intrinsics.fy, p.intrinsics.cx, p.intrinsics.cy, 1}
+                         : IntrDev{0, 0, 0, 0, 0};
+  A.mode = p.mode;
+  A.N = G.N;
+  A.bpe = bpe;
+  A.partials = partials.as<double>();
+  for (int c0 = e0; c0 < e1; c0 += 65535) {
+    const int cn = std::min(65535, e1 - c0);
+    {
+      ProfScope ps(ctx, "k_edge_terms");
+      k_edge_terms<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+    }
+    launch_check(ctx, "k_edge_terms");
+    k_edge_sum<<<cn, 128, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
+    launch_check(ctx, "k_edge_sum");
+  }
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // rel host vector lifetime
+}
+
+struct Assembly {
+  int dim = 0;
+  DevBuf blk_rc, blk_ptr, contrib, g_ptr, g_contrib, adj, S, G, H, grad;
+  int nblocks = 0;
+};
+
+// Contribution lists (edge order) for every non-zero block, gauge-fixed.
+static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
+  const int N = G.N;
+  As.dim = 7 * N;
+  std::map<std::pair<int, int>, std::vector<int>> blocks;
+  std::vector<std::vector<int>> gl(N);
+  for (int e = 0; e < G.E; ++e) {
+    const int i = G.edges[e].x, j = G.edges[e].y;
+    if (i < 0 || j < 0 || i >= N || j >= N) continue;
+    // (i,i) += S, (i,j) -= S, (j,i) -= S, (j,j) += S; g_i += g, g_j -= g
+    const int add[4][3] = {{i, i, 0}, {i, j, 1}, {j, i, 1}, {j, j, 0}};
+    for (auto& a : add) {
+      if (a[0] == G.anchor || a[1] == G.anchor) continue;  // gauge: erase anchor blocks
+      blocks[{a[0], a[1]}].push_back(2 * e + a[2]);
+    }
+    gl[i].push_back(2 * e);
+    gl[j].push_back(2 * e + 1);
+  }
+  std::vector<int> rc, ptr{0}, con;
+  for (auto& [key, v] : blocks) {
+    rc.push_back(key.first);
+    rc.push_back(key.second);
+    con.insert(con.end(), v.begin(), v.end());
+    ptr.push_back((int)con.size());
+  }
+  std::vector<int> gp{0}, gc;
+  for (int k = 0; k < N; ++k) {
+    gc.insert(gc.end(), gl[k].begin(), gl[k].end());
+    gp.push_back((int)gc.size());
+  }
+  As.nblocks = (int)blocks.size();
+  auto up = [&](DevBuf& b, const std::vector<int>& v) {
+    b = DevBuf(sizeof(int) * std::max<size_t>(1, v.size()), ctx.stream);
+    if (!v.empty()) PMX_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, ctx.stream));
+  };
+  up(As.blk_rc, rc);
+  up(As.blk_ptr, ptr);
+  up(As.contrib, con);
+  up(As.g_ptr, gp);
+  up(As.g_contrib, gc);
+  As.adj = DevBuf(sizeof(double) * 49 * std::max(N, 1), ctx.stream);
+  As.S = DevBuf(sizeof(double) * 49 * std::max(G.E, 1), ctx.stream);
+  As.G = DevBuf(sizeof(double) * 7 * std::max(G.E, 1), ctx.stream);
+  As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);
+  As.grad = DevBuf(sizeof(double) * std::max(As.dim, 1), ctx.stream);
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // host vectors lifetime
+}
+
+static void assemble(Context& ctx, const DevGraph& G, Assembly& As, const std::vector<DSim3>& P,
+                     const double* terms) {
+  std::vector<double> adj(49 * (size_t)G.N);
+  for (int k = 0; k < G.N; ++k) sim3_adjoint(sim3_inv(P[k]), adj.data() + 49 * (size_t)k);  // backend.cpp:114
+  PMX_CUDA(cudaMemcpyAsync(As.adj.p, adj.data(), sizeof(double) * adj.size(), cudaMemcpyHostToDevice, ctx.stream));
+  if (G.E) {
+    k_edge_blocks<<<G.E, 64, 0, ctx.stream>>>(terms, G.edges_dev.as<int2>(), As.adj.as<double>(), G.N, G.E,
+                                             As.S.as<double>(), As.G.as<double>());
+    launch_check(ctx, "k_edge_blocks");
+  }
+  PMX_CUDA(cudaMemsetAsync(As.H.p, 0, As.H.bytes, ctx.stream));
+  if (As.nblocks) {
+    k_assemble<<<As.nblocks, 64, 0, ctx.stream>>>(As.blk_rc.as<int>(), As.blk_ptr.as<int>(), As.contrib.as<int>(),
+                                                  As.S.as<double>(), As.dim, As.H.as<double>());
+    launch_check(ctx, "k_assemble");
+  }
+  if (G.N) {
+    k_assemble_grad<<<G.N, 32, 0, ctx.stream>>>(As.g_ptr.as<int>(), As.g_contrib.as<int>(), As.G.as<double>(), G.N,
+                                                G.anchor, As.grad.as<double>(), As.H.as<double>(), As.dim);
+    launch_check(ctx, "k_assemble_grad");
+  }
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // adj lifetime
+}
+
+__global__ void k_negate(const double* a, double* b, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = -a[i];
+}
+
+// Damped solve attempts (backend.cpp:208-230).  Returns solved; tau on host.
+static bool damped_solve(Context& ctx, const pmx_backend_params& p, Assembly& As, std::vector<double>& tau) {
+  const int n = As.dim;
+  DevBuf work(sizeof(double) * (size_t)n * n, ctx.stream), W(sizeof(double) * (size_t)n * NB, ctx.stream),
+      rhs(sizeof(double) * n, ctx.stream), x(sizeof(double) * n, ctx.stream), status(sizeof(int), ctx.stream);
+  k_negate<<<(n + 255) / 256, 256, 0, ctx.stream>>>(As.grad.as<double>(), rhs.as<double>(), n);
+  launch_check(ctx, "k_negate");
+  int per_sm = 0;
+  PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
+  const int nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  double lambda = 0.0;
+  tau.assign(n, 0.0);
+  for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
+    LdltArgs L{work.as<double>(), As.H.as<double>(), lambda, rhs.as<double>(), x.as<double>(), W.as<double>(), n,
+               status.as<int>()};
+    void* args[] = {&L};
+    {
+      ProfScope ps(ctx, "k_ldlt");
+      PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
+    }
+    launch_check(ctx, "k_ldlt");
+    int ok = 0;
+    PMX_CUDA(cudaMemcpyAsync(&ok, status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaMemcpyAsync(tau.data(), x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    if (ok) {
+      bool fin = true;
+      double inf = 0.0;
+      for (double v : tau) {
+        fin = fin && std::isfinite(v);
+        inf = std::max(inf, std::fabs(v));
+      }
+      if (fin && inf < 1e3) return true;
+    }
+    lambda = lambda == 0.0 ? p.damping_init : lambda * 10.0;
+  }
+  return false;
+}
+
+static double read_cost(Context& ctx, const DevGraph& G, const double* terms) {
+  DevBuf c(sizeof(double), ctx.stream);
+  k_cost_sum<<<1, 32, 0, ctx.stream>>>(terms, G.E, c.as<double>());
+  launch_check(ctx, "k_cost_sum");
+  double h = 0.0;
+  PMX_CUDA(cudaMemcpyAsync(&h, c.p, sizeof(double), cudaMemcpyDeviceToHost, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return h;
+}
+
+static pmx_backend_params backend_params(const pmx_backend_params* p) {
+  pmx_backend_params bp;
+  pmx_default_backend_params(&bp);
+  if (p) bp = *p;
+  return bp;
+}
+
+}  // namespace pmx
+
+using namespace pmx;
+
+extern "C" int pmx_impl_backend_edge_terms(pmx_context* c, pmx_memory mem, const pmx_graph* g,
+                                           const pmx_backend_params* pp, int32_t e0, int32_t e1, double* out) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  const pmx_backend_params p = backend_params(pp);
+  require(g && out && e0 >= 0 && e1 >= e0 && e1 <= g->num_edges, "backend_edge_terms: bad range");
+  Stager st(ctx, mem);
+  DevGraph G;
+  stage_graph(ctx, st, g, p, G);
+  const std::vector<DSim3> P = host_poses(g);
+  DevBuf terms(sizeof(double) * PMX_EDGE_TERMS * std::max(G.E, 1), ctx.stream);
+  edge_terms(ctx, G, p, P, e0, e1, terms.as<double>());
+  const size_t cnt = (size_t)(e1 - e0) * PMX_EDGE_TERMS;
+  const cudaMemcpyKind k = mem == PMX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (cnt) PMX_CUDA(cudaMemcpyAsync(out, terms.as<double>() + (size_t)e0 * PMX_EDGE_TERMS, sizeof(double) * cnt, k, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_backend_cost(pmx_context* c, pmx_memory mem, const pmx_graph* g,
+                                     const pmx_backend_params* pp, double* cost) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  const pmx_backend_params p = backend_params(pp);
+  require(g && cost, "backend_cost: null arguments");
+  Stager st(ctx, mem);
+  DevGraph G;
+  stage_graph(ctx, st, g, p, G);
+  const std::vector<DSim3> P = host_poses(g);
+  DevBuf terms(sizeof(double) * PMX_EDGE_TERMS * std::max(G.E, 1), ctx.stream);
+  edge_terms(ctx, G, p, P, 0, G.E, terms.as<double>());
+  *cost = read_cost(ctx, G, terms.as<double>());
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_assemble_system(pmx_context* c, pmx_memory mem, const pmx_graph* g,
+                                        const pmx_backend_params* pp, double* H, double* grad) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  const pmx_backend_params p = backend_params(pp);
+  require(g && H && grad, "assemble_system: null arguments");
+  Stager st(ctx, mem);
+  DevGraph G;
+  stage_graph(ctx, st, g, p, G);
+  const std::vector<DSim3> P = host_poses(g);
+  DevBuf terms(sizeof(double) * PMX_EDGE_TERMS * std::max(G.E, 1), ctx.stream);
+  edge_terms(ctx, G, p, P, 0, G.E, terms.as<double>());
+  Assembly As;
+  build_assembly(ctx, G, As);
+  assemble(ctx, G, As, P, terms.as<double>());
+  const cudaMemcpyKind k = mem == PMX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  PMX_CUDA(cudaMemcpyAsync(H, As.H.p, sizeof(double) * (size_t)As.dim * As.dim, k, ctx.stream));
+  PMX_CUDA(cudaMemcpyAsync(grad, As.grad.p, sizeof(double) * As.dim, k, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_backend_solve_terms(pmx_context* c, pmx_memory mem, const pmx_graph* g,
+                                            const pmx_backend_params* pp, const double* terms, double* tau,
+                                            double* cost, int32_t* solved) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  const pmx_backend_params p = backend_params(pp);
+  require(g && terms && tau && cost && solved, "backend_solve_terms: null arguments");
+  // topology + poses only: no pointmaps / matches are touched
+  DevGraph G;
+  G.N = g->num_keyframes;
+  G.E = g->num_edges;
+  G.anchor = g->anchor_index;
+  G.edges.resize(G.E);
+  for (int e = 0; e < G.E; ++e) G.edges[e] = make_int2(g->edge_i[e], g->edge_j[e]);
+  G.edges_dev = DevBuf(sizeof(int2) * std::max(G.E, 1), ctx.stream);
+  if (G.E) PMX_CUDA(cudaMemcpyAsync(G.edges_dev.p, G.edges.data(), sizeof(int2) * G.E, cudaMemcpyHostToDevice, ctx.stream));
+  Stager st(ctx, mem);
+  const double* dterms = st.in(terms, (size_t)G.E * PMX_EDGE_TERMS);
+  const std::vector<DSim3> P = host_poses(g);
+  *cost = read_cost(ctx, G, dterms);
+  Assembly As;
+  build_assembly(ctx, G, As);
+  assemble(ctx, G, As, P, dterms);
+  std::vector<double> t;
+  *solved = damped_solve(ctx, p, As, t) ? 1 : 0;
+  if (mem == PMX_MEM_HOST)
+    std::memcpy(tau, t.data(), sizeof(double) * t.size());
+  else
+    PMX_CUDA(cudaMemcpy(tau, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_graph* g, const pmx_backend_params* pp,
+                                        pmx_optimize_result* result, pmx_sim3* pose_trace) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  const pmx_backend_params p = backend_params(pp);
+  require(g && result, "global_optimize: null arguments");
+  std::memset(result, 0, sizeof(*result));
+  const int n = g->num_keyframes;
+  if (n < 2 || g->num_edges == 0) {  // backend.cpp:195-198
+    result->converged = 1;
+    return PMX_OK;
+  }
+  Stager st(ctx, mem);
+  DevGraph G;
+  stage_graph(ctx, st, g, p, G);
+  std::vector<DSim3> P = host_poses(g);
+  Assembly As;
+  build_assembly(ctx, G, As);
+  DevBuf terms(sizeof(double) * PMX_EDGE_TERMS * G.E, ctx.stream);
+  edge_terms(ctx, G, p, P, 0, G.E, terms.as<double>());
+  double cost = read_cost(ctx, G, terms.as<double>());
+  auto push = [&](double v) {
+    if (result->cost_trace_len < PMX_MAX_TRACE) result->cost_trace[result->cost_trace_len++] = v;
+  };
+  push(cost);
+  auto record = [&](int it, const std::vector<DSim3>& poses) {
+    if (!pose_trace) return;
+    for (int k = 0; k < n; ++k) pose_trace[(size_t)it * n + k] = to_pmx(poses[k]);
+  };
+  bool done = false;
+  for (int iter = 0; iter < p.max_iterations && !done; ++iter) {
+    result->iterations++;
+    assemble(ctx, G, As, P, terms.as<double>());
+    std::vector<double> tau;
+    if (!damped_solve(ctx, p, As, tau)) {  // state intact, not converged (backend.cpp:228-230)
+      for (int k = 0; k < n; ++k) g->poses[k] = to_pmx(P[k]);
+      return PMX_OK;
+    }
+    const std::vector<DSim3> previous = P;
+    for (int k = 0; k < n; ++k) {
+      if (k == G.anchor) continue;  // anchor pose bit-identical (backend.cpp:236)
+      P[k] = sim3_mul(sim3_exp(tau.data() + 7 * k), P[k]);
+    }
+    edge_terms(ctx, G, p, P, 0, G.E, terms.as<double>());
+    const double cost_new = read_cost(ctx, G, terms.as<double>());
+    if (cost_new > cost * (1.0 + 1e-12) + 1e-300) {  // backend.cpp:242-246
+      P = previous;
+      record(iter, P);
+      break;
+    }
+    record(iter, P);
+    cost = cost_new;
+    push(cost);
+    double n2 = 0.0;
+    for (double v : tau) n2 += v * v;
+    if (std::sqrt(n2) < p.update_tol) done = true;
+  }
+  result->converged = 1;  // backend.cpp:244, 250, 254
+  for (int k = 0; k < n; ++k) g->poses[k] = to_pmx(P[k]);
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_ldlt_solve(pmx_context* c, pmx_memory mem, int32_t n, const double* Ah, const double* bh,
+                                   double* xh, int32_t* ok) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(n > 0 && Ah && bh && xh && ok, "ldlt_solve: bad arguments");
+  Stager st(ctx, mem);
+  const double* A = st.in(Ah, (size_t)n * n);
+  const double* b = st.in(bh, (size_t)n);
+  double* x = st.out(xh, (size_t)n);
+  DevBuf work(sizeof(double) * (size_t)n * n, ctx.stream), W(sizeof(double) * (size_t)n * NB, ctx.stream),
+      status(sizeof(int), ctx.stream);
+  int per_sm = 0;
+  PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
+  const int nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  LdltArgs L{work.as<double>(), A, 0.0, b, x, W.as<double>(), n, status.as<int>()};
+  void* args[] = {&L};
+  PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
+  launch_check(ctx, "k_ldlt");
+  st.back(xh, x, (size_t)n);
+  int h = 0;
+  PMX_CUDA(cudaMemcpyAsync(&h, status.p, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  *ok = h;
+  return PMX_OK;
+}

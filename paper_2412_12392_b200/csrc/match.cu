@@ -1,0 +1,984 @@
+// Iterative projective matching + descriptor refinement (BASELINE path 1).
+//
+// Reference: /root/reference/proj/src/camera.cpp:39-271
+//   normalize_rays (39-56), interpolate_ray (58-100), iterative_project
+//   (115-174), median_scene_distance (178-191), match_pointmaps (195-237),
+//   feature_refine (239-271).
+//
+// Kernels (per chunk of independent pairs, one CUDA grid dimension per pair):
+//   K1 k_prep        one thread per a-pixel: FP64 unit ray + validity into a
+//                    32-byte ray map (L2-resident per chunk), the fp32 norm key
+//                    of median_scene_distance, and pass 1 of the radix select
+//                    (4096-bin shared-memory histogram).
+//   K2 k_sel_scan / k_sel_hist
+//                    exact rank-floor(n/2) radix select (12+12+8 bits) over
+//                    the fp32 norm keys: the upper median of nth_element.
+//   K3 k_match       one thread per b-pixel: FP64 Levenberg-Marquardt on the
+//                    ray-angle error, lround + clamp, q = sqrt(Q_a Q_b), the 3D
+//                    invalidation test, and (K4, fused) the coarse-to-fine
+//                    descriptor refinement with fp32 dots, a rigorous error
+//                    bound and an exact FP64 re-check of every near-tie, so the
+//                    argmax equals the reference's exact-arithmetic argmax
+//                    (strict '>' scan, ties keep the centre / first raster).
+#include <cfloat>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "pmx_common.cuh"
+
+namespace pmx {
+
+constexpr int kHist1 = 4096, kHist2 = 4096, kHist3 = 256;
+constexpr int kHistTotal = kHist1 + kHist2 + kHist3;
+constexpr uint32_t kNoKey = 0xffffffffu;
+
+struct SelState {
+  uint32_t n;       // number of keys
+  uint32_t k;       // target rank (n / 2)
+  uint32_t prefix;  // resolved high bits so far
+  uint32_t krem;    // rank within the current bucket
+  double threshold; // invalidation_median_fraction * median
+};
+
+struct PairDev {
+  int Ha, Wa, Hb, Wb, dim;
+  const float* xa;
+  const uint8_t* va;
+  const float* xb;
+  const uint8_t* vb;
+  const __half* da;
+  const float* qa;
+  const __half* db;
+  const float* qb;
+  // optional seed (init MatchSet): last valid k per pixel_b, and the init pixel_a
+  const int32_t* seed_last;
+  const int32_t* init_pa;
+  // outputs
+  int32_t* out_pa;
+  int32_t* out_pb;
+  float* out_q;
+  uint8_t* out_valid;
+  // per-pair scratch
+  double4* rays;
+  uint32_t* keys;
+  uint32_t* hist;
+  SelState* sel;
+};
+
+struct LMParams {
+  double lambda_init, lambda_up, lambda_down;
+  double cos_tol;  // exact threshold: acos(clamp(d,-1,1)) < tol  <=>  d >= cos_tol
+  int max_iterations;
+  double median_fraction;
+};
+
+struct RefineLevels {
+  int n;
+  int stride[PMX_MAX_REFINE_LEVELS];
+  int radius[PMX_MAX_REFINE_LEVELS];
+};
+
+// ---------------------------------------------------------------- K1
+__global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int HW = P.Ha * P.Wa;
+  __shared__ uint32_t sh[kHist1];
+  for (int i = threadIdx.x; i < kHist1; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const int begin = blockIdx.x * px_per_block;
+  const int end = min(HW, begin + px_per_block);
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+    const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
+    const bool v = P.va ? P.va[i] != 0 : true;
+    // camera.cpp:47-53: norm in FP64, exact division as the reference
+    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    double4 r = make_double4(0.0, 0.0, 1.0, 0.0);
+    if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
+    P.rays[i] = r;
+    // camera.cpp:181-186: median over valid pixels with |p| > 1e-12
+    uint32_t key = kNoKey;
+    if (v && nrm > 1e-12) {
+      const float f = (float)nrm;
+      key = __float_as_uint(f);
+      atomicAdd(&sh[key >> 20], 1u);
+    }
+    P.keys[i] = key;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
+    if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
+}
+
+// ---------------------------------------------------------------- K2
+// One block per pair: locate the bucket holding rank krem.
+template <int PASS>
+__global__ void __launch_bounds__(1024) k_sel_scan(const PairDev* __restrict__ pairs, double fraction) {
+  const PairDev& P = pairs[blockIdx.x];
+  constexpr int NB = PASS == 1 ? kHist1 : PASS == 2 ? kHist2 : kHist3;
+  const uint32_t* h = P.hist + (PASS == 1 ? 0 : PASS == 2 ? kHist1 : kHist1 + kHist2);
+  __shared__ uint32_t wsum[32];
+  __shared__ uint32_t total;
+  const int t = threadIdx.x;
+  constexpr int PER = (NB + 1023) / 1024;
+  uint32_t local[PER];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int b = t * PER + j;
+    local[j] = b < NB ? h[b] : 0u;
+    s += local[j];
+  }
+  // block exclusive scan of per-thread sums
+  uint32_t incl = s;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += y;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    uint32_t w = wsum[t];
+    uint32_t wi = w;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (t >= o) wi += y;
+    }
+    wsum[t] = wi - w;
+    if (t == 31) total = wi;
+  }
+  __syncthreads();
+  uint32_t excl = wsum[t >> 5] + incl - s;
+  SelState* st = P.sel;
+  if (PASS == 1 && t == 0) {
+    st->n = total;
+    st->k = total / 2;
+    st->krem = total / 2;
+  }
+  __syncthreads();
+  const uint32_t krem = st->krem;
+  if (total == 0) {
+    if (t == 0) {
+      st->prefix = 0;
+      if (PASS == 3 || PASS == 1) st->threshold = fraction * 0.0;  // empty -> median 0
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    const int b = t * PER + j;
+    if (b < NB && local[j] > 0 && excl <= krem && krem < excl + local[j]) {
+      if (PASS == 1) {
+        st->prefix = (uint32_t)b;
+      } else if (PASS == 2) {
+        st->prefix = (st->prefix << 12) | (uint32_t)b;
+      } else {
+        const uint32_t key = (st->prefix << 8) | (uint32_t)b;
+        st->threshold = fraction * (double)__uint_as_float(key);
+      }
+      st->krem = krem - excl;
+    }
+    excl += local[j];
+  }
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(256) k_sel_hist(const PairDev* __restrict__ pairs, int px_per_block) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int HW = P.Ha * P.Wa;
+  if (P.sel->n == 0) return;
+  constexpr int NB = PASS == 2 ? kHist2 : kHist3;
+  uint32_t* h = P.hist + (PASS == 2 ? kHist1 : kHist1 + kHist2);
+  __shared__ uint32_t sh[NB];
+  for (int i = threadIdx.x; i < NB; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const uint32_t prefix = P.sel->prefix;
+  const int begin = blockIdx.x * px_per_block;
+  const int end = min(HW, begin + px_per_block);
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+    const uint32_t key = P.keys[i];
+    if (key == kNoKey) continue;
+    if (PASS == 2) {
+      if ((key >> 20) == prefix) atomicAdd(&sh[(key >> 8) & 0xfff], 1u);
+    } else {
+      if ((key >> 8) == prefix) atomicAdd(&sh[key & 0xff], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NB; i += blockDim.x)
+    if (sh[i]) atomicAdd(&h[i], sh[i]);
+}
+
+// ---------------------------------------------------------------- LM
+__device__ __forceinline__ double4 ld_ray(const double4* rays, int i) {
+  const double2* p = reinterpret_cast<const double2*>(rays + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// interpolate_ray, camera.cpp:58-100.  J: col0 = d/du (J[0..2]), col1 = d/dv.
+__device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int W, int H, double u,
+                                           double v, double ray[3], double J[6]) {
+  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+  int u0 = (int)floor(u);
+  int v0 = (int)floor(v);
+  u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
+  v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
+  const int u1 = min(u0 + 1, W - 1);
+  const int v1 = min(v0 + 1, H - 1);
+  const double fu = u - u0;
+  const double fv = v - v0;
+  const double4 r00 = ld_ray(rays, v0 * W + u0);
+  const double4 r10 = ld_ray(rays, v0 * W + u1);
+  const double4 r01 = ld_ray(rays, v1 * W + u0);
+  const double4 r11 = ld_ray(rays, v1 * W + u1);
+  if (r00.w == 0.0 || r10.w == 0.0 || r01.w == 0.0 || r11.w == 0.0) return false;
+  const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
+  const double g0 = w00 * r00.x + w10 * r10.x + w01 * r01.x + w11 * r11.x;
+  const double g1 = w00 * r00.y + w10 * r10.y + w01 * r01.y + w11 * r11.y;
+  const double g2 = w00 * r00.z + w10 * r10.z + w01 * r01.z + w11 * r11.z;
+  const double gn = sqrt(g0 * g0 + g1 * g1 + g2 * g2);
+  if (gn < 1e-12) return false;
+  ray[0] = g0 / gn;
+  ray[1] = g1 / gn;
+  ray[2] = g2 / gn;
+  const double du0 = (1 - fv) * (r10.x - r00.x) + fv * (r11.x - r01.x);
+  const double du1 = (1 - fv) * (r10.y - r00.y) + fv * (r11.y - r01.y);
+  const double du2 = (1 - fv) * (r10.z - r00.z) + fv * (r11.z - r01.z);
+  const double dv0 = (1 - fu) * (r01.x - r00.x) + fu * (r11.x - r10.x);
+  const double dv1 = (1 - fu) * (r01.y - r00.y) + fu * (r11.y - r10.y);
+  const double dv2 = (1 - fu) * (r01.z - r00.z) + fu * (r11.z - r10.z);
+  const double rdu = ray[0] * du0 + ray[1] * du1 + ray[2] * du2;
+  const double rdv = ray[0] * dv0 + ray[1] * dv1 + ray[2] * dv2;
+  J[0] = (du0 - ray[0] * rdu) / gn;
+  J[1] = (du1 - ray[1] * rdu) / gn;
+  J[2] = (du2 - ray[2] * rdu) / gn;
+  J[3] = (dv0 - ray[0] * rdv) / gn;
+  J[4] = (dv1 - ray[1] * rdv) / gn;
+  J[5] = (dv2 - ray[2] * rdv) / gn;
+  return true;
+}
+
+// 2x2 instance of Eigen's pivoted LDLT solve (camera.cpp:147), same ops as
+// ldlt_pivoted_solve(2, ...).
+__device__ __forceinline__ void ldlt2_solve(double h00, double h01, double h11, double b0, double b1,
+                                            double* x0, double* x1) {
+  const bool sw = fabs(h11) > fabs(h00);
+  double m00 = sw ? h11 : h00, m11 = sw ? h00 : h11;
+  double m10 = h01;
+  if (!(fabs(m00) > 0.0)) {
+    *x0 = 0.0;
+    *x1 = 0.0;
+    return;
+  }
+  m10 /= m00;
+  const double temp0 = m00 * m10;
+  m11 -= m10 * temp0;
+  double d0 = sw ? b1 : b0, d1 = sw ? b0 : b1;
+  d1 -= m10 * d0;
+  const double tiny = 2.2250738585072014e-308;
+  d0 = fabs(m00) > tiny ? d0 / m00 : 0.0;
+  d1 = fabs(m11) > tiny ? d1 / m11 : 0.0;
+  d0 -= m10 * d1;
+  *x0 = sw ? d1 : d0;
+  *x1 = sw ? d0 : d1;
+}
+
+struct ProjOut {
+  double pu, pv;
+  bool converged;
+  int iterations;
+};
+
+// iterative_project, camera.cpp:115-174
+__device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W, int H, double x0,
+                                         double x1, double x2, double pu0, double pv0,
+                                         const LMParams& lp) {
+  ProjOut res;
+  res.converged = false;
+  res.iterations = 0;
+  const double cu = fmin(fmax(pu0, 0.0), (double)(W - 1));
+  const double cv = fmin(fmax(pv0, 0.0), (double)(H - 1));
+  const double xn = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
+  if (xn < 1e-12 || !(isfinite(x0) && isfinite(x1) && isfinite(x2))) {
+    res.pu = cu;
+    res.pv = cv;
+    return res;
+  }
+  const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
+  double pu = cu, pv = cv;
+  double ray[3], J[6];
+  if (!interp_ray(rays, W, H, pu, pv, ray, J)) {
+    res.pu = pu;
+    res.pv = pv;
+    return res;
+  }
+  double r0 = ray[0] - t0, r1 = ray[1] - t1, r2 = ray[2] - t2;
+  double cost = r0 * r0 + r1 * r1 + r2 * r2;
+  if (ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol) {
+    res.pu = pu;
+    res.pv = pv;
+    res.converged = true;
+    return res;
+  }
+  double lambda = lp.lambda_init;
+  for (int it = 0; it < lp.max_iterations; ++it) {
+    ++res.iterations;
+    r0 = ray[0] - t0;
+    r1 = ray[1] - t1;
+    r2 = ray[2] - t2;
+    const double a00 = J[0] * J[0] + J[1] * J[1] + J[2] * J[2];
+    const double a01 = J[0] * J[3] + J[1] * J[4] + J[2] * J[5];
+    const double a11 = J[3] * J[3] + J[4] * J[4] + J[5] * J[5];
+    const double g0 = J[0] * r0 + J[1] * r1 + J[2] * r2;
+    const double g1 = J[3] * r0 + J[4] * r1 + J[5] * r2;
+    const double h00 = a00 + lambda * fmax(a00, 1e-12);
+    const double h11 = a11 + lambda * fmax(a11, 1e-12);
+    double s0, s1;
+    ldlt2_solve(h00, a01, h11, g0, g1, &s0, &s1);
+    const double d0 = -s0, d1 = -s1;
+    if (!isfinite(d0) || !isfinite(d1)) break;
+    const double tu = fmin(fmax(pu + d0, 0.0), (double)(W - 1));
+    const double tv = fmin(fmax(pv + d1, 0.0), (double)(H - 1));
+    double rt[3], Jt[6];
+    if (interp_ray(rays, W, H, tu, tv, rt, Jt)) {
+      const double e0 = rt[0] - t0, e1 = rt[1] - t1, e2 = rt[2] - t2;
+      const double ct = e0 * e0 + e1 * e1 + e2 * e2;
+      if (ct < cost) {
+        pu = tu;
+        pv = tv;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) ray[k] = rt[k];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) J[k] = Jt[k];
+        cost = ct;
+        lambda *= lp.lambda_down;
+        if (ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol) {
+          res.pu = pu;
+          res.pv = pv;
+          res.converged = true;
+          return res;
+        }
+        continue;
+      }
+    }
+    lambda *= lp.lambda_up;
+  }
+  res.pu = pu;
+  res.pv = pv;
+  res.converged = ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol;
+  return res;
+}
+
+// ------------------------------------------------------------ refine (K4)
+// Exact dot of two fp16 descriptors exactly as the reference evaluates it
+// in FP64 (products exact; sequential additions, no FMA).
+__device__ __noinline__ double dot_exact(const __half* __restrict__ a, const __half* __restrict__ b,
+                                         int dim) {
+  double s = 0.0;
+  for (int k = 0; k < dim; ++k)
+    s = __dadd_rn(s, __dmul_rn((double)__half2float(a[k]), (double)__half2float(b[k])));
+  return s;
+}
+
+// fp32 dot of a candidate against the register-resident target, with the
+// candidate's max |component| (for the rounding-error bound).
+template <int DIM>
+__device__ __forceinline__ float dot_fast(const __half* __restrict__ a, const float (&bt)[DIM],
+                                          float* amax) {
+  const uint4* p = reinterpret_cast<const uint4*>(a);
+  float s = 0.0f;
+  __half2 m2 = __float2half2_rn(0.0f);
+#pragma unroll
+  for (int q = 0; q < DIM / 8; ++q) {
+    const uint4 w = __ldg(p + q);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      __half2 v;
+      memcpy(&v, &ws[h], 4);
+      m2 = __hmax2(m2, __habs2(v));
+      const float2 f = __half22float2(v);
+      s = fmaf(f.x, bt[8 * q + 2 * h], s);
+      s = fmaf(f.y, bt[8 * q + 2 * h + 1], s);
+    }
+  }
+  const float2 mf = __half22float2(m2);
+  *amax = fmaxf(mf.x, mf.y);
+  return s;
+}
+
+// Coarse-to-fine refinement of one match (camera.cpp:239-271) — returns the
+// refined a-pixel index.  Candidates inside the previous level's window are
+// skipped: they were all scored <= the running best, and only a strict '>'
+// can move the best, so skipping them is exact.
+template <int DIM>
+__device__ int refine_one(const __half* __restrict__ Da, int Wa, int Ha, const __half* __restrict__ bdesc,
+                          int pa, const RefineLevels& L) {
+  float bt[DIM];
+  float bnorm1 = 0.0f;
+  {
+    const uint4* p = reinterpret_cast<const uint4*>(bdesc);
+#pragma unroll
+    for (int q = 0; q < DIM / 8; ++q) {
+      const uint4 w = __ldg(p + q);
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        __half2 v;
+        memcpy(&v, &ws[h], 4);
+        const float2 f = __half22float2(v);
+        bt[8 * q + 2 * h] = f.x;
+        bt[8 * q + 2 * h + 1] = f.y;
+        bnorm1 += fabsf(f.x) + fabsf(f.y);
+      }
+    }
+  }
+  // Error bound of an fp32 FMA chain with exact products:
+  // |s - exact| <= DIM * u * sum|a_k b_k| <= DIM * u * max|a| * ||b||_1.
+  const float gamma = (float)DIM * 5.9604645e-08f * 1.001f;
+  int best_u = pa % Wa, best_v = pa / Wa;
+  int prev_cu = 0, prev_cv = 0, prev_s = 0, prev_r = -1;
+  for (int l = 0; l < L.n; ++l) {
+    const int s = L.stride[l], r = L.radius[l];
+    const int cu = best_u, cv = best_v;
+    // identical window around the same centre: nothing can win (strict '>')
+    if (l > 0 && s == prev_s && r == prev_r && cu == prev_cu && cv == prev_cv) continue;
+    const __half* cdesc = Da + (size_t)(cv * Wa + cu) * DIM;
+    float am;
+    float best_f = dot_fast<DIM>(cdesc, bt, &am);
+    float best_b = gamma * am * bnorm1;
+    double best_x = 0.0;  // exact score when best_known
+    bool best_known = false;
+    for (int dv = -r; dv <= r; ++dv) {
+      const int v = cv + dv * s;
+      if (v < 0 || v >= Ha) continue;
+      for (int du = -r; du <= r; ++du) {
+        const int u = cu + du * s;
+        if (u < 0 || u >= Wa) continue;
+        if (du == 0 && dv == 0) continue;  // the centre never beats itself
+        if (prev_r >= 0) {  // inside the previous level's (already maximised) window?
+          const int eu = u - prev_cu, ev = v - prev_cv;
+          if (eu % prev_s == 0 && ev % prev_s == 0 && abs(eu) <= prev_r * prev_s &&
+              abs(ev) <= prev_r * prev_s)
+            continue;
+        }
+        const __half* adesc = Da + (size_t)(v * Wa + u) * DIM;
+        float amax;
+        const float sc = dot_fast<DIM>(adesc, bt, &amax);
+        const float sb = gamma * amax * bnorm1;
+        bool take;
+        if (sc - sb > best_f + best_b) {
+          take = true;
+        } else if (sc + sb <= best_f - best_b) {
+          take = false;
+        } else {  // near tie / non-finite: decide in exact arithmetic
+          if (!best_known) {
+            best_x = dot_exact(Da + (size_t)(best_v * Wa + best_u) * DIM, bdesc, DIM);
+            best_known = true;
+          }
+          const double ex = dot_exact(adesc, bdesc, DIM);
+          take = ex > best_x;
+          if (take) {
+            best_u = u;
+            best_v = v;
+            best_f = sc;
+            best_b = sb;
+            best_x = ex;
+            continue;
+          }
+        }
+        if (take) {
+          best_u = u;
+          best_v = v;
+          best_f = sc;
+          best_b = sb;
+          best_known = false;
+        }
+      }
+    }
+    prev_cu = cu;
+    prev_cv = cv;
+    prev_s = s;
+    prev_r = r;
+  }
+  return best_v * Wa + best_u;
+}
+
+// Generic-dimension refinement: exact FP64 scores throughout.
+__device__ int refine_one_generic(const __half* __restrict__ Da, int Wa, int Ha, int dim,
+                                  const __half* __restrict__ bdesc, int pa, const RefineLevels& L) {
+  int best_u = pa % Wa, best_v = pa / Wa;
+  for (int l = 0; l < L.n; ++l) {
+    const int s = L.stride[l], r = L.radius[l];
+    const int cu = best_u, cv = best_v;
+    double best = dot_exact(Da + (size_t)(cv * Wa + cu) * dim, bdesc, dim);
+    for (int dv = -r; dv <= r; ++dv)
+      for (int du = -r; du <= r; ++du) {
+        const int u = cu + du * s, v = cv + dv * s;
+        if (u < 0 || v < 0 || u >= Wa || v >= Ha) continue;
+        const double sc = dot_exact(Da + (size_t)(v * Wa + u) * dim, bdesc, dim);
+        if (sc > best) {
+          best = sc;
+          best_u = u;
+          best_v = v;
+        }
+      }
+  }
+  return best_v * Wa + best_u;
+}
+
+__device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb, const RefineLevels& L) {
+  const __half* bdesc = P.db + (size_t)pb * P.dim;
+  if (((uintptr_t)P.da | (uintptr_t)P.db) & 15)  // vector loads need 16-byte rows
+    return refine_one_generic(P.da, P.Wa, P.Ha, P.dim, bdesc, pa, L);
+  if (P.dim == 24) return refine_one<24>(P.da, P.Wa, P.Ha, bdesc, pa, L);
+  if (P.dim == 16) return refine_one<16>(P.da, P.Wa, P.Ha, bdesc, pa, L);
+  if (P.dim == 32) return refine_one<32>(P.da, P.Wa, P.Ha, bdesc, pa, L);
+  return refine_one_generic(P.da, P.Wa, P.Ha, P.dim, bdesc, pa, L);
+}
+
+// ---------------------------------------------------------------- K3 + K4
+// One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair.
+__global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs, LMParams lp,
+                                               RefineLevels L, int do_refine) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int tiles_x = (P.Wb + 31) / 32;
+  const int tiles = tiles_x * ((P.Hb + 7) / 8);
+  if ((int)blockIdx.x >= tiles) return;
+  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+  const int v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+  if (u >= P.Wb || v >= P.Hb) return;
+  const int n = v * P.Wb + u;
+  if (P.out_pb) P.out_pb[n] = n;
+  int32_t pa_out = -1;
+  float q_out = 0.0f;
+  uint8_t valid_out = 0;
+  const bool vb = P.vb ? P.vb[n] != 0 : true;
+  const double x0 = P.xb[3 * n], x1 = P.xb[3 * n + 1], x2 = P.xb[3 * n + 2];
+  // camera.cpp:217-219 (norm < 1e-12 skips; a NaN norm does not)
+  const double xnorm = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
+  if (vb && !(xnorm < 1e-12)) {
+    int seed_pixel = n;
+    if (P.seed_last) {
+      const int k = P.seed_last[n];
+      if (k >= 0) {
+        const int s = P.init_pa[k];
+        if (s >= 0) seed_pixel = s;
+      }
+    }
+    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)(seed_pixel % P.Wa),
+                                             (double)(seed_pixel / P.Wa), lp);
+    const int pu = (int)round(pr.pu);  // std::lround: half away from zero
+    const int pv = (int)round(pr.pv);
+    int pa = min(max(pv, 0), P.Ha - 1) * P.Wa + min(max(pu, 0), P.Wa - 1);
+    bool valid = pr.converged && (P.va ? P.va[pa] != 0 : true);
+    if (valid) {
+      const double a0 = P.xa[3 * pa], a1 = P.xa[3 * pa + 1], a2 = P.xa[3 * pa + 2];
+      const double e0 = a0 - x0, e1 = a1 - x1, e2 = a2 - x2;
+      const double dist = sqrt(e0 * e0 + e1 * e1 + e2 * e2);
+      if (dist > P.sel->threshold) valid = false;
+    }
+    if (valid && do_refine) pa = refine_dispatch(P, pa, n, L);
+    pa_out = pa;
+    q_out = (float)sqrt((double)P.qa[pa] * (double)P.qb[n]);
+    valid_out = valid ? 1 : 0;
+  }
+  P.out_pa[n] = pa_out;
+  P.out_q[n] = q_out;
+  P.out_valid[n] = valid_out;
+}
+
+// Standalone feature_refine over an arbitrary MatchSet (camera.cpp:239-271).
+__global__ void __launch_bounds__(256) k_refine(PairDev P, int64_t count, const int32_t* __restrict__ in_pa,
+                                                const int32_t* __restrict__ in_pb,
+                                                const float* __restrict__ in_q,
+                                                const uint8_t* __restrict__ in_valid, RefineLevels L,
+                                                int32_t* out_pa, int32_t* out_pb, float* out_q,
+                                                uint8_t* out_valid) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  int pa = in_pa[k];
+  const int pb = in_pb ? in_pb[k] : (int)k;
+  float q = in_q ? in_q[k] : 0.0f;
+  const uint8_t valid = in_valid ? in_valid[k] : 1;
+  if (valid && pa >= 0 && pb >= 0 && pa < P.Ha * P.Wa && pb < P.Hb * P.Wb) {
+    pa = refine_dispatch(P, pa, pb, L);
+    q = (float)sqrt((double)P.qa[pa] * (double)P.qb[pb]);
+  }
+  out_pa[k] = pa;
+  if (out_pb) out_pb[k] = pb;
+  out_q[k] = q;
+  out_valid[k] = valid;
+}
+
+// Seed map: last valid init match per pixel_b (camera.cpp:202-210, last write wins).
+__global__ void k_seed_scatter(int64_t m, const int32_t* __restrict__ pb, const uint8_t* __restrict__ valid,
+                               int HWb, int32_t* __restrict__ last) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  const int b = pb ? pb[k] : (int)k;
+  if ((valid ? valid[k] : 1) && b >= 0 && b < HWb) atomicMax(&last[b], (int32_t)k);
+}
+
+__global__ void k_project_points(const double4* __restrict__ rays, int W, int H, int64_t n,
+                                 const float* __restrict__ x, const double* __restrict__ p0, LMParams lp,
+                                 double* pix, uint8_t* conv, int32_t* iters) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const ProjOut r = iterative_project_dev(rays, W, H, x[3 * k], x[3 * k + 1], x[3 * k + 2], p0[2 * k],
+                                          p0[2 * k + 1], lp);
+  pix[2 * k] = r.pu;
+  pix[2 * k + 1] = r.pv;
+  conv[k] = r.converged ? 1 : 0;
+  iters[k] = r.iterations;
+}
+
+__global__ void k_rays_out(const double4* __restrict__ rays, int HW, double* out_rays, double* out_dist,
+                           uint8_t* out_valid, const float* __restrict__ xyz) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= HW) return;
+  const double4 r = rays[i];
+  out_rays[3 * i] = r.x;
+  out_rays[3 * i + 1] = r.y;
+  out_rays[3 * i + 2] = r.z;
+  out_valid[i] = r.w != 0.0 ? 1 : 0;
+  if (r.w != 0.0) {
+    const double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    out_dist[i] = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+  } else {
+    out_dist[i] = 1.0;
+  }
+}
+
+// ------------------------------------------------------------------ host
+// Largest double d with acos(clamp(d, -1, 1)) >= tol, found on the host with
+// the same libm acos the reference uses; the device tests d >= cos_tol.
+static double exact_cos_threshold(double tol) {
+  auto pass = [&](double d) { return std::acos(std::min(1.0, std::max(-1.0, d))) < tol; };
+  if (pass(-1.0)) return -INFINITY;
+  if (!pass(1.0)) return INFINITY;
+  // bisection over the ordered bit patterns of [-1, 1]
+  auto ord = [](double d) {
+    int64_t i;
+    std::memcpy(&i, &d, 8);
+    return i >= 0 ? i : -(i & 0x7fffffffffffffffLL);
+  };
+  auto unord = [](int64_t k) {
+    const uint64_t u = k >= 0 ? (uint64_t)k : ((uint64_t)(-k) | 0x8000000000000000ull);
+    double d;
+    std::memcpy(&d, &u, 8);
+    return d;
+  };
+  int64_t lo = ord(-1.0), hi = ord(1.0);  // pass(lo) false, pass(hi) true
+  while (hi - lo > 1) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (pass(unord(mid)))
+      hi = mid;
+    else
+      lo = mid;
+  }
+  return unord(hi);
+}
+
+static LMParams make_lm(const pmx_match_params& p) {
+  LMParams lp;
+  lp.lambda_init = p.projection.lambda_init;
+  lp.lambda_up = p.projection.lambda_up;
+  lp.lambda_down = p.projection.lambda_down;
+  lp.cos_tol = exact_cos_threshold(p.projection.angle_tol);
+  lp.max_iterations = p.projection.max_iterations;
+  lp.median_fraction = p.invalidation_median_fraction;
+  return lp;
+}
+
+static RefineLevels make_levels(const pmx_refine_params* r) {
+  RefineLevels L;
+  std::memset(&L, 0, sizeof(L));
+  if (!r) return L;
+  require(r->num_levels >= 0 && r->num_levels <= PMX_MAX_REFINE_LEVELS, "refine: bad level count");
+  L.n = r->num_levels;
+  for (int i = 0; i < L.n; ++i) {
+    require(r->stride[i] >= 1 && r->radius[i] >= 0, "refine: stride >= 1 and radius >= 0 required");
+    L.stride[i] = r->stride[i];
+    L.radius[i] = r->radius[i];
+  }
+  return L;
+}
+
+static void check_pointmap(const pmx_pointmap& p) {
+  require(p.height > 0 && p.width > 0 && p.xyz, "pointmap: empty or null");
+}
+
+// Builds ray maps + median threshold for every pair of `dev_pairs[0..n)`
+// (the scratch pointers must be set), enqueued on ctx.stream.
+static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
+  const int ppb = 4096;
+  dim3 g1((max_hwa + ppb - 1) / ppb, n);
+  k_prep<<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_prep");
+  k_sel_scan<1><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
+  launch_check(ctx, "k_sel_scan1");
+  k_sel_hist<2><<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_sel_hist2");
+  k_sel_scan<2><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
+  launch_check(ctx, "k_sel_scan2");
+  k_sel_hist<3><<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_sel_hist3");
+  k_sel_scan<3><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
+  launch_check(ctx, "k_sel_scan3");
+}
+
+struct PairScratch {
+  DevBuf rays, keys, hist, sel, pairs;
+};
+
+// Batched match(+refine).  All pointers in `pairs` are device pointers.
+void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, const pmx_match_params& mp,
+                        const pmx_refine_params* refine) {
+  const LMParams lp = make_lm(mp);
+  const RefineLevels L = make_levels(refine);
+  const int npairs = (int)host_pairs.size();
+  if (npairs == 0) return;
+  int max_hwa = 0, max_hwb = 0;
+  for (const auto& p : host_pairs) {
+    max_hwa = std::max(max_hwa, p.Ha * p.Wa);
+    max_hwb = std::max(max_hwb, p.Hb * p.Wb);
+  }
+  // chunk so that the FP64 ray maps of a chunk stay L2-resident (~56 MB)
+  const size_t ray_bytes = sizeof(double4) * (size_t)max_hwa;
+  const int chunk = std::max(1, std::min(npairs, (int)((56u << 20) / std::max<size_t>(ray_bytes, 1))));
+  DevBuf rays(ray_bytes * chunk, ctx.stream);
+  DevBuf keys(sizeof(uint32_t) * (size_t)max_hwa * chunk, ctx.stream);
+  DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
+  DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
+  DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
+  std::vector<PairDev> hp = host_pairs;
+  for (int i = 0; i < npairs; ++i) {
+    const int slot = i % chunk;
+    hp[i].rays = rays.as<double4>() + (size_t)slot * max_hwa;
+    hp[i].keys = keys.as<uint32_t>() + (size_t)slot * max_hwa;
+    hp[i].hist = hist.as<uint32_t>() + (size_t)kHistTotal * i;
+    hp[i].sel = sel.as<SelState>() + i;
+  }
+  PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
+  PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
+  for (int c0 = 0; c0 < npairs; c0 += chunk) {
+    const int cn = std::min(chunk, npairs - c0);
+    PairDev* dp = dpairs.as<PairDev>() + c0;
+    prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
+    int max_tiles = 0;
+    for (int i = c0; i < c0 + cn; ++i)
+      max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
+    dim3 g(max_tiles, cn);
+    {
+      ProfScope ps(ctx, "k_match");
+      k_match<<<g, 256, 0, ctx.stream>>>(dp, lp, L, refine ? 1 : 0);
+    }
+    launch_check(ctx, "k_match");
+  }
+}
+
+// ------------------------------------------------------------ C-ABI glue
+static PairDev stage_pair(Stager& st, const pmx_pair& p, DevBuf* seed_buf, Context& ctx) {
+  check_pointmap(p.X_a);
+  check_pointmap(p.X_b_in_a);
+  require(p.F_a.descriptors && p.F_b.descriptors && p.F_a.match_confidence && p.F_b.match_confidence,
+          "featuremap: null arrays");
+  require(p.F_a.height == p.X_a.height && p.F_a.width == p.X_a.width, "F_a / X_a size mismatch");
+  require(p.F_b.height == p.X_b_in_a.height && p.F_b.width == p.X_b_in_a.width, "F_b / X_b size mismatch");
+  require(p.F_a.dim == p.F_b.dim && p.F_a.dim > 0, "descriptor dim mismatch");
+  const size_t hwa = (size_t)p.X_a.height * p.X_a.width, hwb = (size_t)p.X_b_in_a.height * p.X_b_in_a.width;
+  PairDev d;
+  std::memset(&d, 0, sizeof(d));
+  d.Ha = p.X_a.height;
+  d.Wa = p.X_a.width;
+  d.Hb = p.X_b_in_a.height;
+  d.Wb = p.X_b_in_a.width;
+  d.dim = p.F_a.dim;
+  d.xa = st.in(p.X_a.xyz, 3 * hwa);
+  d.va = st.in(p.X_a.valid, hwa);
+  d.xb = st.in(p.X_b_in_a.xyz, 3 * hwb);
+  d.vb = st.in(p.X_b_in_a.valid, hwb);
+  d.da = reinterpret_cast<const __half*>(st.in(p.F_a.descriptors, hwa * d.dim));
+  d.db = reinterpret_cast<const __half*>(st.in(p.F_b.descriptors, hwb * d.dim));
+  d.qa = st.in(p.F_a.match_confidence, hwa);
+  d.qb = st.in(p.F_b.match_confidence, hwb);
+  if (p.init && p.init->count > 0) {
+    const int64_t m = p.init->count;
+    const int32_t* ipa = st.in(p.init->pixel_a, (size_t)m);
+    const int32_t* ipb = st.in(p.init->pixel_b, (size_t)m);
+    const uint8_t* iv = st.in(p.init->valid, (size_t)m);
+    *seed_buf = DevBuf(sizeof(int32_t) * hwb, ctx.stream);
+    PMX_CUDA(cudaMemsetAsync(seed_buf->p, 0xff, seed_buf->bytes, ctx.stream));
+    k_seed_scatter<<<(unsigned)((m + 255) / 256), 256, 0, ctx.stream>>>(m, ipb, iv, (int)hwb,
+                                                                        seed_buf->as<int32_t>());
+    launch_check(ctx, "k_seed_scatter");
+    d.seed_last = seed_buf->as<int32_t>();
+    d.init_pa = ipa;
+  }
+  return d;
+}
+
+}  // namespace pmx
+
+using namespace pmx;
+
+extern "C" int pmx_impl_match_batch(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
+                                    const pmx_match_params* params, const pmx_refine_params* refine,
+                                    pmx_matchset* outs) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(num_pairs >= 0 && (num_pairs == 0 || (pairs && outs)), "match_batch: null arguments");
+  pmx_match_params mp;
+  pmx_default_match_params(&mp);
+  if (params) mp = *params;
+  Stager st(ctx, mem);
+  std::vector<PairDev> hp(num_pairs);
+  std::vector<DevBuf> seeds(num_pairs);
+  for (int i = 0; i < num_pairs; ++i) {
+    hp[i] = stage_pair(st, pairs[i], &seeds[i], ctx);
+    const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
+    require(outs[i].count >= (int64_t)hwb && outs[i].pixel_a && outs[i].confidence && outs[i].valid,
+            "match_batch: output matchset too small or null");
+    hp[i].out_pa = st.out(outs[i].pixel_a, hwb);
+    hp[i].out_pb = st.out(outs[i].pixel_b, hwb);
+    hp[i].out_q = st.out(outs[i].confidence, hwb);
+    hp[i].out_valid = st.out(outs[i].valid, hwb);
+  }
+  match_batch_device(ctx, hp, mp, refine);
+  for (int i = 0; i < num_pairs; ++i) {
+    const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
+    st.back(outs[i].pixel_a, hp[i].out_pa, hwb);
+    st.back(outs[i].pixel_b, hp[i].out_pb, hwb);
+    st.back(outs[i].confidence, hp[i].out_q, hwb);
+    st.back(outs[i].valid, hp[i].out_valid, hwb);
+    outs[i].count = (int64_t)hwb;
+  }
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_feature_refine(pmx_context* c, pmx_memory mem, const pmx_matchset* in,
+                                       const pmx_featuremap* F_a, const pmx_featuremap* F_b,
+                                       const pmx_refine_params* params, pmx_matchset* out) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(in && F_a && F_b && out, "feature_refine: null arguments");
+  require(F_a->dim == F_b->dim && F_a->dim > 0, "descriptor dim mismatch");
+  require(out->count >= in->count && out->pixel_a && out->confidence && out->valid,
+          "feature_refine: output too small");
+  pmx_refine_params rp;
+  pmx_default_refine_params(&rp);
+  if (params) rp = *params;
+  const RefineLevels L = make_levels(&rp);
+  Stager st(ctx, mem);
+  PairDev P;
+  std::memset(&P, 0, sizeof(P));
+  P.Ha = F_a->height;
+  P.Wa = F_a->width;
+  P.Hb = F_b->height;
+  P.Wb = F_b->width;
+  P.dim = F_a->dim;
+  const size_t hwa = (size_t)P.Ha * P.Wa, hwb = (size_t)P.Hb * P.Wb;
+  P.da = reinterpret_cast<const __half*>(st.in(F_a->descriptors, hwa * P.dim));
+  P.db = reinterpret_cast<const __half*>(st.in(F_b->descriptors, hwb * P.dim));
+  P.qa = st.in(F_a->match_confidence, hwa);
+  P.qb = st.in(F_b->match_confidence, hwb);
+  const int64_t n = in->count;
+  const int32_t* ipa = st.in(in->pixel_a, n);
+  const int32_t* ipb = st.in(in->pixel_b, n);
+  const float* iq = st.in(in->confidence, n);
+  const uint8_t* iv = st.in(in->valid, n);
+  int32_t* opa = st.out(out->pixel_a, n);
+  int32_t* opb = st.out(out->pixel_b, n);
+  float* oq = st.out(out->confidence, n);
+  uint8_t* ov = st.out(out->valid, n);
+  if (n > 0) {
+    k_refine<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(P, n, ipa, ipb, iq, iv, L, opa, opb, oq, ov);
+    launch_check(ctx, "k_refine");
+  }
+  st.back(out->pixel_a, opa, n);
+  st.back(out->pixel_b, opb, n);
+  st.back(out->confidence, oq, n);
+  st.back(out->valid, ov, n);
+  out->count = n;
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+// Ray map of one pointmap (+ optional median threshold) in a scratch buffer.
+static void build_raymap(Context& ctx, Stager& st, const pmx_pointmap* pm, DevBuf& rays, DevBuf& keys,
+                         DevBuf& hist, DevBuf& sel, DevBuf& dpair, const float** xyz_dev) {
+  check_pointmap(*pm);
+  const size_t hw = (size_t)pm->height * pm->width;
+  PairDev P;
+  std::memset(&P, 0, sizeof(P));
+  P.Ha = pm->height;
+  P.Wa = pm->width;
+  P.xa = st.in(pm->xyz, 3 * hw);
+  P.va = st.in(pm->valid, hw);
+  *xyz_dev = P.xa;
+  rays = DevBuf(sizeof(double4) * hw, ctx.stream);
+  keys = DevBuf(sizeof(uint32_t) * hw, ctx.stream);
+  hist = DevBuf(sizeof(uint32_t) * kHistTotal, ctx.stream);
+  sel = DevBuf(sizeof(SelState), ctx.stream);
+  dpair = DevBuf(sizeof(PairDev), ctx.stream);
+  P.rays = rays.as<double4>();
+  P.keys = keys.as<uint32_t>();
+  P.hist = hist.as<uint32_t>();
+  P.sel = sel.as<SelState>();
+  PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
+  PMX_CUDA(cudaMemcpyAsync(dpair.p, &P, sizeof(P), cudaMemcpyHostToDevice, ctx.stream));
+  prep_and_select(ctx, dpair.as<PairDev>(), 1, (int)hw, 1.0);
+}
+
+extern "C" int pmx_impl_normalize_rays(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, double* rays,
+                                       double* distances, uint8_t* valid) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(pm && rays && distances && valid, "normalize_rays: null arguments");
+  Stager st(ctx, mem);
+  DevBuf r, k, h, s, d;
+  const float* xyz = nullptr;
+  build_raymap(ctx, st, pm, r, k, h, s, d, &xyz);
+  const size_t hw = (size_t)pm->height * pm->width;
+  double* orays = st.out(rays, 3 * hw);
+  double* odist = st.out(distances, hw);
+  uint8_t* ov = st.out(valid, hw);
+  k_rays_out<<<(unsigned)((hw + 255) / 256), 256, 0, ctx.stream>>>(r.as<double4>(), (int)hw, orays, odist, ov,
+                                                                   xyz);
+  launch_check(ctx, "k_rays_out");
+  st.back(rays, orays, 3 * hw);
+  st.back(distances, odist, hw);
+  st.back(valid, ov, hw);
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_iterative_project(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, int64_t n,
+                                          const float* x, const double* p0, const pmx_iter_proj_params* params,
+                                          double* pixel, uint8_t* converged, int32_t* iterations) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(pm && x && p0 && pixel && converged && iterations && n >= 0, "iterative_project: null arguments");
+  pmx_match_params mp;
+  pmx_default_match_params(&mp);
+  if (params) mp.projection = *params;
+  const LMParams lp = make_lm(mp);
+  Stager st(ctx, mem);
+  DevBuf r, k, h, s, d;
+  const float* xyz = nullptr;
+  build_raymap(ctx, st, pm, r, k, h, s, d, &xyz);
+  const float* dx = st.in(x, 3 * (size_t)n);
+  const double* dp0 = st.in(p0, 2 * (size_t)n);
+  double* dpix = st.out(pixel, 2 * (size_t)n);
+  uint8_t* dconv = st.out(converged, (size_t)n);
+  int32_t* dit = st.out(iterations, (size_t)n);
+  if (n > 0) {
+    k_project_points<<<(unsigned)((n + 127) / 128), 128, 0, ctx.stream>>>(r.as<double4>(), pm->width, pm->height,
+                                                                          n, dx, dp0, lp, dpix, dconv, dit);
+    launch_check(ctx, "k_project_points");
+  }
+  st.back(pixel, dpix, 2 * (size_t)n);
+  st.back(converged, dconv, (size_t)n);
+  st.back(iterations, dit, (size_t)n);
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}

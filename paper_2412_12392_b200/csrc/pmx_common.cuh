@@ -1,0 +1,349 @@
+// Shared device/host infrastructure of libpmx_cuda.so (sm_100a only).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pmx.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libpmx_cuda is written for sm_100a (B200) only"
+#endif
+
+namespace pmx {
+
+// ----------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define PMX_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::pmx::Error(e_ == cudaErrorMemoryAllocation ? PMX_ERR_OUT_OF_MEMORY         \
+                                                         : PMX_ERR_CUDA,                 \
+                         std::string(#call) + ": " + cudaGetErrorString(e_));            \
+  } while (0)
+
+inline void require(bool ok, const char* msg) {
+  if (!ok) throw Error(PMX_ERR_INVALID_ARGUMENT, msg);
+}
+
+// --------------------------------------------------------------- context
+struct ProfEvent {
+  const char* name;
+  cudaEvent_t start, stop;
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  int num_sms = 148;
+  bool profiling = false;
+  std::vector<ProfEvent> prof;  // unresolved event pairs (pmx_profile_*)
+};
+
+// CUDA-event bracket around one kernel launch on ctx.stream (when profiling).
+struct ProfScope {
+  Context& c;
+  ProfEvent ev{nullptr, nullptr, nullptr};
+  ProfScope(Context& ctx, const char* name) : c(ctx) {
+    if (!c.profiling) return;
+    ev.name = name;
+    cudaEventCreate(&ev.start);
+    cudaEventCreate(&ev.stop);
+    cudaEventRecord(ev.start, c.stream);
+  }
+  ~ProfScope() {
+    if (!c.profiling) return;
+    cudaEventRecord(ev.stop, c.stream);
+    c.prof.push_back(ev);
+  }
+};
+
+// Device scratch owned for the duration of one API call (stream-ordered).
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t n, cudaStream_t st) : bytes(n), s(st) {
+    if (n) PMX_CUDA(cudaMallocAsync(&p, n, st));
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    release();
+    p = o.p;
+    bytes = o.bytes;
+    s = o.s;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+inline void launch_check(Context& c, const char* what) {
+  c.launches++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw Error(PMX_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Copies host arrays to scratch device memory when mem == HOST; passes
+// device pointers through when mem == DEVICE.
+struct Stager {
+  Context& ctx;
+  pmx_memory mem;
+  std::vector<DevBuf> bufs;
+  Stager(Context& c, pmx_memory m) : ctx(c), mem(m) {}
+  template <class T>
+  const T* in(const T* host_or_dev, size_t count) {
+    if (host_or_dev == nullptr || mem == PMX_MEM_DEVICE || count == 0) return host_or_dev;
+    bufs.emplace_back(sizeof(T) * count, ctx.stream);
+    PMX_CUDA(cudaMemcpyAsync(bufs.back().p, host_or_dev, sizeof(T) * count, cudaMemcpyHostToDevice,
+                             ctx.stream));
+    return bufs.back().as<T>();
+  }
+  template <class T>
+  T* inout(T* host_or_dev, size_t count) {
+    return const_cast<T*>(in<T>(host_or_dev, count));
+  }
+  template <class T>
+  T* out(T* host_or_dev, size_t count) {
+    if (host_or_dev == nullptr || mem == PMX_MEM_DEVICE || count == 0) return host_or_dev;
+    bufs.emplace_back(sizeof(T) * count, ctx.stream);
+    return bufs.back().as<T>();
+  }
+  template <class T>
+  void back(T* host, const T* dev, size_t count) {
+    if (host == nullptr || mem == PMX_MEM_DEVICE || count == 0) return;
+    PMX_CUDA(cudaMemcpyAsync(host, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, ctx.stream));
+  }
+};
+
+// ----------------------------------------------------------- device math
+struct DSim3 {  // Sim(3) in FP64: x -> s R x + t (lie.hpp:36-70)
+  double R[9];
+  double t[3];
+  double s;
+};
+
+inline DSim3 to_dsim3(const pmx_sim3& T) {
+  DSim3 d;
+  for (int i = 0; i < 9; ++i) d.R[i] = T.R[i];
+  for (int i = 0; i < 3; ++i) d.t[i] = T.t[i];
+  d.s = T.s;
+  return d;
+}
+
+__host__ __device__ inline DSim3 sim3_mul(const DSim3& a, const DSim3& b) {  // lie.cpp:131-140
+  DSim3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      r.R[3 * i + j] = a.R[3 * i] * b.R[j] + a.R[3 * i + 1] * b.R[3 + j] + a.R[3 * i + 2] * b.R[6 + j];
+  r.s = a.s * b.s;
+  for (int i = 0; i < 3; ++i)
+    r.t[i] = a.s * (a.R[3 * i] * b.t[0] + a.R[3 * i + 1] * b.t[1] + a.R[3 * i + 2] * b.t[2]) + a.t[i];
+  return r;
+}
+
+__host__ __device__ inline DSim3 sim3_inv(const DSim3& a) {  // lie.cpp:121-129
+  DSim3 r;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) r.R[3 * i + j] = a.R[3 * j + i];
+  r.s = 1.0 / a.s;
+  for (int i = 0; i < 3; ++i)
+    r.t[i] = -r.s * (r.R[3 * i] * a.t[0] + r.R[3 * i + 1] * a.t[1] + r.R[3 * i + 2] * a.t[2]);
+  return r;
+}
+
+// Sim(3) exponential, lie.cpp:23-32, 51-90, 99-108 (tangent order rho, omega, sigma).
+__host__ __device__ inline DSim3 sim3_exp(const double* tau) {
+  const double rho[3] = {tau[0], tau[1], tau[2]};
+  const double w[3] = {tau[3], tau[4], tau[5]};
+  const double sigma = tau[6];
+  const double theta = sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]);
+  double O[9] = {0, -w[2], w[1], w[2], 0, -w[0], -w[1], w[0], 0};
+  double O2[9];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) O2[3 * i + j] = O[3 * i] * O[j] + O[3 * i + 1] * O[3 + j] + O[3 * i + 2] * O[6 + j];
+  const double kSmall = 1e-8;
+  DSim3 r;
+  double a1, a2;
+  if (theta < kSmall) {
+    a1 = 1.0;
+    a2 = 0.5;
+  } else {
+    a1 = sin(theta) / theta;
+    a2 = (1.0 - cos(theta)) / (theta * theta);
+  }
+  for (int i = 0; i < 9; ++i) r.R[i] = ((i % 4 == 0) ? 1.0 : 0.0) + a1 * O[i] + a2 * O2[i];
+  const double scale = exp(sigma);
+  r.s = scale;
+  double A, B, Cc;
+  if (fabs(sigma) < kSmall) {
+    Cc = 1.0 + 0.5 * sigma + sigma * sigma / 6.0;
+    if (theta < kSmall) {
+      A = 0.5 + sigma / 3.0;
+      B = 1.0 / 6.0 + sigma / 8.0;
+    } else {
+      const double th2 = theta * theta, den = sigma * sigma + th2;
+      A = (scale * (sigma * sin(theta) - theta * cos(theta)) + theta) / (theta * den);
+      B = (Cc - (scale * (sigma * cos(theta) + theta * sin(theta)) - sigma) / den) / th2;
+    }
+  } else {
+    Cc = (scale - 1.0) / sigma;
+    if (theta < kSmall) {
+      const double s2 = sigma * sigma;
+      A = (scale * (sigma - 1.0) + 1.0) / s2;
+      B = (scale * (s2 - 2.0 * sigma + 2.0) - 2.0) / (2.0 * s2 * sigma);
+    } else {
+      const double th2 = theta * theta, den = sigma * sigma + th2;
+      A = (scale * (sigma * sin(theta) - theta * cos(theta)) + theta) / (theta * den);
+      B = (Cc - (scale * (sigma * cos(theta) + theta * sin(theta)) - sigma) / den) / th2;
+    }
+  }
+  double Wm[9];
+  for (int i = 0; i < 9; ++i) Wm[i] = ((i % 4 == 0) ? Cc : 0.0) + A * O[i] + B * O2[i];
+  for (int i = 0; i < 3; ++i) r.t[i] = Wm[3 * i] * rho[0] + Wm[3 * i + 1] * rho[1] + Wm[3 * i + 2] * rho[2];
+  return r;
+}
+
+// 7x7 adjoint, lie.cpp:155-163 (row-major)
+__host__ __device__ inline void sim3_adjoint(const DSim3& T, double* ad) {
+  for (int i = 0; i < 49; ++i) ad[i] = 0.0;
+  const double* R = T.R;
+  const double* t = T.t;
+  const double S[9] = {0, -t[2], t[1], t[2], 0, -t[0], -t[1], t[0], 0};
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) {
+      ad[r * 7 + c] = T.s * R[3 * r + c];
+      ad[r * 7 + 3 + c] = S[3 * r] * R[c] + S[3 * r + 1] * R[3 + c] + S[3 * r + 2] * R[6 + c];
+      ad[(3 + r) * 7 + 3 + c] = R[3 * r + c];
+    }
+  for (int r = 0; r < 3; ++r) ad[r * 7 + 6] = -t[r];
+  ad[48] = 1.0;
+}
+
+inline pmx_sim3 to_pmx(const DSim3& d) {
+  pmx_sim3 T;
+  for (int i = 0; i < 9; ++i) T.R[i] = d.R[i];
+  for (int i = 0; i < 3; ++i) T.t[i] = d.t[i];
+  T.s = d.s;
+  return T;
+}
+
+// Eigen-style pivoted LDL^T solve (LDLT.h restated; see oracle.cpp) for n<=7,
+// used for the tracking 7x7 step (tracking.cpp:203) on host and device.
+__host__ __device__ inline void ldlt_pivoted_solve(int n, const double* A_in, const double* b, double* x) {
+  double M[49];
+  for (int i = 0; i < n * n; ++i) M[i] = A_in[i];
+  int tr[7];
+  double temp[7];
+  for (int k = 0; k < n; ++k) {
+    int big = k;
+    double bigv = fabs(M[k * n + k]);
+    for (int i = k + 1; i < n; ++i)
+      if (fabs(M[i * n + i]) > bigv) {
+        bigv = fabs(M[i * n + i]);
+        big = i;
+      }
+    tr[k] = big;
+    if (k != big) {
+      for (int c = 0; c < k; ++c) {
+        double t = M[k * n + c];
+        M[k * n + c] = M[big * n + c];
+        M[big * n + c] = t;
+      }
+      for (int r = big + 1; r < n; ++r) {
+        double t = M[r * n + k];
+        M[r * n + k] = M[r * n + big];
+        M[r * n + big] = t;
+      }
+      double t = M[k * n + k];
+      M[k * n + k] = M[big * n + big];
+      M[big * n + big] = t;
+      for (int i = k + 1; i < big; ++i) {
+        double tmp = M[i * n + k];
+        M[i * n + k] = M[big * n + i];
+        M[big * n + i] = tmp;
+      }
+    }
+    if (k > 0) {
+      for (int c = 0; c < k; ++c) temp[c] = M[c * n + c] * M[k * n + c];
+      double acc = 0.0;
+      for (int c = 0; c < k; ++c) acc += M[k * n + c] * temp[c];
+      M[k * n + k] -= acc;
+      for (int r = k + 1; r < n; ++r) {
+        double a = 0.0;
+        for (int c = 0; c < k; ++c) a += M[r * n + c] * temp[c];
+        M[r * n + k] -= a;
+      }
+    }
+    const double akk = M[k * n + k];
+    const bool ok = fabs(akk) > 0.0;
+    if (k == 0 && !ok) {
+      for (int i = 0; i < n; ++i) x[i] = 0.0;
+      return;
+    }
+    if (ok)
+      for (int r = k + 1; r < n; ++r) M[r * n + k] /= akk;
+  }
+  double d[7];
+  for (int i = 0; i < n; ++i) d[i] = b[i];
+  for (int k = 0; k < n; ++k) {
+    double t = d[k];
+    d[k] = d[tr[k]];
+    d[tr[k]] = t;
+  }
+  for (int i = 0; i < n; ++i)
+    for (int c = 0; c < i; ++c) d[i] -= M[i * n + c] * d[c];
+  for (int i = 0; i < n; ++i) {
+    if (fabs(M[i * n + i]) > 2.2250738585072014e-308)
+      d[i] /= M[i * n + i];
+    else
+      d[i] = 0.0;
+  }
+  for (int i = n - 1; i >= 0; --i)
+    for (int r = i + 1; r < n; ++r) d[i] -= M[r * n + i] * d[r];
+  for (int k = n - 1; k >= 0; --k) {
+    double t = d[k];
+    d[k] = d[tr[k]];
+    d[tr[k]] = t;
+  }
+  for (int i = 0; i < n; ++i) x[i] = d[i];
+}
+
+// --------------------------------------------------------- reductions
+__device__ inline double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ inline float warp_sumf(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace pmx

@@ -1,0 +1,226 @@
+"""GPU parity of iterative projective matching + refinement (reference
+src/camera.cpp:39-271) against the FP64 oracle, through the C ABI.
+
+Bar (BASELINE north_star): match indices bit-exact on >= 99.9% of valid
+pixels, every mismatch within 1 px; confidences q = sqrt(Q_a Q_b) exact to
+fp32 rounding.
+"""
+import numpy as np
+import pytest
+
+import pmxgen
+import pyoracle
+from helpers import (BASELINE_REFINE, baseline_match_params, compare_matches, pmx_pair, to_torch_pair)
+from paper_2412_12392_b200 import FeatureMap, MatchSet, Pointmap, abi
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(stats, min_equal=0.999, max_valid_mismatch_frac=1e-3):
+    assert stats["worst_px"] <= 1, stats
+    assert stats["index_equal_frac"] >= min_equal, stats
+    assert stats["valid_mismatch"] <= max_valid_mismatch_frac * stats["n"], stats
+
+
+@pytest.mark.parametrize("shape,noise", [((96, 128), "radial"), ((384, 512), "radial"), ((96, 128), "isotropic")])
+def test_match_pointmaps_parity(ctx, shape, noise):
+    pair = pmxgen.config0(seed=3, height=shape[0], width=shape[1], noise=noise)
+    params = baseline_match_params()
+    orc = pyoracle.match_pointmaps(pair, params)
+    Xa, Xb, Fa, Fb = pmx_pair(pair)
+    gpu = ctx.match_pointmaps(Xa, Xb, Fa, Fb, params=params)
+    st = compare_matches(gpu, orc, shape[1])
+    _check(st)
+    # q is written even for invalid matches (camera.cpp:229-230)
+    both = np.asarray(gpu.pixel_a) == orc.pixel_a
+    np.testing.assert_allclose(np.asarray(gpu.confidence)[both], orc.confidence[both], rtol=1e-7)
+
+
+@pytest.mark.parametrize("levels", [BASELINE_REFINE, [(2, 2), (1, 2)]])
+def test_match_and_refine_parity(ctx, levels):
+    pair = pmxgen.config0(seed=5)
+    params = baseline_match_params()
+    rp = abi.refine_params(levels)
+    orc = pyoracle.feature_refine(pyoracle.match_pointmaps(pair, params), pair, rp)
+    Xa, Xb, Fa, Fb = pmx_pair(pair)
+    gpu = ctx.match_batch([(Xa, Xb, Fa, Fb)], params=params, refine=rp)[0]
+    _check(compare_matches(gpu, orc, pair["width"]))
+
+
+def test_device_memory_path_matches_host_path(ctx):
+    import torch
+    pair = pmxgen.config0(seed=6, height=96, width=128)
+    params = baseline_match_params()
+    rp = abi.refine_params(BASELINE_REFINE)
+    Xa, Xb, Fa, Fb = pmx_pair(pair)
+    host = ctx.match_batch([(Xa, Xb, Fa, Fb)], params=params, refine=rp)[0]
+    tp = to_torch_pair(pair)
+    dXa, dXb, dFa, dFb = pmx_pair(tp)
+    dev = ctx.match_batch([(dXa, dXb, dFa, dFb)], params=params, refine=rp)[0]
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.pixel_a.cpu().numpy(), host.pixel_a)
+    assert np.array_equal(dev.valid.cpu().numpy(), host.valid)
+    assert np.array_equal(dev.confidence.cpu().numpy(), host.confidence)
+
+
+def test_batched_pairs_equal_single_calls(ctx):
+    params = baseline_match_params()
+    rp = abi.refine_params(BASELINE_REFINE)
+    pairs = [pmxgen.config0(seed=s, height=96, width=128) for s in (10, 11, 12)]
+    batch = ctx.match_batch([pmx_pair(p) for p in pairs], params=params, refine=rp)
+    for p, b in zip(pairs, batch):
+        single = ctx.match_batch([pmx_pair(p)], params=params, refine=rp)[0]
+        assert np.array_equal(single.pixel_a, b.pixel_a)
+        assert np.array_equal(single.valid, b.valid)
+
+
+def test_seeded_matching_parity(ctx):
+    # camera.cpp:202-210: seed map keyed by pixel_b, last valid write wins
+    pair = pmxgen.config0(seed=7, height=96, width=128)
+    n = 96 * 128
+    params = baseline_match_params()
+    rng = np.random.default_rng(0)
+    pa = rng.integers(-5, n + 5, size=n + 300).astype(np.int32)
+    pb = np.concatenate([np.arange(n), rng.integers(-3, n + 3, size=300)]).astype(np.int32)
+    valid = (rng.random(n + 300) < 0.8).astype(np.uint8)
+    conf = np.ones(n + 300)
+    orc_init = pyoracle.MatchSet(pa, pb, conf, valid)
+    orc = pyoracle.match_pointmaps(pair, params, init=orc_init)
+    Xa, Xb, Fa, Fb = pmx_pair(pair)
+    init = MatchSet(pa, conf.astype(np.float32), valid, pb)
+    gpu = ctx.match_pointmaps(Xa, Xb, Fa, Fb, init=init, params=params)
+    st = compare_matches(gpu, orc, 128)
+    _check(st)
+
+
+def test_invalid_and_degenerate_pixels(ctx):
+    # invalid b pixels -> pixel_a = -1, q = 0, invalid; zero points; NaN points
+    pair = pmxgen.config0(seed=8, height=48, width=64)
+    n = 48 * 64
+    rng = np.random.default_rng(1)
+    vb = (rng.random(n) > 0.1).astype(np.uint8)
+    va = (rng.random(n) > 0.05).astype(np.uint8)
+    Xb = pair["X_b"].copy()
+    Xb[::97] = 0.0
+    Xb[5::101] = np.nan
+    pair = dict(pair, valid_a=va, valid_b=vb, X_b=Xb)
+    params = baseline_match_params()
+    orc = pyoracle.match_pointmaps(pair, params)
+    Xa, Xb_, Fa, Fb = pmx_pair(pair)
+    gpu = ctx.match_pointmaps(Xa, Xb_, Fa, Fb, params=params)
+    assert np.array_equal(np.asarray(gpu.pixel_a)[vb == 0], np.full((vb == 0).sum(), -1))
+    _check(compare_matches(gpu, orc, 64))
+    assert np.array_equal(np.asarray(gpu.pixel_a), orc.pixel_a)
+
+
+def test_gross_outliers_invalidated(ctx):
+    # test_camera.cpp:177-196 on the CUDA path: 20% x3 depth outliers -> <= 2% valid
+    pair = pmxgen.config0(seed=9, height=96, width=128)
+    rng = np.random.default_rng(2)
+    sel = rng.random(96 * 128) < 0.2
+    Xb = pair["X_b"].copy()
+    Xb[sel] *= 3.0
+    pair = dict(pair, X_b=Xb)
+    Xa, Xb_, Fa, Fb = pmx_pair(pair)
+    gpu = ctx.match_pointmaps(Xa, Xb_, Fa, Fb)
+    assert np.asarray(gpu.valid)[sel].mean() <= 0.02
+
+
+def test_feature_refine_planted_peak_and_ties(ctx):
+    # test_camera.cpp:219-247
+    h, w, d = 16, 16, 8
+    Fa = np.zeros((h * w, d), np.float32)
+    Fb = np.zeros((h * w, d), np.float32)
+    Fa[:, 1] = 1.0
+    Fb[:, 0] = 1.0
+    gu, gv = 8, 8
+    peak = gv * w + gu + 2
+    Fa[peak] = 0.0
+    Fa[peak, 0] = 1.0
+    q = np.ones(h * w, np.float32)
+    m = MatchSet(np.array([gv * w + gu], np.int32), np.ones(1, np.float32), np.ones(1, np.uint8),
+                 np.array([5 * w + 5], np.int32))
+    FA = FeatureMap(Fa.astype(np.float16).view(np.uint16), q, h, w)
+    FB = FeatureMap(Fb.astype(np.float16).view(np.uint16), q, h, w)
+    out = ctx.feature_refine(m, FA, FB)
+    assert int(out.pixel_a[0]) == peak
+    flat = FeatureMap(np.full((h * w, d), 0.5, np.float16).view(np.uint16), q, h, w)
+    out = ctx.feature_refine(m, flat, flat)
+    assert int(out.pixel_a[0]) == gv * w + gu
+
+
+def test_feature_refine_exact_near_ties(ctx):
+    # candidates whose exact scores differ by one fp16 product ulp: the fp32
+    # filter must defer to the exact FP64 re-check (strict '>' semantics).
+    h, w, d = 12, 12, 24
+    rng = np.random.default_rng(3)
+    base = rng.standard_normal(d)
+    base /= np.linalg.norm(base)
+    Fa = np.tile(base, (h * w, 1)).astype(np.float16)
+    # perturb a few pixels by one fp16 ulp in one component
+    for idx in (30, 31, 42, 55, 66):
+        k = idx % d
+        Fa[idx, k] = np.nextafter(Fa[idx, k], np.float16(2.0))
+    Fb = np.tile(base, (h * w, 1)).astype(np.float16)
+    q = np.ones(h * w, np.float32)
+    n = h * w
+    pa = np.arange(n, dtype=np.int32)
+    m = MatchSet(pa, np.ones(n, np.float32), np.ones(n, np.uint8), pa.copy())
+    pair = {"D_a": Fa.view(np.uint16), "D_b": Fb.view(np.uint16), "Q_a": q, "Q_b": q, "height": h, "width": w}
+    for levels in ([(1, 3), (1, 3)], [(2, 2), (1, 2)]):
+        rp = abi.refine_params(levels)
+        gpu = ctx.feature_refine(m, FeatureMap(pair["D_a"], q, h, w), FeatureMap(pair["D_b"], q, h, w), rp)
+        orc = pyoracle.feature_refine(pyoracle.MatchSet(pa, pa, np.ones(n), np.ones(n, np.uint8)), pair, rp)
+        assert np.array_equal(np.asarray(gpu.pixel_a), orc.pixel_a)
+
+
+def test_iterative_project_parity(ctx):
+    pair = pmxgen.config0(seed=4, height=96, width=128)
+    h, w = 96, 128
+    rng = np.random.default_rng(4)
+    idx = rng.integers(0, h * w, 2000)
+    x = pair["X_b"][idx]
+    p0 = np.stack([idx % w + rng.uniform(-6, 6, idx.size), idx // w + rng.uniform(-6, 6, idx.size)], 1)
+    params = baseline_match_params().projection
+    pix_o, conv_o, it_o = pyoracle.iterative_project(pair["X_a"], None, h, w, x, p0, params)
+    pm = Pointmap(pair["X_a"], None, h, w)
+    pix_g, conv_g, it_g = ctx.iterative_project(pm, x, p0, params)
+    assert (conv_g == conv_o).mean() >= 0.999
+    assert (it_g == it_o).mean() >= 0.999
+    same = conv_g == conv_o
+    np.testing.assert_allclose(pix_g[same], pix_o[same], atol=1e-9)
+
+
+def test_normalize_rays_parity(ctx):
+    pair = pmxgen.config0(seed=2, height=48, width=64)
+    X = pair["X_a"].copy()
+    X[3] = 0.0
+    X[7] = np.inf
+    valid = np.ones(48 * 64, np.uint8)
+    valid[11] = 0
+    r_o, d_o, v_o = pyoracle.normalize_rays(X, valid, 48, 64)
+    r_g, d_g, v_g = ctx.normalize_rays(Pointmap(X, valid, 48, 64))
+    assert np.array_equal(v_g, v_o)
+    assert np.array_equal(r_g, r_o)  # bit-exact: same FP64 ops, IEEE div / sqrt
+    assert np.array_equal(d_g[v_o == 1], d_o[v_o == 1])
+
+
+def test_match_stats_and_keyframe_decision(ctx):
+    # camera.cpp:10-28, tracking.cpp:249-257 (test_tracking.cpp:381+)
+    h, w = 10, 10
+    full = MatchSet(np.arange(100, dtype=np.int32), np.ones(100, np.float32), np.ones(100, np.uint8),
+                    np.arange(100, dtype=np.int32))
+    assert not ctx.keyframe_decision(full, h, w, 0.333)
+    sparse = MatchSet(np.arange(30, dtype=np.int32), np.ones(30, np.float32), np.ones(30, np.uint8),
+                      np.arange(30, dtype=np.int32))
+    assert ctx.keyframe_decision(sparse, h, w, 0.333)
+    collapsed = MatchSet(np.zeros(90, np.int32), np.ones(90, np.float32), np.ones(90, np.uint8),
+                         np.arange(90, dtype=np.int32))
+    assert ctx.keyframe_decision(collapsed, h, w, 0.333)
+    rng = np.random.default_rng(5)
+    pa = rng.integers(-2, 120, 500).astype(np.int32)
+    v = (rng.random(500) < 0.7).astype(np.uint8)
+    m = MatchSet(pa, np.ones(500, np.float32), v, np.arange(500, dtype=np.int32))
+    vc, uf = ctx.match_stats(m, 100)
+    vo, uo = pyoracle.match_stats(pyoracle.MatchSet(pa, np.arange(500), np.ones(500), v), 100)
+    assert vc == vo and uf == uo
