@@ -169,7 +169,9 @@ def run_pmx(args):
 
     dev_pairs = [structs(p, to_dev) for p in host_pairs]
     ctx = Context(local)
-    stream = torch.cuda.current_stream()
+    # a real (non-default) stream shared by torch's events and the library
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream)
     mp, rp = match_params()
     outs = [MatchSet.empty(H * W, dev) for _ in mine]

@@ -340,6 +340,38 @@ int gen_express(const double* scene, int64_t image_id, const pmx_sim3* T_wk, con
   return 0;
 }
 
+/* Pair-predicted descriptors of edge (a, b) (MASt3R predicts D_i, D_j per
+ * pair): the identity of a surface point is its rounded pixel in camera a's
+ * grid (config 0: camera i), so the descriptor peak of a correspondence is
+ * the nearest camera-a pixel.  D_a[i] = h(a, u_i, v_i) + noise; D_b[n] =
+ * h(a, round(K proj_a(P_b[n]))) + noise; h = hash-seeded unit vector. */
+int gen_pair_desc(const double* scene, int64_t image_a, const pmx_sim3* T_wa, const uint8_t* valid_a,
+                  int64_t image_b, const double* P_b, const uint8_t* valid_b, uint16_t* D_a, uint16_t* D_b,
+                  int threads) {
+  const Scene s = to_scene(scene);
+  const pmx_sim3 Ta = *T_wa;
+  const int64_t ns = (int64_t)1 << 24;  // id namespace per camera a
+  parallel_rows(s.H, threads, [&](int v) {
+    for (int u = 0; u < s.W; ++u) {
+      const int64_t i = (int64_t)v * s.W + u;
+      int64_t iu = valid_a[i] ? u : -1000000 - i, iv = valid_a[i] ? v : -1000000;
+      descriptor(s, iu + ns * image_a, iv, (uint64_t)image_a, i, D_a + (size_t)i * s.dim);
+      iu = -2000000 - i;
+      iv = -2000000;
+      if (valid_b[i]) {
+        double Xa[3];
+        apply_inv(Ta, P_b + 3 * i, Xa);
+        if (Xa[2] > 1e-9) {
+          iu = (int64_t)std::llround(s.f * Xa[0] / Xa[2] + s.cx);
+          iv = (int64_t)std::llround(s.f * Xa[1] / Xa[2] + s.cy);
+        }
+      }
+      descriptor(s, iu + ns * image_a, iv, (uint64_t)image_b, i, D_b + (size_t)i * s.dim);
+    }
+  });
+  return 0;
+}
+
 /* Ground-truth correspondences of edge (a, b): for every pixel n of camera b,
  * its surface point projected into camera a, rounded (pixel_a, -1 when it
  * falls outside the image or behind the camera).  q = sqrt(Q_a Q_b). */

@@ -158,12 +158,9 @@ class Scene:
     def pair(self, ia: int, T_wa: Pose, ib: int, T_wb: Pose, salt: int = 0):
         """Pair prediction of edge (a, b) in frame a (what MASt3R predicts):
         X_a = camera a's points in frame a, X_b_in_a = camera b's points in
-        frame a, per-image Q and fp16 descriptors."""
-        A = self.image(ia, T_wa, T_wa, salt)
-        B = self.image(ib, T_wb, T_wa, salt + 1)
-        return {"X_a": A["X"], "valid_a": A["valid"], "Q_a": A["Q"], "D_a": A["D"],
-                "X_b": B["X"], "valid_b": B["valid"], "Q_b": B["Q"], "D_b": B["D"],
-                "height": self.height, "width": self.width}
+        frame a, per-image Q, pair-predicted fp16 descriptors (ids on camera
+        a's pixel grid, gen_pair_desc)."""
+        return pair_from_cameras(Camera(self, ia, T_wa), Camera(self, ib, T_wb), salt)
 
     def gt_matches(self, ia, T_wa, ib, T_wb, subpixel=False):
         from paper_2412_12392_b200.abi import pmx_sim3
@@ -313,10 +310,9 @@ class Camera:
         self.P = np.empty((n, 3), np.float64)
         self.valid = np.empty(n, np.uint8)
         self.Q = np.empty(n, np.float32)
-        self.D = np.empty((n, scene.dim), np.uint16)
         a = T_wk.to_struct(pmx_sim3)
         _load().gen_camera(_p(scene.params), C.c_int64(image_id), C.byref(a), _p(self.P), _p(self.valid),
-                           _p(self.Q), _p(self.D), C.c_int(_threads()))
+                           _p(self.Q), None, C.c_int(_threads()))
 
     def express(self, T_frame: Pose, salt: int) -> np.ndarray:
         from paper_2412_12392_b200.abi import pmx_sim3
@@ -329,9 +325,17 @@ class Camera:
 
 def pair_from_cameras(ca: Camera, cb: Camera, salt: int):
     """Pair prediction of edge (a, b) in frame a from cached cameras."""
-    return {"X_a": ca.express(ca.T, salt), "valid_a": ca.valid, "Q_a": ca.Q, "D_a": ca.D,
-            "X_b": cb.express(ca.T, salt + 1), "valid_b": cb.valid, "Q_b": cb.Q, "D_b": cb.D,
-            "height": ca.scene.height, "width": ca.scene.width}
+    from paper_2412_12392_b200.abi import pmx_sim3
+    sc = ca.scene
+    n = sc.height * sc.width
+    Da = np.empty((n, sc.dim), np.uint16)
+    Db = np.empty((n, sc.dim), np.uint16)
+    a = ca.T.to_struct(pmx_sim3)
+    _load().gen_pair_desc(_p(sc.params), C.c_int64(ca.image_id), C.byref(a), _p(ca.valid), C.c_int64(cb.image_id),
+                          _p(cb.P), _p(cb.valid), _p(Da), _p(Db), C.c_int(_threads()))
+    return {"X_a": ca.express(ca.T, salt), "valid_a": ca.valid, "Q_a": ca.Q, "D_a": Da,
+            "X_b": cb.express(ca.T, salt + 1), "valid_b": cb.valid, "Q_b": cb.Q, "D_b": Db,
+            "height": sc.height, "width": sc.width}
 
 
 def config2(seed: int = 2, height=H, width=W, n_kf: int = 32, edges=None):

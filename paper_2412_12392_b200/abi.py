@@ -229,12 +229,13 @@ def default_backend_params() -> pmx_backend_params:
 # ------------------------------------------------------------ struct helpers
 
 def ptr(a):
-    """Raw address of a numpy array or torch tensor (None -> NULL)."""
+    """Address of a numpy array or torch tensor as a c_void_p (None -> NULL).
+    (A bare Python int would be passed to C as a 32-bit int.)"""
     if a is None:
         return None
     if hasattr(a, "data_ptr"):
-        return a.data_ptr()
-    return a.ctypes.data
+        return C.c_void_p(a.data_ptr())
+    return C.c_void_p(a.ctypes.data)
 
 
 def pointmap(xyz, valid, height: int, width: int) -> pmx_pointmap:

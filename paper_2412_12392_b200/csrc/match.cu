@@ -64,6 +64,10 @@ struct PairDev {
   uint32_t* keys;
   uint32_t* hist;
   SelState* sel;
+  // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
+  // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
+  uint4* dhead;
+  float2* dnorm;
 };
 
 struct LMParams {
@@ -78,6 +82,48 @@ struct RefineLevels {
   int stride[PMX_MAX_REFINE_LEVELS];
   int radius[PMX_MAX_REFINE_LEVELS];
 };
+
+// fp32 FMA with fp16 sources (SASS FHFMA, .H0/.H1 half selects): the fp16 x
+// fp16 product is exact, one rounding per accumulation.
+__device__ __forceinline__ float fh_lo(uint32_t a, uint32_t b, float c) {
+  float r;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;"
+      : "=f"(r)
+      : "h"((unsigned short)(a & 0xffffu)), "h"((unsigned short)(b & 0xffffu)), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fh_hi(uint32_t a, uint32_t b, float c) {
+  float r;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(r) : "h"((unsigned short)(a >> 16)), "h"((unsigned short)(b >> 16)), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float dot8(const uint4& a, const uint4& b, float s) {
+  s = fh_lo(a.x, b.x, s);
+  s = fh_hi(a.x, b.x, s);
+  s = fh_lo(a.y, b.y, s);
+  s = fh_hi(a.y, b.y, s);
+  s = fh_lo(a.z, b.z, s);
+  s = fh_hi(a.z, b.z, s);
+  s = fh_lo(a.w, b.w, s);
+  s = fh_hi(a.w, b.w, s);
+  return s;
+}
+constexpr float kU = 5.9604645e-08f;  // fp32 unit roundoff 2^-24
+
+// Upper bound of sqrt(sum of squares) accumulated by an n-term FHFMA chain.
+__device__ __forceinline__ float norm_ub(float ss, int n) {
+  return sqrtf(ss * (1.0f + (n + 2) * kU)) * (1.0f + 2.0f * kU);
+}
+
+// Planar head + norm bounds of one 24-dim descriptor row.
+__device__ __forceinline__ void desc_aux(const __half* row, uint4* head, float2* nrm) {
+  const uint4* p = reinterpret_cast<const uint4*>(row);
+  const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
+  const float hs = dot8(a, a, 0.0f);
+  const float ts = dot8(c, c, dot8(b, b, 0.0f));
+  *head = a;
+  *nrm = make_float2(norm_ub(hs + ts, 24), norm_ub(ts, 16));
+}
 
 // ---------------------------------------------------------------- K1
 __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
@@ -104,10 +150,17 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       atomicAdd(&sh[key >> 20], 1u);
     }
     P.keys[i] = key;
+    if (P.dhead) desc_aux(P.da + (size_t)i * 24, P.dhead + i, P.dnorm + i);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
     if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(256) k_desc_prep(const __half* __restrict__ da, int hw, uint4* dhead,
+                                                   float2* dnorm) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hw) desc_aux(da + (size_t)i * 24, dhead + i, dnorm + i);
 }
 
 // ---------------------------------------------------------------- K2
@@ -216,9 +269,18 @@ __device__ __forceinline__ double4 ld_ray(const double4* rays, int i) {
   return make_double4(a.x, a.y, b.x, b.y);
 }
 
-// interpolate_ray, camera.cpp:58-100.  J: col0 = d/du (J[0..2]), col1 = d/dv.
-__device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int W, int H, double u,
-                                           double v, double ray[3], double J[6]) {
+// interpolate_ray, camera.cpp:58-100, split so the 3x2 Jacobian is only
+// formed for accepted points (the reference computes it for every trial;
+// the value is identical, it is just never used when a trial is rejected).
+struct Interp {
+  double r0, r1, r2;  // unit ray g / |g|
+  double rs;          // 1 / |g|
+  double fu, fv;
+  double4 c00, c10, c01, c11;
+};
+
+__device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, int W, int H, double u, double v,
+                                            Interp& I) {
   if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
   int u0 = (int)floor(u);
   int v0 = (int)floor(v);
@@ -226,36 +288,55 @@ __device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int
   v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
   const int u1 = min(u0 + 1, W - 1);
   const int v1 = min(v0 + 1, H - 1);
-  const double fu = u - u0;
-  const double fv = v - v0;
-  const double4 r00 = ld_ray(rays, v0 * W + u0);
-  const double4 r10 = ld_ray(rays, v0 * W + u1);
-  const double4 r01 = ld_ray(rays, v1 * W + u0);
-  const double4 r11 = ld_ray(rays, v1 * W + u1);
-  if (r00.w == 0.0 || r10.w == 0.0 || r01.w == 0.0 || r11.w == 0.0) return false;
+  I.fu = u - u0;
+  I.fv = v - v0;
+  I.c00 = ld_ray(rays, v0 * W + u0);
+  I.c10 = ld_ray(rays, v0 * W + u1);
+  I.c01 = ld_ray(rays, v1 * W + u0);
+  I.c11 = ld_ray(rays, v1 * W + u1);
+  if (I.c00.w == 0.0 || I.c10.w == 0.0 || I.c01.w == 0.0 || I.c11.w == 0.0) return false;
+  const double fu = I.fu, fv = I.fv;
   const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
-  const double g0 = w00 * r00.x + w10 * r10.x + w01 * r01.x + w11 * r11.x;
-  const double g1 = w00 * r00.y + w10 * r10.y + w01 * r01.y + w11 * r11.y;
-  const double g2 = w00 * r00.z + w10 * r10.z + w01 * r01.z + w11 * r11.z;
-  const double gn = sqrt(g0 * g0 + g1 * g1 + g2 * g2);
-  if (gn < 1e-12) return false;
-  ray[0] = g0 / gn;
-  ray[1] = g1 / gn;
-  ray[2] = g2 / gn;
-  const double du0 = (1 - fv) * (r10.x - r00.x) + fv * (r11.x - r01.x);
-  const double du1 = (1 - fv) * (r10.y - r00.y) + fv * (r11.y - r01.y);
-  const double du2 = (1 - fv) * (r10.z - r00.z) + fv * (r11.z - r01.z);
-  const double dv0 = (1 - fu) * (r01.x - r00.x) + fu * (r11.x - r10.x);
-  const double dv1 = (1 - fu) * (r01.y - r00.y) + fu * (r11.y - r10.y);
-  const double dv2 = (1 - fu) * (r01.z - r00.z) + fu * (r11.z - r10.z);
-  const double rdu = ray[0] * du0 + ray[1] * du1 + ray[2] * du2;
-  const double rdv = ray[0] * dv0 + ray[1] * dv1 + ray[2] * dv2;
-  J[0] = (du0 - ray[0] * rdu) / gn;
-  J[1] = (du1 - ray[1] * rdu) / gn;
-  J[2] = (du2 - ray[2] * rdu) / gn;
-  J[3] = (dv0 - ray[0] * rdv) / gn;
-  J[4] = (dv1 - ray[1] * rdv) / gn;
-  J[5] = (dv2 - ray[2] * rdv) / gn;
+  const double g0 = w00 * I.c00.x + w10 * I.c10.x + w01 * I.c01.x + w11 * I.c11.x;
+  const double g1 = w00 * I.c00.y + w10 * I.c10.y + w01 * I.c01.y + w11 * I.c11.y;
+  const double g2 = w00 * I.c00.z + w10 * I.c10.z + w01 * I.c01.z + w11 * I.c11.z;
+  const double gg = g0 * g0 + g1 * g1 + g2 * g2;
+  if (gg < 1e-24) return false;  // |g| < 1e-12
+  I.rs = rsqrt(gg);
+  I.r0 = g0 * I.rs;
+  I.r1 = g1 * I.rs;
+  I.r2 = g2 * I.rs;
+  return true;
+}
+
+// J = (I - r r^T) / |g| [dg/du, dg/dv]  (camera.cpp:92-98)
+__device__ __forceinline__ void interp_jac(const Interp& I, double J[6]) {
+  const double fu = I.fu, fv = I.fv;
+  const double du0 = (1 - fv) * (I.c10.x - I.c00.x) + fv * (I.c11.x - I.c01.x);
+  const double du1 = (1 - fv) * (I.c10.y - I.c00.y) + fv * (I.c11.y - I.c01.y);
+  const double du2 = (1 - fv) * (I.c10.z - I.c00.z) + fv * (I.c11.z - I.c01.z);
+  const double dv0 = (1 - fu) * (I.c01.x - I.c00.x) + fu * (I.c11.x - I.c10.x);
+  const double dv1 = (1 - fu) * (I.c01.y - I.c00.y) + fu * (I.c11.y - I.c10.y);
+  const double dv2 = (1 - fu) * (I.c01.z - I.c00.z) + fu * (I.c11.z - I.c10.z);
+  const double rdu = I.r0 * du0 + I.r1 * du1 + I.r2 * du2;
+  const double rdv = I.r0 * dv0 + I.r1 * dv1 + I.r2 * dv2;
+  J[0] = (du0 - I.r0 * rdu) * I.rs;
+  J[1] = (du1 - I.r1 * rdu) * I.rs;
+  J[2] = (du2 - I.r2 * rdu) * I.rs;
+  J[3] = (dv0 - I.r0 * rdv) * I.rs;
+  J[4] = (dv1 - I.r1 * rdv) * I.rs;
+  J[5] = (dv2 - I.r2 * rdv) * I.rs;
+}
+
+// Full form (ray + Jacobian), kept for the fine-grained entry points.
+__device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int W, int H, double u,
+                                           double v, double ray[3], double J[6]) {
+  Interp I;
+  if (!interp_eval(rays, W, H, u, v, I)) return false;
+  ray[0] = I.r0;
+  ray[1] = I.r1;
+  ray[2] = I.r2;
+  interp_jac(I, J);
   return true;
 }
 
@@ -307,26 +388,29 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
   }
   const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
   double pu = cu, pv = cv;
-  double ray[3], J[6];
-  if (!interp_ray(rays, W, H, pu, pv, ray, J)) {
+  Interp I;
+  if (!interp_eval(rays, W, H, pu, pv, I)) {
     res.pu = pu;
     res.pv = pv;
     return res;
   }
-  double r0 = ray[0] - t0, r1 = ray[1] - t1, r2 = ray[2] - t2;
+  double ray0 = I.r0, ray1 = I.r1, ray2 = I.r2;
+  double r0 = ray0 - t0, r1 = ray1 - t1, r2 = ray2 - t2;
   double cost = r0 * r0 + r1 * r1 + r2 * r2;
-  if (ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol) {
+  if (ray0 * t0 + ray1 * t1 + ray2 * t2 >= lp.cos_tol) {
     res.pu = pu;
     res.pv = pv;
     res.converged = true;
     return res;
   }
+  double J[6];
+  interp_jac(I, J);
   double lambda = lp.lambda_init;
   for (int it = 0; it < lp.max_iterations; ++it) {
     ++res.iterations;
-    r0 = ray[0] - t0;
-    r1 = ray[1] - t1;
-    r2 = ray[2] - t2;
+    r0 = ray0 - t0;
+    r1 = ray1 - t1;
+    r2 = ray2 - t2;
     const double a00 = J[0] * J[0] + J[1] * J[1] + J[2] * J[2];
     const double a01 = J[0] * J[3] + J[1] * J[4] + J[2] * J[5];
     const double a11 = J[3] * J[3] + J[4] * J[4] + J[5] * J[5];
@@ -340,25 +424,24 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     if (!isfinite(d0) || !isfinite(d1)) break;
     const double tu = fmin(fmax(pu + d0, 0.0), (double)(W - 1));
     const double tv = fmin(fmax(pv + d1, 0.0), (double)(H - 1));
-    double rt[3], Jt[6];
-    if (interp_ray(rays, W, H, tu, tv, rt, Jt)) {
-      const double e0 = rt[0] - t0, e1 = rt[1] - t1, e2 = rt[2] - t2;
+    if (interp_eval(rays, W, H, tu, tv, I)) {
+      const double e0 = I.r0 - t0, e1 = I.r1 - t1, e2 = I.r2 - t2;
       const double ct = e0 * e0 + e1 * e1 + e2 * e2;
       if (ct < cost) {
         pu = tu;
         pv = tv;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) ray[k] = rt[k];
-#pragma unroll
-        for (int k = 0; k < 6; ++k) J[k] = Jt[k];
+        ray0 = I.r0;
+        ray1 = I.r1;
+        ray2 = I.r2;
         cost = ct;
         lambda *= lp.lambda_down;
-        if (ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol) {
+        if (ray0 * t0 + ray1 * t1 + ray2 * t2 >= lp.cos_tol) {
           res.pu = pu;
           res.pv = pv;
           res.converged = true;
           return res;
         }
+        interp_jac(I, J);
         continue;
       }
     }
@@ -366,7 +449,7 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
   }
   res.pu = pu;
   res.pv = pv;
-  res.converged = ray[0] * t0 + ray[1] * t1 + ray[2] * t2 >= lp.cos_tol;
+  res.converged = ray0 * t0 + ray1 * t1 + ray2 * t2 >= lp.cos_tol;
   return res;
 }
 
@@ -413,7 +496,7 @@ __device__ __forceinline__ float dot_fast(const __half* __restrict__ a, const fl
 // skipped: they were all scored <= the running best, and only a strict '>'
 // can move the best, so skipping them is exact.
 template <int DIM>
-__device__ int refine_one(const __half* __restrict__ Da, int Wa, int Ha, const __half* __restrict__ bdesc,
+__device__ __noinline__ int refine_one(const __half* __restrict__ Da, int Wa, int Ha, const __half* __restrict__ bdesc,
                           int pa, const RefineLevels& L) {
   float bt[DIM];
   float bnorm1 = 0.0f;
@@ -506,7 +589,7 @@ __device__ int refine_one(const __half* __restrict__ Da, int Wa, int Ha, const _
 }
 
 // Generic-dimension refinement: exact FP64 scores throughout.
-__device__ int refine_one_generic(const __half* __restrict__ Da, int Wa, int Ha, int dim,
+__device__ __noinline__ int refine_one_generic(const __half* __restrict__ Da, int Wa, int Ha, int dim,
                                   const __half* __restrict__ bdesc, int pa, const RefineLevels& L) {
   int best_u = pa % Wa, best_v = pa / Wa;
   for (int l = 0; l < L.n; ++l) {
@@ -528,10 +611,132 @@ __device__ int refine_one_generic(const __half* __restrict__ Da, int Wa, int Ha,
   return best_v * Wa + best_u;
 }
 
+// Pruned refinement for 24-dim descriptors (the hot path).  Every candidate
+// first costs one 8-dim head dot from the planar head array; by
+// Cauchy-Schwarz its exact score is <= head + ||a_t|| ||b_t|| (+ rounding
+// bounds), and when that cannot beat the current best (strict '>') the
+// candidate is skipped exactly.  Otherwise the full fp32 dot is decided with
+// a rigorous error bound, and near-ties in exact FP64 (as the reference).
+struct ExactBest {
+  float f;    // fp32 score
+  float err;  // |f - exact| bound
+};
+
+__device__ __forceinline__ bool certainly_gt(float x, float ex, float y, float ey) {
+  const float d = (x - ex) - (y + ey);
+  return d > 4.0f * kU * (fabsf(x) + ex + fabsf(y) + ey);
+}
+__device__ __forceinline__ bool certainly_le(float x, float ex, float y, float ey) {
+  const float d = (y - ey) - (x + ex);
+  return d >= 4.0f * kU * (fabsf(x) + ex + fabsf(y) + ey);
+}
+
+// Running best of one refinement level (exact-argmax bookkeeping).
+struct BestState {
+  int u, v;
+  float f, err;   // fp32 score and its rounding bound
+  float thr;      // prune threshold: candidates with ub <= thr cannot win
+  double x;       // exact score when known
+  bool known;
+};
+
+__device__ __forceinline__ void best_set(BestState& B, int u, int v, float f, float err) {
+  B.u = u;
+  B.v = v;
+  B.f = f;
+  B.err = err;
+  B.thr = (f - err) - 4.0f * kU * (fabsf(f) + err);
+  B.known = false;
+}
+
+// Full-dot decision for one unpruned candidate (rare path).
+__device__ __noinline__ void refine_full(const PairDev& P, const __half* __restrict__ bdesc, uint4 b1, uint4 b2,
+                                         float nb, int u, int v, float hd, float na, BestState& B) {
+  const int pix = v * P.Wa + u;
+  const uint4* ap = reinterpret_cast<const uint4*>(P.da + (size_t)pix * 24);
+  const float sc = dot8(__ldg(ap + 2), b2, dot8(__ldg(ap + 1), b1, hd));
+  const float err = 24.01f * kU * na * nb;
+  if (certainly_gt(sc, err, B.f, B.err)) {
+    best_set(B, u, v, sc, err);
+  } else if (!certainly_le(sc, err, B.f, B.err)) {
+    if (!B.known) {
+      B.x = dot_exact(P.da + (size_t)(B.v * P.Wa + B.u) * 24, bdesc, 24);
+      B.known = true;
+    }
+    const double ex = dot_exact(P.da + (size_t)pix * 24, bdesc, 24);
+    if (ex > B.x) {
+      best_set(B, u, v, sc, err);
+      B.x = ex;
+      B.known = true;
+    }
+  }
+}
+
+__device__ __forceinline__ int refine_pruned(const PairDev& P, int pa, const __half* __restrict__ bdesc, const RefineLevels& L) {
+  const int Wa = P.Wa, Ha = P.Ha;
+  const uint4* bp = reinterpret_cast<const uint4*>(bdesc);
+  const uint4 b0 = __ldg(bp), b1 = __ldg(bp + 1), b2 = __ldg(bp + 2);
+  const float bh_ss = dot8(b0, b0, 0.0f);
+  const float bt_ss = dot8(b2, b2, dot8(b1, b1, 0.0f));
+  const float nb = norm_ub(bh_ss + bt_ss, 24);
+  // exact(cand) <= head + 8u ||a|| ||b_h|| + ||a_t|| ||b_t||   (Cauchy-Schwarz)
+  const float c_head = 8.01f * kU * norm_ub(bh_ss, 8);
+  const float c_tail = norm_ub(bt_ss, 16) * (1.0f + 4.0f * kU);
+  const uint4* __restrict__ heads = P.dhead;
+  const float2* __restrict__ norms = P.dnorm;
+  int cu = pa % Wa, cv = pa / Wa;
+  int prev_cu = 0, prev_cv = 0, prev_s = 1, prev_r = -1;
+  for (int l = 0; l < L.n; ++l) {
+    const int s = L.stride[l], r = L.radius[l];
+    if (l > 0 && s == prev_s && r == prev_r && cu == prev_cu && cv == prev_cv) continue;
+    BestState B;
+    {
+      const int pix = cv * Wa + cu;
+      const uint4* ap = reinterpret_cast<const uint4*>(P.da + (size_t)pix * 24);
+      const float f = dot8(__ldg(ap + 2), b2, dot8(__ldg(ap + 1), b1, dot8(__ldg(ap), b0, 0.0f)));
+      best_set(B, cu, cv, f, 24.01f * kU * __ldg(norms + pix).x * nb);
+      B.x = 0.0;
+    }
+    // window clipped to the image: no per-candidate bounds checks
+    const int du_lo = -min(r, cu / s), du_hi = min(r, (Wa - 1 - cu) / s);
+    const int dv_lo = -min(r, cv / s), dv_hi = min(r, (Ha - 1 - cv) / s);
+    const bool check_prev = prev_r >= 0;
+    for (int dv = dv_lo; dv <= dv_hi; ++dv) {
+      const int v = cv + dv * s;
+      const int row = v * Wa;
+#pragma unroll 2
+      for (int du = du_lo; du <= du_hi; ++du) {
+        const int u = cu + du * s;
+        if (du == 0 && dv == 0) continue;
+        if (check_prev) {  // inside the previous level's (already maximised) window: cannot win
+          const int eu = u - prev_cu, ev = v - prev_cv, lim = prev_r * prev_s;
+          if (abs(eu) <= lim && abs(ev) <= lim && (prev_s == 1 || (eu % prev_s == 0 && ev % prev_s == 0)))
+            continue;
+        }
+        const int pix = row + u;
+        const float2 nr = __ldg(norms + pix);
+        const float hd = dot8(__ldg(heads + pix), b0, 0.0f);
+        const float ub = fmaf(nr.x, c_head, nr.y * c_tail);
+        const float t = hd + ub;
+        if (fmaf(4.0f * kU, fabsf(hd) + ub, t) <= B.thr) continue;  // certainly <= best: strict '>' fails
+        refine_full(P, bdesc, b1, b2, nb, u, v, hd, nr.x, B);
+      }
+    }
+    prev_cu = cu;
+    prev_cv = cv;
+    prev_s = s;
+    prev_r = r;
+    cu = B.u;
+    cv = B.v;
+  }
+  return cv * Wa + cu;
+}
+
 __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb, const RefineLevels& L) {
   const __half* bdesc = P.db + (size_t)pb * P.dim;
   if (((uintptr_t)P.da | (uintptr_t)P.db) & 15)  // vector loads need 16-byte rows
     return refine_one_generic(P.da, P.Wa, P.Ha, P.dim, bdesc, pa, L);
+  if (P.dhead && P.dim == 24) return refine_pruned(P, pa, bdesc, L);
   if (P.dim == 24) return refine_one<24>(P.da, P.Wa, P.Ha, bdesc, pa, L);
   if (P.dim == 16) return refine_one<16>(P.da, P.Wa, P.Ha, bdesc, pa, L);
   if (P.dim == 32) return refine_one<32>(P.da, P.Wa, P.Ha, bdesc, pa, L);
@@ -540,8 +745,7 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 
 // ---------------------------------------------------------------- K3 + K4
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair.
-__global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs, LMParams lp,
-                                               RefineLevels L, int do_refine) {
+__global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
   const PairDev& P = pairs[blockIdx.y];
   const int tiles_x = (P.Wb + 31) / 32;
   const int tiles = tiles_x * ((P.Hb + 7) / 8);
@@ -579,7 +783,6 @@ __global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs
       const double dist = sqrt(e0 * e0 + e1 * e1 + e2 * e2);
       if (dist > P.sel->threshold) valid = false;
     }
-    if (valid && do_refine) pa = refine_dispatch(P, pa, n, L);
     pa_out = pa;
     q_out = (float)sqrt((double)P.qa[pa] * (double)P.qb[n]);
     valid_out = valid ? 1 : 0;
@@ -587,6 +790,22 @@ __global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs
   P.out_pa[n] = pa_out;
   P.out_q[n] = q_out;
   P.out_valid[n] = valid_out;
+}
+
+// K4: feature_refine of the valid matches just written by k_match (in place).
+__global__ void __launch_bounds__(128) k_refine_pairs(const PairDev* __restrict__ pairs, RefineLevels L) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int tiles_x = (P.Wb + 31) / 32;
+  const int tiles = tiles_x * ((P.Hb + 3) / 4);
+  if ((int)blockIdx.x >= tiles) return;
+  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+  const int v = (blockIdx.x / tiles_x) * 4 + (threadIdx.x >> 5);
+  if (u >= P.Wb || v >= P.Hb) return;
+  const int n = v * P.Wb + u;
+  if (!P.out_valid[n]) return;
+  const int pa = refine_dispatch(P, P.out_pa[n], n, L);
+  P.out_pa[n] = pa;
+  P.out_q[n] = (float)sqrt((double)P.qa[pa] * (double)P.qb[n]);
 }
 
 // Standalone feature_refine over an arbitrary MatchSet (camera.cpp:239-271).
@@ -729,10 +948,6 @@ static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa
   launch_check(ctx, "k_sel_scan3");
 }
 
-struct PairScratch {
-  DevBuf rays, keys, hist, sel, pairs;
-};
-
 // Batched match(+refine).  All pointers in `pairs` are device pointers.
 void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, const pmx_match_params& mp,
                         const pmx_refine_params* refine) {
@@ -745,21 +960,33 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     max_hwa = std::max(max_hwa, p.Ha * p.Wa);
     max_hwb = std::max(max_hwb, p.Hb * p.Wb);
   }
-  // chunk so that the FP64 ray maps of a chunk stay L2-resident (~56 MB)
-  const size_t ray_bytes = sizeof(double4) * (size_t)max_hwa;
-  const int chunk = std::max(1, std::min(npairs, (int)((56u << 20) / std::max<size_t>(ray_bytes, 1))));
-  DevBuf rays(ray_bytes * chunk, ctx.stream);
-  DevBuf keys(sizeof(uint32_t) * (size_t)max_hwa * chunk, ctx.stream);
+  // chunk so that a chunk's FP64 ray maps + descriptor heads / norms + keys
+  // (60 B per a-pixel) stay L2-resident between k_prep and k_match/k_refine
+  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(float2) + sizeof(uint32_t);
+  const size_t pair_bytes = per_px * (size_t)max_hwa;
+  const int chunk = std::max(1, std::min(npairs, (int)((64u << 20) / std::max<size_t>(pair_bytes, 1))));
+  DevBuf scratch(pair_bytes * chunk, ctx.stream);
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
   DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
   DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
   std::vector<PairDev> hp = host_pairs;
+  char* base = scratch.as<char>();
+  const size_t nslot = (size_t)max_hwa * chunk;
+  double4* rays = reinterpret_cast<double4*>(base);
+  uint4* heads = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
+  float2* norms = reinterpret_cast<float2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(float2)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
-    hp[i].rays = rays.as<double4>() + (size_t)slot * max_hwa;
-    hp[i].keys = keys.as<uint32_t>() + (size_t)slot * max_hwa;
+    hp[i].rays = rays + (size_t)slot * max_hwa;
+    hp[i].keys = keys + (size_t)slot * max_hwa;
     hp[i].hist = hist.as<uint32_t>() + (size_t)kHistTotal * i;
     hp[i].sel = sel.as<SelState>() + i;
+    const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
+    if (refine && hp[i].dim == 24 && aligned) {
+      hp[i].dhead = heads + (size_t)slot * max_hwa;
+      hp[i].dnorm = norms + (size_t)slot * max_hwa;
+    }
   }
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
@@ -767,16 +994,25 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
     prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
-    int max_tiles = 0;
-    for (int i = c0; i < c0 + cn; ++i)
+    int max_tiles = 0, max_tiles4 = 0;
+    for (int i = c0; i < c0 + cn; ++i) {
       max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
-    dim3 g(max_tiles, cn);
+      max_tiles4 = std::max(max_tiles4, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 3) / 4));
+    }
     {
       ProfScope ps(ctx, "k_match");
-      k_match<<<g, 256, 0, ctx.stream>>>(dp, lp, L, refine ? 1 : 0);
+      k_match<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp);
     }
     launch_check(ctx, "k_match");
+    if (refine && L.n > 0) {
+      {
+        ProfScope ps(ctx, "k_refine");
+        k_refine_pairs<<<dim3(max_tiles4, cn), 128, 0, ctx.stream>>>(dp, L);
+      }
+      launch_check(ctx, "k_refine_pairs");
+    }
   }
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // hp lifetime / scratch reuse by the caller
 }
 
 // ------------------------------------------------------------ C-ABI glue
@@ -892,6 +1128,14 @@ extern "C" int pmx_impl_feature_refine(pmx_context* c, pmx_memory mem, const pmx
   int32_t* opb = st.out(out->pixel_b, n);
   float* oq = st.out(out->confidence, n);
   uint8_t* ov = st.out(out->valid, n);
+  DevBuf aux;
+  if (P.dim == 24 && ((uintptr_t)P.da % 16 == 0) && ((uintptr_t)P.db % 16 == 0) && hwa > 0) {
+    aux = DevBuf((sizeof(uint4) + sizeof(float2)) * hwa, ctx.stream);
+    P.dhead = aux.as<uint4>();
+    P.dnorm = reinterpret_cast<float2*>(aux.as<char>() + sizeof(uint4) * hwa);
+    k_desc_prep<<<(unsigned)((hwa + 255) / 256), 256, 0, ctx.stream>>>(P.da, (int)hwa, P.dhead, P.dnorm);
+    launch_check(ctx, "k_desc_prep");
+  }
   if (n > 0) {
     k_refine<<<(unsigned)((n + 255) / 256), 256, 0, ctx.stream>>>(P, n, ipa, ipb, iq, iv, L, opa, opb, oq, ov);
     launch_check(ctx, "k_refine");
