@@ -193,6 +193,10 @@ void pmx_default_robust_weight_params(pmx_robust_weight_params* p);
 void pmx_default_solve_pose_params(pmx_solve_pose_params* p);
 void pmx_default_backend_params(pmx_backend_params* p);
 void pmx_sim3_identity(pmx_sim3* T);
+/* Host-only FP64 Sim(3) helpers (no device needed): left-plus retract
+ * Exp(tau) * T (lie.hpp:54) and relative_pose T_wi^-1 T_wj (lie.cpp:171). */
+void pmx_sim3_retract(const pmx_sim3* T, const double* tau7, pmx_sim3* out);
+void pmx_sim3_relative(const pmx_sim3* T_wi, const pmx_sim3* T_wj, pmx_sim3* out);
 
 /* ----------------------------------------------------------- lifecycle */
 int pmx_abi_version(void);

@@ -525,6 +525,10 @@ int orc_ldlt_solve(int32_t n, const double* A, const double* b, double* x, int32
   });
 }
 
+double orc_robust_weight(double q, double sigma2, double q_min) { return robust_weight(q, sigma2, q_min); }
+double orc_huber_cost(double e, double delta) { return huber_cost(e, delta); }
+double orc_huber_factor(double e, double delta) { return huber_factor(e, delta); }
+
 int orc_sim3_exp(const double* tau7, pmx_sim3* out) {
   return guard([&] {
     Vec7 t;

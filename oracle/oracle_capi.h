@@ -82,6 +82,10 @@ int orc_backend_edge_terms(const orc_graph* g, const pmx_backend_params* p, int3
 int orc_global_optimize(orc_graph* g, const pmx_backend_params* p, pmx_optimize_result* result,
                         pmx_sim3* pose_trace);
 int orc_ldlt_solve(int32_t n, const double* A, const double* b, double* x, int32_t* ok);
+/* tracking.cpp:10-30 scalar helpers. */
+double orc_robust_weight(double q, double sigma2, double q_min);
+double orc_huber_cost(double e, double delta);
+double orc_huber_factor(double e, double delta);
 /* Lie helpers for tests: exp/log/compose/inverse/adjoint. */
 int orc_sim3_exp(const double* tau7, pmx_sim3* out);
 int orc_sim3_log(const pmx_sim3* T, double* tau7);

@@ -143,6 +143,7 @@ PMX_SYMBOLS = [
     "pmx_solve_pose", "pmx_fuse_canonical", "pmx_assemble_system", "pmx_backend_cost",
     "pmx_global_optimize", "pmx_backend_edge_terms", "pmx_backend_solve_terms",
     "pmx_ldlt_solve", "pmx_profile_enable", "pmx_profile_reset", "pmx_profile_get",
+    "pmx_sim3_retract", "pmx_sim3_relative",
 ]
 
 _lib = None

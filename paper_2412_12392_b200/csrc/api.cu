@@ -122,6 +122,14 @@ void pmx_sim3_identity(pmx_sim3* T) {
   T->s = 1.0;
 }
 
+void pmx_sim3_retract(const pmx_sim3* T, const double* tau7, pmx_sim3* out) {
+  *out = pmx::to_pmx(pmx::sim3_mul(pmx::sim3_exp(tau7), pmx::to_dsim3(*T)));
+}
+
+void pmx_sim3_relative(const pmx_sim3* T_wi, const pmx_sim3* T_wj, pmx_sim3* out) {
+  *out = pmx::to_pmx(pmx::sim3_mul(pmx::sim3_inv(pmx::to_dsim3(*T_wi)), pmx::to_dsim3(*T_wj)));
+}
+
 int pmx_abi_version(void) { return PMX_ABI_VERSION; }
 
 int pmx_create(int device, pmx_context** out) {
