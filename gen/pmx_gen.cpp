@@ -165,21 +165,45 @@ void parallel_rows(int H, int threads, F&& fn) {
   for (auto& th : pool) th.join();
 }
 
-void descriptor(const Scene& s, int64_t id_u, int64_t id_v, uint64_t image, int64_t pixel,
-                uint16_t* out) {
-  double base[64], nrm = 0.0;
-  for (int c = 0; c < s.dim; ++c) {
-    base[c] = gauss(hkey(s.seed, kDescBase, (uint64_t)id_u, (uint64_t)id_v, (uint64_t)c));
-    nrm += base[c] * base[c];
+// Two N(0,1) draws from one counter hash (both Box-Muller outputs).
+inline void gauss2(uint64_t h, double* z0, double* z1) {
+  const double u1 = u01(h);
+  const double u2 = u01(mix(h ^ 0xa0761d6478bd642full));
+  const double r = std::sqrt(-2.0 * std::log(u1));
+  const double t = 6.283185307179586 * u2;
+  *z0 = r * std::cos(t);
+  *z1 = r * std::sin(t);
+}
+
+// Unit base vector h(id) of a descriptor identity (dim even).
+void desc_base(const Scene& s, int64_t id_u, int64_t id_v, double* base) {
+  double nrm = 0.0;
+  for (int c = 0; c < s.dim; c += 2) {
+    gauss2(hkey(s.seed, kDescBase, (uint64_t)id_u, (uint64_t)id_v, (uint64_t)c), &base[c], &base[c + 1]);
+    nrm += base[c] * base[c] + base[c + 1] * base[c + 1];
   }
   nrm = std::sqrt(nrm);
+  for (int c = 0; c < s.dim; ++c) base[c] /= nrm;
+}
+
+// normalise(base + N(0, desc_sigma^2)) -> fp16, noise keyed by (image, pixel).
+void desc_finish(const Scene& s, const double* base, uint64_t image, int64_t pixel, uint16_t* out) {
   double v[64], n2 = 0.0;
-  for (int c = 0; c < s.dim; ++c) {
-    v[c] = base[c] / nrm + s.desc_sigma * gauss(hkey(s.seed, kDescNoise, image, (uint64_t)pixel, (uint64_t)c));
-    n2 += v[c] * v[c];
+  for (int c = 0; c < s.dim; c += 2) {
+    double z0, z1;
+    gauss2(hkey(s.seed, kDescNoise, image, (uint64_t)pixel, (uint64_t)c), &z0, &z1);
+    v[c] = base[c] + s.desc_sigma * z0;
+    v[c + 1] = base[c + 1] + s.desc_sigma * z1;
+    n2 += v[c] * v[c] + v[c + 1] * v[c + 1];
   }
   n2 = std::sqrt(n2);
   for (int c = 0; c < s.dim; ++c) out[c] = float_to_half((float)(v[c] / n2));
+}
+
+void descriptor(const Scene& s, int64_t id_u, int64_t id_v, uint64_t image, int64_t pixel, uint16_t* out) {
+  double base[64];
+  desc_base(s, id_u, id_v, base);
+  desc_finish(s, base, image, pixel, out);
 }
 
 Scene to_scene(const double* p) {
@@ -351,13 +375,25 @@ int gen_pair_desc(const double* scene, int64_t image_a, const pmx_sim3* T_wa, co
   const Scene s = to_scene(scene);
   const pmx_sim3 Ta = *T_wa;
   const int64_t ns = (int64_t)1 << 24;  // id namespace per camera a
+  // base vectors of camera a's pixel grid, shared by D_a and the in-image ids of D_b
+  std::vector<double> grid((size_t)s.H * s.W * s.dim);
   parallel_rows(s.H, threads, [&](int v) {
     for (int u = 0; u < s.W; ++u) {
       const int64_t i = (int64_t)v * s.W + u;
-      int64_t iu = valid_a[i] ? u : -1000000 - i, iv = valid_a[i] ? v : -1000000;
-      descriptor(s, iu + ns * image_a, iv, (uint64_t)image_a, i, D_a + (size_t)i * s.dim);
-      iu = -2000000 - i;
-      iv = -2000000;
+      desc_base(s, u + ns * image_a, v, grid.data() + (size_t)i * s.dim);
+    }
+  });
+  parallel_rows(s.H, threads, [&](int v) {
+    double base[64];
+    for (int u = 0; u < s.W; ++u) {
+      const int64_t i = (int64_t)v * s.W + u;
+      if (valid_a[i]) {
+        desc_finish(s, grid.data() + (size_t)i * s.dim, (uint64_t)image_a, i, D_a + (size_t)i * s.dim);
+      } else {
+        desc_base(s, -1000000 - i + ns * image_a, -1000000, base);
+        desc_finish(s, base, (uint64_t)image_a, i, D_a + (size_t)i * s.dim);
+      }
+      int64_t iu = -2000000 - i, iv = -2000000;
       if (valid_b[i]) {
         double Xa[3];
         apply_inv(Ta, P_b + 3 * i, Xa);
@@ -366,7 +402,42 @@ int gen_pair_desc(const double* scene, int64_t image_a, const pmx_sim3* T_wa, co
           iv = (int64_t)std::llround(s.f * Xa[1] / Xa[2] + s.cy);
         }
       }
-      descriptor(s, iu + ns * image_a, iv, (uint64_t)image_b, i, D_b + (size_t)i * s.dim);
+      const double* b;
+      if (iu >= 0 && iv >= 0 && iu < s.W && iv < s.H) {
+        b = grid.data() + (size_t)(iv * s.W + iu) * s.dim;
+      } else {
+        desc_base(s, iu + ns * image_a, iv, base);
+        b = base;
+      }
+      desc_finish(s, b, (uint64_t)image_b, i, D_b + (size_t)i * s.dim);
+    }
+  });
+  return 0;
+}
+
+/* Ground-truth matches of edge (a, b) from cached world points of camera b:
+ * pixel_a = rounded projection into camera a (-1 outside / behind),
+ * q = sqrt(Q_a[pixel_a] Q_b[n]). */
+int gen_gt_from_points(const double* scene, const pmx_sim3* T_wa, const double* P_b, const uint8_t* valid_b,
+                       const float* Q_a, const float* Q_b, int32_t* pixel_a, float* confidence, uint8_t* valid,
+                       int threads) {
+  const Scene s = to_scene(scene);
+  const pmx_sim3 Ta = *T_wa;
+  parallel_rows(s.H, threads, [&](int v) {
+    for (int u = 0; u < s.W; ++u) {
+      const int64_t i = (int64_t)v * s.W + u;
+      int32_t pa = -1;
+      if (valid_b[i]) {
+        double Xa[3];
+        apply_inv(Ta, P_b + 3 * i, Xa);
+        if (Xa[2] > 1e-9) {
+          const long ru = std::lround(s.f * Xa[0] / Xa[2] + s.cx), rv = std::lround(s.f * Xa[1] / Xa[2] + s.cy);
+          if (ru >= 0 && rv >= 0 && ru < s.W && rv < s.H) pa = (int32_t)(rv * s.W + ru);
+        }
+      }
+      pixel_a[i] = pa;
+      valid[i] = pa >= 0 ? 1 : 0;
+      confidence[i] = pa >= 0 ? (float)std::sqrt((double)Q_a[pa] * (double)Q_b[i]) : 0.0f;
     }
   });
   return 0;

@@ -277,6 +277,19 @@ def loop_edges(n_kf: int, reach: int):
     return [(k, (k + d) % n_kf) for k in range(n_kf) for d in range(1, reach + 1)]
 
 
+def gt_from_cameras(ca: "Camera", cb: "Camera"):
+    """Ground-truth matches of edge (a, b) from cached world points (gen_gt_from_points)."""
+    from paper_2412_12392_b200.abi import pmx_sim3
+    n = ca.scene.height * ca.scene.width
+    pa = np.empty(n, np.int32)
+    q = np.empty(n, np.float32)
+    v = np.empty(n, np.uint8)
+    a = ca.T.to_struct(pmx_sim3)
+    _load().gen_gt_from_points(_p(ca.scene.params), C.byref(a), _p(cb.P), _p(cb.valid), _p(ca.Q), _p(cb.Q),
+                               _p(pa), _p(q), _p(v), C.c_int(_threads()))
+    return {"pixel_a": pa, "confidence": q, "valid": v}
+
+
 def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: int = 1,
                   radius: float = 5.0, rot_deg=2.0, trans=0.05, scale_frac=0.03,
                   edges=None):
@@ -285,15 +298,10 @@ def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: in
     perturbed initial poses (anchor = keyframe 0, unperturbed)."""
     sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
     gt = loop_trajectory(n_kf, radius, loops, seed)
-    canon = []
-    for k in range(n_kf):
-        im = sc.image(k, gt[k], gt[k], salt=1000 + k, want=("X", "valid"))
-        canon.append((im["X"], im["valid"]))
+    cams = [Camera(sc, k, gt[k]) for k in range(n_kf)]
+    canon = [(c.express(c.T, 1000 + k), c.valid) for k, c in enumerate(cams)]
     edges = edges if edges is not None else loop_edges(n_kf, reach)
-    matches = []
-    for (i, j) in edges:
-        m = sc.gt_matches(i, gt[i], j, gt[j])
-        matches.append(m)
+    matches = [gt_from_cameras(cams[i], cams[j]) for (i, j) in edges]
     init = [gt[0]] + [perturb_pose(gt[k], seed, 5000 + 3 * k, rot_deg, trans, scale_frac)
                       for k in range(1, n_kf)]
     return {"scene": sc, "gt": gt, "init": init, "canonicals": canon, "edges": edges,

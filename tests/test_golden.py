@@ -1,0 +1,132 @@
+"""Committed golden fixtures (tests/golden/make_golden.py): the oracle must
+reproduce them bit for bit (CPU), and the CUDA path must match them within
+the BASELINE tolerances (GPU).  Inputs are read from the fixtures, so these
+tests do not depend on the generator."""
+import os
+
+import numpy as np
+import pytest
+
+import pyoracle
+from helpers import BASELINE_REFINE, baseline_match_params
+from paper_2412_12392_b200 import FeatureMap, Graph, MatchSet, Pointmap, abi
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return dict(np.load(os.path.join(GOLD, name)))
+
+
+def pair_of(z):
+    h, w = (int(x) for x in z["shape"])
+    return {"X_a": z["X_a"], "X_b": z["X_b"], "Q_a": z["Q_a"], "Q_b": z["Q_b"], "D_a": z["D_a"], "D_b": z["D_b"],
+            "valid_a": z["valid_a"], "valid_b": z["valid_b"], "height": h, "width": w}
+
+
+@pytest.mark.parametrize("name", ["match_radial_48x64.npz", "match_isotropic_48x64.npz"])
+def test_oracle_reproduces_match_fixture(name):
+    z = load(name)
+    p = pair_of(z)
+    m = pyoracle.match_pointmaps(p, baseline_match_params())
+    r = pyoracle.feature_refine(m, p, abi.refine_params(BASELINE_REFINE))
+    assert np.array_equal(m.pixel_a, z["lm_pixel_a"]) and np.array_equal(m.valid, z["lm_valid"])
+    assert np.array_equal(r.pixel_a, z["pixel_a"]) and np.array_equal(r.confidence, z["confidence"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["match_radial_48x64.npz", "match_isotropic_48x64.npz"])
+def test_gpu_matches_match_fixture(ctx, name):
+    z = load(name)
+    p = pair_of(z)
+    h, w = p["height"], p["width"]
+    pairs = [(Pointmap(p["X_a"], p["valid_a"], h, w), Pointmap(p["X_b"], p["valid_b"], h, w),
+              FeatureMap(p["D_a"], p["Q_a"], h, w), FeatureMap(p["D_b"], p["Q_b"], h, w))]
+    g = ctx.match_batch(pairs, params=baseline_match_params(), refine=abi.refine_params(BASELINE_REFINE))[0]
+    both = (g.valid == 1) & (z["valid"] == 1)
+    assert (g.valid != z["valid"]).sum() <= max(1, int(1e-3 * h * w))
+    assert (g.pixel_a[both] == z["pixel_a"][both]).mean() >= 0.999
+    d = np.maximum(np.abs(g.pixel_a[both] % w - z["pixel_a"][both] % w),
+                   np.abs(g.pixel_a[both] // w - z["pixel_a"][both] // w))
+    assert d.max(initial=0) <= 1
+
+
+def _track_args(z):
+    h, w = (int(x) for x in z["shape"])
+    return h, w, pyoracle.MatchSet(z["pixel_a"], np.arange(h * w), z["confidence"].astype(np.float64), z["valid"])
+
+
+def _track_params():
+    p = abi.default_solve_pose_params()
+    p.max_iterations = 10
+    p.weights.distance_weight = 0.1
+    return p
+
+
+def test_oracle_reproduces_track_fixture():
+    z = load("track_48x64.npz")
+    h, w, om = _track_args(z)
+    T0 = abi.pmx_sim3()
+    T0.R[0] = T0.R[4] = T0.R[8] = 1.0
+    T0.s = 1.0
+    r = pyoracle.track_given_matches(z["canonical"], z["canonical_valid"], z["X_f_f"], z["valid_f"], h, w, om, T0,
+                                     params=_track_params())
+    assert np.array_equal(np.array(r.T_kf.t[:]), z["t"]) and r.iterations == int(z["iterations"][0])
+
+
+@pytest.mark.gpu
+def test_gpu_matches_track_fixture(ctx):
+    from paper_2412_12392_b200 import sim3
+    z = load("track_48x64.npz")
+    h, w, _ = _track_args(z)
+    r = ctx.track_given_matches(Pointmap(z["canonical"], z["canonical_valid"], h, w),
+                                Pointmap(z["X_f_f"], z["valid_f"], h, w),
+                                MatchSet(z["pixel_a"], z["confidence"], z["valid"]), sim3(), params=_track_params())
+    assert np.abs(np.array(r.T_kf.t[:]) - z["t"]).max() < 1e-5
+    R = np.array(r.T_kf.R[:]).reshape(3, 3)
+    ang = np.arccos(np.clip((np.trace(R.T @ z["R"].reshape(3, 3)) - 1) / 2, -1, 1))
+    assert ang < 1e-5 and abs(r.T_kf.s - z["s"][0]) < 1e-5
+
+
+def _graph_parts(z):
+    h, w = (int(x) for x in z["shape"])
+    n = z["init"].shape[0]
+    E = z["edges"].shape[0]
+    poses = []
+    for row in z["init"]:
+        T = abi.pmx_sim3()
+        for i in range(9):
+            T.R[i] = row[i]
+        for i in range(3):
+            T.t[i] = row[9 + i]
+        T.s = row[12]
+        poses.append(T)
+    cans = [z[f"can{k}"] for k in range(n)]
+    ms = [(z[f"pa{e}"], z[f"q{e}"], z[f"v{e}"]) for e in range(E)]
+    return h, w, poses, cans, [tuple(e) for e in z["edges"]], ms
+
+
+def test_oracle_reproduces_backend_fixture():
+    z = load("backend_6kf_24x32.npz")
+    h, w, poses, cans, edges, ms = _graph_parts(z)
+    O = pyoracle.Graph([(c, None) for c in cans], poses, edges,
+                       [pyoracle.MatchSet(pa, np.arange(h * w), q.astype(np.float64), v) for pa, q, v in ms], h, w)
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    res, _ = pyoracle.global_optimize(O, p)
+    final = np.array([list(T.R) + list(T.t) + [T.s] for T in O.poses])
+    assert np.array_equal(final, z["final"]) and res.iterations == int(z["iterations"][0])
+
+
+@pytest.mark.gpu
+def test_gpu_matches_backend_fixture(ctx):
+    z = load("backend_6kf_24x32.npz")
+    h, w, poses, cans, edges, ms = _graph_parts(z)
+    G = Graph([Pointmap(c, None, h, w) for c in cans], poses, edges, [MatchSet(pa, q, v) for pa, q, v in ms])
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    r = ctx.global_optimize(G, p)
+    final = np.array([list(T.R) + list(T.t) + [T.s] for T in G.poses])
+    assert np.abs(final[:, 9:12] - z["final"][:, 9:12]).max() < 1e-5
+    assert np.abs(final[:, :9] - z["final"][:, :9]).max() < 1e-5
+    assert r.converged == bool(z["converged"][0])
