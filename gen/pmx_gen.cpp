@@ -84,6 +84,7 @@ struct Scene {
   int H, W, dim;
   double point_sigma, desc_sigma;
   int noise_mode;  // 0 = radial in the view's own frame (reference synth.cpp:221-226), 1 = isotropic
+  int surface;     // 0 = depth map of the reference camera (config 0/1), 1 = world heightfield (configs 2-4)
 };
 
 inline double surf(const Scene& s, double x, double y, double* zx, double* zy) {
@@ -94,8 +95,42 @@ inline double surf(const Scene& s, double x, double y, double* zx, double* zy) {
   return 2.0 + 0.3 * sx * cy + s.a * x + s.b * y;
 }
 
+// World heightfield Z = h(X, Y) (configs 2-4): the config-0 relief in
+// coordinates normalised at the nominal depth 2, a proper graph everywhere.
+inline double height(const Scene& s, double X, double Y, double* hx, double* hy) {
+  const double x = 0.5 * X, y = 0.5 * Y;
+  const double sx = std::sin(3 * x), cx = std::cos(3 * x), sy = std::sin(2 * y), cy = std::cos(2 * y);
+  if (hx) *hx = 0.5 * (0.9 * cx * cy + s.a);
+  if (hy) *hy = 0.5 * (-0.6 * sx * sy + s.b);
+  return 2.0 + 0.3 * sx * cy + s.a * x + s.b * y;
+}
+
+bool cast_heightfield(const Scene& s, const double o[3], const double d[3], double P[3], double* px, double* py) {
+  if (!(d[2] > 1e-9)) return false;
+  double lam = (2.0 - o[2]) / d[2];
+  for (int it = 0; it < 50; ++it) {
+    double hx, hy;
+    const double X = o[0] + lam * d[0], Y = o[1] + lam * d[1];
+    const double F = o[2] + lam * d[2] - height(s, X, Y, &hx, &hy);
+    const double dF = d[2] - hx * d[0] - hy * d[1];
+    if (std::abs(dF) < 1e-12) return false;
+    const double step = F / dF;
+    lam -= step;
+    if (std::abs(step) < 1e-14 * (1.0 + std::abs(lam))) break;
+  }
+  P[0] = o[0] + lam * d[0];
+  P[1] = o[1] + lam * d[1];
+  P[2] = o[2] + lam * d[2];
+  const double F = P[2] - height(s, P[0], P[1], nullptr, nullptr);
+  if (!(std::abs(F) < 1e-9) || !(lam > 0)) return false;
+  *px = P[0] / P[2];
+  *py = P[1] / P[2];
+  return true;
+}
+
 // Ray cast o + lambda d into the surface.  Returns false when Newton fails.
 bool cast(const Scene& s, const double o[3], const double d[3], double P[3], double* px, double* py) {
+  if (s.surface == 1) return cast_heightfield(s, o, d, P, px, py);
   // Initial guess: plane Z = 2.
   if (std::abs(d[2]) < 1e-9) return false;
   double lam = (2.0 - o[2]) / d[2];
@@ -220,6 +255,7 @@ Scene to_scene(const double* p) {
   s.point_sigma = p[9];
   s.desc_sigma = p[10];
   s.noise_mode = (int)p[11];
+  s.surface = (int)p[12];
   return s;
 }
 

@@ -133,12 +133,13 @@ class Scene:
     coordinate (a rough ray field; an adversarial parity case)."""
 
     def __init__(self, seed: int, height=H, width=W, f=F, cx=CX, cy=CY, dim=DIM,
-                 point_sigma=0.005, desc_sigma=0.05, noise="radial"):
+                 point_sigma=0.005, desc_sigma=0.05, noise="radial", surface="depthmap"):
         ab = uniform(seed, 7, 2) * 0.4 - 0.2
         self.seed, self.height, self.width, self.dim = seed, height, width, dim
         self.f, self.cx, self.cy = f, cx, cy
         self.params = np.array([seed, ab[0], ab[1], f, cx, cy, height, width, dim,
-                                point_sigma, desc_sigma, 0 if noise == "radial" else 1],
+                                point_sigma, desc_sigma, 0 if noise == "radial" else 1,
+                                0 if surface == "depthmap" else 1],
                                dtype=np.float64)
 
     def image(self, image_id: int, T_wk: Pose, T_frame: Pose, salt: int = 0,
@@ -241,7 +242,7 @@ def edges_config2(seed: int = 2, n_kf: int = 32, n_consecutive: int = 28, n_long
         edges.append((k, k + 1))
         edges.append((k + 1, k))
     poses = poses or trajectory_config2(seed, n_kf)
-    sc = scene or Scene(seed, 48, 64, f=F * 64 / W, cx=CX * 64 / W, cy=CY * 48 / H)
+    sc = scene or Scene(seed, 48, 64, f=F * 64 / W, cx=CX * 64 / W, cy=CY * 48 / H, surface="heightfield")
     u = uniform(seed, 400, 4096)
     k = 0
     longs = []
@@ -296,7 +297,7 @@ def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: in
     """Configs 3/4: GT loop poses, canonical pointmaps (own view + noise),
     edges with ground-truth matches (pixel_a in i, pixel_b in j, dense), and
     perturbed initial poses (anchor = keyframe 0, unperturbed)."""
-    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H, surface="heightfield")
     gt = loop_trajectory(n_kf, radius, loops, seed)
     cams = [Camera(sc, k, gt[k]) for k in range(n_kf)]
     canon = [(c.express(c.T, 1000 + k), c.valid) for k, c in enumerate(cams)]
@@ -349,7 +350,7 @@ def pair_from_cameras(ca: Camera, cb: Camera, salt: int):
 def config2(seed: int = 2, height=H, width=W, n_kf: int = 32, edges=None):
     """BASELINE config 2: 32 keyframes on a smooth trajectory, 64 directed edges.
     Returns (scene, cameras, edges, make_pair(e))."""
-    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H)
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H, surface="heightfield")
     poses = trajectory_config2(seed, n_kf)
     edges = edges if edges is not None else edges_config2(seed, n_kf, poses=poses)
     cams = {}
