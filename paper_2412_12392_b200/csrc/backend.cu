@@ -85,6 +85,180 @@ __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ray mode, closed form (the hot path).  For x = T X_src, d = |x|, n = x/d,
+// P = I - n n^T and the rows J_ray = [-P/d, [x]x/d, 0], J_d = [-n^T, 0, -d]
+// of tracking.cpp:82-87, the per-match normal equations collapse to
+//   H_tt = (w/d^2) I + (w_d - w/d^2) n n^T     H_tw = -[(w/d) n]x
+//   H_ww = w I - w n n^T                         H_ts = w_d d n,  H_ss = w_d d^2
+//   g_t  = -(w/d)(r - n (n.r)) - w_d r_d n      g_w = -w (n x r),  g_s = -w_d d r_d
+// so one direction needs 29 running sums instead of 28+7 per row of J:
+//   0 sum(w/d^2)  1 sum(w)  2-7 sum(beta n n^T)  8-13 sum(w n n^T)
+//   14-16 sum((w/d) n)  17-19 sum(w_d d n)  20 sum(w_d d^2)  21-27 g  28 cost
+constexpr int kRayAcc = 29;
+
+struct RayDir {  // per-direction pose in fp32 (s R, t)
+  float sR[9];
+  float t[3];
+};
+
+__device__ __forceinline__ float rsqrt_nr(float a) {  // ~0.5 ulp reciprocal square root
+  const float y = rsqrtf(a);
+  return y * fmaf(-0.5f * a * y, y, 1.5f);
+}
+
+__device__ __forceinline__ void ray_accumulate(const PoseR<float>& T, const float* ref, const float* src,
+                                               float info, const WeightsDev& wp, float* acc) {
+  const float x0 = fmaf(T.sR[0], src[0], fmaf(T.sR[1], src[1], fmaf(T.sR[2], src[2], T.t[0])));
+  const float x1 = fmaf(T.sR[3], src[0], fmaf(T.sR[4], src[1], fmaf(T.sR[5], src[2], T.t[1])));
+  const float x2 = fmaf(T.sR[6], src[0], fmaf(T.sR[7], src[1], fmaf(T.sR[8], src[2], T.t[2])));
+  const float dd = x0 * x0 + x1 * x1 + x2 * x2;
+  const float rr = ref[0] * ref[0] + ref[1] * ref[1] + ref[2] * ref[2];
+  if (!(dd >= 1e-24f) || !(rr >= 1e-24f)) return;  // d, d_ref < 1e-12 (tracking.cpp:71, 78)
+  const float id = rsqrt_nr(dd), ir = rsqrt_nr(rr);
+  const float d = dd * id, dref = rr * ir;
+  const float n0 = x0 * id, n1 = x1 * id, n2 = x2 * id;
+  const float r0 = ref[0] * ir - n0, r1 = ref[1] * ir - n1, r2 = ref[2] * ir - n2;
+  const float rd = dref - d;
+  const float delta = (float)wp.huber_delta;
+  const float sq = r0 * r0 + r1 * r1 + r2 * r2;
+  const float e = sqrtf(info) * sqrtf(sq);
+  const float info_d = (float)wp.distance_weight * info;
+  const float e_d = sqrtf(info_d) * fabsf(rd);
+  const float w = info * (e <= delta ? 1.0f : delta / e);
+  const float wd = info_d * (e_d <= delta ? 1.0f : delta / e_d);
+  acc[28] += (e <= delta ? 0.5f * e * e : delta * (e - 0.5f * delta)) +
+             (e_d <= delta ? 0.5f * e_d * e_d : delta * (e_d - 0.5f * delta));
+  const float nr = n0 * r0 + n1 * r1 + n2 * r2;
+  if (w > 0.0f) {  // tracking.cpp:193-194: rows with w <= 0 are skipped
+    const float a = w * id * id, wi = w * id;
+    acc[0] += a;
+    acc[1] += w;
+    acc[8] += w * n0 * n0;
+    acc[9] += w * n0 * n1;
+    acc[10] += w * n0 * n2;
+    acc[11] += w * n1 * n1;
+    acc[12] += w * n1 * n2;
+    acc[13] += w * n2 * n2;
+    acc[14] += wi * n0;
+    acc[15] += wi * n1;
+    acc[16] += wi * n2;
+    acc[2] -= a * n0 * n0;
+    acc[3] -= a * n0 * n1;
+    acc[4] -= a * n0 * n2;
+    acc[5] -= a * n1 * n1;
+    acc[6] -= a * n1 * n2;
+    acc[7] -= a * n2 * n2;
+    acc[21] -= wi * (r0 - n0 * nr);
+    acc[22] -= wi * (r1 - n1 * nr);
+    acc[23] -= wi * (r2 - n2 * nr);
+    acc[24] -= w * (n1 * r2 - n2 * r1);
+    acc[25] -= w * (n2 * r0 - n0 * r2);
+    acc[26] -= w * (n0 * r1 - n1 * r0);
+  }
+  if (wd > 0.0f) {
+    const float wdd = wd * d;
+    acc[2] += wd * n0 * n0;
+    acc[3] += wd * n0 * n1;
+    acc[4] += wd * n0 * n2;
+    acc[5] += wd * n1 * n1;
+    acc[6] += wd * n1 * n2;
+    acc[7] += wd * n2 * n2;
+    acc[17] += wdd * n0;
+    acc[18] += wdd * n1;
+    acc[19] += wdd * n2;
+    acc[20] += wdd * d;
+    acc[21] -= wd * rd * n0;
+    acc[22] -= wd * rd * n1;
+    acc[23] -= wd * rd * n2;
+    acc[27] -= wdd * rd;
+  }
+}
+
+template <int N>
+__device__ inline void block_reduce_n(const float* acc, double* __restrict__ out_row) {
+  __shared__ double sh[8][N];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll 1
+  for (int i = 0; i < N; ++i) {
+    const double v = warp_sum((double)acc[i]);
+    if (lane == 0) sh[warp][i] = v;
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += sh[w][i];
+    out_row[i] = s;
+  }
+  __syncthreads();
+}
+
+// Both directed constraints of an edge from one read of every match.
+__global__ void __launch_bounds__(256, 3) k_edge_terms_ray(EdgeArgs A, int e0) {
+  const int e = e0 + blockIdx.y;
+  const int b = blockIdx.x;
+  const int2 ij = A.edges[e];
+  const MatchesDev M = A.matches[e];
+  float acc[2 * kRayAcc];
+#pragma unroll
+  for (int i = 0; i < 2 * kRayAcc; ++i) acc[i] = 0.0f;
+  if (ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N) {
+    const CloudDev Xi = A.clouds[ij.x], Xj = A.clouds[ij.y];
+    const PoseR<float> T1 = A.rel[2 * e], T2 = A.rel[2 * e + 1];
+    const double q_min = A.qmin[e];
+    const float inv_s2 = (float)(1.0 / A.wp.sigma2);
+    const int64_t stride = (int64_t)A.bpe * blockDim.x;
+    const int hwi = Xi.H * Xi.W, hwj = Xj.H * Xj.W;
+    for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < M.count; k += stride) {
+      const int pa = __ldg(M.pa + k);
+      const int pb = M.pb ? __ldg(M.pb + k) : (int)k;
+      if ((M.valid && !__ldg(M.valid + k)) || pa < 0 || pb < 0 || pa >= hwi || pb >= hwj) continue;
+      float pi[3], pj[3];
+      if (!load_point(Xi, pa, pi) || !load_point(Xj, pb, pj)) continue;  // tracking.cpp:62
+      const float q = __ldg(M.q + k);
+      if (!((double)q > q_min)) continue;  // robust_weight (tracking.cpp:10-13)
+      const float info = q * inv_s2;
+      ray_accumulate(T1, pi, pj, info, A.wp, acc);             // ref = i, src = j (swapped)
+      ray_accumulate(T2, pj, pi, info, A.wp, acc + kRayAcc);   // ref = j, src = i
+    }
+  }
+  block_reduce_n<2 * kRayAcc>(acc, A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
+}
+
+// Sum the closed-form partials of an edge and expand to {H 28, g 7, cost} x 2.
+__global__ void k_edge_sum_ray(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ terms) {
+  const int e = e0 + blockIdx.x;
+  __shared__ double s[2 * kRayAcc];
+  for (int t = threadIdx.x; t < 2 * kRayAcc; t += blockDim.x) {
+    double a = 0.0;
+    for (int b = 0; b < bpe; ++b) a += partials[((size_t)e * bpe + b) * (2 * kRayAcc) + t];
+    s[t] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x >= 2) return;
+  const double* c = s + kRayAcc * threadIdx.x;
+  double H[7][7] = {};
+  const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      H[i][j] = (i == j ? c[0] : 0.0) + c[2 + sym[i][j]];
+      H[3 + i][3 + j] = (i == j ? c[1] : 0.0) - c[8 + sym[i][j]];
+    }
+  const double v0 = c[14], v1 = c[15], v2 = c[16];  // H_tw = -[v]x
+  const double S[3][3] = {{0, -v2, v1}, {v2, 0, -v0}, {-v1, v0, 0}};
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) H[i][3 + j] = -S[i][j];
+  for (int i = 0; i < 3; ++i) H[i][6] = c[17 + i];
+  H[6][6] = c[20];
+  double* out = terms + (size_t)e * PMX_EDGE_TERMS + 36 * threadIdx.x;
+  int idx = 0;
+  for (int a = 0; a < 7; ++a)
+    for (int b = a; b < 7; ++b) out[idx++] = H[a][b];
+  for (int a = 0; a < 7; ++a) out[28 + a] = c[21 + a];
+  out[35] = c[28];
+}
+
 // terms[e] = {H1 (28), g1 (7), cost1, H2 (28), g2 (7), cost2}
 __global__ void k_edge_sum(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ terms) {
   const int e = e0 + blockIdx.x;
@@ -346,6 +520,153 @@ __global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
   }
 }
 
+// ------------------------------------------------------- K9, envelope form
+// The gauge-fixed system is block-sparse (edges) and LDL^T in natural order
+// fills in only inside the envelope [first[i], i] of every row i.  Panel p
+// (NB columns) updates only the rows whose envelope reaches into it
+// (R_p = {i >= p_end : first[i] < p_end}, precomputed on the host), so a
+// banded graph with a few loop closures costs O(n (b + border)^2) instead of
+// O(n^3).  Same factorisation as the dense path (no pivoting, exact-zero
+// pivot -> failure); zero blocks are skipped, fill-in can only appear where
+// the dense algorithm would write it.  One CTA of 1024 threads.
+constexpr int kEnvRows = 320;  // max active rows per panel held in shared memory
+
+struct EnvArgs {
+  double* A;         // work matrix (n x n row-major; envelope entries valid)
+  int n;
+  const int* first;  // first[i]: first column of row i's envelope
+  const int* rp_ptr; // panel p: active rows rp_rows[rp_ptr[p] .. rp_ptr[p+1])
+  const int* rp_rows;
+  const double* b;
+  double* x;
+  int* status;
+};
+
+__global__ void k_env_copy(const double* __restrict__ H, double* __restrict__ A, int n, const int* __restrict__ first,
+                           double lambda) {
+  const int i = blockIdx.x;
+  for (int j = first[i] + (int)threadIdx.x; j <= i; j += blockDim.x)
+    A[(size_t)i * n + j] = H[(size_t)i * n + j] + (i == j ? lambda : 0.0);
+}
+
+__global__ void __launch_bounds__(1024) k_ldlt_env(EnvArgs P) {
+  extern __shared__ double smem[];
+  double(*sD)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(smem);
+  double* sW = smem + NB * (NB + 1);  // [kEnvRows][NB]
+  double* sL = sW + kEnvRows * NB;    // [kEnvRows][NB]
+  const int n = P.n;
+  double* A = P.A;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
+  if (tid == 0) *P.status = 1;
+  const int npanel = (n + NB - 1) / NB;
+  for (int pi = 0; pi < npanel; ++pi) {
+    const int p = pi * NB, nb = min(NB, n - p);
+    // (a) diagonal block
+    for (int i = tid; i < nb * nb; i += nth) {
+      const int r = i / nb, c = i % nb;
+      sD[r][c] = (c <= r && c + p >= P.first[p + r]) ? A[(size_t)(p + r) * n + p + c] : 0.0;
+    }
+    __syncthreads();
+    for (int c = 0; c < nb; ++c) {
+      const double d = sD[c][c];
+      if (tid == 0 && d == 0.0) *P.status = 0;  // SimplicialLDLT: exact zero pivot fails
+      const int m = nb - c - 1;
+      for (int i = tid; i < m * m; i += nth) {
+        const int r = c + 1 + i / m, s = c + 1 + i % m;
+        if (s <= r) sD[r][s] -= sD[r][c] * sD[s][c] / d;
+      }
+      __syncthreads();
+      for (int r = c + 1 + tid; r < nb; r += nth) sD[r][c] /= d;
+      __syncthreads();
+    }
+    for (int i = tid; i < nb * nb; i += nth) {
+      const int r = i / nb, c = i % nb;
+      if (c <= r && c + p >= P.first[p + r]) A[(size_t)(p + r) * n + p + c] = sD[r][c];
+    }
+    // (b) panel rows: W = A_R,panel L11^-T (one warp per row), L21 = W / D
+    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
+    for (int q = warp; q < ns; q += nth / 32) {
+      const int i = P.rp_rows[r0 + q];
+      double a = (lane < nb && p + lane >= P.first[i]) ? A[(size_t)i * n + p + lane] : 0.0;
+      for (int m = 0; m < nb; ++m) {
+        const double wm = __shfl_sync(0xffffffffu, a, m);
+        if (lane > m && lane < nb) a -= wm * sD[lane][m];
+      }
+      if (lane < nb) {
+        const double l = a / sD[lane][lane];
+        sW[q * NB + lane] = a;
+        sL[q * NB + lane] = l;
+        A[(size_t)i * n + p + lane] = l;
+      }
+    }
+    __syncthreads();
+    // (c) trailing update over active pairs (j <= i, inside row i's envelope)
+    const int npair = ns * (ns + 1) / 2;
+    for (int t = tid; t < npair; t += nth) {
+      int qi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      while ((qi + 1) * (qi + 2) / 2 <= t) ++qi;
+      while (qi * (qi + 1) / 2 > t) --qi;
+      const int qj = t - qi * (qi + 1) / 2;
+      const int i = P.rp_rows[r0 + qi], j = P.rp_rows[r0 + qj];
+      if (j < P.first[i]) continue;
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += sW[qi * NB + k] * sL[qj * NB + k];
+      A[(size_t)i * n + j] -= s;
+    }
+    __syncthreads();
+  }
+  // forward: L y = b
+  for (int i = tid; i < n; i += nth) P.x[i] = P.b[i];
+  __syncthreads();
+  for (int pi = 0; pi < npanel; ++pi) {
+    const int p = pi * NB, nb = min(NB, n - p);
+    if (warp == 0) {
+      double y = lane < nb ? P.x[p + lane] : 0.0;
+      for (int m = 0; m < nb; ++m) {
+        const double ym = __shfl_sync(0xffffffffu, y, m);
+        if (lane > m && lane < nb && p + m >= P.first[p + lane]) y -= A[(size_t)(p + lane) * n + p + m] * ym;
+      }
+      if (lane < nb) P.x[p + lane] = y;
+    }
+    __syncthreads();
+    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
+    for (int q = tid; q < ns; q += nth) {
+      const int i = P.rp_rows[r0 + q];
+      double s = 0.0;
+      for (int k = max(0, P.first[i] - p); k < nb; ++k) s += A[(size_t)i * n + p + k] * P.x[p + k];
+      P.x[i] -= s;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n; i += nth) P.x[i] /= A[(size_t)i * n + i];
+  __syncthreads();
+  // backward: L^T x = z
+  for (int pi = npanel - 1; pi >= 0; --pi) {
+    const int p = pi * NB, nb = min(NB, n - p);
+    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
+    if (warp < nb) {
+      const int k = p + warp;
+      double s = 0.0;
+      for (int q = lane; q < ns; q += 32) {
+        const int i = P.rp_rows[r0 + q];
+        if (k >= P.first[i]) s += A[(size_t)i * n + k] * P.x[i];
+      }
+      s = warp_sum(s);
+      if (lane == 0) P.x[k] -= s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double xv = lane < nb ? P.x[p + lane] : 0.0;
+      for (int m = nb - 1; m >= 0; --m) {
+        const double xm = __shfl_sync(0xffffffffu, xv, m);
+        if (lane < m && p + lane >= P.first[p + m]) xv -= A[(size_t)(p + m) * n + p + lane] * xm;
+      }
+      if (lane < nb) P.x[p + lane] = xv;
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------------ host
 struct DevGraph {
   int N = 0, E = 0, anchor = -1;
@@ -455,14 +776,25 @@ static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, c
   A.N = G.N;
   A.bpe = bpe;
   A.partials = partials.as<double>();
+  const bool ray = p.mode == PMX_TRACK_RAY;
+  if (ray) {  // closed-form partials are 2 x 29 per block
+    partials = DevBuf(sizeof(double) * (size_t)G.E * bpe * 2 * kRayAcc, ctx.stream);
+    A.partials = partials.as<double>();
+  }
   for (int c0 = e0; c0 < e1; c0 += 65535) {
     const int cn = std::min(65535, e1 - c0);
     {
       ProfScope ps(ctx, "k_edge_terms");
-      k_edge_terms<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+      if (ray)
+        k_edge_terms_ray<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+      else
+        k_edge_terms<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
     }
     launch_check(ctx, "k_edge_terms");
-    k_edge_sum<<<cn, 128, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
+    if (ray)
+      k_edge_sum_ray<<<cn, 64, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
+    else
+      k_edge_sum<<<cn, 128, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
     launch_check(ctx, "k_edge_sum");
   }
   PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // rel host vector lifetime
@@ -472,6 +804,9 @@ struct Assembly {
   int dim = 0;
   DevBuf blk_rc, blk_ptr, contrib, g_ptr, g_contrib, adj, S, G, H, grad;
   int nblocks = 0;
+  // envelope structure for k_ldlt_env (env_ok = every panel fits in shared memory)
+  bool env_ok = false;
+  DevBuf first, rp_ptr, rp_rows;
 };
 
 // Contribution lists (edge order) for every non-zero block, gauge-fixed.
@@ -514,7 +849,32 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
   up(As.contrib, con);
   up(As.g_ptr, gp);
   up(As.g_contrib, gc);
-  As.adj = DevBuf(sizeof(double) * 49 * std::max(N, 1), ctx.stream);
+  {  // envelope of the gauge-fixed system: first non-zero block column of every block row
+    std::vector<int> fb(N);
+    for (int k = 0; k < N; ++k) fb[k] = k;
+    for (auto& kv : blocks)
+      if (kv.first.second <= kv.first.first) fb[kv.first.first] = std::min(fb[kv.first.first], kv.first.second);
+    std::vector<int> first(7 * N), rptr{0}, rrows;
+    for (int k = 0; k < N; ++k)
+      for (int r = 0; r < 7; ++r) first[7 * k + r] = 7 * fb[k];
+    const int n = 7 * N, npanel = (n + NB - 1) / NB;
+    bool fits = true;
+    for (int pi = 0; pi < npanel && fits; ++pi) {
+      const int pend = std::min(n, (pi + 1) * NB);
+      for (int i = pend; i < n; ++i)
+        if (first[i] < pend) rrows.push_back(i);
+      if ((int)rrows.size() - rptr.back() > kEnvRows) fits = false;
+      rptr.push_back((int)rrows.size());
+    }
+    As.env_ok = fits && N > 0;
+    if (As.env_ok) {
+      up(As.first, first);
+      up(As.rp_ptr, rptr);
+      up(As.rp_rows, rrows);
+      PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+  }
+  As.adj =DevBuf(sizeof(double) * 49 * std::max(N, 1), ctx.stream);
   As.S = DevBuf(sizeof(double) * 49 * std::max(G.E, 1), ctx.stream);
   As.G = DevBuf(sizeof(double) * 7 * std::max(G.E, 1), ctx.stream);
   As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);
@@ -554,22 +914,36 @@ __global__ void k_negate(const double* a, double* b, int n) {
 // Damped solve attempts (backend.cpp:208-230).  Returns solved; tau on host.
 static bool damped_solve(Context& ctx, const pmx_backend_params& p, Assembly& As, std::vector<double>& tau) {
   const int n = As.dim;
-  DevBuf work(sizeof(double) * (size_t)n * n, ctx.stream), W(sizeof(double) * (size_t)n * NB, ctx.stream),
-      rhs(sizeof(double) * n, ctx.stream), x(sizeof(double) * n, ctx.stream), status(sizeof(int), ctx.stream);
+  DevBuf work(sizeof(double) * (size_t)n * n, ctx.stream), rhs(sizeof(double) * n, ctx.stream),
+      x(sizeof(double) * n, ctx.stream), status(sizeof(int), ctx.stream), W;
   k_negate<<<(n + 255) / 256, 256, 0, ctx.stream>>>(As.grad.as<double>(), rhs.as<double>(), n);
   launch_check(ctx, "k_negate");
-  int per_sm = 0;
-  PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
-  const int nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  int nb = 0;
+  const size_t env_smem = sizeof(double) * (NB * (NB + 1) + 2 * kEnvRows * NB);
+  if (As.env_ok) {
+    PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_env, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env_smem));
+  } else {
+    W = DevBuf(sizeof(double) * (size_t)n * NB, ctx.stream);
+    int per_sm = 0;
+    PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
+    nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
+  }
   double lambda = 0.0;
   tau.assign(n, 0.0);
   for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
-    LdltArgs L{work.as<double>(), As.H.as<double>(), lambda, rhs.as<double>(), x.as<double>(), W.as<double>(), n,
-               status.as<int>()};
-    void* args[] = {&L};
     {
       ProfScope ps(ctx, "k_ldlt");
-      PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
+      if (As.env_ok) {
+        k_env_copy<<<n, 128, 0, ctx.stream>>>(As.H.as<double>(), work.as<double>(), n, As.first.as<int>(), lambda);
+        EnvArgs E{work.as<double>(), n, As.first.as<int>(), As.rp_ptr.as<int>(), As.rp_rows.as<int>(),
+                  rhs.as<double>(), x.as<double>(), status.as<int>()};
+        k_ldlt_env<<<1, 1024, env_smem, ctx.stream>>>(E);
+      } else {
+        LdltArgs L{work.as<double>(), As.H.as<double>(), lambda, rhs.as<double>(), x.as<double>(), W.as<double>(), n,
+                   status.as<int>()};
+        void* args[] = {&L};
+        PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
+      }
     }
     launch_check(ctx, "k_ldlt");
     int ok = 0;
