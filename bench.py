@@ -64,7 +64,7 @@ class ClockSampler:
              "clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100", "-i", str(gpu)], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20", "-i", str(gpu)], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -139,6 +139,126 @@ def run_reference(args):
                              "sample": f"{sample_edges} edges x {H}x{W} px per step, {threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def bench_backend(ctx, dev, cpu: bool):
+    """BASELINE config 3: N=100 keyframes, 400 edges, 10 GN iterations,
+    ray mode, lambda_d 0.1 -> ms per global GN iteration (lower is better)."""
+    import torch
+    import pmxgen
+    from paper_2412_12392_b200 import Graph, MatchSet, Pointmap, abi
+    g = pmxgen.backend_graph(100, 4, 3)
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    cans = [Pointmap(T(x), T(v), H, W) for x, v in g["canonicals"]]
+    ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["matches"]]
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    p.max_iterations = 10
+    init = [P.to_struct(abi.pmx_sim3) for P in g["init"]]
+    nmatch = sum(int(m["valid"].size) for m in g["matches"])
+    for _ in range(2):  # warm-up
+        ctx.global_optimize(Graph(cans, list(init), g["edges"], ms), p)
+    runs = []
+    for _ in range(3):
+        G = Graph(cans, list(init), g["edges"], ms)
+        ctx.profile_enable(True)
+        ctx.profile_reset()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = ctx.global_optimize(G, p)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        et, en = ctx.profile_get("k_edge_terms")
+        lt, ln = ctx.profile_get("k_ldlt")
+        ctx.profile_enable(False)
+        runs.append((dt * 1e3 / max(1, r.iterations), dt, r, et, en, lt, ln, G))
+    best = min(runs, key=lambda x: x[0])
+    ms_it, dt, r, et, en, lt, ln, G = best
+    err0 = max(float(np.abs(P.t - Q.t).max()) for P, Q in zip(g["init"], g["gt"]))
+    err = max(float(np.abs(np.array(P.t[:]) - Q.t).max()) for P, Q in zip(G.poses, g["gt"]))
+    peaks, peak_kind = _peaks()
+    acc_ms = et / max(1, en)
+    achieved = 32.0 * nmatch / (acc_ms * 1e-3) / 1e9
+    out = {"metric": "global GN iteration ms at N=100", "value": ms_it, "unit": "ms", "higher_is_better": False,
+           "config": {"workload": "config3: 100 keyframes, radius-5 m loop, 400 bidirectional edges (k<->k+1..k+4), "
+                                  "512x384, 10 GN iterations, ray mode, lambda_d 0.1",
+                      "iterations_run": r.iterations, "converged": r.converged,
+                      "max_translation_error_m": {"init": err0, "final": err}},
+           "breakdown_ms_per_iteration": {"accumulate_k_edge_terms": acc_ms, "solve_k_ldlt": lt / max(1, ln),
+                                          "other_assembly_host": ms_it - acc_ms - lt / max(1, ln)},
+           "roofline": {"bound": "hbm", "kernel": "k_edge_terms", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                        "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                        "alg_bytes_per_match": 32, "matches_per_launch": nmatch, "peak_kind": peak_kind}}
+    if cpu:
+        import pyoracle
+        O = pyoracle.Graph(g["canonicals"], init, g["edges"],
+                           [pyoracle.MatchSet(m["pixel_a"], np.arange(H * W), m["confidence"].astype(np.float64),
+                                              m["valid"]) for m in g["matches"]], H, W)
+        k = 4
+        t0 = time.perf_counter()
+        pyoracle.backend_edge_terms(O, p, 0, k, threads=1)
+        per_edge = (time.perf_counter() - t0) / k
+        # the reference evaluates every edge twice per iteration (assemble_system + backend_cost)
+        out["cpu_baseline"] = {"value": 2 * per_edge * len(g["edges"]) * 1e3, "unit": "ms", "cores": 1, "kind": "port",
+                               "sample": f"{k} of 400 edges timed (FP64 oracle, 1 thread), extrapolated x400 edges "
+                                         "x2 residual passes per iteration"}
+    return out
+
+
+def bench_tracking(ctx, dev):
+    """BASELINE config 1: 10 GN iterations on one Sim(3) over 196,608 matches
+    (10% outliers) + confidence-weighted fusion."""
+    import torch
+    import pmxgen
+    import pyoracle  # matching for the setup only (not timed)
+    from paper_2412_12392_b200 import MatchSet, Pointmap, abi, sim3
+    c = pmxgen.config1(seed=1)
+    pair = {"X_a": c["X_f_f"], "valid_a": c["valid_f"], "Q_a": c["C_f"], "D_a": c["D_f"],
+            "X_b": c["X_k_f"], "valid_b": c["valid_k"], "Q_b": c["C_k"], "D_b": c["D_k"], "height": H, "width": W}
+    mp, rp = match_params()
+    from paper_2412_12392_b200 import FeatureMap
+    Tt = lambda x: torch.from_numpy(np.ascontiguousarray(x.view(np.int16) if x.dtype == np.uint16 else x)).to(dev)
+    m = ctx.match_batch([(Pointmap(Tt(pair["X_a"]), Tt(pair["valid_a"]), H, W),
+                          Pointmap(Tt(pair["X_b"]), Tt(pair["valid_b"]), H, W),
+                          FeatureMap(Tt(pair["D_a"]), Tt(pair["Q_a"]), H, W),
+                          FeatureMap(Tt(pair["D_b"]), Tt(pair["Q_b"]), H, W))], params=mp, refine=rp)[0]
+    pa, v = pmxgen.inject_outliers(m.pixel_a.cpu().numpy(), m.valid.cpu().numpy(), 0.1, 1, H * W)
+    q = np.sqrt(c["C_f"][np.clip(pa, 0, None)].astype(np.float64) * c["C_k"].astype(np.float64)).astype(np.float32)
+    M = MatchSet(Tt(pa), Tt(q), Tt(v))
+    can = Pointmap(Tt(c["canonical"]), Tt(c["canonical_valid"]), H, W)
+    src = Pointmap(Tt(c["X_f_f"]), Tt(c["valid_f"]), H, W)
+    p = abi.default_solve_pose_params()
+    p.max_iterations = 10
+    p.weights.distance_weight = 0.1
+    for _ in range(3):
+        r = ctx.track_given_matches(can, src, M, sim3(), params=p)
+    ts = []
+    for _ in range(5):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = ctx.track_given_matches(can, src, M, sim3(), params=p)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    cx, cv, cc = Tt(c["canonical"]).clone(), Tt(c["canonical_valid"]).clone(), Tt(c["canonical_conf"]).clone()
+    kf = Pointmap(Tt(c["X_k_f"]), Tt(c["valid_k"]), H, W)
+    conf = Tt(c["C_k"])
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ctx.fuse_canonical(cx, cv, cc, kf, conf, r.T_kf, H, W)
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(10):
+        ctx.fuse_canonical(cx, cv, cc, kf, conf, r.T_kf, H, W)
+    ev[1].record()
+    torch.cuda.synchronize()
+    fuse_ms = ev[0].elapsed_time(ev[1]) / 10
+    Ttrue = c["T_kf"]
+    return {"metric": "tracking GN (10 it) + fusion ms per frame", "value": min(ts) + fuse_ms, "unit": "ms",
+            "higher_is_better": False,
+            "config": {"workload": "config1: 512x384 frame vs keyframe, 10% outlier matches, 10 GN iterations, "
+                                   "lambda_d 0.1, then fusion", "iterations_run": r.iterations, "lost": r.lost,
+                       "translation_error_m": float(np.abs(np.array(r.T_kf.t[:]) - Ttrue.t).max())},
+            "breakdown_ms": {"track_gn_k_track_gn_call": min(ts), "fusion_k_fuse": fuse_ms},
+            "fusion_roofline": {"bound": "hbm", "achieved": 48.0 * H * W / (fuse_ms * 1e-3) / 1e9, "unit": "GB/s",
+                                "alg_bytes_per_px": 48}}
 
 
 def run_pmx(args):
@@ -265,6 +385,8 @@ def run_pmx(args):
             "gpu_launches": gpu_launches,
             "clocks": clocks,
         }
+        if world == 1 and not args.no_secondary:
+            line["secondary"] = [bench_backend(ctx, dev, cpu=not args.no_cpu), bench_tracking(ctx, dev)]
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -278,6 +400,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["pmx", "reference"], default="pmx")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 / config-1 secondary lines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
