@@ -219,6 +219,7 @@ int pmx_profile_reset(pmx_context* c) {
     Context& ctx = *reinterpret_cast<Context*>(c);
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     prof_clear(ctx);
+    ctx.counters.clear();
     return (int)PMX_OK;
   });
 }
@@ -237,6 +238,8 @@ int pmx_profile_get(pmx_context* c, const char* kernel, double* total_ms, int64_
       t += ms;
       ++n;
     }
+    auto it = ctx.counters.find(kernel);
+    if (it != ctx.counters.end()) n = it->second;  // counters report through `launches`
     *total_ms = t;
     *launches = n;
     return (int)PMX_OK;

@@ -21,8 +21,10 @@
 //                    argmax equals the reference's exact-arithmetic argmax
 //                    (strict '>' scan, ties keep the centre / first raster).
 #include <cfloat>
+#include <climits>
 #include <cmath>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "pmx_common.cuh"
@@ -66,8 +68,7 @@ struct PairDev {
   SelState* sel;
   // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
   // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
-  uint4* dhead;
-  float2* dnorm;
+  float4* dnorm;  // {||a||, ||a[8:24]||, ||a[16:24]||} upper bounds, .w = qa (staged with the norms)
 };
 
 struct LMParams {
@@ -97,16 +98,19 @@ __device__ __forceinline__ float fh_hi(uint32_t a, uint32_t b, float c) {
   asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(r) : "h"((unsigned short)(a >> 16)), "h"((unsigned short)(b >> 16)), "f"(c));
   return r;
 }
+// 8-term fp16 dot accumulated onto s in two independent FHFMA chains (half the
+// dependency latency); at most 8 roundings, so the n*u error bounds used
+// below stay valid for any chaining of these calls.
 __device__ __forceinline__ float dot8(const uint4& a, const uint4& b, float s) {
+  float t = fh_hi(a.x, b.x, 0.0f);
   s = fh_lo(a.x, b.x, s);
-  s = fh_hi(a.x, b.x, s);
+  t = fh_hi(a.y, b.y, t);
   s = fh_lo(a.y, b.y, s);
-  s = fh_hi(a.y, b.y, s);
+  t = fh_hi(a.z, b.z, t);
   s = fh_lo(a.z, b.z, s);
-  s = fh_hi(a.z, b.z, s);
+  t = fh_hi(a.w, b.w, t);
   s = fh_lo(a.w, b.w, s);
-  s = fh_hi(a.w, b.w, s);
-  return s;
+  return s + t;
 }
 constexpr float kU = 5.9604645e-08f;  // fp32 unit roundoff 2^-24
 
@@ -115,14 +119,12 @@ __device__ __forceinline__ float norm_ub(float ss, int n) {
   return sqrtf(ss * (1.0f + (n + 2) * kU)) * (1.0f + 2.0f * kU);
 }
 
-// Planar head + norm bounds of one 24-dim descriptor row.
-__device__ __forceinline__ void desc_aux(const __half* row, uint4* head, float2* nrm) {
+// Norm bounds of one 24-dim descriptor row (+ the pixel's match confidence).
+__device__ __forceinline__ void desc_aux(const __half* row, float q, float4* nrm) {
   const uint4* p = reinterpret_cast<const uint4*>(row);
   const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
-  const float hs = dot8(a, a, 0.0f);
-  const float ts = dot8(c, c, dot8(b, b, 0.0f));
-  *head = a;
-  *nrm = make_float2(norm_ub(hs + ts, 24), norm_ub(ts, 16));
+  const float s0 = dot8(a, a, 0.0f), s1 = dot8(b, b, 0.0f), s2 = dot8(c, c, 0.0f);
+  *nrm = make_float4(norm_ub(s0 + s1 + s2, 24), norm_ub(s1 + s2, 16), norm_ub(s2, 8), q);
 }
 
 // ---------------------------------------------------------------- K1
@@ -150,17 +152,17 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       atomicAdd(&sh[key >> 20], 1u);
     }
     P.keys[i] = key;
-    if (P.dhead) desc_aux(P.da + (size_t)i * 24, P.dhead + i, P.dnorm + i);
+    if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
     if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
 }
 
-__global__ void __launch_bounds__(256) k_desc_prep(const __half* __restrict__ da, int hw, uint4* dhead,
-                                                   float2* dnorm) {
+__global__ void __launch_bounds__(256) k_desc_prep(const __half* __restrict__ da, const float* __restrict__ qa,
+                                                   int hw, float4* dnorm) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < hw) desc_aux(da + (size_t)i * 24, dhead + i, dnorm + i);
+  if (i < hw) desc_aux(da + (size_t)i * 24, qa[i], dnorm + i);
 }
 
 // ---------------------------------------------------------------- K2
@@ -649,41 +651,168 @@ __device__ __forceinline__ void best_set(BestState& B, int u, int v, float f, fl
   B.known = false;
 }
 
-// Full-dot decision for one unpruned candidate (rare path).
-__device__ __noinline__ void refine_full(const PairDev& P, const __half* __restrict__ bdesc, uint4 b1, uint4 b2,
-                                         float nb, int u, int v, float hd, float na, BestState& B) {
-  const int pix = v * P.Wa + u;
-  const uint4* ap = reinterpret_cast<const uint4*>(P.da + (size_t)pix * 24);
-  const float sc = dot8(__ldg(ap + 2), b2, dot8(__ldg(ap + 1), b1, hd));
-  const float err = 24.01f * kU * na * nb;
+// Exact decision for a candidate whose full fp32 dot is within rounding of
+// the running best (rare): FP64 replay of the reference's exact sums.
+__device__ __noinline__ void refine_exact(const PairDev& P, const __half* __restrict__ bdesc, int u, int v, float sc,
+                                          float err, BestState& B) {
+  if (!B.known) {
+    B.x = dot_exact(P.da + (size_t)(B.v * P.Wa + B.u) * 24, bdesc, 24);
+    B.known = true;
+  }
+  const double ex = dot_exact(P.da + (size_t)(v * P.Wa + u) * 24, bdesc, 24);
+  if (ex > B.x) {
+    best_set(B, u, v, sc, err);
+    B.x = ex;
+    B.known = true;
+  }
+}
+
+// Where the candidates' descriptors and norm bounds come from: the block's
+// shared-memory tile (three 16-byte planes + norms, staged once, reused by ~49
+// candidates each) or global memory (incoherent tiles, standalone refine).
+struct GlobalAux {
+  const uint4* rows;  // 3 uint4 per pixel
+  const float4* norms;
+  int W;
+  __device__ __forceinline__ int at(int u, int v) const { return v * W + u; }
+  __device__ __forceinline__ uint4 d0(int i) const { return __ldg(rows + 3 * i); }
+  __device__ __forceinline__ uint4 d1(int i) const { return __ldg(rows + 3 * i + 1); }
+  __device__ __forceinline__ uint4 d2(int i) const { return __ldg(rows + 3 * i + 2); }
+  __device__ __forceinline__ float4 nrm(int i) const { return __ldg(norms + i); }
+};
+struct SmemAux {
+  const uint4 *p0, *p1, *p2;
+  const float4* n4;
+  int u0, v0, bw;
+  __device__ __forceinline__ int at(int u, int v) const { return (v - v0) * bw + (u - u0); }
+  __device__ __forceinline__ uint4 d0(int i) const { return p0[i]; }
+  __device__ __forceinline__ uint4 d1(int i) const { return p1[i]; }
+  __device__ __forceinline__ uint4 d2(int i) const { return p2[i]; }
+  __device__ __forceinline__ float4 nrm(int i) const { return n4[i]; }
+};
+
+struct BConst {  // register-resident target descriptor and its bound constants
+  uint4 b0, b1, b2;
+  float c8, t8, c16, t16, c24;
+};
+
+// Full decision for one candidate that survived the 8-dim bound against the
+// current best: 16-dim bound, then the full fp32 dot with its rounding bound,
+// then (near tie) the exact FP64 replay.
+template <class Aux>
+__device__ __forceinline__ void refine_candidate(const PairDev& P, const Aux& X, const BConst& K,
+                                                 const __half* __restrict__ bdesc, int u, int v, int i, float h8,
+                                                 float4 nr, BestState& B) {
+  const float h16 = dot8(X.d1(i), K.b1, h8);
+  const float u16 = fmaf(nr.x, K.c16, fmaf(nr.z, K.t16, h16));
+  if (fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) <= B.thr) return;
+  const float sc = dot8(X.d2(i), K.b2, h16);
+  const float err = K.c24 * nr.x;
   if (certainly_gt(sc, err, B.f, B.err)) {
     best_set(B, u, v, sc, err);
   } else if (!certainly_le(sc, err, B.f, B.err)) {
-    if (!B.known) {
-      B.x = dot_exact(P.da + (size_t)(B.v * P.Wa + B.u) * 24, bdesc, 24);
-      B.known = true;
-    }
-    const double ex = dot_exact(P.da + (size_t)pix * 24, bdesc, 24);
-    if (ex > B.x) {
-      best_set(B, u, v, sc, err);
-      B.x = ex;
-      B.known = true;
+    refine_exact(P, bdesc, u, v, sc, err, B);
+  }
+}
+
+__device__ __forceinline__ bool bound8_fails(float h8, float4 nr, const BConst& K, float thr) {
+  const float u8 = fmaf(nr.x, K.c8, fmaf(nr.y, K.t8, h8));
+  return fmaf(8.0f * kU, fabsf(h8) + fabsf(u8), u8) <= thr;  // cannot beat the best: skip
+}
+
+// One refinement level (camera.cpp:247-265) around (cu, cv), general form.
+template <bool CHECK_PREV, class Aux>
+__device__ __forceinline__ void refine_level(const PairDev& P, const Aux& X, const BConst& K,
+                                             const __half* __restrict__ bdesc, int cu, int cv, int s, int r,
+                                             int prev_cu, int prev_cv, int prev_s, int prev_r, BestState& B) {
+  const int Wa = P.Wa, Ha = P.Ha;
+  const int du_lo = -min(r, cu / s), du_hi = min(r, (Wa - 1 - cu) / s);
+  const int dv_lo = -min(r, cv / s), dv_hi = min(r, (Ha - 1 - cv) / s);
+  const int lim = prev_r * prev_s;
+  for (int dv = dv_lo; dv <= dv_hi; ++dv) {
+    const int v = cv + dv * s;
+    for (int du = du_lo; du <= du_hi; ++du) {
+      if (du == 0 && dv == 0) continue;
+      const int u = cu + du * s;
+      if (CHECK_PREV) {  // already maximised by the previous level: cannot win (strict '>')
+        const int eu = u - prev_cu, ev = v - prev_cv;
+        if (abs(eu) <= lim && abs(ev) <= lim && (prev_s == 1 || (eu % prev_s == 0 && ev % prev_s == 0))) continue;
+      }
+      const int i = X.at(u, v);
+      const float4 nr = X.nrm(i);
+      const float h8 = dot8(X.d0(i), K.b0, 0.0f);
+      if (bound8_fails(h8, nr, K, B.thr)) continue;
+      refine_candidate(P, X, K, bdesc, u, v, i, h8, nr, B);
     }
   }
 }
 
-__device__ __forceinline__ int refine_pruned(const PairDev& P, int pa, const __half* __restrict__ bdesc, const RefineLevels& L) {
-  const int Wa = P.Wa, Ha = P.Ha;
-  const uint4* bp = reinterpret_cast<const uint4*>(bdesc);
-  const uint4 b0 = __ldg(bp), b1 = __ldg(bp + 1), b2 = __ldg(bp + 2);
-  const float bh_ss = dot8(b0, b0, 0.0f);
-  const float bt_ss = dot8(b2, b2, dot8(b1, b1, 0.0f));
-  const float nb = norm_ub(bh_ss + bt_ss, 24);
-  // exact(cand) <= head + 8u ||a|| ||b_h|| + ||a_t|| ||b_t||   (Cauchy-Schwarz)
-  const float c_head = 8.01f * kU * norm_ub(bh_ss, 8);
-  const float c_tail = norm_ub(bt_ss, 16) * (1.0f + 4.0f * kU);
-  const uint4* __restrict__ heads = P.dhead;
-  const float2* __restrict__ norms = P.dnorm;
+// Interior window, compile-time radius / stride, candidates in shared memory.
+// The running best only increases during the scan, so a candidate whose upper
+// bound cannot beat the INITIAL best (the centre) can never win: all head
+// bounds are evaluated branch-free against the centre's threshold into a
+// bitmask, then only the survivors are processed, in raster order, with the
+// running best (exactly the reference's strict-'>' scan).
+template <int R, int S>
+__device__ __forceinline__ void refine_level_fast(const PairDev& P, const SmemAux& X, const BConst& K,
+                                                  const __half* __restrict__ bdesc, int cu, int cv, BestState& B) {
+  constexpr int D = 2 * R + 1;
+  static_assert(D * D <= 64, "window too large for the survivor mask");
+  const int base = X.at(cu - R * S, cv - R * S);
+  const float thr0 = B.thr;
+  unsigned long long mask = 0ull;
+#pragma unroll
+  for (int dv = 0; dv < D; ++dv) {
+#pragma unroll
+    for (int du = 0; du < D; ++du) {
+      if (dv == R && du == R) continue;
+      const int i = base + dv * S * X.bw + du * S;
+      if (!bound8_fails(dot8(X.d0(i), K.b0, 0.0f), X.nrm(i), K, thr0)) mask |= 1ull << (dv * D + du);
+    }
+  }
+  while (mask) {
+    const int k = __ffsll((long long)mask) - 1;
+    mask &= mask - 1;
+    const int dv = k / D, du = k % D;
+    const int i = base + dv * S * X.bw + du * S;
+    const float4 nr = X.nrm(i);
+    const float h8 = dot8(X.d0(i), K.b0, 0.0f);
+    if (bound8_fails(h8, nr, K, B.thr)) continue;  // the best has grown meanwhile
+    refine_candidate(P, X, K, bdesc, cu + (du - R) * S, cv + (dv - R) * S, i, h8, nr, B);
+  }
+}
+
+template <int R, int S, class Aux>
+__device__ __forceinline__ bool try_fast(const PairDev& P, const Aux& X, const BConst& K, const __half* bdesc, int cu,
+                                         int cv, int s, int r, BestState& B) {
+  if constexpr (std::is_same<Aux, SmemAux>::value) {
+    if (s == S && r == R && cu - R * S >= 0 && cu + R * S < P.Wa && cv - R * S >= 0 && cv + R * S < P.Ha) {
+      refine_level_fast<R, S>(P, X, K, bdesc, cu, cv, B);
+      return true;
+    }
+  }
+  return false;
+}
+
+template <class Aux>
+__device__ __forceinline__ int refine_pruned(const PairDev& P, const Aux& X, int pa, const __half* __restrict__ bdesc,
+                                             const RefineLevels& L) {
+  const int Wa = P.Wa;
+  BConst K;
+  {
+    const uint4* bp = reinterpret_cast<const uint4*>(bdesc);
+    K.b0 = __ldg(bp);
+    K.b1 = __ldg(bp + 1);
+    K.b2 = __ldg(bp + 2);
+    const float s0 = dot8(K.b0, K.b0, 0.0f), s1 = dot8(K.b1, K.b1, 0.0f), s2 = dot8(K.b2, K.b2, 0.0f);
+    // Three-stage Cauchy-Schwarz pruning: after the first 8 (16) dims,
+    //   exact(cand) <= partial + k u ||a|| ||b_head|| + ||a_tail|| ||b_tail||
+    K.c8 = 8.01f * kU * norm_ub(s0, 8);
+    K.t8 = norm_ub(s1 + s2, 16) * (1.0f + 4.0f * kU);
+    K.c16 = 16.01f * kU * norm_ub(s0 + s1, 16);
+    K.t16 = norm_ub(s2, 8) * (1.0f + 4.0f * kU);
+    K.c24 = 24.01f * kU * norm_ub(s0 + s1 + s2, 24);
+  }
   int cu = pa % Wa, cv = pa / Wa;
   int prev_cu = 0, prev_cv = 0, prev_s = 1, prev_r = -1;
   for (int l = 0; l < L.n; ++l) {
@@ -691,36 +820,17 @@ __device__ __forceinline__ int refine_pruned(const PairDev& P, int pa, const __h
     if (l > 0 && s == prev_s && r == prev_r && cu == prev_cu && cv == prev_cv) continue;
     BestState B;
     {
-      const int pix = cv * Wa + cu;
-      const uint4* ap = reinterpret_cast<const uint4*>(P.da + (size_t)pix * 24);
-      const float f = dot8(__ldg(ap + 2), b2, dot8(__ldg(ap + 1), b1, dot8(__ldg(ap), b0, 0.0f)));
-      best_set(B, cu, cv, f, 24.01f * kU * __ldg(norms + pix).x * nb);
+      const int i = X.at(cu, cv);
+      const float f = dot8(X.d2(i), K.b2, dot8(X.d1(i), K.b1, dot8(X.d0(i), K.b0, 0.0f)));
+      best_set(B, cu, cv, f, K.c24 * X.nrm(i).x);
       B.x = 0.0;
     }
-    // window clipped to the image: no per-candidate bounds checks
-    const int du_lo = -min(r, cu / s), du_hi = min(r, (Wa - 1 - cu) / s);
-    const int dv_lo = -min(r, cv / s), dv_hi = min(r, (Ha - 1 - cv) / s);
-    const bool check_prev = prev_r >= 0;
-    for (int dv = dv_lo; dv <= dv_hi; ++dv) {
-      const int v = cv + dv * s;
-      const int row = v * Wa;
-#pragma unroll 2
-      for (int du = du_lo; du <= du_hi; ++du) {
-        const int u = cu + du * s;
-        if (du == 0 && dv == 0) continue;
-        if (check_prev) {  // inside the previous level's (already maximised) window: cannot win
-          const int eu = u - prev_cu, ev = v - prev_cv, lim = prev_r * prev_s;
-          if (abs(eu) <= lim && abs(ev) <= lim && (prev_s == 1 || (eu % prev_s == 0 && ev % prev_s == 0)))
-            continue;
-        }
-        const int pix = row + u;
-        const float2 nr = __ldg(norms + pix);
-        const float hd = dot8(__ldg(heads + pix), b0, 0.0f);
-        const float ub = fmaf(nr.x, c_head, nr.y * c_tail);
-        const float t = hd + ub;
-        if (fmaf(4.0f * kU, fabsf(hd) + ub, t) <= B.thr) continue;  // certainly <= best: strict '>' fails
-        refine_full(P, bdesc, b1, b2, nb, u, v, hd, nr.x, B);
-      }
+    if (prev_r < 0) {
+      if (!try_fast<3, 1>(P, X, K, bdesc, cu, cv, s, r, B) && !try_fast<2, 2>(P, X, K, bdesc, cu, cv, s, r, B) &&
+          !try_fast<2, 1>(P, X, K, bdesc, cu, cv, s, r, B))
+        refine_level<false>(P, X, K, bdesc, cu, cv, s, r, 0, 0, 1, -1, B);
+    } else {
+      refine_level<true>(P, X, K, bdesc, cu, cv, s, r, prev_cu, prev_cv, prev_s, prev_r, B);
     }
     prev_cu = cu;
     prev_cv = cv;
@@ -736,7 +846,8 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
   const __half* bdesc = P.db + (size_t)pb * P.dim;
   if (((uintptr_t)P.da | (uintptr_t)P.db) & 15)  // vector loads need 16-byte rows
     return refine_one_generic(P.da, P.Wa, P.Ha, P.dim, bdesc, pa, L);
-  if (P.dhead && P.dim == 24) return refine_pruned(P, pa, bdesc, L);
+  if (P.dnorm && P.dim == 24)
+    return refine_pruned(P, GlobalAux{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa}, pa, bdesc, L);
   if (P.dim == 24) return refine_one<24>(P.da, P.Wa, P.Ha, bdesc, pa, L);
   if (P.dim == 16) return refine_one<16>(P.da, P.Wa, P.Ha, bdesc, pa, L);
   if (P.dim == 32) return refine_one<32>(P.da, P.Wa, P.Ha, bdesc, pa, L);
@@ -792,20 +903,418 @@ __global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs
   P.out_valid[n] = valid_out;
 }
 
-// K4: feature_refine of the valid matches just written by k_match (in place).
-__global__ void __launch_bounds__(128) k_refine_pairs(const PairDev* __restrict__ pairs, RefineLevels L) {
-  const PairDev& P = pairs[blockIdx.y];
-  const int tiles_x = (P.Wb + 31) / 32;
-  const int tiles = tiles_x * ((P.Hb + 3) / 4);
-  if ((int)blockIdx.x >= tiles) return;
-  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
-  const int v = (blockIdx.x / tiles_x) * 4 + (threadIdx.x >> 5);
-  if (u >= P.Wb || v >= P.Hb) return;
-  const int n = v * P.Wb + u;
-  if (!P.out_valid[n]) return;
-  const int pa = refine_dispatch(P, P.out_pa[n], n, L);
-  P.out_pa[n] = pa;
-  P.out_q[n] = (float)sqrt((double)P.qa[pa] * (double)P.qb[n]);
+// K4: feature_refine of the valid matches just written by k_match (in place),
+// in two passes so that no warp waits on one slow lane:
+//  * k_refine_pairs — persistent blocks walk 32x8 tiles of b-pixels; the
+//    first 16 descriptor dims + norm bounds (+ qa) of a tile's centres'
+//    bounding box (grown by the refinement reach) are staged in shared memory
+//    with cp.async, double-buffered so the next tile's staging overlaps this
+//    tile's refinement.  Every pixel bounds all the
+//    candidates of its window against the centre's threshold (8-dim, then
+//    16-dim Cauchy-Schwarz bounds; branch-free on interior windows).  "Easy"
+//    pixels (<= 2 survivors per level) are finished in place; the rest (in
+//    practice: LM centre != descriptor peak) are appended to a queue.
+//  * k_refine_hard — one warp per queued pixel: the window's candidates are
+//    spread over the lanes, the exact argmax (max score, ties to the centre,
+//    then raster order) comes from warp reductions over rigorous fp32 bounds,
+//    with an exact FP64 replay when several candidates are within rounding.
+constexpr int kTileCap = 1024;  // staged a-pixels per buffer (48 B each: 2 planes + norms/qa)
+constexpr size_t kTileBytes = (size_t)kTileCap * (2 * sizeof(uint4) + sizeof(float4));
+constexpr size_t kRefineSmem = 2 * kTileBytes;
+
+struct HeadTile {
+  const uint4* h0;  // dims 0-7
+  const uint4* h1;  // dims 8-15
+  const float4* n;  // {||a||, ||a[8:]||, ||a[16:]||, qa}
+  int u0, v0, bw;
+};
+
+struct PrevWin {  // the previous level's window (already maximised: cannot win, strict '>')
+  int cu, cv, s, lim;
+  bool on;
+};
+
+// One level with compile-time radius / stride.  The running best only grows
+// during the scan, so bounding every candidate against the centre's threshold
+// is exact: survivors are then processed in raster order with the running
+// best (the reference's strict-'>' scan).  Pass 1 bounds every candidate with
+// its 8-dim head (branch-free), pass 2 tightens the ~1% survivors to 16 dims,
+// pass 3 decides the rest.  Returns false to defer (> 2 survivors).  CLIP:
+// the window may leave the image, or a previous window must be skipped.
+template <int R, int S, bool CLIP>
+__device__ __forceinline__ bool easy_level(const PairDev& P, const HeadTile& T, const BConst& K,
+                                           const __half* __restrict__ bdesc, int cu, int cv, BestState& B,
+                                           const PrevWin& W) {
+  constexpr int D = 2 * R + 1;
+  const float thr0 = B.thr;
+  const int base = (cv - R * S - T.v0) * T.bw + (cu - R * S - T.u0);
+  unsigned long long mask = 0ull;
+#pragma unroll
+  for (int dv = 0; dv < D; ++dv) {
+#pragma unroll
+    for (int du = 0; du < D; ++du) {
+      if (dv == R && du == R) continue;
+      int i = base + dv * S * T.bw + du * S;
+      bool ok = true;
+      if (CLIP) {
+        const int u = cu + (du - R) * S, v = cv + (dv - R) * S;
+        ok = (unsigned)u < (unsigned)P.Wa && (unsigned)v < (unsigned)P.Ha;  // out of image: skipped
+        if (W.on) {
+          const int eu = u - W.cu, ev = v - W.cv;
+          ok = ok && !(abs(eu) <= W.lim && abs(ev) <= W.lim && (W.s == 1 || (eu % W.s == 0 && ev % W.s == 0)));
+        }
+        i = ok ? i : 0;
+      }
+      const float2 nr = *reinterpret_cast<const float2*>(T.n + i);
+      const float h8 = dot8(T.h0[i], K.b0, 0.0f);
+      const float u8 = fmaf(nr.x, K.c8, fmaf(nr.y, K.t8, h8));
+      if (ok && fmaf(8.0f * kU, fabsf(h8) + fabsf(u8), u8) > thr0) mask |= 1ull << (dv * D + du);
+    }
+  }
+  unsigned long long keep = 0ull;
+  for (unsigned long long m = mask; m; m &= m - 1) {  // pass 2: 16-dim bound
+    const int k = __ffsll((long long)m) - 1;
+    const int i = base + (k / D) * S * T.bw + (k % D) * S;
+    const float4 nr = T.n[i];
+    const float h16 = dot8(T.h1[i], K.b1, dot8(T.h0[i], K.b0, 0.0f));
+    const float u16 = fmaf(nr.x, K.c16, fmaf(nr.z, K.t16, h16));
+    if (fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) > thr0) keep |= 1ull << k;
+  }
+  if (__popcll(keep) > 2) return false;
+  const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
+  while (keep) {
+    const int k = __ffsll((long long)keep) - 1;
+    keep &= keep - 1;
+    const int u = cu + (k % D - R) * S, v = cv + (k / D - R) * S;
+    const int i = G.at(u, v);
+    const float4 nr = G.nrm(i);
+    const float h8 = dot8(G.d0(i), K.b0, 0.0f);
+    if (bound8_fails(h8, nr, K, B.thr)) continue;
+    refine_candidate(P, G, K, bdesc, u, v, i, h8, nr, B);
+  }
+  return true;
+}
+
+template <int R, int S>
+__device__ __forceinline__ int try_easy(const PairDev& P, const HeadTile& T, const BConst& K, const __half* bdesc,
+                                        int cu, int cv, int s, int r, BestState& B, const PrevWin& W) {
+  if (s != S || r != R) return -1;  // not this instantiation
+  const bool interior = cu - R * S >= 0 && cu + R * S < P.Wa && cv - R * S >= 0 && cv + R * S < P.Ha;
+  if (interior && !W.on) return easy_level<R, S, false>(P, T, K, bdesc, cu, cv, B, W) ? 1 : 0;
+  return easy_level<R, S, true>(P, T, K, bdesc, cu, cv, B, W) ? 1 : 0;
+}
+
+__device__ __forceinline__ BConst make_bconst(const __half* bdesc) {
+  BConst K;
+  const uint4* bp = reinterpret_cast<const uint4*>(bdesc);
+  K.b0 = __ldg(bp);
+  K.b1 = __ldg(bp + 1);
+  K.b2 = __ldg(bp + 2);
+  const float s0 = dot8(K.b0, K.b0, 0.0f), s1 = dot8(K.b1, K.b1, 0.0f), s2 = dot8(K.b2, K.b2, 0.0f);
+  K.c8 = 8.01f * kU * norm_ub(s0, 8);
+  K.t8 = norm_ub(s1 + s2, 16) * (1.0f + 4.0f * kU);
+  K.c16 = 16.01f * kU * norm_ub(s0 + s1, 16);
+  K.t16 = norm_ub(s2, 8) * (1.0f + 4.0f * kU);
+  K.c24 = 24.01f * kU * norm_ub(s0 + s1 + s2, 24);
+  return K;
+}
+
+// Easy path of one pixel; returns the refined pixel or -1 to defer.
+// K and the level-0 centre score fc were loaded before the tile landed.
+__device__ __forceinline__ int refine_easy(const PairDev& P, const HeadTile& T, int pa, const __half* bdesc,
+                                           const BConst& K, float fc, const RefineLevels& L) {
+  const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
+  int cu = pa % P.Wa, cv = pa / P.Wa;
+  PrevWin W{0, 0, 1, 0, false};
+  for (int l = 0; l < L.n; ++l) {
+    const int s = L.stride[l], r = L.radius[l];
+    if (W.on && s == W.s && r * s == W.lim && cu == W.cu && cv == W.cv) continue;  // identical window
+    BestState B;
+    if (l == 0) {
+      best_set(B, cu, cv, fc, K.c24 * T.n[(cv - T.v0) * T.bw + (cu - T.u0)].x);
+    } else {
+      const int i = G.at(cu, cv);
+      const float f = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
+      best_set(B, cu, cv, f, K.c24 * G.nrm(i).x);
+    }
+    B.x = 0.0;
+    int ok = try_easy<3, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
+    if (ok < 0) ok = try_easy<2, 2>(P, T, K, bdesc, cu, cv, s, r, B, W);
+    if (ok < 0) ok = try_easy<2, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
+    if (ok < 0) ok = try_easy<1, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
+    if (ok <= 0) return -1;
+    W = PrevWin{cu, cv, s, r * s, true};
+    cu = B.u;
+    cv = B.v;
+  }
+  return cv * P.Wa + cu;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+struct TileJob {
+  int p, n, pa;  // pair (in the launch's chunk), b-pixel, LM match
+  bool work;     // this thread has a valid match to refine
+  bool aux;      // the pair has pruning aux (else: per-thread exact path)
+  int u0, v0, bw;  // staged a-box origin / width; bw == 0: not staged (defer)
+};
+
+// Decode tile g, reduce its a-box over the block (one barrier) and issue the
+// box's staging into buffer `buf` as one cp.async group (committed even when
+// empty, so the wait counts stay uniform).  Every thread calls this.
+__device__ __forceinline__ TileJob tile_begin(const PairDev* __restrict__ pairs, int g, int total, int max_tiles,
+                                              int reach, int (*sbox)[4], char* buf) {
+  TileJob J{0, 0, 0, false, false, 0, 0, 0};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+  if (g < total) {
+    J.p = g / max_tiles;
+    const PairDev& P = pairs[J.p];
+    J.aux = P.dnorm != nullptr;
+    const int t = g % max_tiles, tiles_x = (P.Wb + 31) / 32;
+    if (t < tiles_x * ((P.Hb + 7) / 8)) {
+      const int u = (t % tiles_x) * 32 + lane, v = (t / tiles_x) * 8 + warp;
+      J.n = v * P.Wb + u;
+      J.work = u < P.Wb && v < P.Hb && P.out_valid[J.n];
+      if (J.work) {
+        J.pa = P.out_pa[J.n];
+        bx0 = bx1 = J.pa % P.Wa;
+        by0 = by1 = J.pa / P.Wa;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bx0 = min(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
+    bx1 = max(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
+    by0 = min(by0, __shfl_xor_sync(0xffffffffu, by0, o));
+    by1 = max(by1, __shfl_xor_sync(0xffffffffu, by1, o));
+  }
+  if (lane == 0) {
+    sbox[warp][0] = bx0;
+    sbox[warp][1] = bx1;
+    sbox[warp][2] = by0;
+    sbox[warp][3] = by1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    bx0 = min(bx0, sbox[w][0]);
+    bx1 = max(bx1, sbox[w][1]);
+    by0 = min(by0, sbox[w][2]);
+    by1 = max(by1, sbox[w][3]);
+  }
+  if (g < total && J.aux && bx0 != INT_MAX) {
+    const PairDev& P = pairs[J.p];
+    const int u0 = max(0, bx0 - reach), u1 = min(P.Wa - 1, bx1 + reach);
+    const int v0 = max(0, by0 - reach), v1 = min(P.Ha - 1, by1 + reach);
+    const int bw = u1 - u0 + 1, bh = v1 - v0 + 1;
+    if (bw * bh <= kTileCap) {
+      J.u0 = u0;
+      J.v0 = v0;
+      J.bw = bw;
+      uint4* s0 = reinterpret_cast<uint4*>(buf);
+      uint4* s1 = s0 + kTileCap;
+      float4* sn = reinterpret_cast<float4*>(s1 + kTileCap);
+      const uint4* rows = reinterpret_cast<const uint4*>(P.da);
+      for (int rr = warp; rr < bh; rr += 8) {  // one warp per staged row, coalesced
+        const int grow = (v0 + rr) * P.Wa + u0;
+        for (int cc = lane; cc < bw; cc += 32) {
+          const int gp = grow + cc, sp = rr * bw + cc;
+          cp_async16(s0 + sp, rows + 3 * gp);
+          cp_async16(s1 + sp, rows + 3 * gp + 1);
+          cp_async16(sn + sp, P.dnorm + gp);
+        }
+      }
+    }
+  }
+  cp_async_commit();
+  return J;
+}
+
+__global__ void __launch_bounds__(256, 2) k_refine_pairs(const PairDev* __restrict__ pairs, int total, int max_tiles,
+                                                         RefineLevels L, int reach, int2* __restrict__ queue,
+                                                         int* __restrict__ qcount) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ int s_box[8][4];
+  int buf = 0;
+  TileJob cur = tile_begin(pairs, blockIdx.x, total, max_tiles, reach, s_box, smem);
+  for (int g = blockIdx.x; g < total; g += gridDim.x) {
+    const TileJob nxt = tile_begin(pairs, g + gridDim.x, total, max_tiles, reach, s_box, smem + (buf ^ 1) * kTileBytes);
+    const PairDev& P = pairs[cur.p];
+    const __half* bdesc = P.db + (size_t)cur.n * 24;
+    int out = -1;
+    if (cur.work && !cur.aux) {  // no pruning aux (dim != 24 or unaligned rows): per-thread exact path
+      out = refine_dispatch(P, cur.pa, cur.n, L);
+      P.out_pa[cur.n] = out;
+      P.out_q[cur.n] = (float)sqrt((double)P.qa[out] * (double)P.qb[cur.n]);
+    }
+    // loads that do not need the tile: b descriptor, centre descriptor, qb
+    BConst K;
+    float fc = 0.0f, qb = 0.0f;
+    const bool easy = cur.work && cur.aux && cur.bw > 0;
+    if (easy) {
+      K = make_bconst(bdesc);
+      const uint4* ca = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)cur.pa;
+      fc = dot8(__ldg(ca + 2), K.b2, dot8(__ldg(ca + 1), K.b1, dot8(__ldg(ca), K.b0, 0.0f)));
+      qb = P.qb[cur.n];
+    }
+    cp_async_wait1();
+    __syncthreads();
+    if (cur.work && cur.aux) {
+      if (easy) {
+        const uint4* s0 = reinterpret_cast<const uint4*>(smem + buf * kTileBytes);
+        const HeadTile T{s0, s0 + kTileCap, reinterpret_cast<const float4*>(s0 + 2 * kTileCap), cur.u0, cur.v0,
+                         cur.bw};
+        out = refine_easy(P, T, cur.pa, bdesc, K, fc, L);
+        if (out >= 0) {
+          const float qa = T.n[(out / P.Wa - T.v0) * T.bw + (out % P.Wa - T.u0)].w;
+          P.out_pa[cur.n] = out;
+          P.out_q[cur.n] = (float)sqrt((double)qa * (double)qb);
+        }
+      }
+      if (out < 0) queue[atomicAdd(qcount, 1)] = make_int2(cur.p, cur.n);
+    }
+    __syncthreads();  // buffer `buf` is restaged two tiles from now
+    cur = nxt;
+    buf ^= 1;
+  }
+}
+
+// Persistent grid: resident blocks on every SM, capped by the tile count.
+static unsigned refine_grid(const Context& ctx, int tiles) {
+  static int per_sm = -1;
+  if (per_sm < 0) {
+    PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_pairs, 256, kRefineSmem));
+    per_sm = std::max(per_sm, 1);
+  }
+  return (unsigned)std::max(1, std::min(tiles, per_sm * ctx.num_sms));
+}
+
+// Warp-cooperative exact refinement of one queued pixel (all levels): lanes
+// score the window's candidates (<= 2 per lane, kept in registers), the exact
+// argmax (max score, ties to the centre, then raster order) comes from warp
+// reductions over rigorous fp32 bounds, with an exact FP64 replay of the
+// contenders when several are within rounding of the best.
+__global__ void __launch_bounds__(256) k_refine_hard(const PairDev* __restrict__ pairs, RefineLevels L,
+                                                     const int2* __restrict__ queue, const int* __restrict__ qcount) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int count = *qcount;
+  for (int q = gw; q < count; q += nw) {
+    const int2 e = queue[q];
+    const PairDev& P = pairs[e.x];
+    const int n = e.y;
+    const __half* bdesc = P.db + (size_t)n * 24;
+    const BConst K = make_bconst(bdesc);
+    const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
+    const int pa = P.out_pa[n];
+    int cu = pa % P.Wa, cv = pa / P.Wa;
+    int prev_cu = -1, prev_cv = -1, prev_s = 0, prev_r = -1;
+    for (int l = 0; l < L.n; ++l) {
+      const int s = L.stride[l], r = L.radius[l];
+      if (l > 0 && s == prev_s && r == prev_r && cu == prev_cu && cv == prev_cv) continue;
+      const int D = 2 * r + 1, ncand = D * D;
+      const float invD = 1.0f / (float)D;
+      float best_lo = -INFINITY;
+      float sc_[2], er_[2];
+      int u_[2], v_[2], k_[2];
+      int nmine = 0;
+      for (int k = lane - 1; k < ncand; k += 32) {  // k = -1: the centre (rank -1)
+        int u = cu, v = cv;
+        if (k >= 0) {
+          const int dv = (int)(((float)k + 0.5f) * invD), du = k - dv * D;
+          u = cu + (du - r) * s;
+          v = cv + (dv - r) * s;
+          if (u < 0 || v < 0 || u >= P.Wa || v >= P.Ha || (u == cu && v == cv)) continue;
+        }
+        const int i = G.at(u, v);
+        const float sc = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
+        const float err = K.c24 * G.nrm(i).x;
+        best_lo = fmaxf(best_lo, (sc - err) - 4.0f * kU * (fabsf(sc) + err));
+        if (nmine < 2) {
+          sc_[nmine] = sc;
+          er_[nmine] = err;
+          u_[nmine] = u;
+          v_[nmine] = v;
+          k_[nmine] = k;
+        }
+        ++nmine;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best_lo = fmaxf(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
+      // contenders: candidates whose upper bound reaches the best lower bound
+      int ncont = 0, cu_w = cu, cv_w = cv;
+      const bool spilled = nmine > 2;  // radius > 3: scores not all kept
+      for (int j = 0; j < 2 && j < nmine; ++j) {
+        if ((sc_[j] + er_[j]) + 4.0f * kU * (fabsf(sc_[j]) + er_[j]) < best_lo) continue;
+        if (ncont == 0) {
+          cu_w = u_[j];
+          cv_w = v_[j];
+        }
+        ++ncont;
+      }
+      const int total = __reduce_add_sync(0xffffffffu, ncont);
+      const bool any_spill = __any_sync(0xffffffffu, spilled);
+      int win_u = cu, win_v = cv;
+      if (total == 1 && !any_spill) {
+        const int src = __ffs(__ballot_sync(0xffffffffu, ncont == 1)) - 1;
+        win_u = __shfl_sync(0xffffffffu, cu_w, src);
+        win_v = __shfl_sync(0xffffffffu, cv_w, src);
+      } else {  // exact FP64 scores of every contender; argmax with ties to the lowest rank
+        double bx = -INFINITY;
+        int br = INT_MAX;
+        for (int k = lane - 1; k < ncand; k += 32) {
+          int u = cu, v = cv;
+          if (k >= 0) {
+            const int dv = (int)(((float)k + 0.5f) * invD), du = k - dv * D;
+            u = cu + (du - r) * s;
+            v = cv + (dv - r) * s;
+            if (u < 0 || v < 0 || u >= P.Wa || v >= P.Ha || (u == cu && v == cv)) continue;
+          }
+          const int i = G.at(u, v);
+          const float sc = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
+          const float err = K.c24 * G.nrm(i).x;
+          if ((sc + err) + 4.0f * kU * (fabsf(sc) + err) < best_lo) continue;
+          const double ex = dot_exact(P.da + (size_t)i * 24, bdesc, 24);
+          if (ex > bx || (ex == bx && k < br)) {
+            bx = ex;
+            br = k;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ox = __shfl_xor_sync(0xffffffffu, bx, o);
+          const int orank = __shfl_xor_sync(0xffffffffu, br, o);
+          if (ox > bx || (ox == bx && orank < br)) {
+            bx = ox;
+            br = orank;
+          }
+        }
+        if (br >= 0 && br != INT_MAX) {
+          win_u = cu + (br % D - r) * s;
+          win_v = cv + (br / D - r) * s;
+        }
+      }
+      (void)k_;
+      prev_cu = cu;
+      prev_cv = cv;
+      prev_s = s;
+      prev_r = r;
+      cu = win_u;
+      cv = win_v;
+    }
+    if (lane == 0) {
+      const int out = cv * P.Wa + cu;
+      P.out_pa[n] = out;
+      P.out_q[n] = (float)sqrt((double)P.qa[out] * (double)P.qb[n]);
+    }
+  }
 }
 
 // Standalone feature_refine over an arbitrary MatchSet (camera.cpp:239-271).
@@ -962,20 +1471,22 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   }
   // chunk so that a chunk's FP64 ray maps + descriptor heads / norms + keys
   // (60 B per a-pixel) stay L2-resident between k_prep and k_match/k_refine
-  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(float2) + sizeof(uint32_t);
+  const size_t per_px = sizeof(double4) + sizeof(float4) + sizeof(uint32_t);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   const int chunk = std::max(1, std::min(npairs, (int)((64u << 20) / std::max<size_t>(pair_bytes, 1))));
   DevBuf scratch(pair_bytes * chunk, ctx.stream);
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
   DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
   DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
+  DevBuf qbuf(sizeof(int2) * (size_t)max_hwb * chunk + sizeof(int) * 4, ctx.stream);
+  int* qcount = reinterpret_cast<int*>(qbuf.as<char>() + sizeof(int2) * (size_t)max_hwb * chunk);
+  int2* queue = qbuf.as<int2>();
   std::vector<PairDev> hp = host_pairs;
   char* base = scratch.as<char>();
   const size_t nslot = (size_t)max_hwa * chunk;
   double4* rays = reinterpret_cast<double4*>(base);
-  uint4* heads = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
-  float2* norms = reinterpret_cast<float2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(float2)) * nslot);
+  float4* norms = reinterpret_cast<float4*>(base + sizeof(double4) * nslot);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(float4)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
@@ -984,7 +1495,6 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     hp[i].sel = sel.as<SelState>() + i;
     const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
     if (refine && hp[i].dim == 24 && aligned) {
-      hp[i].dhead = heads + (size_t)slot * max_hwa;
       hp[i].dnorm = norms + (size_t)slot * max_hwa;
     }
   }
@@ -1007,7 +1517,23 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     if (refine && L.n > 0) {
       {
         ProfScope ps(ctx, "k_refine");
-        k_refine_pairs<<<dim3(max_tiles4, cn), 128, 0, ctx.stream>>>(dp, L);
+        int reach = 0;
+        for (int l = 0; l < L.n; ++l) reach += L.radius[l] * L.stride[l];
+        PMX_CUDA(cudaFuncSetAttribute((const void*)k_refine_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kRefineSmem));
+        PMX_CUDA(cudaMemsetAsync(qcount, 0, sizeof(int), ctx.stream));
+        k_refine_pairs<<<refine_grid(ctx, cn * max_tiles), 256, kRefineSmem, ctx.stream>>>(dp, cn * max_tiles, max_tiles, L, reach, queue, qcount);
+      }
+      {
+        ProfScope ps(ctx, "k_refine_hard");
+        k_refine_hard<<<ctx.num_sms * 8, 256, 0, ctx.stream>>>(dp, L, queue, qcount);
+      }
+      if (ctx.profiling) {  // hard-queue occupancy, reported through pmx_profile_get("refine_hard_px")
+        int h = 0;
+        PMX_CUDA(cudaMemcpyAsync(&h, qcount, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
+        PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+        ctx.counters["refine_hard_px"] += h;
+        ctx.counters["refine_px"] += 0;
       }
       launch_check(ctx, "k_refine_pairs");
     }
@@ -1130,10 +1656,9 @@ extern "C" int pmx_impl_feature_refine(pmx_context* c, pmx_memory mem, const pmx
   uint8_t* ov = st.out(out->valid, n);
   DevBuf aux;
   if (P.dim == 24 && ((uintptr_t)P.da % 16 == 0) && ((uintptr_t)P.db % 16 == 0) && hwa > 0) {
-    aux = DevBuf((sizeof(uint4) + sizeof(float2)) * hwa, ctx.stream);
-    P.dhead = aux.as<uint4>();
-    P.dnorm = reinterpret_cast<float2*>(aux.as<char>() + sizeof(uint4) * hwa);
-    k_desc_prep<<<(unsigned)((hwa + 255) / 256), 256, 0, ctx.stream>>>(P.da, (int)hwa, P.dhead, P.dnorm);
+    aux = DevBuf(sizeof(float4) * hwa, ctx.stream);
+    P.dnorm = aux.as<float4>();
+    k_desc_prep<<<(unsigned)((hwa + 255) / 256), 256, 0, ctx.stream>>>(P.da, P.qa, (int)hwa, P.dnorm);
     launch_check(ctx, "k_desc_prep");
   }
   if (n > 0) {

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <cmath>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -52,6 +53,7 @@ struct Context {
   int num_sms = 148;
   bool profiling = false;
   std::vector<ProfEvent> prof;  // unresolved event pairs (pmx_profile_*)
+  std::map<std::string, int64_t> counters;  // profiling counters (pmx_profile_get, total_ms = 0)
 };
 
 // CUDA-event bracket around one kernel launch on ctx.stream (when profiling).

@@ -45,8 +45,10 @@ mp.projection.lambda_init = 1e-8
 mp.projection.angle_tol = 1e-6
 rp = abi.refine_params([(1, 3), (1, 3)])
 outs = [MatchSet.empty(H * W, dev) for _ in pairs]
+variants = {"refine": rp, "r0": abi.refine_params([(1, 0)]), "r1": abi.refine_params([(1, 1)]),
+            "r3x1": abi.refine_params([(1, 3)]), "lm": None}
 for mode in a.modes.split(","):
-    ref = rp if mode == "refine" else None
+    ref = variants[mode]
     ctx.match_batch(pairs, params=mp, refine=ref, outs=outs)
     torch.cuda.synchronize()
     ctx.profile_enable(True)
@@ -56,7 +58,10 @@ for mode in a.modes.split(","):
     torch.cuda.synchronize()
     ms, n = ctx.profile_get("k_match")
     rms, rn = ctx.profile_get("k_refine")
+    hms, hn = ctx.profile_get("k_refine_hard")
+    _, hard_px = ctx.profile_get("refine_hard_px")
     ctx.profile_enable(False)
     print(f"{mode}: k_match {ms / a.reps / a.edges * 1e3:.1f} us/edge ({n} launches), k_refine "
-          f"{rms / a.reps / a.edges * 1e3:.1f} us/edge ({rn})  "
+          f"{rms / a.reps / a.edges * 1e3:.1f} us/edge ({rn}), hard {hms / a.reps / a.edges * 1e3:.1f} us/edge "
+          f"({hard_px / a.reps / a.edges:.0f} px/edge)  "
           f"valid {np.mean([o.valid.float().mean().item() for o in outs]):.4f}")
