@@ -68,7 +68,7 @@ struct PairDev {
   SelState* sel;
   // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
   // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
-  float4* dnorm;  // {||a||, ||a[8:24]||, ||a[16:24]||} upper bounds, .w = qa (staged with the norms)
+  float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (staged with the norms)
 };
 
 struct LMParams {
@@ -112,6 +112,25 @@ __device__ __forceinline__ float dot8(const uint4& a, const uint4& b, float s) {
   s = fh_lo(a.w, b.w, s);
   return s + t;
 }
+// 16-term dot in four independent 4-deep chains (<= 6 roundings on any path,
+// within the 16u bound).
+__device__ __forceinline__ float dot16(const uint4& a0, const uint4& a1, const uint4& b0, const uint4& b1) {
+  float p = fh_lo(a0.x, b0.x, 0.0f), q = fh_hi(a0.x, b0.x, 0.0f);
+  float r = fh_lo(a1.x, b1.x, 0.0f), t = fh_hi(a1.x, b1.x, 0.0f);
+  p = fh_lo(a0.y, b0.y, p);
+  q = fh_hi(a0.y, b0.y, q);
+  r = fh_lo(a1.y, b1.y, r);
+  t = fh_hi(a1.y, b1.y, t);
+  p = fh_lo(a0.z, b0.z, p);
+  q = fh_hi(a0.z, b0.z, q);
+  r = fh_lo(a1.z, b1.z, r);
+  t = fh_hi(a1.z, b1.z, t);
+  p = fh_lo(a0.w, b0.w, p);
+  q = fh_hi(a0.w, b0.w, q);
+  r = fh_lo(a1.w, b1.w, r);
+  t = fh_hi(a1.w, b1.w, t);
+  return (p + q) + (r + t);
+}
 constexpr float kU = 5.9604645e-08f;  // fp32 unit roundoff 2^-24
 
 // Upper bound of sqrt(sum of squares) accumulated by an n-term FHFMA chain.
@@ -124,7 +143,7 @@ __device__ __forceinline__ void desc_aux(const __half* row, float q, float4* nrm
   const uint4* p = reinterpret_cast<const uint4*>(row);
   const uint4 a = __ldg(p), b = __ldg(p + 1), c = __ldg(p + 2);
   const float s0 = dot8(a, a, 0.0f), s1 = dot8(b, b, 0.0f), s2 = dot8(c, c, 0.0f);
-  *nrm = make_float4(norm_ub(s0 + s1 + s2, 24), norm_ub(s1 + s2, 16), norm_ub(s2, 8), q);
+  *nrm = make_float4(norm_ub(s0 + s1 + s2, 24), norm_ub(s2, 8), norm_ub(s1 + s2, 16), q);
 }
 
 // ---------------------------------------------------------------- K1
@@ -704,7 +723,7 @@ __device__ __forceinline__ void refine_candidate(const PairDev& P, const Aux& X,
                                                  const __half* __restrict__ bdesc, int u, int v, int i, float h8,
                                                  float4 nr, BestState& B) {
   const float h16 = dot8(X.d1(i), K.b1, h8);
-  const float u16 = fmaf(nr.x, K.c16, fmaf(nr.z, K.t16, h16));
+  const float u16 = fmaf(nr.x, K.c16, fmaf(nr.y, K.t16, h16));
   if (fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) <= B.thr) return;
   const float sc = dot8(X.d2(i), K.b2, h16);
   const float err = K.c24 * nr.x;
@@ -716,7 +735,7 @@ __device__ __forceinline__ void refine_candidate(const PairDev& P, const Aux& X,
 }
 
 __device__ __forceinline__ bool bound8_fails(float h8, float4 nr, const BConst& K, float thr) {
-  const float u8 = fmaf(nr.x, K.c8, fmaf(nr.y, K.t8, h8));
+  const float u8 = fmaf(nr.x, K.c8, fmaf(nr.z, K.t8, h8));
   return fmaf(8.0f * kU, fabsf(h8) + fabsf(u8), u8) <= thr;  // cannot beat the best: skip
 }
 
@@ -925,7 +944,7 @@ constexpr size_t kRefineSmem = 2 * kTileBytes;
 struct HeadTile {
   const uint4* h0;  // dims 0-7
   const uint4* h1;  // dims 8-15
-  const float4* n;  // {||a||, ||a[8:]||, ||a[16:]||, qa}
+  const float4* n;  // dnorm layout: {||a||, ||a[16:]||, ||a[8:]||, qa}
   int u0, v0, bw;
 };
 
@@ -937,10 +956,10 @@ struct PrevWin {  // the previous level's window (already maximised: cannot win,
 // One level with compile-time radius / stride.  The running best only grows
 // during the scan, so bounding every candidate against the centre's threshold
 // is exact: survivors are then processed in raster order with the running
-// best (the reference's strict-'>' scan).  Pass 1 bounds every candidate with
-// its 8-dim head (branch-free), pass 2 tightens the ~1% survivors to 16 dims,
-// pass 3 decides the rest.  Returns false to defer (> 2 survivors).  CLIP:
-// the window may leave the image, or a previous window must be skipped.
+// best (the reference's strict-'>' scan).  Every candidate gets the 16-dim
+// bound, branch-free (the 8-dim bound is too weak on 24-dim descriptors to
+// pay for a branch); returns false to defer (> 2 survivors).  CLIP: the
+// window may leave the image, or a previous window must be skipped.
 template <int R, int S, bool CLIP>
 __device__ __forceinline__ bool easy_level(const PairDev& P, const HeadTile& T, const BConst& K,
                                            const __half* __restrict__ bdesc, int cu, int cv, BestState& B,
@@ -948,7 +967,7 @@ __device__ __forceinline__ bool easy_level(const PairDev& P, const HeadTile& T, 
   constexpr int D = 2 * R + 1;
   const float thr0 = B.thr;
   const int base = (cv - R * S - T.v0) * T.bw + (cu - R * S - T.u0);
-  unsigned long long mask = 0ull;
+  unsigned long long keep = 0ull;
 #pragma unroll
   for (int dv = 0; dv < D; ++dv) {
 #pragma unroll
@@ -965,20 +984,11 @@ __device__ __forceinline__ bool easy_level(const PairDev& P, const HeadTile& T, 
         }
         i = ok ? i : 0;
       }
-      const float2 nr = *reinterpret_cast<const float2*>(T.n + i);
-      const float h8 = dot8(T.h0[i], K.b0, 0.0f);
-      const float u8 = fmaf(nr.x, K.c8, fmaf(nr.y, K.t8, h8));
-      if (ok && fmaf(8.0f * kU, fabsf(h8) + fabsf(u8), u8) > thr0) mask |= 1ull << (dv * D + du);
+      const float2 nr = *reinterpret_cast<const float2*>(T.n + i);  // {||a||, ||a[16:]||}
+      const float h16 = dot16(T.h0[i], T.h1[i], K.b0, K.b1);
+      const float u16 = fmaf(nr.x, K.c16, fmaf(nr.y, K.t16, h16));
+      if (ok && fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) > thr0) keep |= 1ull << (dv * D + du);
     }
-  }
-  unsigned long long keep = 0ull;
-  for (unsigned long long m = mask; m; m &= m - 1) {  // pass 2: 16-dim bound
-    const int k = __ffsll((long long)m) - 1;
-    const int i = base + (k / D) * S * T.bw + (k % D) * S;
-    const float4 nr = T.n[i];
-    const float h16 = dot8(T.h1[i], K.b1, dot8(T.h0[i], K.b0, 0.0f));
-    const float u16 = fmaf(nr.x, K.c16, fmaf(nr.z, K.t16, h16));
-    if (fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) > thr0) keep |= 1ull << k;
   }
   if (__popcll(keep) > 2) return false;
   const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
@@ -1023,26 +1033,23 @@ __device__ __forceinline__ BConst make_bconst(const __half* bdesc) {
 // K and the level-0 centre score fc were loaded before the tile landed.
 __device__ __forceinline__ int refine_easy(const PairDev& P, const HeadTile& T, int pa, const __half* bdesc,
                                            const BConst& K, float fc, const RefineLevels& L) {
-  const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
   int cu = pa % P.Wa, cv = pa / P.Wa;
+  const float ec = K.c24 * T.n[(cv - T.v0) * T.bw + (cu - T.u0)].x;
   PrevWin W{0, 0, 1, 0, false};
   for (int l = 0; l < L.n; ++l) {
     const int s = L.stride[l], r = L.radius[l];
     if (W.on && s == W.s && r * s == W.lim && cu == W.cu && cv == W.cv) continue;  // identical window
-    BestState B;
-    if (l == 0) {
-      best_set(B, cu, cv, fc, K.c24 * T.n[(cv - T.v0) * T.bw + (cu - T.u0)].x);
-    } else {
-      const int i = G.at(cu, cv);
-      const float f = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
-      best_set(B, cu, cv, f, K.c24 * G.nrm(i).x);
-    }
+    BestState B;  // every level starts at the LM match (else deferred below)
+    best_set(B, cu, cv, fc, ec);
     B.x = 0.0;
     int ok = try_easy<3, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
     if (ok < 0) ok = try_easy<2, 2>(P, T, K, bdesc, cu, cv, s, r, B, W);
     if (ok < 0) ok = try_easy<2, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
     if (ok < 0) ok = try_easy<1, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
     if (ok <= 0) return -1;
+    // the staged box covers windows centred on the LM match only: a centre
+    // that moves with levels still to go is deferred to k_refine_hard
+    if ((B.u != cu || B.v != cv) && l + 1 < L.n) return -1;
     W = PrevWin{cu, cv, s, r * s, true};
     cu = B.u;
     cv = B.v;
@@ -1057,37 +1064,50 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// Per-buffer job of one staged tile.  Block-uniform fields + per-thread
+// (b-pixel, LM match) kept in shared memory so that the prefetched tile costs
+// no registers while the current one is refined.
 struct TileJob {
-  int p, n, pa;  // pair (in the launch's chunk), b-pixel, LM match
-  bool work;     // this thread has a valid match to refine
-  bool aux;      // the pair has pruning aux (else: per-thread exact path)
+  int p;           // pair (in the launch's chunk)
+  int aux;         // the pair has pruning aux (else: per-thread exact path)
   int u0, v0, bw;  // staged a-box origin / width; bw == 0: not staged (defer)
 };
+struct TileSmem {
+  TileJob job[2];
+  int n[2][256];   // b-pixel, -1: nothing to refine
+  int pa[2][256];  // LM match
+  int box[8][4];
+};
 
-// Decode tile g, reduce its a-box over the block (one barrier) and issue the
-// box's staging into buffer `buf` as one cp.async group (committed even when
+// Decode tile g into slot `b`, reduce its a-box over the block (one barrier)
+// and issue the box's staging as one cp.async group (committed even when
 // empty, so the wait counts stay uniform).  Every thread calls this.
-__device__ __forceinline__ TileJob tile_begin(const PairDev* __restrict__ pairs, int g, int total, int max_tiles,
-                                              int reach, int (*sbox)[4], char* buf) {
-  TileJob J{0, 0, 0, false, false, 0, 0, 0};
+__device__ __forceinline__ void tile_begin(const PairDev* __restrict__ pairs, int g, int total, int max_tiles,
+                                           int reach, TileSmem& S, int b, char* buf) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+  int n = -1, pa = 0, p = 0;
+  bool aux = false;
   if (g < total) {
-    J.p = g / max_tiles;
-    const PairDev& P = pairs[J.p];
-    J.aux = P.dnorm != nullptr;
+    p = g / max_tiles;
+    const PairDev& P = pairs[p];
+    aux = P.dnorm != nullptr;
     const int t = g % max_tiles, tiles_x = (P.Wb + 31) / 32;
     if (t < tiles_x * ((P.Hb + 7) / 8)) {
       const int u = (t % tiles_x) * 32 + lane, v = (t / tiles_x) * 8 + warp;
-      J.n = v * P.Wb + u;
-      J.work = u < P.Wb && v < P.Hb && P.out_valid[J.n];
-      if (J.work) {
-        J.pa = P.out_pa[J.n];
-        bx0 = bx1 = J.pa % P.Wa;
-        by0 = by1 = J.pa / P.Wa;
+      const int m = v * P.Wb + u;
+      const bool in = u < P.Wb && v < P.Hb;
+      const int pm = in ? P.out_pa[m] : 0;  // loaded alongside the flag (no dependent round trip)
+      if (in && P.out_valid[m]) {
+        n = m;
+        pa = pm;
+        bx0 = bx1 = pa % P.Wa;
+        by0 = by1 = pa / P.Wa;
       }
     }
   }
+  S.n[b][threadIdx.x] = n;
+  S.pa[b][threadIdx.x] = pa;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     bx0 = min(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
@@ -1096,21 +1116,22 @@ __device__ __forceinline__ TileJob tile_begin(const PairDev* __restrict__ pairs,
     by1 = max(by1, __shfl_xor_sync(0xffffffffu, by1, o));
   }
   if (lane == 0) {
-    sbox[warp][0] = bx0;
-    sbox[warp][1] = bx1;
-    sbox[warp][2] = by0;
-    sbox[warp][3] = by1;
+    S.box[warp][0] = bx0;
+    S.box[warp][1] = bx1;
+    S.box[warp][2] = by0;
+    S.box[warp][3] = by1;
   }
   __syncthreads();
 #pragma unroll
   for (int w = 0; w < 8; ++w) {
-    bx0 = min(bx0, sbox[w][0]);
-    bx1 = max(bx1, sbox[w][1]);
-    by0 = min(by0, sbox[w][2]);
-    by1 = max(by1, sbox[w][3]);
+    bx0 = min(bx0, S.box[w][0]);
+    bx1 = max(bx1, S.box[w][1]);
+    by0 = min(by0, S.box[w][2]);
+    by1 = max(by1, S.box[w][3]);
   }
-  if (g < total && J.aux && bx0 != INT_MAX) {
-    const PairDev& P = pairs[J.p];
+  TileJob J{p, aux ? 1 : 0, 0, 0, 0};
+  if (aux && bx0 != INT_MAX) {
+    const PairDev& P = pairs[p];
     const int u0 = max(0, bx0 - reach), u1 = min(P.Wa - 1, bx1 + reach);
     const int v0 = max(0, by0 - reach), v1 = min(P.Ha - 1, by1 + reach);
     const int bw = u1 - u0 + 1, bh = v1 - v0 + 1;
@@ -1133,56 +1154,56 @@ __device__ __forceinline__ TileJob tile_begin(const PairDev* __restrict__ pairs,
       }
     }
   }
+  if (threadIdx.x == 0) S.job[b] = J;
   cp_async_commit();
-  return J;
 }
 
 __global__ void __launch_bounds__(256, 2) k_refine_pairs(const PairDev* __restrict__ pairs, int total, int max_tiles,
                                                          RefineLevels L, int reach, int2* __restrict__ queue,
                                                          int* __restrict__ qcount) {
   extern __shared__ __align__(16) char smem[];
-  __shared__ int s_box[8][4];
-  int buf = 0;
-  TileJob cur = tile_begin(pairs, blockIdx.x, total, max_tiles, reach, s_box, smem);
+  __shared__ TileSmem S;
+  int b = 0;
+  tile_begin(pairs, blockIdx.x, total, max_tiles, reach, S, 0, smem);
   for (int g = blockIdx.x; g < total; g += gridDim.x) {
-    const TileJob nxt = tile_begin(pairs, g + gridDim.x, total, max_tiles, reach, s_box, smem + (buf ^ 1) * kTileBytes);
-    const PairDev& P = pairs[cur.p];
-    const __half* bdesc = P.db + (size_t)cur.n * 24;
-    int out = -1;
-    if (cur.work && !cur.aux) {  // no pruning aux (dim != 24 or unaligned rows): per-thread exact path
-      out = refine_dispatch(P, cur.pa, cur.n, L);
-      P.out_pa[cur.n] = out;
-      P.out_q[cur.n] = (float)sqrt((double)P.qa[out] * (double)P.qb[cur.n]);
+    __syncthreads();  // S.job[b] visible; slot b^1 free
+    tile_begin(pairs, g + gridDim.x, total, max_tiles, reach, S, b ^ 1, smem + (b ^ 1) * kTileBytes);
+    const TileJob J = S.job[b];
+    const int n = S.n[b][threadIdx.x], pa = S.pa[b][threadIdx.x];
+    const PairDev& P = pairs[J.p];
+    const __half* bdesc = P.db + (size_t)(n < 0 ? 0 : n) * 24;
+    if (n >= 0 && !J.aux) {  // no pruning aux (dim != 24 or unaligned rows): per-thread exact path
+      const int o = refine_dispatch(P, pa, n, L);
+      P.out_pa[n] = o;
+      P.out_q[n] = (float)sqrt((double)P.qa[o] * (double)P.qb[n]);
     }
     // loads that do not need the tile: b descriptor, centre descriptor, qb
+    const bool easy = n >= 0 && J.aux && J.bw > 0;
     BConst K;
     float fc = 0.0f, qb = 0.0f;
-    const bool easy = cur.work && cur.aux && cur.bw > 0;
     if (easy) {
       K = make_bconst(bdesc);
-      const uint4* ca = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)cur.pa;
+      const uint4* ca = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)pa;
       fc = dot8(__ldg(ca + 2), K.b2, dot8(__ldg(ca + 1), K.b1, dot8(__ldg(ca), K.b0, 0.0f)));
-      qb = P.qb[cur.n];
+      qb = P.qb[n];
     }
     cp_async_wait1();
     __syncthreads();
-    if (cur.work && cur.aux) {
+    if (n >= 0 && J.aux) {
+      int out = -1;
       if (easy) {
-        const uint4* s0 = reinterpret_cast<const uint4*>(smem + buf * kTileBytes);
-        const HeadTile T{s0, s0 + kTileCap, reinterpret_cast<const float4*>(s0 + 2 * kTileCap), cur.u0, cur.v0,
-                         cur.bw};
-        out = refine_easy(P, T, cur.pa, bdesc, K, fc, L);
+        const uint4* s0 = reinterpret_cast<const uint4*>(smem + b * kTileBytes);
+        const HeadTile T{s0, s0 + kTileCap, reinterpret_cast<const float4*>(s0 + 2 * kTileCap), J.u0, J.v0, J.bw};
+        out = refine_easy(P, T, pa, bdesc, K, fc, L);
         if (out >= 0) {
           const float qa = T.n[(out / P.Wa - T.v0) * T.bw + (out % P.Wa - T.u0)].w;
-          P.out_pa[cur.n] = out;
-          P.out_q[cur.n] = (float)sqrt((double)qa * (double)qb);
+          P.out_pa[n] = out;
+          P.out_q[n] = (float)sqrt((double)qa * (double)qb);
         }
       }
-      if (out < 0) queue[atomicAdd(qcount, 1)] = make_int2(cur.p, cur.n);
+      if (out < 0) queue[atomicAdd(qcount, 1)] = make_int2(J.p, n);
     }
-    __syncthreads();  // buffer `buf` is restaged two tiles from now
-    cur = nxt;
-    buf ^= 1;
+    b ^= 1;
   }
 }
 
@@ -1517,8 +1538,8 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     if (refine && L.n > 0) {
       {
         ProfScope ps(ctx, "k_refine");
-        int reach = 0;
-        for (int l = 0; l < L.n; ++l) reach += L.radius[l] * L.stride[l];
+        int reach = 0;  // windows stay centred on the LM match in k_refine_pairs
+        for (int l = 0; l < L.n; ++l) reach = std::max(reach, L.radius[l] * L.stride[l]);
         PMX_CUDA(cudaFuncSetAttribute((const void*)k_refine_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kRefineSmem));
         PMX_CUDA(cudaMemsetAsync(qcount, 0, sizeof(int), ctx.stream));
