@@ -37,6 +37,13 @@ UNIT = "px/s"
 H, W = 384, 512
 N_EDGES = 64
 ALG_BYTES_PER_PX = 133  # X_b 12 + X_a 12 + Q_a 4 + Q_b 4 + D_a 48 + D_b 48 + idx 4 + valid 1
+# Algorithmic bytes per b-pixel of each matching kernel:
+#  k_prep   X_a 12 + valid_a 1 + D_a 48 + Q_a 4                       = 65
+#  k_match  X_b 12 + valid_b 1 + X_a (one ray per pixel) 12 + pa/valid/q out 9 = 34
+#  k_refine D_a 48 + D_b 48 + Q_a 4 + Q_b 4 + pa/valid in 5 + pa/q out 8 = 117
+#  k_refine_hard: the same 117 B per queued pixel
+KERNEL_BYTES_PER_PX = {"k_prep": 65, "k_match": 34, "k_refine": 117}
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
 
 
 def _dist():
@@ -295,7 +302,8 @@ def run_pmx(args):
     ctx.set_stream(stream)
     mp, rp = match_params()
     outs = [MatchSet.empty(H * W, dev) for _ in mine]
-    batch = [p[1] for p in dev_pairs]
+    # resident buffers: the C-ABI argument arrays are built once (no per-step host work)
+    batch = ctx.prepare_match_batch([p[1] for p in dev_pairs], outs)
     # warm-up
     for _ in range(args.warmup):
         ctx.match_batch(batch, params=mp, refine=rp, outs=outs)
@@ -316,7 +324,8 @@ def run_pmx(args):
     ctx.profile_enable(False)
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    k_ms, k_n = ctx.profile_get("k_match")
+    kern = {k: ctx.profile_get(k) for k in ("k_prep", "k_match", "k_refine", "k_refine_hard")}
+    _, hard_px = ctx.profile_get("refine_hard_px")
     gpu_launches = ctx.kernel_launches - launches0
     ms_local = float(sum(step_ms))
     if dist:
@@ -358,8 +367,27 @@ def run_pmx(args):
 
     peaks, peak_kind = _peaks()
     if rank == 0:
-        kernel_bytes = ALG_BYTES_PER_PX * H * W * len(mine) * args.steps
-        achieved = kernel_bytes / (k_ms / 1e3) / 1e9 if k_ms > 0 else None
+        px_steps = H * W * len(mine) * args.steps
+        breakdown = {}
+        for k, (kms, kn) in kern.items():
+            px = hard_px if k == "k_refine_hard" else px_steps
+            nbytes = KERNEL_BYTES_PER_PX.get(k, 117) * px
+            breakdown[k] = {"ms_per_step": kms / args.steps, "launches_per_step": kn / args.steps,
+                            "share_of_step": kms / ms_local if ms_local > 0 else None,
+                            "alg_bytes_per_px": KERNEL_BYTES_PER_PX.get(k, 117),
+                            "achieved_gbs": nbytes / (kms / 1e3) / 1e9 if kms > 0 else None}
+        breakdown["k_refine_hard"]["queued_px_per_step"] = hard_px / args.steps
+        dom = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
+        achieved = breakdown[dom]["achieved_gbs"]
+        traffic = None
+        try:
+            with open(TRAFFIC_FILE) as f:
+                tr = json.load(f)
+            # ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch, per b-pixel,
+            # scaled to this run's average launch
+            traffic = tr[dom]["dram_bytes_per_px"] * px_steps / max(1, kern[dom][1])
+        except Exception:
+            pass
         cpu = None
         if world == 1 and not args.no_cpu:
             nedge = 6
@@ -376,9 +404,13 @@ def run_pmx(args):
                        "edges_per_rank": len(mine), "l2": "inputs larger than L2 (1.6 GB per step)",
                        "valid_fraction": valid_frac, "outputs_match_host_path": ok},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": None,
-                         "kernel": "k_match", "kernel_ms_per_step": k_ms / args.steps,
-                         "alg_bytes_per_px": ALG_BYTES_PER_PX, "peak_kind": peak_kind},
+                         "frac": (achieved / peaks["hbm_gbs"]) if achieved else None, "traffic": traffic,
+                         "kernel": dom, "alg_bytes_per_launch": breakdown[dom]["alg_bytes_per_px"] * px_steps
+                         / max(1, kern[dom][1]), "peak_kind": peak_kind,
+                         "path": {"alg_bytes_per_px": ALG_BYTES_PER_PX,
+                                  "achieved_gbs": ALG_BYTES_PER_PX * px_steps / (ms_local / 1e3) / 1e9},
+                         "note": "issue-bound (FP64 LM, fp16 FHFMA window search), not HBM-bound: see DESIGN.md"},
+            "kernels": breakdown,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_local},

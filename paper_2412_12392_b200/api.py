@@ -266,9 +266,21 @@ class Context:
             out.pixel_b = matches.pixel_b
         return out
 
+    def prepare_match_batch(self, pairs, outs: Optional[List[MatchSet]] = None) -> "PreparedBatch":
+        """Build the C-ABI pair/output arrays of a batch once (for buffers that
+        stay resident and are matched repeatedly, e.g. a benchmark loop)."""
+        return PreparedBatch(self, pairs, outs)
+
     def match_batch(self, pairs, params=None, refine=None, outs: Optional[List[MatchSet]] = None) -> List[MatchSet]:
         """Fused match_pointmaps (+ feature_refine when ``refine`` is given)
-        over independent pairs (X_a, X_b_in_a, F_a, F_b[, init])."""
+        over independent pairs (X_a, X_b_in_a, F_a, F_b[, init]), or over a
+        PreparedBatch (then ``outs`` is the batch's own)."""
+        if isinstance(pairs, PreparedBatch):
+            b = pairs
+            params = params or abi.default_match_params()
+            self._check(self.lib.pmx_match_batch(self.h, b.mem, C.c_int32(b.n), b.arr, C.byref(params),
+                                                 C.byref(refine) if refine is not None else None, b.oarr))
+            return b.outs
         keep = []
         structs = []
         mem = None
@@ -476,3 +488,34 @@ def sim3(R=None, t=None, s=1.0) -> abi.pmx_sim3:
         T.t[i] = float(t[i])
     T.s = float(s)
     return T
+
+
+class PreparedBatch:
+    """pmx_pair / pmx_matchset arrays of one batch, built once (see
+    Context.prepare_match_batch).  Holds references to every buffer."""
+
+    def __init__(self, ctx: "Context", pairs, outs: Optional[List[MatchSet]] = None):
+        self.keep = []
+        structs = []
+        mem = None
+        for p in pairs:
+            X_a, X_b, F_a, F_b = p[:4]
+            init = p[4] if len(p) > 4 else None
+            m = ctx._mem(X_a.xyz, X_b.xyz, F_a.descriptors, F_b.descriptors)
+            if mem is not None and m != mem:
+                raise PmxInvalidArgument(abi.PMX_ERR_INVALID_ARGUMENT, "mixed host and device pairs")
+            mem = m
+            ip = None
+            if init is not None:
+                ist = init.struct()
+                self.keep.append(ist)
+                ip = C.pointer(ist)
+            structs.append(abi.pmx_pair(X_a.struct(), X_b.struct(), F_a.struct(), F_b.struct(), ip))
+        self.n = len(structs)
+        self.mem = mem if mem is not None else abi.PMX_MEM_HOST
+        if outs is None:
+            outs = [MatchSet.empty(p[1].height * p[1].width, p[1].xyz.device if self.mem == abi.PMX_MEM_DEVICE
+                                   else None) for p in pairs]
+        self.pairs, self.outs = list(pairs), outs
+        self.arr = (abi.pmx_pair * max(1, self.n))(*structs)
+        self.oarr = (abi.pmx_matchset * max(1, self.n))(*[o.struct() for o in outs])

@@ -165,10 +165,12 @@ int pmx_destroy(pmx_context* c) {
   if (!c) return (int)PMX_OK;
   Context* ctx = reinterpret_cast<Context*>(c);
   cudaSetDevice(ctx->device);
+  if (ctx->stream && ctx->stream != ctx->own_stream) cudaStreamSynchronize(ctx->stream);  // adopted stream
   if (ctx->own_stream) {
     cudaStreamSynchronize(ctx->own_stream);
     cudaStreamDestroy(ctx->own_stream);
   }
+  for (auto& kv : ctx->dev_counters) cudaFree(kv.second);
   delete ctx;
   return (int)PMX_OK;
 }
@@ -220,6 +222,7 @@ int pmx_profile_reset(pmx_context* c) {
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     prof_clear(ctx);
     ctx.counters.clear();
+    for (auto& kv : ctx.dev_counters) PMX_CUDA(cudaMemset(kv.second, 0, sizeof(unsigned long long)));
     return (int)PMX_OK;
   });
 }
@@ -240,6 +243,13 @@ int pmx_profile_get(pmx_context* c, const char* kernel, double* total_ms, int64_
     }
     auto it = ctx.counters.find(kernel);
     if (it != ctx.counters.end()) n = it->second;  // counters report through `launches`
+    auto dc = ctx.dev_counters.find(kernel);
+    if (dc != ctx.dev_counters.end()) {
+      unsigned long long v = 0;
+      PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+      PMX_CUDA(cudaMemcpy(&v, dc->second, sizeof(v), cudaMemcpyDeviceToHost));
+      n += (int64_t)v;
+    }
     *total_ms = t;
     *launches = n;
     return (int)PMX_OK;

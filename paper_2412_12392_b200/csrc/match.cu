@@ -1207,6 +1207,13 @@ __global__ void __launch_bounds__(256, 2) k_refine_pairs(const PairDev* __restri
   }
 }
 
+__global__ void k_add_counts(const int* __restrict__ c, int n, unsigned long long* total) {
+  unsigned long long s = 0;
+  for (int i = threadIdx.x; i < n; i += 32) s += (unsigned)c[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (threadIdx.x == 0) *total += s;
+}
+
 // Persistent grid: resident blocks on every SM, capped by the tile count.
 static unsigned refine_grid(const Context& ctx, int tiles) {
   static int per_sm = -1;
@@ -1499,8 +1506,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
   DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
   DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
-  DevBuf qbuf(sizeof(int2) * (size_t)max_hwb * chunk + sizeof(int) * 4, ctx.stream);
-  int* qcount = reinterpret_cast<int*>(qbuf.as<char>() + sizeof(int2) * (size_t)max_hwb * chunk);
+  const int nchunks = (npairs + chunk - 1) / chunk;
+  DevBuf qbuf(sizeof(int2) * (size_t)max_hwb * chunk + sizeof(int) * nchunks, ctx.stream);
+  int* qcounts = reinterpret_cast<int*>(qbuf.as<char>() + sizeof(int2) * (size_t)max_hwb * chunk);  // per chunk
   int2* queue = qbuf.as<int2>();
   std::vector<PairDev> hp = host_pairs;
   char* base = scratch.as<char>();
@@ -1521,15 +1529,18 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   }
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
+  PMX_CUDA(cudaMemsetAsync(qcounts, 0, sizeof(int) * nchunks, ctx.stream));
   for (int c0 = 0; c0 < npairs; c0 += chunk) {
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
-    prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
-    int max_tiles = 0, max_tiles4 = 0;
-    for (int i = c0; i < c0 + cn; ++i) {
-      max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
-      max_tiles4 = std::max(max_tiles4, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 3) / 4));
+    int* qcount = qcounts + c0 / chunk;
+    {
+      ProfScope ps(ctx, "k_prep");
+      prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
     }
+    int max_tiles = 0;
+    for (int i = c0; i < c0 + cn; ++i)
+      max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
     {
       ProfScope ps(ctx, "k_match");
       k_match<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp);
@@ -1542,24 +1553,26 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
         for (int l = 0; l < L.n; ++l) reach = std::max(reach, L.radius[l] * L.stride[l]);
         PMX_CUDA(cudaFuncSetAttribute((const void*)k_refine_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kRefineSmem));
-        PMX_CUDA(cudaMemsetAsync(qcount, 0, sizeof(int), ctx.stream));
         k_refine_pairs<<<refine_grid(ctx, cn * max_tiles), 256, kRefineSmem, ctx.stream>>>(dp, cn * max_tiles, max_tiles, L, reach, queue, qcount);
       }
       {
         ProfScope ps(ctx, "k_refine_hard");
         k_refine_hard<<<ctx.num_sms * 8, 256, 0, ctx.stream>>>(dp, L, queue, qcount);
       }
-      if (ctx.profiling) {  // hard-queue occupancy, reported through pmx_profile_get("refine_hard_px")
-        int h = 0;
-        PMX_CUDA(cudaMemcpyAsync(&h, qcount, sizeof(int), cudaMemcpyDeviceToHost, ctx.stream));
-        PMX_CUDA(cudaStreamSynchronize(ctx.stream));
-        ctx.counters["refine_hard_px"] += h;
-        ctx.counters["refine_px"] += 0;
-      }
       launch_check(ctx, "k_refine_pairs");
     }
   }
-  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // hp lifetime / scratch reuse by the caller
+  if (ctx.profiling && refine && L.n > 0) {  // hard-queue occupancy: pmx_profile_get("refine_hard_px")
+    if (unsigned long long* hc = dev_counter(ctx, "refine_hard_px")) {
+      k_add_counts<<<1, 32, 0, ctx.stream>>>(qcounts, nchunks, hc);
+      launch_check(ctx, "k_add_counts");
+    }
+  }
+  // Device-memory calls on a caller-adopted stream (pmx_set_stream) stay
+  // asynchronous like any CUDA library call (scratch is stream-ordered and
+  // the pageable PairDev upload is staged before cudaMemcpyAsync returns);
+  // on the context's own stream they complete before returning.
+  if (ctx.stream == ctx.own_stream) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
 }
 
 // ------------------------------------------------------------ C-ABI glue

@@ -54,7 +54,19 @@ struct Context {
   bool profiling = false;
   std::vector<ProfEvent> prof;  // unresolved event pairs (pmx_profile_*)
   std::map<std::string, int64_t> counters;  // profiling counters (pmx_profile_get, total_ms = 0)
+  std::map<std::string, unsigned long long*> dev_counters;  // device-side counters, read at pmx_profile_get
 };
+
+// Device-side profiling counter `name` (allocated on first use, zeroed).
+inline unsigned long long* dev_counter(Context& ctx, const char* name) {
+  auto it = ctx.dev_counters.find(name);
+  if (it != ctx.dev_counters.end()) return it->second;
+  unsigned long long* p = nullptr;
+  if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  cudaMemsetAsync(p, 0, sizeof(unsigned long long), ctx.stream);
+  ctx.dev_counters[name] = p;
+  return p;
+}
 
 // CUDA-event bracket around one kernel launch on ctx.stream (when profiling).
 struct ProfScope {
