@@ -49,6 +49,11 @@ struct EdgeArgs {
   int N;
   int bpe;           // blocks per edge
   double* partials;  // [E][bpe][2][kAcc]
+  // ray mode: frozen-match preprocessing (k_pack_cloud / k_compact)
+  const float4* const* c4;  // [N]
+  const int4* packed;       // [E][seg]
+  const int* pk_total;      // [E]
+  int64_t seg;
 };
 
 __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
@@ -107,82 +112,99 @@ __device__ __forceinline__ float rsqrt_nr(float a) {  // ~0.5 ulp reciprocal squ
   return y * fmaf(-0.5f * a * y, y, 1.5f);
 }
 
-__device__ __forceinline__ void ray_accumulate(const PoseR<float>& T, const float* ref, const float* src,
-                                               float info, const WeightsDev& wp, float* acc) {
+struct RayW {  // per-edge weight constants (fp32)
+  float delta, delta2, lambda_d;
+};
+
+// Huber weight and cost of a whitened squared residual s2 = e^2 (tracking.cpp:
+// 22-30, 116-127) without a square root or a division on the quadratic side.
+__device__ __forceinline__ void huber2(float info, float s2, const RayW& c, float& w, float& cost) {
+  const float r = rsqrtf(s2);  // 1 / e  (inf at e = 0: quadratic side)
+  const bool quad = s2 <= c.delta2;
+  w = quad ? info : info * c.delta * r;
+  cost = quad ? 0.5f * s2 : c.delta * fmaf(s2, r, -0.5f * c.delta);
+}
+
+// One direction: ref point (with |ref| and 1/|ref| precomputed), src point
+// mapped by T.  info = q / sigma^2 of the match.
+__device__ __forceinline__ void ray_accumulate(const PoseR<float>& T, const float* ref, float dref, float iref,
+                                               const float* src, float info, const RayW& c, float* acc) {
   const float x0 = fmaf(T.sR[0], src[0], fmaf(T.sR[1], src[1], fmaf(T.sR[2], src[2], T.t[0])));
   const float x1 = fmaf(T.sR[3], src[0], fmaf(T.sR[4], src[1], fmaf(T.sR[5], src[2], T.t[1])));
   const float x2 = fmaf(T.sR[6], src[0], fmaf(T.sR[7], src[1], fmaf(T.sR[8], src[2], T.t[2])));
-  const float dd = x0 * x0 + x1 * x1 + x2 * x2;
-  const float rr = ref[0] * ref[0] + ref[1] * ref[1] + ref[2] * ref[2];
-  if (!(dd >= 1e-24f) || !(rr >= 1e-24f)) return;  // d, d_ref < 1e-12 (tracking.cpp:71, 78)
-  const float id = rsqrt_nr(dd), ir = rsqrt_nr(rr);
-  const float d = dd * id, dref = rr * ir;
+  const float dd = fmaf(x0, x0, fmaf(x1, x1, x2 * x2));
+  if (!(dd >= 1e-24f)) return;  // d < 1e-12 (tracking.cpp:71)
+  const float id = rsqrt_nr(dd);
+  const float d = dd * id;
   const float n0 = x0 * id, n1 = x1 * id, n2 = x2 * id;
-  const float r0 = ref[0] * ir - n0, r1 = ref[1] * ir - n1, r2 = ref[2] * ir - n2;
+  const float r0 = fmaf(ref[0], iref, -n0), r1 = fmaf(ref[1], iref, -n1), r2 = fmaf(ref[2], iref, -n2);
   const float rd = dref - d;
-  const float delta = (float)wp.huber_delta;
-  const float sq = r0 * r0 + r1 * r1 + r2 * r2;
-  const float e = sqrtf(info) * sqrtf(sq);
-  const float info_d = (float)wp.distance_weight * info;
-  const float e_d = sqrtf(info_d) * fabsf(rd);
-  const float w = info * (e <= delta ? 1.0f : delta / e);
-  const float wd = info_d * (e_d <= delta ? 1.0f : delta / e_d);
-  acc[28] += (e <= delta ? 0.5f * e * e : delta * (e - 0.5f * delta)) +
-             (e_d <= delta ? 0.5f * e_d * e_d : delta * (e_d - 0.5f * delta));
-  const float nr = n0 * r0 + n1 * r1 + n2 * r2;
-  if (w > 0.0f) {  // tracking.cpp:193-194: rows with w <= 0 are skipped
-    const float a = w * id * id, wi = w * id;
-    acc[0] += a;
-    acc[1] += w;
-    acc[8] += w * n0 * n0;
-    acc[9] += w * n0 * n1;
-    acc[10] += w * n0 * n2;
-    acc[11] += w * n1 * n1;
-    acc[12] += w * n1 * n2;
-    acc[13] += w * n2 * n2;
-    acc[14] += wi * n0;
-    acc[15] += wi * n1;
-    acc[16] += wi * n2;
-    acc[2] -= a * n0 * n0;
-    acc[3] -= a * n0 * n1;
-    acc[4] -= a * n0 * n2;
-    acc[5] -= a * n1 * n1;
-    acc[6] -= a * n1 * n2;
-    acc[7] -= a * n2 * n2;
-    acc[21] -= wi * (r0 - n0 * nr);
-    acc[22] -= wi * (r1 - n1 * nr);
-    acc[23] -= wi * (r2 - n2 * nr);
-    acc[24] -= w * (n1 * r2 - n2 * r1);
-    acc[25] -= w * (n2 * r0 - n0 * r2);
-    acc[26] -= w * (n0 * r1 - n1 * r0);
-  }
-  if (wd > 0.0f) {
-    const float wdd = wd * d;
-    acc[2] += wd * n0 * n0;
-    acc[3] += wd * n0 * n1;
-    acc[4] += wd * n0 * n2;
-    acc[5] += wd * n1 * n1;
-    acc[6] += wd * n1 * n2;
-    acc[7] += wd * n2 * n2;
-    acc[17] += wdd * n0;
-    acc[18] += wdd * n1;
-    acc[19] += wdd * n2;
-    acc[20] += wdd * d;
-    acc[21] -= wd * rd * n0;
-    acc[22] -= wd * rd * n1;
-    acc[23] -= wd * rd * n2;
-    acc[27] -= wdd * rd;
-  }
+  const float sq = fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
+  const float info_d = c.lambda_d * info;
+  float w, wd, cr, cd;
+  huber2(info, info * sq, c, w, cr);
+  huber2(info_d, info_d * rd * rd, c, wd, cd);
+  acc[28] += cr + cd;
+  const float nr = fmaf(n0, r0, fmaf(n1, r1, n2 * r2));
+  // tracking.cpp:193-194 skips rows with w <= 0; here w, wd > 0 always (info > 0)
+  const float a = w * id * id, wi = w * id, wdd = wd * d;
+  const float m00 = n0 * n0, m01 = n0 * n1, m02 = n0 * n2, m11 = n1 * n1, m12 = n1 * n2, m22 = n2 * n2;
+  const float dt = wd - a;  // beta = w_d - w/d^2 on n n^T in H_tt
+  acc[0] += a;
+  acc[1] += w;
+  acc[2] = fmaf(dt, m00, acc[2]);
+  acc[3] = fmaf(dt, m01, acc[3]);
+  acc[4] = fmaf(dt, m02, acc[4]);
+  acc[5] = fmaf(dt, m11, acc[5]);
+  acc[6] = fmaf(dt, m12, acc[6]);
+  acc[7] = fmaf(dt, m22, acc[7]);
+  acc[8] = fmaf(w, m00, acc[8]);
+  acc[9] = fmaf(w, m01, acc[9]);
+  acc[10] = fmaf(w, m02, acc[10]);
+  acc[11] = fmaf(w, m11, acc[11]);
+  acc[12] = fmaf(w, m12, acc[12]);
+  acc[13] = fmaf(w, m22, acc[13]);
+  acc[14] = fmaf(wi, n0, acc[14]);
+  acc[15] = fmaf(wi, n1, acc[15]);
+  acc[16] = fmaf(wi, n2, acc[16]);
+  acc[17] = fmaf(wdd, n0, acc[17]);
+  acc[18] = fmaf(wdd, n1, acc[18]);
+  acc[19] = fmaf(wdd, n2, acc[19]);
+  acc[20] = fmaf(wdd, d, acc[20]);
+  const float wdr = wd * rd;
+  acc[21] -= fmaf(wi, fmaf(-n0, nr, r0), wdr * n0);
+  acc[22] -= fmaf(wi, fmaf(-n1, nr, r1), wdr * n1);
+  acc[23] -= fmaf(wi, fmaf(-n2, nr, r2), wdr * n2);
+  acc[24] -= w * fmaf(n1, r2, -n2 * r1);
+  acc[25] -= w * fmaf(n2, r0, -n0 * r2);
+  acc[26] -= w * fmaf(n0, r1, -n1 * r0);
+  acc[27] -= wdd * rd;
 }
 
+// Block sum of N per-thread fp32 accumulators into FP64 (out_row[N]): each
+// warp transposes its 32 x N partials through shared memory (two halves) so
+// that lane l sums column l in FP64, then the warps' sums are added.
 template <int N>
 __device__ inline void block_reduce_n(const float* acc, double* __restrict__ out_row) {
+  constexpr int HALF = (N + 1) / 2;
+  constexpr int LD = HALF | 1;  // odd row stride: conflict-free rows and columns
+  __shared__ float tr[8][32 * LD];
   __shared__ double sh[8][N];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll 1
-  for (int i = 0; i < N; ++i) {
-    const double v = warp_sum((double)acc[i]);
-    if (lane == 0) sh[warp][i] = v;
+  float* t = tr[warp];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int i = 0; i < HALF; ++i)
+      if (h * HALF + i < N) t[lane * LD + i] = acc[h * HALF + i];
+    __syncwarp();
+    if (lane < HALF && h * HALF + lane < N) {
+      double s = 0.0;
+#pragma unroll 8
+      for (int r = 0; r < 32; ++r) s += (double)t[r * LD + lane];
+      sh[warp][h * HALF + lane] = s;
+    }
+    __syncwarp();
   }
   __syncthreads();
   const int nw = blockDim.x >> 5;
@@ -194,33 +216,144 @@ __device__ inline void block_reduce_n(const float* acc, double* __restrict__ out
   __syncthreads();
 }
 
-// Both directed constraints of an edge from one read of every match.
-__global__ void __launch_bounds__(256, 3) k_edge_terms_ray(EdgeArgs A, int e0) {
+// Frozen-match preprocessing (once per backend call; matches and canonicals do
+// not change during global_optimize): clouds -> float4 {x, y, z, |p|^2} (w < 0
+// = invalid pixel), and every edge's matches -> a compacted int4 list
+// {pa, pb, q bits, 0} of the matches that pass all the pose-independent skips
+// (valid flag, index range, both pointmaps valid, q > q_min), in match order.
+__global__ void k_pack_cloud(const float* __restrict__ xyz, const uint8_t* __restrict__ valid, int hw,
+                             float4* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= hw) return;
+  const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+  const bool v = valid ? valid[i] != 0 : true;
+  out[i] = make_float4(x, y, z, v ? fmaf(x, x, fmaf(y, y, z * z)) : -1.0f);
+}
+
+constexpr int kCompactPer = 8;                     // consecutive matches per thread
+constexpr int kCompactChunk = 256 * kCompactPer;   // matches per block
+
+struct CompactArgs {
+  const MatchesDev* matches;
+  const int2* edges;
+  const float4* const* c4;  // [N]
+  const CloudDev* clouds;
+  const double* qmin;
+  int N, chunks;
+  int64_t seg;     // slots per edge in `packed`
+  int* cnt;        // [E][chunks]
+  int* total;      // [E]
+  int4* packed;    // [E][seg]
+};
+
+__device__ __forceinline__ bool match_survives(const CompactArgs& A, const MatchesDev& M, int2 ij, double qmin,
+                                               int64_t k, int4& rec) {
+  if (k >= M.count) return false;
+  if (M.valid && !M.valid[k]) return false;
+  const int pa = M.pa[k], pb = M.pb ? M.pb[k] : (int)k;
+  const CloudDev& Ci = A.clouds[ij.x];
+  const CloudDev& Cj = A.clouds[ij.y];
+  if (pa < 0 || pb < 0 || pa >= Ci.H * Ci.W || pb >= Cj.H * Cj.W) return false;
+  if (A.c4[ij.x][pa].w < 0.0f || A.c4[ij.y][pb].w < 0.0f) return false;  // tracking.cpp:62
+  const float q = M.q[k];
+  if (!((double)q > qmin)) return false;  // robust_weight excludes (tracking.cpp:10-13)
+  rec = make_int4(pa, pb, __float_as_int(q), 0);
+  return true;
+}
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
+  const int e = blockIdx.y, c = blockIdx.x;
+  const int2 ij = A.edges[e];
+  const MatchesDev M = A.matches[e];
+  const bool ok = ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N;  // backend.cpp:61
+  const double qmin = A.qmin[e];
+  const int64_t k0 = (int64_t)c * kCompactChunk + (int64_t)threadIdx.x * kCompactPer;
+  unsigned keep = 0;
+  int4 rec[kCompactPer];
+#pragma unroll
+  for (int j = 0; j < kCompactPer; ++j)
+    if (ok && match_survives(A, M, ij, qmin, k0 + j, rec[j])) keep |= 1u << j;
+  const int n = __popc(keep);
+  // block exclusive scan of the per-thread counts
+  __shared__ int wsum[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int before = 0, block_total = 0;
+  for (int w = 0; w < 8; ++w) {
+    before += w < warp ? wsum[w] : 0;
+    block_total += wsum[w];
+  }
+  if (!WRITE) {
+    if (threadIdx.x == 0) A.cnt[(size_t)e * A.chunks + c] = block_total;
+    return;
+  }
+  int64_t off = 0;
+  for (int cc = 0; cc < c; ++cc) off += A.cnt[(size_t)e * A.chunks + cc];
+  if (c == 0 && threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int cc = 0; cc < A.chunks; ++cc) t += A.cnt[(size_t)e * A.chunks + cc];
+    A.total[e] = (int)t;
+  }
+  int4* out = A.packed + (size_t)e * A.seg + off + before + (incl - n);
+#pragma unroll
+  for (int j = 0; j < kCompactPer; ++j)
+    if (keep & (1u << j)) *out++ = rec[j];
+}
+
+// Both directed constraints of one compacted match.
+__device__ __forceinline__ void ray_match(const PoseR<float>& T1, const PoseR<float>& T2, const int4 m,
+                                          const float4 Pi, const float4 Pj, float inv_s2, const RayW& c,
+                                          float* acc) {
+  const float pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
+  const float info = __int_as_float(m.z) * inv_s2;
+  if (Pi.w >= 1e-24f) {  // ref = i; |ref| < 1e-12 (or NaN) skips the row (tracking.cpp:78)
+    const float ii = rsqrt_nr(Pi.w);
+    ray_accumulate(T1, pi, Pi.w * ii, ii, pj, info, c, acc);  // ref = i, src = j (swapped)
+  }
+  if (Pj.w >= 1e-24f) {
+    const float ij = rsqrt_nr(Pj.w);
+    ray_accumulate(T2, pj, Pj.w * ij, ij, pi, info, c, acc + kRayAcc);  // ref = j, src = i
+  }
+}
+
+// Both directed constraints of an edge from one read of its compacted matches
+// (two matches in flight per thread).
+__global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
-  const MatchesDev M = A.matches[e];
   float acc[2 * kRayAcc];
 #pragma unroll
   for (int i = 0; i < 2 * kRayAcc; ++i) acc[i] = 0.0f;
   if (ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N) {
-    const CloudDev Xi = A.clouds[ij.x], Xj = A.clouds[ij.y];
+    const float4* __restrict__ Ci = A.c4[ij.x];
+    const float4* __restrict__ Cj = A.c4[ij.y];
+    const int4* __restrict__ P = A.packed + (size_t)e * A.seg;
+    const int64_t cnt = A.pk_total[e];
     const PoseR<float> T1 = A.rel[2 * e], T2 = A.rel[2 * e + 1];
-    const double q_min = A.qmin[e];
     const float inv_s2 = (float)(1.0 / A.wp.sigma2);
+    const RayW c{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta),
+                 (float)A.wp.distance_weight};
     const int64_t stride = (int64_t)A.bpe * blockDim.x;
-    const int hwi = Xi.H * Xi.W, hwj = Xj.H * Xj.W;
-    for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < M.count; k += stride) {
-      const int pa = __ldg(M.pa + k);
-      const int pb = M.pb ? __ldg(M.pb + k) : (int)k;
-      if ((M.valid && !__ldg(M.valid + k)) || pa < 0 || pb < 0 || pa >= hwi || pb >= hwj) continue;
-      float pi[3], pj[3];
-      if (!load_point(Xi, pa, pi) || !load_point(Xj, pb, pj)) continue;  // tracking.cpp:62
-      const float q = __ldg(M.q + k);
-      if (!((double)q > q_min)) continue;  // robust_weight (tracking.cpp:10-13)
-      const float info = q * inv_s2;
-      ray_accumulate(T1, pi, pj, info, A.wp, acc);             // ref = i, src = j (swapped)
-      ray_accumulate(T2, pj, pi, info, A.wp, acc + kRayAcc);   // ref = j, src = i
+    int64_t k = (int64_t)b * blockDim.x + threadIdx.x;
+    for (; k + stride < cnt; k += 2 * stride) {
+      const int4 m0 = __ldg(P + k), m1 = __ldg(P + k + stride);
+      const float4 a0 = __ldg(Ci + m0.x), b0 = __ldg(Cj + m0.y);
+      const float4 a1 = __ldg(Ci + m1.x), b1 = __ldg(Cj + m1.y);
+      ray_match(T1, T2, m0, a0, b0, inv_s2, c, acc);
+      ray_match(T1, T2, m1, a1, b1, inv_s2, c, acc);
+    }
+    if (k < cnt) {
+      const int4 m0 = __ldg(P + k);
+      ray_match(T1, T2, m0, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
     }
   }
   block_reduce_n<2 * kRayAcc>(acc, A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
@@ -675,7 +808,63 @@ struct DevGraph {
   std::vector<CloudDev> hclouds;
   std::vector<MatchesDev> hmatches;
   int64_t max_count = 0;
+  // ray mode: frozen-match preprocessing
+  bool packed = false;
+  DevBuf c4buf, c4ptrs, pk, pk_cnt, pk_total;
+  int64_t seg = 0;
 };
+
+// Pack clouds / compact the matches of every edge (ray mode, once per call).
+static void pack_graph(Context& ctx, DevGraph& G) {
+  size_t tot = 0;
+  for (const auto& c : G.hclouds) tot += (size_t)c.H * c.W;
+  G.c4buf = DevBuf(sizeof(float4) * std::max<size_t>(tot, 1), ctx.stream);
+  std::vector<const float4*> ptrs(std::max(G.N, 1), nullptr);
+  size_t off = 0;
+  for (int k = 0; k < G.N; ++k) {
+    const int hw = G.hclouds[k].H * G.hclouds[k].W;
+    float4* dst = G.c4buf.as<float4>() + off;
+    k_pack_cloud<<<(hw + 255) / 256, 256, 0, ctx.stream>>>(G.hclouds[k].xyz, G.hclouds[k].valid, hw, dst);
+    launch_check(ctx, "k_pack_cloud");
+    ptrs[k] = dst;
+    off += hw;
+  }
+  G.c4ptrs = DevBuf(sizeof(float4*) * ptrs.size(), ctx.stream);
+  PMX_CUDA(cudaMemcpyAsync(G.c4ptrs.p, ptrs.data(), G.c4ptrs.bytes, cudaMemcpyHostToDevice, ctx.stream));
+  G.seg = std::max<int64_t>(G.max_count, 1);
+  const int chunks = (int)std::max<int64_t>(1, (G.max_count + kCompactChunk - 1) / kCompactChunk);
+  G.pk = DevBuf(sizeof(int4) * (size_t)G.seg * std::max(G.E, 1), ctx.stream);
+  G.pk_cnt = DevBuf(sizeof(int) * (size_t)chunks * std::max(G.E, 1), ctx.stream);
+  G.pk_total = DevBuf(sizeof(int) * std::max(G.E, 1), ctx.stream);
+  PMX_CUDA(cudaMemsetAsync(G.pk_total.p, 0, G.pk_total.bytes, ctx.stream));
+  CompactArgs A;
+  A.matches = G.matches.as<MatchesDev>();
+  A.edges = G.edges_dev.as<int2>();
+  A.c4 = G.c4ptrs.as<const float4*>();
+  A.clouds = G.clouds.as<CloudDev>();
+  A.qmin = G.qmin.as<double>();
+  A.N = G.N;
+  A.chunks = chunks;
+  A.seg = G.seg;
+  A.cnt = G.pk_cnt.as<int>();
+  A.total = G.pk_total.as<int>();
+  A.packed = G.pk.as<int4>();
+  for (int e0 = 0; e0 < G.E; e0 += 65535) {
+    const int en = std::min(65535, G.E - e0);
+    CompactArgs B = A;
+    B.matches += e0;
+    B.edges += e0;
+    B.qmin += e0;
+    B.cnt += (size_t)e0 * chunks;
+    B.total += e0;
+    B.packed += (size_t)e0 * G.seg;
+    k_compact<false><<<dim3(chunks, en), 256, 0, ctx.stream>>>(B);
+    launch_check(ctx, "k_compact_count");
+    k_compact<true><<<dim3(chunks, en), 256, 0, ctx.stream>>>(B);
+    launch_check(ctx, "k_compact");
+  }
+  G.packed = true;
+}
 
 static WeightsDev backend_weights(const pmx_backend_params& p) {
   WeightsDev w;
@@ -735,6 +924,7 @@ static void stage_graph(Context& ctx, Stager& st, const pmx_graph* g, const pmx_
     G.segs = DevBuf(sizeof(SelSeg) * G.E, ctx.stream);
     PMX_CUDA(cudaMemcpyAsync(G.segs.p, segs.data(), sizeof(SelSeg) * G.E, cudaMemcpyHostToDevice, ctx.stream));
     segmented_median(ctx, G.segs.as<SelSeg>(), G.E, G.max_count, G.selscratch);
+    if (p.mode == PMX_TRACK_RAY) pack_graph(ctx, G);
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // segs host vector goes out of scope
   }
 }
@@ -761,7 +951,9 @@ static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, c
   }
   DevBuf drel(sizeof(PoseR<float>) * rel.size(), ctx.stream);
   PMX_CUDA(cudaMemcpyAsync(drel.p, rel.data(), drel.bytes, cudaMemcpyHostToDevice, ctx.stream));
-  const int bpe = (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 4095) / 4096));
+  // about two waves of 2 resident blocks per SM, >= 16 matches per thread
+  const int64_t want = (2LL * 2 * ctx.num_sms + G.E - 1) / std::max(1, G.E);
+  const int bpe = (int)std::max<int64_t>(1, std::min<int64_t>(want, (G.max_count + 4095) / 4096));
   DevBuf partials(sizeof(double) * (size_t)G.E * bpe * 2 * kAcc, ctx.stream);
   EdgeArgs A;
   A.clouds = G.clouds.as<CloudDev>();
@@ -777,6 +969,11 @@ static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, c
   A.bpe = bpe;
   A.partials = partials.as<double>();
   const bool ray = p.mode == PMX_TRACK_RAY;
+  require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
+  A.c4 = ray ? G.c4ptrs.as<const float4*>() : nullptr;
+  A.packed = ray ? G.pk.as<int4>() : nullptr;
+  A.pk_total = ray ? G.pk_total.as<int>() : nullptr;
+  A.seg = G.seg;
   if (ray) {  // closed-form partials are 2 x 29 per block
     partials = DevBuf(sizeof(double) * (size_t)G.E * bpe * 2 * kRayAcc, ctx.stream);
     A.partials = partials.as<double>();
