@@ -42,6 +42,7 @@ struct EdgeArgs {
   const MatchesDev* matches;  // [E]  (pixel_a in i, pixel_b in j)
   const int2* edges;          // [E]
   const PoseR<float>* rel;    // [E][2]: dir1 = T_i^-1 T_j (ref i), dir2 = T_j^-1 T_i (ref j)
+  const PoseR<double>* rel64; // [E][2]: the same poses in FP64 (ray mode)
   const double* qmin;         // [E]
   WeightsDev wp;
   IntrDev K;
@@ -88,132 +89,6 @@ __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
     }
     block_reduce_to(acc, A.partials + (((size_t)e * A.bpe + b) * 2 + dir) * kAcc);
   }
-}
-
-// ---------------------------------------------------------------------------
-// Ray mode, closed form (the hot path).  For x = T X_src, d = |x|, n = x/d,
-// P = I - n n^T and the rows J_ray = [-P/d, [x]x/d, 0], J_d = [-n^T, 0, -d]
-// of tracking.cpp:82-87, the per-match normal equations collapse to
-//   H_tt = (w/d^2) I + (w_d - w/d^2) n n^T     H_tw = -[(w/d) n]x
-//   H_ww = w I - w n n^T                         H_ts = w_d d n,  H_ss = w_d d^2
-//   g_t  = -(w/d)(r - n (n.r)) - w_d r_d n      g_w = -w (n x r),  g_s = -w_d d r_d
-// so one direction needs 29 running sums instead of 28+7 per row of J:
-//   0 sum(w/d^2)  1 sum(w)  2-7 sum(beta n n^T)  8-13 sum(w n n^T)
-//   14-16 sum((w/d) n)  17-19 sum(w_d d n)  20 sum(w_d d^2)  21-27 g  28 cost
-constexpr int kRayAcc = 29;
-
-struct RayDir {  // per-direction pose in fp32 (s R, t)
-  float sR[9];
-  float t[3];
-};
-
-__device__ __forceinline__ float rsqrt_nr(float a) {  // ~0.5 ulp reciprocal square root
-  const float y = rsqrtf(a);
-  return y * fmaf(-0.5f * a * y, y, 1.5f);
-}
-
-struct RayW {  // per-edge weight constants (fp32)
-  float delta, delta2, lambda_d;
-};
-
-// Huber weight and cost of a whitened squared residual s2 = e^2 (tracking.cpp:
-// 22-30, 116-127) without a square root or a division on the quadratic side.
-__device__ __forceinline__ void huber2(float info, float s2, const RayW& c, float& w, float& cost) {
-  const float r = rsqrtf(s2);  // 1 / e  (inf at e = 0: quadratic side)
-  const bool quad = s2 <= c.delta2;
-  w = quad ? info : info * c.delta * r;
-  cost = quad ? 0.5f * s2 : c.delta * fmaf(s2, r, -0.5f * c.delta);
-}
-
-// One direction: ref point (with |ref| and 1/|ref| precomputed), src point
-// mapped by T.  info = q / sigma^2 of the match.
-__device__ __forceinline__ void ray_accumulate(const PoseR<float>& T, const float* ref, float dref, float iref,
-                                               const float* src, float info, const RayW& c, float* acc) {
-  const float x0 = fmaf(T.sR[0], src[0], fmaf(T.sR[1], src[1], fmaf(T.sR[2], src[2], T.t[0])));
-  const float x1 = fmaf(T.sR[3], src[0], fmaf(T.sR[4], src[1], fmaf(T.sR[5], src[2], T.t[1])));
-  const float x2 = fmaf(T.sR[6], src[0], fmaf(T.sR[7], src[1], fmaf(T.sR[8], src[2], T.t[2])));
-  const float dd = fmaf(x0, x0, fmaf(x1, x1, x2 * x2));
-  if (!(dd >= 1e-24f)) return;  // d < 1e-12 (tracking.cpp:71)
-  const float id = rsqrt_nr(dd);
-  const float d = dd * id;
-  const float n0 = x0 * id, n1 = x1 * id, n2 = x2 * id;
-  const float r0 = fmaf(ref[0], iref, -n0), r1 = fmaf(ref[1], iref, -n1), r2 = fmaf(ref[2], iref, -n2);
-  const float rd = dref - d;
-  const float sq = fmaf(r0, r0, fmaf(r1, r1, r2 * r2));
-  const float info_d = c.lambda_d * info;
-  float w, wd, cr, cd;
-  huber2(info, info * sq, c, w, cr);
-  huber2(info_d, info_d * rd * rd, c, wd, cd);
-  acc[28] += cr + cd;
-  const float nr = fmaf(n0, r0, fmaf(n1, r1, n2 * r2));
-  // tracking.cpp:193-194 skips rows with w <= 0; here w, wd > 0 always (info > 0)
-  const float a = w * id * id, wi = w * id, wdd = wd * d;
-  const float m00 = n0 * n0, m01 = n0 * n1, m02 = n0 * n2, m11 = n1 * n1, m12 = n1 * n2, m22 = n2 * n2;
-  const float dt = wd - a;  // beta = w_d - w/d^2 on n n^T in H_tt
-  acc[0] += a;
-  acc[1] += w;
-  acc[2] = fmaf(dt, m00, acc[2]);
-  acc[3] = fmaf(dt, m01, acc[3]);
-  acc[4] = fmaf(dt, m02, acc[4]);
-  acc[5] = fmaf(dt, m11, acc[5]);
-  acc[6] = fmaf(dt, m12, acc[6]);
-  acc[7] = fmaf(dt, m22, acc[7]);
-  acc[8] = fmaf(w, m00, acc[8]);
-  acc[9] = fmaf(w, m01, acc[9]);
-  acc[10] = fmaf(w, m02, acc[10]);
-  acc[11] = fmaf(w, m11, acc[11]);
-  acc[12] = fmaf(w, m12, acc[12]);
-  acc[13] = fmaf(w, m22, acc[13]);
-  acc[14] = fmaf(wi, n0, acc[14]);
-  acc[15] = fmaf(wi, n1, acc[15]);
-  acc[16] = fmaf(wi, n2, acc[16]);
-  acc[17] = fmaf(wdd, n0, acc[17]);
-  acc[18] = fmaf(wdd, n1, acc[18]);
-  acc[19] = fmaf(wdd, n2, acc[19]);
-  acc[20] = fmaf(wdd, d, acc[20]);
-  const float wdr = wd * rd;
-  acc[21] -= fmaf(wi, fmaf(-n0, nr, r0), wdr * n0);
-  acc[22] -= fmaf(wi, fmaf(-n1, nr, r1), wdr * n1);
-  acc[23] -= fmaf(wi, fmaf(-n2, nr, r2), wdr * n2);
-  acc[24] -= w * fmaf(n1, r2, -n2 * r1);
-  acc[25] -= w * fmaf(n2, r0, -n0 * r2);
-  acc[26] -= w * fmaf(n0, r1, -n1 * r0);
-  acc[27] -= wdd * rd;
-}
-
-// Block sum of N per-thread fp32 accumulators into FP64 (out_row[N]): each
-// warp transposes its 32 x N partials through shared memory (two halves) so
-// that lane l sums column l in FP64, then the warps' sums are added.
-template <int N>
-__device__ inline void block_reduce_n(const float* acc, double* __restrict__ out_row) {
-  constexpr int HALF = (N + 1) / 2;
-  constexpr int LD = HALF | 1;  // odd row stride: conflict-free rows and columns
-  __shared__ float tr[8][32 * LD];
-  __shared__ double sh[8][N];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float* t = tr[warp];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-#pragma unroll
-    for (int i = 0; i < HALF; ++i)
-      if (h * HALF + i < N) t[lane * LD + i] = acc[h * HALF + i];
-    __syncwarp();
-    if (lane < HALF && h * HALF + lane < N) {
-      double s = 0.0;
-#pragma unroll 8
-      for (int r = 0; r < 32; ++r) s += (double)t[r * LD + lane];
-      sh[warp][h * HALF + lane] = s;
-    }
-    __syncwarp();
-  }
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < nw; ++w) s += sh[w][i];
-    out_row[i] = s;
-  }
-  __syncthreads();
 }
 
 // Frozen-match preprocessing (once per backend call; matches and canonicals do
@@ -309,18 +184,21 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
 }
 
 // Both directed constraints of one compacted match.
-__device__ __forceinline__ void ray_match(const PoseR<float>& T1, const PoseR<float>& T2, const int4 m,
+__device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<double>& T2, const int4 m,
                                           const float4 Pi, const float4 Pj, float inv_s2, const RayW& c,
                                           float* acc) {
   const float pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
+  const double di[3] = {Pi.x, Pi.y, Pi.z}, dj[3] = {Pj.x, Pj.y, Pj.z};
   const float info = __int_as_float(m.z) * inv_s2;
   if (Pi.w >= 1e-24f) {  // ref = i; |ref| < 1e-12 (or NaN) skips the row (tracking.cpp:78)
     const float ii = rsqrt_nr(Pi.w);
-    ray_accumulate(T1, pi, Pi.w * ii, ii, pj, info, c, acc);  // ref = i, src = j (swapped)
+    const double rr = fma(di[0], di[0], fma(di[1], di[1], di[2] * di[2]));
+    ray_accumulate(T1, di, rr, Pi.w * ii, ii, pi, dj, info, c, acc);  // ref = i, src = j (swapped)
   }
   if (Pj.w >= 1e-24f) {
     const float ij = rsqrt_nr(Pj.w);
-    ray_accumulate(T2, pj, Pj.w * ij, ij, pi, info, c, acc + kRayAcc);  // ref = j, src = i
+    const double rr = fma(dj[0], dj[0], fma(dj[1], dj[1], dj[2] * dj[2]));
+    ray_accumulate(T2, dj, rr, Pj.w * ij, ij, pj, di, info, c, acc + kRayAcc);  // ref = j, src = i
   }
 }
 
@@ -338,7 +216,7 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
     const float4* __restrict__ Cj = A.c4[ij.y];
     const int4* __restrict__ P = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
-    const PoseR<float> T1 = A.rel[2 * e], T2 = A.rel[2 * e + 1];
+    const PoseR<double> T1 = A.rel64[2 * e], T2 = A.rel64[2 * e + 1];
     const float inv_s2 = (float)(1.0 / A.wp.sigma2);
     const RayW c{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta),
                  (float)A.wp.distance_weight};
@@ -370,26 +248,14 @@ __global__ void k_edge_sum_ray(const double* __restrict__ partials, int bpe, int
   }
   __syncthreads();
   if (threadIdx.x >= 2) return;
-  const double* c = s + kRayAcc * threadIdx.x;
-  double H[7][7] = {};
-  const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      H[i][j] = (i == j ? c[0] : 0.0) + c[2 + sym[i][j]];
-      H[3 + i][3 + j] = (i == j ? c[1] : 0.0) - c[8 + sym[i][j]];
-    }
-  const double v0 = c[14], v1 = c[15], v2 = c[16];  // H_tw = -[v]x
-  const double S[3][3] = {{0, -v2, v1}, {v2, 0, -v0}, {-v1, v0, 0}};
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) H[i][3 + j] = -S[i][j];
-  for (int i = 0; i < 3; ++i) H[i][6] = c[17 + i];
-  H[6][6] = c[20];
+  double H[49], g[7], cost;
+  ray_expand(s + kRayAcc * threadIdx.x, H, g, &cost);
   double* out = terms + (size_t)e * PMX_EDGE_TERMS + 36 * threadIdx.x;
   int idx = 0;
   for (int a = 0; a < 7; ++a)
-    for (int b = a; b < 7; ++b) out[idx++] = H[a][b];
-  for (int a = 0; a < 7; ++a) out[28 + a] = c[21 + a];
-  out[35] = c[28];
+    for (int b = a; b < 7; ++b) out[idx++] = H[a * 7 + b];
+  for (int a = 0; a < 7; ++a) out[28 + a] = g[a];
+  out[35] = cost;
 }
 
 // terms[e] = {H1 (28), g1 (7), cost1, H2 (28), g2 (7), cost2}
@@ -943,14 +809,21 @@ static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, c
                        int e1, double* terms) {
   if (e1 <= e0) return;
   std::vector<PoseR<float>> rel(2 * (size_t)G.E);
+  std::vector<PoseR<double>> rel64(2 * (size_t)G.E);
   for (int e = e0; e < e1; ++e) {
     const int i = G.edges[e].x, j = G.edges[e].y;
     if (i < 0 || j < 0 || i >= G.N || j >= G.N) continue;
-    rel[2 * e] = make_pose<float>(sim3_mul(sim3_inv(P[i]), P[j]));      // relative_pose(ref=i, src=j)
-    rel[2 * e + 1] = make_pose<float>(sim3_mul(sim3_inv(P[j]), P[i]));  // relative_pose(ref=j, src=i)
+    const DSim3 a = sim3_mul(sim3_inv(P[i]), P[j]);  // relative_pose(ref=i, src=j)
+    const DSim3 b = sim3_mul(sim3_inv(P[j]), P[i]);  // relative_pose(ref=j, src=i)
+    rel[2 * e] = make_pose<float>(a);
+    rel[2 * e + 1] = make_pose<float>(b);
+    rel64[2 * e] = make_pose<double>(a);
+    rel64[2 * e + 1] = make_pose<double>(b);
   }
   DevBuf drel(sizeof(PoseR<float>) * rel.size(), ctx.stream);
   PMX_CUDA(cudaMemcpyAsync(drel.p, rel.data(), drel.bytes, cudaMemcpyHostToDevice, ctx.stream));
+  DevBuf drel64(sizeof(PoseR<double>) * rel64.size(), ctx.stream);
+  PMX_CUDA(cudaMemcpyAsync(drel64.p, rel64.data(), drel64.bytes, cudaMemcpyHostToDevice, ctx.stream));
   // about two waves of 2 resident blocks per SM, >= 16 matches per thread
   const int64_t want = (2LL * 2 * ctx.num_sms + G.E - 1) / std::max(1, G.E);
   const int bpe = (int)std::max<int64_t>(1, std::min<int64_t>(want, (G.max_count + 4095) / 4096));
@@ -960,6 +833,7 @@ static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, c
   A.matches = G.matches.as<MatchesDev>();
   A.edges = G.edges_dev.as<int2>();
   A.rel = drel.as<PoseR<float>>();
+  A.rel64 = drel64.as<PoseR<double>>();
   A.qmin = G.qmin.as<double>();
   A.wp = backend_weights(p);
   A.K = p.has_intrinsics ? IntrDev{p.intrinsics.fx, p.intrinsics.fy, p.intrinsics.cx, p.intrinsics.cy, 1}

@@ -43,6 +43,36 @@ __device__ void eval_pass(const PoseR<float>& T, const MatchesDev& M, const Clou
   block_reduce_to(acc, partials + (size_t)blockIdx.x * kAcc);
 }
 
+// Ray mode (the tracking configuration): closed-form sums with the cancelling
+// parts of the residual in FP64 (residual.cuh ray_accumulate) -> kRayAcc
+// partials per block (stride kAcc).  Same skips as eval_match.
+__device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const CloudDev& Xref,
+                              const CloudDev& Xsrc, const WeightsDev& wp, double* __restrict__ partials) {
+  float acc[kRayAcc];
+#pragma unroll
+  for (int i = 0; i < kRayAcc; ++i) acc[i] = 0.0f;
+  const RayW c{(float)wp.huber_delta, (float)(wp.huber_delta * wp.huber_delta), (float)wp.distance_weight};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M.count; k += stride) {
+    const int pa = M.pa ? __ldg(M.pa + k) : (int)k;
+    const int pb = M.pb ? __ldg(M.pb + k) : (int)k;
+    const bool mv = M.valid ? __ldg(M.valid + k) != 0 : true;
+    if (!mv || pa < 0 || pb < 0 || pb >= Xref.H * Xref.W || pa >= Xsrc.H * Xsrc.W) continue;
+    float rf[3], sf[3];
+    if (!load_point(Xref, pb, rf) || !load_point(Xsrc, pa, sf)) continue;
+    const double q = (double)__ldg(M.q + k);
+    if (!(q > wp.q_min)) continue;  // robust_weight: infinite denom -> excluded
+    const float info = (float)(1.0 / (wp.sigma2 / q));
+    const double rd[3] = {rf[0], rf[1], rf[2]}, sd[3] = {sf[0], sf[1], sf[2]};
+    const double rr = fma(rd[0], rd[0], fma(rd[1], rd[1], rd[2] * rd[2]));
+    if (!(rr >= 1e-24)) continue;  // |ref| < 1e-12 (tracking.cpp:78)
+    const float rrf = (float)rr;
+    const float ir = rsqrt_nr(rrf);
+    ray_accumulate(T, rd, rr, rrf * ir, ir, rf, sd, info, c, acc);
+  }
+  block_reduce_n<kRayAcc>(acc, partials + (size_t)blockIdx.x * kAcc);
+}
+
 __global__ void __launch_bounds__(256) k_normal_eq(PoseR<float> T, MatchesDev M, CloudDev Xref, CloudDev Xsrc,
                                                    int mode, WeightsDev wp, const double* qmin_dev, IntrDev K,
                                                    double* partials) {
@@ -109,16 +139,20 @@ struct TrackArgs {
   GNState* st;
 };
 
-__device__ void load_sums(const double* __restrict__ partials, int nblocks, double* H, double* g, double* cost) {
+__device__ void load_sums(const double* __restrict__ partials, int nblocks, bool ray, double* H, double* g,
+                          double* cost) {
   // block 0, all threads: deterministic ordered sum; results into shared
   __shared__ double s[kAcc];
-  for (int i = threadIdx.x; i < kAcc; i += blockDim.x) {
+  const int n = ray ? kRayAcc : kAcc;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double a = 0.0;
     for (int b = 0; b < nblocks; ++b) a += partials[(size_t)b * kAcc + i];
     s[i] = a;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && ray) {
+    ray_expand(s, H, g, cost);
+  } else if (threadIdx.x == 0) {
     int idx = 0;
     for (int a = 0; a < 7; ++a)
       for (int b = a; b < 7; ++b) {
@@ -163,14 +197,17 @@ __global__ void __launch_bounds__(256) k_track_gn(TrackArgs A) {
   if (st->stop) return;
   WeightsDev wp = A.wp;
   wp.q_min = st->q_min;
-  {
+  const bool ray = A.mode == PMX_TRACK_RAY;
+  if (ray) {
+    eval_pass_ray(make_pose<double>(st->T), A.M, A.Xref, A.Xsrc, wp, A.partials);
+  } else {
     const PoseR<float> T = make_pose<float>(st->T);
     eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, A.partials);
   }
   grid.sync();
   if (blockIdx.x == 0) {
     double H[49], g[7], c;
-    load_sums(A.partials, nb, H, g, &c);
+    load_sums(A.partials, nb, ray, H, g, &c);
     if (threadIdx.x == 0) {
       for (int i = 0; i < 49; ++i) st->H[i] = H[i];
       for (int i = 0; i < 7; ++i) st->g[i] = g[i];
@@ -207,14 +244,16 @@ __global__ void __launch_bounds__(256) k_track_gn(TrackArgs A) {
     grid.sync();
     if (st->stop) break;
     if (!st->trial_ok) continue;
-    {
+    if (ray) {
+      eval_pass_ray(make_pose<double>(st->Ttrial), A.M, A.Xref, A.Xsrc, wp, A.partials);
+    } else {
       const PoseR<float> T = make_pose<float>(st->Ttrial);
       eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, A.partials);
     }
     grid.sync();
     if (blockIdx.x == 0) {
       double H[49], g[7], c;
-      load_sums(A.partials, nb, H, g, &c);
+      load_sums(A.partials, nb, ray, H, g, &c);
       if (threadIdx.x == 0) {
         // tracking.cpp:210-223
         if (c <= st->cost * (1.0 + 1e-12) + 1e-300) {
