@@ -41,7 +41,6 @@ ALG_BYTES_PER_PX = 133  # X_b 12 + X_a 12 + Q_a 4 + Q_b 4 + D_
 #  k_prep   X_a 12 + valid_a 1 + D_a 48 + Q_a 4                       = 65
 #  k_match  X_b 12 + valid_b 1 + X_a (one ray per pixel) 12 + pa/valid/q out 9 = 34
 #  k_refine D_a 48 + D_b 48 + Q_a 4 + Q_b 4 + pa/valid in 5 + pa/q out 8 = 117
-#  k_refine_hard: the same 117 B per queued pixel
 KERNEL_BYTES_PER_PX = {"k_prep": 65, "k_match": 34, "k_refine": 117}
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
 
@@ -352,8 +351,8 @@ def run_pmx(args):
     torch.cuda.synchronize()
     ctx.profile_enable(False)
     prof_ms = pe[0].elapsed_time(pe[1])
-    kern = {k: ctx.profile_get(k) for k in ("k_prep", "k_match", "k_refine", "k_refine_hard")}
-    _, hard_px = ctx.profile_get("refine_hard_px")
+    kern = {k: ctx.profile_get(k) for k in ("k_prep", "k_match", "k_refine")}
+    _, exact_px = ctx.profile_get("refine_exact_px")
     ms_local = float(sum(step_ms))
     if dist:
         t = torch.tensor([ms_local], device=dev)
@@ -397,13 +396,12 @@ def run_pmx(args):
         px_steps = H * W * len(mine) * args.steps
         breakdown = {}
         for k, (kms, kn) in kern.items():
-            px = hard_px if k == "k_refine_hard" else px_steps
-            nbytes = KERNEL_BYTES_PER_PX.get(k, 117) * px
+            nbytes = KERNEL_BYTES_PER_PX.get(k, 117) * px_steps
             breakdown[k] = {"ms_per_step": kms / args.steps, "launches_per_step": kn / args.steps,
                             "share_of_step": kms / prof_ms if prof_ms > 0 else None,
                             "alg_bytes_per_px": KERNEL_BYTES_PER_PX.get(k, 117),
                             "achieved_gbs": nbytes / (kms / 1e3) / 1e9 if kms > 0 else None}
-        breakdown["k_refine_hard"]["queued_px_per_step"] = hard_px / args.steps
+        breakdown["k_refine"]["exact_path_px_per_step"] = exact_px / args.steps
         dom = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
         achieved = breakdown[dom]["achieved_gbs"]
         traffic = None

@@ -41,6 +41,8 @@ struct SelState {
   uint32_t prefix;  // resolved high bits so far
   uint32_t krem;    // rank within the current bucket
   double threshold; // invalidation_median_fraction * median
+  int a1max;        // max over a-pixels of sum q8(D_a)^2 (int8 refinement error bound)
+  int qbad;         // some |D_a component| * 127 >= 127.5: no int8 fast path for this pair
 };
 
 struct PairDev {
@@ -68,7 +70,10 @@ struct PairDev {
   SelState* sel;
   // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
   // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
-  float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (staged with the norms)
+  float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (standalone refine)
+  // int8 descriptors of every a-pixel, round(127 x), dims 0-15 / 16-23 (batched refine)
+  uint4* q8a;
+  uint2* q8b;
 };
 
 struct LMParams {
@@ -146,6 +151,52 @@ __device__ __forceinline__ void desc_aux(const __half* row, float q, float4* nrm
   *nrm = make_float4(norm_ub(s0 + s1 + s2, 24), norm_ub(s2, 8), norm_ub(s1 + s2, 16), q);
 }
 
+// int8 image of a 24-dim fp16 descriptor: q_k = rne(127 x_k), computed
+// exactly in fp16 as the low byte of fma(x, 127, 1536) (the product is exact
+// in the FMA, and 1536 + q is representable with ulp 1 for |q| <= 511).
+// Valid (|127 x| <= 127.49, so q fits int8) iff max |x_k| <= 1 + 2^-8.
+// l2 = sum q_k^2 (exact, DP4A), which bounds sum |q_k| <= sqrt(24 l2).
+struct Q8 {
+  uint4 a;  // dims 0-15
+  uint2 b;  // dims 16-23
+  int l2;
+  int bad;
+};
+__device__ __forceinline__ uint32_t q8_word(uint32_t w0, uint32_t w1, __half2& amax) {
+  const __half2 k127 = __float2half2_rn(127.0f), k1536 = __float2half2_rn(1536.0f);
+  __half2 x0, x1;
+  memcpy(&x0, &w0, 4);
+  memcpy(&x1, &w1, 4);
+  amax = __hmax2_nan(amax, __habs2(x0));  // NaN-propagating
+  amax = __hmax2_nan(amax, __habs2(x1));
+  const __half2 r0 = __hfma2(x0, k127, k1536), r1 = __hfma2(x1, k127, k1536);
+  uint32_t u0, u1;
+  memcpy(&u0, &r0, 4);
+  memcpy(&u1, &r1, 4);
+  return __byte_perm(u0, u1, 0x6420);  // low bytes of the four fp16 results
+}
+__device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const uint4 d2) {
+  Q8 q;
+  __half2 amax = __float2half2_rn(0.0f);
+  q.a.x = q8_word(d0.x, d0.y, amax);
+  q.a.y = q8_word(d0.z, d0.w, amax);
+  q.a.z = q8_word(d1.x, d1.y, amax);
+  q.a.w = q8_word(d1.z, d1.w, amax);
+  q.b.x = q8_word(d2.x, d2.y, amax);
+  q.b.y = q8_word(d2.z, d2.w, amax);
+  const float2 m = __half22float2(amax);
+  q.bad = !(m.x <= 1.00390625f && m.y <= 1.00390625f);  // also NaN / inf
+  int l2 = __dp4a((int)q.a.x, (int)q.a.x, 0);
+  l2 = __dp4a((int)q.a.y, (int)q.a.y, l2);
+  l2 = __dp4a((int)q.a.z, (int)q.a.z, l2);
+  l2 = __dp4a((int)q.a.w, (int)q.a.w, l2);
+  l2 = __dp4a((int)q.b.x, (int)q.b.x, l2);
+  q.l2 = __dp4a((int)q.b.y, (int)q.b.y, l2);
+  return q;
+}
+// Upper bound of sum |q_k| from sum q_k^2 (Cauchy-Schwarz over 24 dims).
+__device__ __forceinline__ float q8_l1_bound(int l2) { return sqrtf(24.0f * (float)l2) * 1.0001f + 1.0f; }
+
 // ---------------------------------------------------------------- K1
 __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
   const PairDev& P = pairs[blockIdx.y];
@@ -155,6 +206,7 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
   __syncthreads();
   const int begin = blockIdx.x * px_per_block;
   const int end = min(HW, begin + px_per_block);
+  int a1max = 0, qbad = 0;
   for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
     const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
     const bool v = P.va ? P.va[i] != 0 : true;
@@ -172,6 +224,25 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     }
     P.keys[i] = key;
     if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
+    if (P.q8a) {
+      const uint4* row = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)i;
+      const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
+      P.q8a[i] = q.a;
+      P.q8b[i] = q.b;
+      a1max = max(a1max, q.l2);
+      qbad |= q.bad;
+    }
+  }
+  if (P.q8a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1max = max(a1max, __shfl_xor_sync(0xffffffffu, a1max, o));
+      qbad |= __shfl_xor_sync(0xffffffffu, qbad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (a1max) atomicMax(&P.sel->a1max, a1max);
+      if (qbad) atomicOr(&P.sel->qbad, qbad);
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
@@ -686,9 +757,8 @@ __device__ __noinline__ void refine_exact(const PairDev& P, const __half* __rest
   }
 }
 
-// Where the candidates' descriptors and norm bounds come from: the block's
-// shared-memory tile (three 16-byte planes + norms, staged once, reused by ~49
-// candidates each) or global memory (incoherent tiles, standalone refine).
+// Where the candidates' descriptors and norm bounds come from (global memory:
+// standalone refine and the batched path's exact fallback).
 struct GlobalAux {
   const uint4* rows;  // 3 uint4 per pixel
   const float4* norms;
@@ -699,17 +769,6 @@ struct GlobalAux {
   __device__ __forceinline__ uint4 d2(int i) const { return __ldg(rows + 3 * i + 2); }
   __device__ __forceinline__ float4 nrm(int i) const { return __ldg(norms + i); }
 };
-struct SmemAux {
-  const uint4 *p0, *p1, *p2;
-  const float4* n4;
-  int u0, v0, bw;
-  __device__ __forceinline__ int at(int u, int v) const { return (v - v0) * bw + (u - u0); }
-  __device__ __forceinline__ uint4 d0(int i) const { return p0[i]; }
-  __device__ __forceinline__ uint4 d1(int i) const { return p1[i]; }
-  __device__ __forceinline__ uint4 d2(int i) const { return p2[i]; }
-  __device__ __forceinline__ float4 nrm(int i) const { return n4[i]; }
-};
-
 struct BConst {  // register-resident target descriptor and its bound constants
   uint4 b0, b1, b2;
   float c8, t8, c16, t16, c24;
@@ -766,53 +825,6 @@ __device__ __forceinline__ void refine_level(const PairDev& P, const Aux& X, con
   }
 }
 
-// Interior window, compile-time radius / stride, candidates in shared memory.
-// The running best only increases during the scan, so a candidate whose upper
-// bound cannot beat the INITIAL best (the centre) can never win: all head
-// bounds are evaluated branch-free against the centre's threshold into a
-// bitmask, then only the survivors are processed, in raster order, with the
-// running best (exactly the reference's strict-'>' scan).
-template <int R, int S>
-__device__ __forceinline__ void refine_level_fast(const PairDev& P, const SmemAux& X, const BConst& K,
-                                                  const __half* __restrict__ bdesc, int cu, int cv, BestState& B) {
-  constexpr int D = 2 * R + 1;
-  static_assert(D * D <= 64, "window too large for the survivor mask");
-  const int base = X.at(cu - R * S, cv - R * S);
-  const float thr0 = B.thr;
-  unsigned long long mask = 0ull;
-#pragma unroll
-  for (int dv = 0; dv < D; ++dv) {
-#pragma unroll
-    for (int du = 0; du < D; ++du) {
-      if (dv == R && du == R) continue;
-      const int i = base + dv * S * X.bw + du * S;
-      if (!bound8_fails(dot8(X.d0(i), K.b0, 0.0f), X.nrm(i), K, thr0)) mask |= 1ull << (dv * D + du);
-    }
-  }
-  while (mask) {
-    const int k = __ffsll((long long)mask) - 1;
-    mask &= mask - 1;
-    const int dv = k / D, du = k % D;
-    const int i = base + dv * S * X.bw + du * S;
-    const float4 nr = X.nrm(i);
-    const float h8 = dot8(X.d0(i), K.b0, 0.0f);
-    if (bound8_fails(h8, nr, K, B.thr)) continue;  // the best has grown meanwhile
-    refine_candidate(P, X, K, bdesc, cu + (du - R) * S, cv + (dv - R) * S, i, h8, nr, B);
-  }
-}
-
-template <int R, int S, class Aux>
-__device__ __forceinline__ bool try_fast(const PairDev& P, const Aux& X, const BConst& K, const __half* bdesc, int cu,
-                                         int cv, int s, int r, BestState& B) {
-  if constexpr (std::is_same<Aux, SmemAux>::value) {
-    if (s == S && r == R && cu - R * S >= 0 && cu + R * S < P.Wa && cv - R * S >= 0 && cv + R * S < P.Ha) {
-      refine_level_fast<R, S>(P, X, K, bdesc, cu, cv, B);
-      return true;
-    }
-  }
-  return false;
-}
-
 template <class Aux>
 __device__ __forceinline__ int refine_pruned(const PairDev& P, const Aux& X, int pa, const __half* __restrict__ bdesc,
                                              const RefineLevels& L) {
@@ -845,9 +857,7 @@ __device__ __forceinline__ int refine_pruned(const PairDev& P, const Aux& X, int
       B.x = 0.0;
     }
     if (prev_r < 0) {
-      if (!try_fast<3, 1>(P, X, K, bdesc, cu, cv, s, r, B) && !try_fast<2, 2>(P, X, K, bdesc, cu, cv, s, r, B) &&
-          !try_fast<2, 1>(P, X, K, bdesc, cu, cv, s, r, B))
-        refine_level<false>(P, X, K, bdesc, cu, cv, s, r, 0, 0, 1, -1, B);
+      refine_level<false>(P, X, K, bdesc, cu, cv, s, r, 0, 0, 1, -1, B);
     } else {
       refine_level<true>(P, X, K, bdesc, cu, cv, s, r, prev_cu, prev_cv, prev_s, prev_r, B);
     }
@@ -875,7 +885,7 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 
 // ---------------------------------------------------------------- K3 + K4
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair.
-__global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
+__global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
   const PairDev& P = pairs[blockIdx.y];
   const int tiles_x = (P.Wb + 31) / 32;
   const int tiles = tiles_x * ((P.Hb + 7) / 8);
@@ -922,426 +932,242 @@ __global__ void __launch_bounds__(256) k_match(const PairDev* __restrict__ pairs
   P.out_valid[n] = valid_out;
 }
 
-// K4: feature_refine of the valid matches just written by k_match (in place),
-// in two passes so that no warp waits on one slow lane:
-//  * k_refine_pairs — persistent blocks walk 32x8 tiles of b-pixels; the
-//    first 16 descriptor dims + norm bounds (+ qa) of a tile's centres'
-//    bounding box (grown by the refinement reach) are staged in shared memory
-//    with cp.async, double-buffered so the next tile's staging overlaps this
-//    tile's refinement.  Every pixel bounds all the
-//    candidates of its window against the centre's threshold (8-dim, then
-//    16-dim Cauchy-Schwarz bounds; branch-free on interior windows).  "Easy"
-//    pixels (<= 2 survivors per level) are finished in place; the rest (in
-//    practice: LM centre != descriptor peak) are appended to a queue.
-//  * k_refine_hard — one warp per queued pixel: the window's candidates are
-//    spread over the lanes, the exact argmax (max score, ties to the centre,
-//    then raster order) comes from warp reductions over rigorous fp32 bounds,
-//    with an exact FP64 replay when several candidates are within rounding.
-constexpr int kTileCap = 1024;  // staged a-pixels per buffer (48 B each: 2 planes + norms/qa)
-constexpr size_t kTileBytes = (size_t)kTileCap * (2 * sizeof(uint4) + sizeof(float4));
-constexpr size_t kRefineSmem = 2 * kTileBytes;
-
-struct HeadTile {
-  const uint4* h0;  // dims 0-7
-  const uint4* h1;  // dims 8-15
-  const float4* n;  // dnorm layout: {||a||, ||a[16:]||, ||a[8:]||, qa}
-  int u0, v0, bw;
+// K4: feature_refine of the valid matches just written by k_match, in place.
+//
+// One thread per b-pixel, 32x8 tiles.  k_prep wrote the int8 image q8(a) =
+// rne(127 a) of every a-descriptor (24 B/pixel, L2-resident per chunk); the
+// windows of a tile overlap, so candidates are read through L1 (an earlier
+// shared-memory staging variant with cp.async double buffering was slower:
+// its per-tile box reduction and barriers cost more than the L1 misses).
+// Every window candidate gets an exact integer score q_c = q8(a_c) . q8(b)
+// (6 DP4A).
+// With q8(x) = 127 x + e, |e| <= 1/2, the exact score satisfies
+//   |127^2 (a_c . b) - q_c| <= E = 0.5 (sum|q8(a)| + sum|q8(b)|) + 6,
+// so if the best integer score beats the second best by more than 2E, its
+// candidate is the unique exact argmax, whatever the scan order and the tie
+// rule.  Otherwise (true near-ties; never on well-separated peaks) the pixel
+// is refined by the exact scalar path (refine_dispatch: fp32 + FP64 replay),
+// so the result always equals the reference's exact-arithmetic argmax
+// (camera.cpp:247-265: strict '>', centre first, raster order).
+//
+// A later level whose centre moved only needs the candidates outside the
+// previous window (those were all strictly below the moved-to centre); a level
+// whose window is unchanged is skipped (camera.cpp semantics, strict '>').
+struct QB {  // register-resident int8 target descriptor
+  uint32_t w[6];
 };
 
-struct PrevWin {  // the previous level's window (already maximised: cannot win, strict '>')
-  int cu, cv, s, lim;
-  bool on;
+__device__ __forceinline__ int qdot(const uint4 a, const uint2 b, const QB& B) {
+  int s = __dp4a((int)a.x, (int)B.w[0], 0);
+  s = __dp4a((int)a.y, (int)B.w[1], s);
+  s = __dp4a((int)a.z, (int)B.w[2], s);
+  s = __dp4a((int)a.w, (int)B.w[3], s);
+  s = __dp4a((int)b.x, (int)B.w[4], s);
+  return __dp4a((int)b.y, (int)B.w[5], s);
+}
+
+// Best and second-best candidate of a scan as packed keys score * 256 + rank
+// (|score| <= 24 * 127^2 < 2^19, rank < 256): one max/min pair per candidate.
+struct Top2 {
+  int b1, b2;
+  __device__ __forceinline__ int score1() const { return b1 >> 8; }
+  __device__ __forceinline__ int rank1() const { return b1 & 255; }
+  // unique exact argmax: the best beats the second by more than 2E
+  __device__ __forceinline__ bool decided(int tgap) const { return (b1 >> 8) - (b2 >> 8) > tgap; }
+};
+__device__ __forceinline__ int qkey(int s, int k) { return s * 256 + k; }
+__device__ __forceinline__ void top2_add(Top2& T, int key) {
+  T.b2 = max(T.b2, min(T.b1, key));
+  T.b1 = max(T.b1, key);
+}
+
+// The int8 a-image read in place from the (L2-resident) chunk scratch
+// through the L1 cache: no staging, no block barriers.
+struct QGlob {
+  const uint4* __restrict__ a;
+  const uint2* __restrict__ b;
+  int bw;  // row pitch (= W)
+  __device__ __forceinline__ int at(int u, int v) const { return v * bw + u; }
+  __device__ __forceinline__ int score(int i, const QB& B) const { return qdot(__ldg(a + i), __ldg(b + i), B); }
 };
 
-// One level with compile-time radius / stride.  The running best only grows
-// during the scan, so bounding every candidate against the centre's threshold
-// is exact: survivors are then processed in raster order with the running
-// best (the reference's strict-'>' scan).  Every candidate gets the 16-dim
-// bound, branch-free (the 8-dim bound is too weak on 24-dim descriptors to
-// pay for a branch); returns false to defer (> 2 survivors).  CLIP: the
-// window may leave the image, or a previous window must be skipped.
-template <int R, int S, bool CLIP>
-__device__ __forceinline__ bool easy_level(const PairDev& P, const HeadTile& T, const BConst& K,
-                                           const __half* __restrict__ bdesc, int cu, int cv, BestState& B,
-                                           const PrevWin& W) {
+// First level, compile-time radius / stride, window inside the image: all
+// (2R+1)^2 candidates, unrolled (LDS immediate offsets, 6 DP4A each).
+template <int R, int S, class Tile>
+__device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int cv) {
   constexpr int D = 2 * R + 1;
-  const float thr0 = B.thr;
-  const int base = (cv - R * S - T.v0) * T.bw + (cu - R * S - T.u0);
-  unsigned long long keep = 0ull;
+  Top2 t{INT_MIN, INT_MIN};
+  const int base = T.at(cu - R * S, cv - R * S);
 #pragma unroll
   for (int dv = 0; dv < D; ++dv) {
 #pragma unroll
-    for (int du = 0; du < D; ++du) {
-      if (dv == R && du == R) continue;
-      int i = base + dv * S * T.bw + du * S;
-      bool ok = true;
-      if (CLIP) {
-        const int u = cu + (du - R) * S, v = cv + (dv - R) * S;
-        ok = (unsigned)u < (unsigned)P.Wa && (unsigned)v < (unsigned)P.Ha;  // out of image: skipped
-        if (W.on) {
-          const int eu = u - W.cu, ev = v - W.cv;
-          ok = ok && !(abs(eu) <= W.lim && abs(ev) <= W.lim && (W.s == 1 || (eu % W.s == 0 && ev % W.s == 0)));
-        }
-        i = ok ? i : 0;
+    for (int du = 0; du < D; ++du) top2_add(t, qkey(T.score(base + dv * S * T.bw + du * S, B), dv * D + du));
+  }
+  return t;
+}
+
+// One level at run-time radius / stride for one lane (border windows and
+// uncommon level shapes).  Candidates of the previous window (pr >= 0) are
+// skipped; the centre enters with score `centre` (its rank r*D+r).
+template <class Tile>
+__device__ __forceinline__ Top2 q_level_lane(const Tile& T, const QB& B, int cu, int cv, int s, int r, int Wa,
+                                             int Ha, int centre, int pcu, int pcv, int ps, int pr) {
+  const int D = 2 * r + 1;
+  Top2 t{qkey(centre, r * D + r), INT_MIN};
+  const int lim = pr * ps;
+  for (int dv = -r; dv <= r; ++dv) {
+    const int v = cv + dv * s;
+    if (v < 0 || v >= Ha) continue;
+    for (int du = -r; du <= r; ++du) {
+      const int u = cu + du * s;
+      if (u < 0 || u >= Wa || (du == 0 && dv == 0)) continue;
+      if (pr >= 0) {
+        const int eu = u - pcu, ev = v - pcv;
+        if (abs(eu) <= lim && abs(ev) <= lim && (ps == 1 || (eu % ps == 0 && ev % ps == 0))) continue;
       }
-      const float2 nr = *reinterpret_cast<const float2*>(T.n + i);  // {||a||, ||a[16:]||}
-      const float h16 = dot16(T.h0[i], T.h1[i], K.b0, K.b1);
-      const float u16 = fmaf(nr.x, K.c16, fmaf(nr.y, K.t16, h16));
-      if (ok && fmaf(8.0f * kU, fabsf(h16) + fabsf(u16), u16) > thr0) keep |= 1ull << (dv * D + du);
+      top2_add(t, qkey(T.score(T.at(u, v), B), (dv + r) * D + (du + r)));
     }
   }
-  if (__popcll(keep) > 2) return false;
-  const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
-  while (keep) {
-    const int k = __ffsll((long long)keep) - 1;
-    keep &= keep - 1;
-    const int u = cu + (k % D - R) * S, v = cv + (k / D - R) * S;
-    const int i = G.at(u, v);
-    const float4 nr = G.nrm(i);
-    const float h8 = dot8(G.d0(i), K.b0, 0.0f);
-    if (bound8_fails(h8, nr, K, B.thr)) continue;
-    refine_candidate(P, G, K, bdesc, u, v, i, h8, nr, B);
+  return t;
+}
+
+// Refinement state of one lane between levels.
+struct QState {
+  int cu, cv;         // current centre
+  int pcu, pcv, ps, pr;  // previous window (pr < 0: none)
+  int best;           // integer score of the centre
+  int st;             // 0 active, 1 undecided (exact path), 2 no pixel
+};
+
+// Level l of one lane from its top-2: move the centre, or mark undecided.
+__device__ __forceinline__ void q_advance(QState& q, const Top2& t, int tgap, int s, int r) {
+  if (!t.decided(tgap)) {
+    q.st = 1;
+    return;
   }
-  return true;
+  const int D = 2 * r + 1, k = t.rank1();
+  q.pcu = q.cu;
+  q.pcv = q.cv;
+  q.ps = s;
+  q.pr = r;
+  q.cu += (k % D - r) * s;
+  q.cv += (k / D - r) * s;
+  q.best = t.score1();
 }
 
-template <int R, int S>
-__device__ __forceinline__ int try_easy(const PairDev& P, const HeadTile& T, const BConst& K, const __half* bdesc,
-                                        int cu, int cv, int s, int r, BestState& B, const PrevWin& W) {
-  if (s != S || r != R) return -1;  // not this instantiation
-  const bool interior = cu - R * S >= 0 && cu + R * S < P.Wa && cv - R * S >= 0 && cv + R * S < P.Ha;
-  if (interior && !W.on) return easy_level<R, S, false>(P, T, K, bdesc, cu, cv, B, W) ? 1 : 0;
-  return easy_level<R, S, true>(P, T, K, bdesc, cu, cv, B, W) ? 1 : 0;
-}
-
-__device__ __forceinline__ BConst make_bconst(const __half* bdesc) {
-  BConst K;
-  const uint4* bp = reinterpret_cast<const uint4*>(bdesc);
-  K.b0 = __ldg(bp);
-  K.b1 = __ldg(bp + 1);
-  K.b2 = __ldg(bp + 2);
-  const float s0 = dot8(K.b0, K.b0, 0.0f), s1 = dot8(K.b1, K.b1, 0.0f), s2 = dot8(K.b2, K.b2, 0.0f);
-  K.c8 = 8.01f * kU * norm_ub(s0, 8);
-  K.t8 = norm_ub(s1 + s2, 16) * (1.0f + 4.0f * kU);
-  K.c16 = 16.01f * kU * norm_ub(s0 + s1, 16);
-  K.t16 = norm_ub(s2, 8) * (1.0f + 4.0f * kU);
-  K.c24 = 24.01f * kU * norm_ub(s0 + s1 + s2, 24);
-  return K;
-}
-
-// Easy path of one pixel; returns the refined pixel or -1 to defer.
-// K and the level-0 centre score fc were loaded before the tile landed.
-__device__ __forceinline__ int refine_easy(const PairDev& P, const HeadTile& T, int pa, const __half* bdesc,
-                                           const BConst& K, float fc, const RefineLevels& L) {
-  int cu = pa % P.Wa, cv = pa / P.Wa;
-  const float ec = K.c24 * T.n[(cv - T.v0) * T.bw + (cu - T.u0)].x;
-  PrevWin W{0, 0, 1, 0, false};
+// All levels of the warp's 32 pixels.  Level 0 runs per
+// lane (unrolled for the common shapes); a later level that only some lanes
+// need (their centre moved: BASELINE's second level) is evaluated by the whole
+// warp, one such pixel at a time, lanes spread over its window.
+template <class Tile>
+__device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tgap, int Wa, int Ha,
+                                              const RefineLevels& L, QState& q) {
+  const int lane = threadIdx.x & 31;
   for (int l = 0; l < L.n; ++l) {
     const int s = L.stride[l], r = L.radius[l];
-    if (W.on && s == W.s && r * s == W.lim && cu == W.cu && cv == W.cv) continue;  // identical window
-    BestState B;  // every level starts at the LM match (else deferred below)
-    best_set(B, cu, cv, fc, ec);
-    B.x = 0.0;
-    int ok = try_easy<3, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
-    if (ok < 0) ok = try_easy<2, 2>(P, T, K, bdesc, cu, cv, s, r, B, W);
-    if (ok < 0) ok = try_easy<2, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
-    if (ok < 0) ok = try_easy<1, 1>(P, T, K, bdesc, cu, cv, s, r, B, W);
-    if (ok <= 0) return -1;
-    // the staged box covers windows centred on the LM match only: a centre
-    // that moves with levels still to go is deferred to k_refine_hard
-    if ((B.u != cu || B.v != cv) && l + 1 < L.n) return -1;
-    W = PrevWin{cu, cv, s, r * s, true};
-    cu = B.u;
-    cv = B.v;
-  }
-  return cv * P.Wa + cu;
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned a = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(a), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-
-// Per-buffer job of one staged tile.  Block-uniform fields + per-thread
-// (b-pixel, LM match) kept in shared memory so that the prefetched tile costs
-// no registers while the current one is refined.
-struct TileJob {
-  int p;           // pair (in the launch's chunk)
-  int aux;         // the pair has pruning aux (else: per-thread exact path)
-  int u0, v0, bw;  // staged a-box origin / width; bw == 0: not staged (defer)
-};
-struct TileSmem {
-  TileJob job[2];
-  int n[2][256];   // b-pixel, -1: nothing to refine
-  int pa[2][256];  // LM match
-  int box[8][4];
-};
-
-// Decode tile g into slot `b`, reduce its a-box over the block (one barrier)
-// and issue the box's staging as one cp.async group (committed even when
-// empty, so the wait counts stay uniform).  Every thread calls this.
-__device__ __forceinline__ void tile_begin(const PairDev* __restrict__ pairs, int g, int total, int max_tiles,
-                                           int reach, TileSmem& S, int b, char* buf) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
-  int n = -1, pa = 0, p = 0;
-  bool aux = false;
-  if (g < total) {
-    p = g / max_tiles;
-    const PairDev& P = pairs[p];
-    aux = P.dnorm != nullptr;
-    const int t = g % max_tiles, tiles_x = (P.Wb + 31) / 32;
-    if (t < tiles_x * ((P.Hb + 7) / 8)) {
-      const int u = (t % tiles_x) * 32 + lane, v = (t / tiles_x) * 8 + warp;
-      const int m = v * P.Wb + u;
-      const bool in = u < P.Wb && v < P.Hb;
-      const int pm = in ? P.out_pa[m] : 0;  // loaded alongside the flag (no dependent round trip)
-      if (in && P.out_valid[m]) {
-        n = m;
-        pa = pm;
-        bx0 = bx1 = pa % P.Wa;
-        by0 = by1 = pa / P.Wa;
+    const bool same = q.pr >= 0 && s == q.ps && r == q.pr && q.cu == q.pcu && q.cv == q.pcv;  // identical window
+    const bool need = q.st == 0 && !same;
+    const unsigned m = __ballot_sync(0xffffffffu, need);
+    if (!m) continue;
+    if (l == 0 || __popc(m) > 8) {  // per lane
+      if (need) {
+        Top2 t;
+        const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
+                              q.cv + r * s < Ha;
+        if (interior && s == 1 && r == 3) {
+          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv);
+        } else if (interior && s == 2 && r == 2) {
+          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv);
+        } else {
+          if (q.best == INT_MIN) q.best = T.score(T.at(q.cu, q.cv), B);
+          t = q_level_lane(T, B, q.cu, q.cv, s, r, Wa, Ha, q.best, q.pcu, q.pcv, q.ps, q.pr);
+        }
+        q_advance(q, t, tgap, s, r);
       }
-    }
-  }
-  S.n[b][threadIdx.x] = n;
-  S.pa[b][threadIdx.x] = pa;
+    } else {  // warp-cooperative, one pending pixel at a time
+      const int D = 2 * r + 1, nc = D * D, lim0 = r * D + r;
+      for (unsigned mm = m; mm; mm &= mm - 1) {
+        const int src = __ffs(mm) - 1;
+        const int cu = __shfl_sync(0xffffffffu, q.cu, src), cv = __shfl_sync(0xffffffffu, q.cv, src);
+        const int pcu = __shfl_sync(0xffffffffu, q.pcu, src), pcv = __shfl_sync(0xffffffffu, q.pcv, src);
+        const int ps = __shfl_sync(0xffffffffu, q.ps, src), pr = __shfl_sync(0xffffffffu, q.pr, src);
+        const int centre = __shfl_sync(0xffffffffu, q.best, src);
+        QB Bs;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    bx0 = min(bx0, __shfl_xor_sync(0xffffffffu, bx0, o));
-    bx1 = max(bx1, __shfl_xor_sync(0xffffffffu, bx1, o));
-    by0 = min(by0, __shfl_xor_sync(0xffffffffu, by0, o));
-    by1 = max(by1, __shfl_xor_sync(0xffffffffu, by1, o));
-  }
-  if (lane == 0) {
-    S.box[warp][0] = bx0;
-    S.box[warp][1] = bx1;
-    S.box[warp][2] = by0;
-    S.box[warp][3] = by1;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    bx0 = min(bx0, S.box[w][0]);
-    bx1 = max(bx1, S.box[w][1]);
-    by0 = min(by0, S.box[w][2]);
-    by1 = max(by1, S.box[w][3]);
-  }
-  TileJob J{p, aux ? 1 : 0, 0, 0, 0};
-  if (aux && bx0 != INT_MAX) {
-    const PairDev& P = pairs[p];
-    const int u0 = max(0, bx0 - reach), u1 = min(P.Wa - 1, bx1 + reach);
-    const int v0 = max(0, by0 - reach), v1 = min(P.Ha - 1, by1 + reach);
-    const int bw = u1 - u0 + 1, bh = v1 - v0 + 1;
-    if (bw * bh <= kTileCap) {
-      J.u0 = u0;
-      J.v0 = v0;
-      J.bw = bw;
-      uint4* s0 = reinterpret_cast<uint4*>(buf);
-      uint4* s1 = s0 + kTileCap;
-      float4* sn = reinterpret_cast<float4*>(s1 + kTileCap);
-      const uint4* rows = reinterpret_cast<const uint4*>(P.da);
-      for (int rr = warp; rr < bh; rr += 8) {  // one warp per staged row, coalesced
-        const int grow = (v0 + rr) * P.Wa + u0;
-        for (int cc = lane; cc < bw; cc += 32) {
-          const int gp = grow + cc, sp = rr * bw + cc;
-          cp_async16(s0 + sp, rows + 3 * gp);
-          cp_async16(s1 + sp, rows + 3 * gp + 1);
-          cp_async16(sn + sp, P.dnorm + gp);
-        }
-      }
-    }
-  }
-  if (threadIdx.x == 0) S.job[b] = J;
-  cp_async_commit();
-}
-
-__global__ void __launch_bounds__(256, 2) k_refine_pairs(const PairDev* __restrict__ pairs, int total, int max_tiles,
-                                                         RefineLevels L, int reach, int2* __restrict__ queue,
-                                                         int* __restrict__ qcount) {
-  extern __shared__ __align__(16) char smem[];
-  __shared__ TileSmem S;
-  int b = 0;
-  tile_begin(pairs, blockIdx.x, total, max_tiles, reach, S, 0, smem);
-  for (int g = blockIdx.x; g < total; g += gridDim.x) {
-    __syncthreads();  // S.job[b] visible; slot b^1 free
-    tile_begin(pairs, g + gridDim.x, total, max_tiles, reach, S, b ^ 1, smem + (b ^ 1) * kTileBytes);
-    const TileJob J = S.job[b];
-    const int n = S.n[b][threadIdx.x], pa = S.pa[b][threadIdx.x];
-    const PairDev& P = pairs[J.p];
-    const __half* bdesc = P.db + (size_t)(n < 0 ? 0 : n) * 24;
-    if (n >= 0 && !J.aux) {  // no pruning aux (dim != 24 or unaligned rows): per-thread exact path
-      const int o = refine_dispatch(P, pa, n, L);
-      P.out_pa[n] = o;
-      P.out_q[n] = (float)sqrt((double)P.qa[o] * (double)P.qb[n]);
-    }
-    // loads that do not need the tile: b descriptor, centre descriptor, qb
-    const bool easy = n >= 0 && J.aux && J.bw > 0;
-    BConst K;
-    float fc = 0.0f, qb = 0.0f;
-    if (easy) {
-      K = make_bconst(bdesc);
-      const uint4* ca = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)pa;
-      fc = dot8(__ldg(ca + 2), K.b2, dot8(__ldg(ca + 1), K.b1, dot8(__ldg(ca), K.b0, 0.0f)));
-      qb = P.qb[n];
-    }
-    cp_async_wait1();
-    __syncthreads();
-    if (n >= 0 && J.aux) {
-      int out = -1;
-      if (easy) {
-        const uint4* s0 = reinterpret_cast<const uint4*>(smem + b * kTileBytes);
-        const HeadTile T{s0, s0 + kTileCap, reinterpret_cast<const float4*>(s0 + 2 * kTileCap), J.u0, J.v0, J.bw};
-        out = refine_easy(P, T, pa, bdesc, K, fc, L);
-        if (out >= 0) {
-          const float qa = T.n[(out / P.Wa - T.v0) * T.bw + (out % P.Wa - T.u0)].w;
-          P.out_pa[n] = out;
-          P.out_q[n] = (float)sqrt((double)qa * (double)qb);
-        }
-      }
-      if (out < 0) queue[atomicAdd(qcount, 1)] = make_int2(J.p, n);
-    }
-    b ^= 1;
-  }
-}
-
-__global__ void k_add_counts(const int* __restrict__ c, int n, unsigned long long* total) {
-  unsigned long long s = 0;
-  for (int i = threadIdx.x; i < n; i += 32) s += (unsigned)c[i];
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (threadIdx.x == 0) *total += s;
-}
-
-// Persistent grid: resident blocks on every SM, capped by the tile count.
-static unsigned refine_grid(const Context& ctx, int tiles) {
-  static int per_sm = -1;
-  if (per_sm < 0) {
-    PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_pairs, 256, kRefineSmem));
-    per_sm = std::max(per_sm, 1);
-  }
-  return (unsigned)std::max(1, std::min(tiles, per_sm * ctx.num_sms));
-}
-
-// Warp-cooperative exact refinement of one queued pixel (all levels): lanes
-// score the window's candidates (<= 2 per lane, kept in registers), the exact
-// argmax (max score, ties to the centre, then raster order) comes from warp
-// reductions over rigorous fp32 bounds, with an exact FP64 replay of the
-// contenders when several are within rounding of the best.
-__global__ void __launch_bounds__(256) k_refine_hard(const PairDev* __restrict__ pairs, RefineLevels L,
-                                                     const int2* __restrict__ queue, const int* __restrict__ qcount) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
-  const int count = *qcount;
-  for (int q = gw; q < count; q += nw) {
-    const int2 e = queue[q];
-    const PairDev& P = pairs[e.x];
-    const int n = e.y;
-    const __half* bdesc = P.db + (size_t)n * 24;
-    const BConst K = make_bconst(bdesc);
-    const GlobalAux G{reinterpret_cast<const uint4*>(P.da), P.dnorm, P.Wa};
-    const int pa = P.out_pa[n];
-    int cu = pa % P.Wa, cv = pa / P.Wa;
-    int prev_cu = -1, prev_cv = -1, prev_s = 0, prev_r = -1;
-    for (int l = 0; l < L.n; ++l) {
-      const int s = L.stride[l], r = L.radius[l];
-      if (l > 0 && s == prev_s && r == prev_r && cu == prev_cu && cv == prev_cv) continue;
-      const int D = 2 * r + 1, ncand = D * D;
-      const float invD = 1.0f / (float)D;
-      float best_lo = -INFINITY;
-      float sc_[2], er_[2];
-      int u_[2], v_[2], k_[2];
-      int nmine = 0;
-      for (int k = lane - 1; k < ncand; k += 32) {  // k = -1: the centre (rank -1)
-        int u = cu, v = cv;
-        if (k >= 0) {
-          const int dv = (int)(((float)k + 0.5f) * invD), du = k - dv * D;
-          u = cu + (du - r) * s;
-          v = cv + (dv - r) * s;
-          if (u < 0 || v < 0 || u >= P.Wa || v >= P.Ha || (u == cu && v == cv)) continue;
-        }
-        const int i = G.at(u, v);
-        const float sc = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
-        const float err = K.c24 * G.nrm(i).x;
-        best_lo = fmaxf(best_lo, (sc - err) - 4.0f * kU * (fabsf(sc) + err));
-        if (nmine < 2) {
-          sc_[nmine] = sc;
-          er_[nmine] = err;
-          u_[nmine] = u;
-          v_[nmine] = v;
-          k_[nmine] = k;
-        }
-        ++nmine;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) best_lo = fmaxf(best_lo, __shfl_xor_sync(0xffffffffu, best_lo, o));
-      // contenders: candidates whose upper bound reaches the best lower bound
-      int ncont = 0, cu_w = cu, cv_w = cv;
-      const bool spilled = nmine > 2;  // radius > 3: scores not all kept
-      for (int j = 0; j < 2 && j < nmine; ++j) {
-        if ((sc_[j] + er_[j]) + 4.0f * kU * (fabsf(sc_[j]) + er_[j]) < best_lo) continue;
-        if (ncont == 0) {
-          cu_w = u_[j];
-          cv_w = v_[j];
-        }
-        ++ncont;
-      }
-      const int total = __reduce_add_sync(0xffffffffu, ncont);
-      const bool any_spill = __any_sync(0xffffffffu, spilled);
-      int win_u = cu, win_v = cv;
-      if (total == 1 && !any_spill) {
-        const int src = __ffs(__ballot_sync(0xffffffffu, ncont == 1)) - 1;
-        win_u = __shfl_sync(0xffffffffu, cu_w, src);
-        win_v = __shfl_sync(0xffffffffu, cv_w, src);
-      } else {  // exact FP64 scores of every contender; argmax with ties to the lowest rank
-        double bx = -INFINITY;
-        int br = INT_MAX;
-        for (int k = lane - 1; k < ncand; k += 32) {
-          int u = cu, v = cv;
-          if (k >= 0) {
-            const int dv = (int)(((float)k + 0.5f) * invD), du = k - dv * D;
-            u = cu + (du - r) * s;
-            v = cv + (dv - r) * s;
-            if (u < 0 || v < 0 || u >= P.Wa || v >= P.Ha || (u == cu && v == cv)) continue;
-          }
-          const int i = G.at(u, v);
-          const float sc = dot8(G.d2(i), K.b2, dot8(G.d1(i), K.b1, dot8(G.d0(i), K.b0, 0.0f)));
-          const float err = K.c24 * G.nrm(i).x;
-          if ((sc + err) + 4.0f * kU * (fabsf(sc) + err) < best_lo) continue;
-          const double ex = dot_exact(P.da + (size_t)i * 24, bdesc, 24);
-          if (ex > bx || (ex == bx && k < br)) {
-            bx = ex;
-            br = k;
-          }
+        for (int w = 0; w < 6; ++w) Bs.w[w] = __shfl_sync(0xffffffffu, B.w[w], src);
+        Top2 t{lane == 0 ? qkey(centre, lim0) : INT_MIN, INT_MIN};
+        const int lim = pr * ps;
+        for (int k = lane; k < nc; k += 32) {
+          const int dv = k / D - r, du = k % D - r;
+          const int u = cu + du * s, v = cv + dv * s;
+          if (u < 0 || u >= Wa || v < 0 || v >= Ha || (du == 0 && dv == 0)) continue;
+          const int eu = u - pcu, ev = v - pcv;
+          if (pr >= 0 && abs(eu) <= lim && abs(ev) <= lim && (ps == 1 || (eu % ps == 0 && ev % ps == 0))) continue;
+          top2_add(t, qkey(T.score(T.at(u, v), Bs), k));
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ox = __shfl_xor_sync(0xffffffffu, bx, o);
-          const int orank = __shfl_xor_sync(0xffffffffu, br, o);
-          if (ox > bx || (ox == bx && orank < br)) {
-            bx = ox;
-            br = orank;
-          }
+        for (int o = 16; o > 0; o >>= 1) {  // merge the top-2 keys over the warp
+          const int ob1 = __shfl_xor_sync(0xffffffffu, t.b1, o);
+          const int ob2 = __shfl_xor_sync(0xffffffffu, t.b2, o);
+          t.b2 = max(max(t.b2, ob2), min(t.b1, ob1));
+          t.b1 = max(t.b1, ob1);
         }
-        if (br >= 0 && br != INT_MAX) {
-          win_u = cu + (br % D - r) * s;
-          win_v = cv + (br / D - r) * s;
-        }
+        if (lane == src) q_advance(q, t, tgap, s, r);
       }
-      (void)k_;
-      prev_cu = cu;
-      prev_cv = cv;
-      prev_s = s;
-      prev_r = r;
-      cu = win_u;
-      cv = win_v;
     }
-    if (lane == 0) {
-      const int out = cv * P.Wa + cu;
-      P.out_pa[n] = out;
-      P.out_q[n] = (float)sqrt((double)P.qa[out] * (double)P.qb[n]);
-    }
+  }
+}
+
+// Undecided pixels (near ties, unstageable tiles, no int8 image): the
+// per-thread exact refinement, kept out of line (rare).
+__device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, const RefineLevels& L) {
+  return refine_dispatch(P, pa, n, L);
+}
+
+// One thread per b-pixel of a 32x8 tile (blockIdx.x = tile, blockIdx.y =
+// pair); the int8 a-image (L2-resident chunk scratch) is read through L1,
+// where a tile's windows overlap: no staging, no block barriers.
+__global__ void __launch_bounds__(256, 4) k_refine_q8(const PairDev* __restrict__ pairs, RefineLevels L,
+                                                       unsigned long long* __restrict__ exact_px) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int tiles_x = (P.Wb + 31) / 32;
+  if ((int)blockIdx.x >= tiles_x * ((P.Hb + 7) / 8)) return;
+  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31), v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+  const int m = v * P.Wb + u;
+  int n = -1, pa = 0;
+  if (u < P.Wb && v < P.Hb) {
+    pa = P.out_pa[m];
+    if (P.out_valid[m]) n = m;
+  }
+  const bool fast_pair = P.q8a != nullptr && P.sel->qbad == 0;
+  QB B;
+  int tgap = 0;
+  bool fast = n >= 0 && fast_pair;
+  if (fast) {
+    const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
+    const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
+    B.w[0] = q.a.x;
+    B.w[1] = q.a.y;
+    B.w[2] = q.a.z;
+    B.w[3] = q.a.w;
+    B.w[4] = q.b.x;
+    B.w[5] = q.b.y;
+    tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
+    fast = !q.bad;
+  }
+  QState q{pa % P.Wa, pa / P.Wa, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
+  if (__any_sync(0xffffffffu, fast)) {
+    const QGlob T{P.q8a, P.q8b, P.Wa};
+    q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
+  }
+  if (exact_px) {
+    const unsigned c = __popc(__ballot_sync(0xffffffffu, q.st == 1));
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(exact_px, (unsigned long long)c);
+  }
+  if (q.st != 2) {
+    const int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
+    P.out_pa[n] = out;
+    P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
   }
 }
 
@@ -1497,43 +1323,41 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     max_hwa = std::max(max_hwa, p.Ha * p.Wa);
     max_hwb = std::max(max_hwb, p.Hb * p.Wb);
   }
-  // chunk so that a chunk's FP64 ray maps + descriptor heads / norms + keys
+  // chunk so that a chunk's FP64 ray maps + int8 descriptors + norm keys
   // (60 B per a-pixel) stay L2-resident between k_prep and k_match/k_refine
-  const size_t per_px = sizeof(double4) + sizeof(float4) + sizeof(uint32_t);
+  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2) + sizeof(uint32_t);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   const int chunk = std::max(1, std::min(npairs, (int)((64u << 20) / std::max<size_t>(pair_bytes, 1))));
   DevBuf scratch(pair_bytes * chunk, ctx.stream);
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
   DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
   DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
-  const int nchunks = (npairs + chunk - 1) / chunk;
-  DevBuf qbuf(sizeof(int2) * (size_t)max_hwb * chunk + sizeof(int) * nchunks, ctx.stream);
-  int* qcounts = reinterpret_cast<int*>(qbuf.as<char>() + sizeof(int2) * (size_t)max_hwb * chunk);  // per chunk
-  int2* queue = qbuf.as<int2>();
   std::vector<PairDev> hp = host_pairs;
   char* base = scratch.as<char>();
   const size_t nslot = (size_t)max_hwa * chunk;
   double4* rays = reinterpret_cast<double4*>(base);
-  float4* norms = reinterpret_cast<float4*>(base + sizeof(double4) * nslot);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(float4)) * nslot);
+  uint4* q8a = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
+  uint2* q8b = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(uint2)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
     hp[i].keys = keys + (size_t)slot * max_hwa;
     hp[i].hist = hist.as<uint32_t>() + (size_t)kHistTotal * i;
     hp[i].sel = sel.as<SelState>() + i;
+    hp[i].dnorm = nullptr;
     const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
     if (refine && hp[i].dim == 24 && aligned) {
-      hp[i].dnorm = norms + (size_t)slot * max_hwa;
+      hp[i].q8a = q8a + (size_t)slot * max_hwa;
+      hp[i].q8b = q8b + (size_t)slot * max_hwa;
     }
   }
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
-  PMX_CUDA(cudaMemsetAsync(qcounts, 0, sizeof(int) * nchunks, ctx.stream));
+  PMX_CUDA(cudaMemsetAsync(sel.p, 0, sel.bytes, ctx.stream));
   for (int c0 = 0; c0 < npairs; c0 += chunk) {
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
-    int* qcount = qcounts + c0 / chunk;
     {
       ProfScope ps(ctx, "k_prep");
       prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
@@ -1547,25 +1371,10 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     }
     launch_check(ctx, "k_match");
     if (refine && L.n > 0) {
-      {
-        ProfScope ps(ctx, "k_refine");
-        int reach = 0;  // windows stay centred on the LM match in k_refine_pairs
-        for (int l = 0; l < L.n; ++l) reach = std::max(reach, L.radius[l] * L.stride[l]);
-        PMX_CUDA(cudaFuncSetAttribute((const void*)k_refine_pairs, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kRefineSmem));
-        k_refine_pairs<<<refine_grid(ctx, cn * max_tiles), 256, kRefineSmem, ctx.stream>>>(dp, cn * max_tiles, max_tiles, L, reach, queue, qcount);
-      }
-      {
-        ProfScope ps(ctx, "k_refine_hard");
-        k_refine_hard<<<ctx.num_sms * 8, 256, 0, ctx.stream>>>(dp, L, queue, qcount);
-      }
-      launch_check(ctx, "k_refine_pairs");
-    }
-  }
-  if (ctx.profiling && refine && L.n > 0) {  // hard-queue occupancy: pmx_profile_get("refine_hard_px")
-    if (unsigned long long* hc = dev_counter(ctx, "refine_hard_px")) {
-      k_add_counts<<<1, 32, 0, ctx.stream>>>(qcounts, nchunks, hc);
-      launch_check(ctx, "k_add_counts");
+      ProfScope ps(ctx, "k_refine");
+      unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
+      k_refine_q8<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, L, exact_px);
+      launch_check(ctx, "k_refine_q8");
     }
   }
   // Device-memory calls on a caller-adopted stream (pmx_set_stream) stay

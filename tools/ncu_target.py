@@ -1,0 +1,58 @@
+"""Small, fixed workloads for `ncu --set full` captures (dev tool).
+
+python tools/ncu_target.py match [edges]   -> 2 match_batch calls over config-2 edges
+python tools/ncu_target.py backend [kf]    -> 2 GN iterations of a config-3-shaped graph
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "gen")]
+
+import torch  # noqa: E402
+
+import pmxgen  # noqa: E402
+from paper_2412_12392_b200 import Context, FeatureMap, Graph, MatchSet, Pointmap, abi  # noqa: E402
+
+H, W = 384, 512
+dev = torch.device("cuda")
+
+
+def T(a):
+    a = np.ascontiguousarray(a)
+    return torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).to(dev)
+
+
+mode = sys.argv[1]
+ctx = Context(0)
+if mode == "match":
+    n = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    sc, poses, edges, mk = pmxgen.config2(seed=2)
+    pairs = []
+    for e in range(n):
+        p = mk(e)
+        pairs.append((Pointmap(T(p["X_a"]), T(p["valid_a"]), H, W), Pointmap(T(p["X_b"]), T(p["valid_b"]), H, W),
+                      FeatureMap(T(p["D_a"]), T(p["Q_a"]), H, W), FeatureMap(T(p["D_b"]), T(p["Q_b"]), H, W)))
+    mp = abi.default_match_params()
+    mp.projection.lambda_init = 1e-8
+    mp.projection.angle_tol = 1e-6
+    rp = abi.refine_params([(1, 3), (1, 3)])
+    outs = [MatchSet.empty(H * W, dev) for _ in range(n)]
+    for _ in range(2):
+        ctx.match_batch(pairs, params=mp, refine=rp, outs=outs)
+    torch.cuda.synchronize()
+    print("valid", float(np.mean([o.valid.float().mean().item() for o in outs])))
+else:
+    kf = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+    g = pmxgen.backend_graph(kf, 4, 3)
+    cans = [Pointmap(T(x), T(v), H, W) for x, v in g["canonicals"]]
+    ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["matches"]]
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    p.max_iterations = 2
+    init = [P.to_struct(abi.pmx_sim3) for P in g["init"]]
+    r = ctx.global_optimize(Graph(cans, list(init), g["edges"], ms), p)
+    torch.cuda.synchronize()
+    print("iterations", r.iterations)
