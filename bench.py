@@ -38,10 +38,11 @@ H, W = 384, 512
 N_EDGES = 64
 ALG_BYTES_PER_PX = 133  # X_b 12 + X_a 12 + Q_a 4 + Q_b 4 + D_a 48 + D_b 48 + idx 4 + valid 1
 # Algorithmic bytes per b-pixel of each matching kernel:
-#  k_prep   X_a 12 + valid_a 1 + D_a 48 + Q_a 4                       = 65
+#  k_select X_a 12 + valid_a 1 (norm keys + 3 radix-select rounds)        = 13
+#  k_prep   X_a 12 + valid_a 1 + D_a 48                               = 61
 #  k_match  X_b 12 + valid_b 1 + X_a (one ray per pixel) 12 + pa/valid/q out 9 = 34
-#  k_refine D_a 48 + D_b 48 + Q_a 4 + Q_b 4 + pa/valid in 5 + pa/q out 8 = 117
-KERNEL_BYTES_PER_PX = {"k_prep": 65, "k_match": 34, "k_refine": 117}
+#  k_refine D_b 48 + Q_a 4 + Q_b 4 + pa/valid in 5 + pa/q out 8        = 69
+KERNEL_BYTES_PER_PX = {"k_select": 13, "k_prep": 61, "k_match": 34, "k_refine": 69}
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
 
 
@@ -351,7 +352,7 @@ def run_pmx(args):
     torch.cuda.synchronize()
     ctx.profile_enable(False)
     prof_ms = pe[0].elapsed_time(pe[1])
-    kern = {k: ctx.profile_get(k) for k in ("k_prep", "k_match", "k_refine")}
+    kern = {k: ctx.profile_get(k) for k in KERNEL_BYTES_PER_PX}
     _, exact_px = ctx.profile_get("refine_exact_px")
     ms_local = float(sum(step_ms))
     if dist:

@@ -5,21 +5,24 @@
 //   (115-174), median_scene_distance (178-191), match_pointmaps (195-237),
 //   feature_refine (239-271).
 //
-// Kernels (per chunk of independent pairs, one CUDA grid dimension per pair):
+// Kernels (one CUDA grid dimension per pair):
+//   K2 k_keys / k_sel_scan / k_sel_hist   (all pairs of a batch at once)
+//                    fp32 keys of the FP64 point norms, then an exact
+//                    rank-floor(n/2) radix select (12+12+8 bits): the upper
+//                    median of median_scene_distance's nth_element.
+//   then per chunk of pairs (sized so a chunk's scratch stays L2-resident):
 //   K1 k_prep        one thread per a-pixel: FP64 unit ray + validity into a
-//                    32-byte ray map (L2-resident per chunk), the fp32 norm key
-//                    of median_scene_distance, and pass 1 of the radix select
-//                    (4096-bin shared-memory histogram).
-//   K2 k_sel_scan / k_sel_hist
-//                    exact rank-floor(n/2) radix select (12+12+8 bits) over
-//                    the fp32 norm keys: the upper median of nth_element.
+//                    32-byte ray map, and the int8 image of the descriptor
+//                    (24 B) for the refinement.
 //   K3 k_match       one thread per b-pixel: FP64 Levenberg-Marquardt on the
 //                    ray-angle error, lround + clamp, q = sqrt(Q_a Q_b), the 3D
-//                    invalidation test, and (K4, fused) the coarse-to-fine
-//                    descriptor refinement with fp32 dots, a rigorous error
-//                    bound and an exact FP64 re-check of every near-tie, so the
-//                    argmax equals the reference's exact-arithmetic argmax
-//                    (strict '>' scan, ties keep the centre / first raster).
+//                    invalidation test.
+//   K4 k_refine_q8   one thread per valid b-pixel: coarse-to-fine descriptor
+//                    refinement on exact int8 scores with a rigorous
+//                    uniqueness gap; undecided pixels (near ties) take the
+//                    exact path, so the argmax equals the reference's
+//                    exact-arithmetic argmax (strict '>' scan, ties keep the
+//                    centre / first raster).
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -198,7 +201,9 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
 __device__ __forceinline__ float q8_l1_bound(int l2) { return sqrtf(24.0f * (float)l2) * 1.0001f + 1.0f; }
 
 // ---------------------------------------------------------------- K1
-__global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
+// Norm keys of median_scene_distance (camera.cpp:181-186: valid pixels with
+// |p| > 1e-12, FP64 norm as normalize_rays) + pass 1 of the radix select.
+__global__ void __launch_bounds__(256) k_keys(const PairDev* __restrict__ pairs, int px_per_block) {
   const PairDev& P = pairs[blockIdx.y];
   const int HW = P.Ha * P.Wa;
   __shared__ uint32_t sh[kHist1];
@@ -206,23 +211,39 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
   __syncthreads();
   const int begin = blockIdx.x * px_per_block;
   const int end = min(HW, begin + px_per_block);
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+    const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
+    const bool v = P.va ? P.va[i] != 0 : true;
+    const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    uint32_t key = kNoKey;
+    if (v && nrm > 1e-12) {
+      key = __float_as_uint((float)nrm);
+      atomicAdd(&sh[key >> 20], 1u);
+    }
+    P.keys[i] = key;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
+    if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
+}
+
+// Per-chunk a-side maps: FP64 unit rays (camera.cpp:39-56: norm in FP64,
+// exact division as the reference), the int8 descriptor image for the
+// refinement (+ its per-pair error-bound statistics), or the fp32 norm bounds
+// of the standalone refine.
+__global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int HW = P.Ha * P.Wa;
+  const int begin = blockIdx.x * px_per_block;
+  const int end = min(HW, begin + px_per_block);
   int a1max = 0, qbad = 0;
   for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
     const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
     const bool v = P.va ? P.va[i] != 0 : true;
-    // camera.cpp:47-53: norm in FP64, exact division as the reference
     const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
     double4 r = make_double4(0.0, 0.0, 1.0, 0.0);
     if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
     P.rays[i] = r;
-    // camera.cpp:181-186: median over valid pixels with |p| > 1e-12
-    uint32_t key = kNoKey;
-    if (v && nrm > 1e-12) {
-      const float f = (float)nrm;
-      key = __float_as_uint(f);
-      atomicAdd(&sh[key >> 20], 1u);
-    }
-    P.keys[i] = key;
     if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
     if (P.q8a) {
       const uint4* row = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)i;
@@ -244,9 +265,6 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       if (qbad) atomicOr(&P.sel->qbad, qbad);
     }
   }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
-    if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
 }
 
 __global__ void __launch_bounds__(256) k_desc_prep(const __half* __restrict__ da, const float* __restrict__ qa,
@@ -1292,13 +1310,14 @@ static void check_pointmap(const pmx_pointmap& p) {
   require(p.height > 0 && p.width > 0 && p.xyz, "pointmap: empty or null");
 }
 
-// Builds ray maps + median threshold for every pair of `dev_pairs[0..n)`
-// (the scratch pointers must be set), enqueued on ctx.stream.
-static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
+// Median threshold (camera.cpp:178-200) of every pair of `dev_pairs[0..n)`
+// (keys / hist / sel set), enqueued on ctx.stream: one key pass and three
+// radix-select rounds over all pairs at once.
+static void select_median(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
   const int ppb = 4096;
   dim3 g1((max_hwa + ppb - 1) / ppb, n);
-  k_prep<<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
-  launch_check(ctx, "k_prep");
+  k_keys<<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_keys");
   k_sel_scan<1><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
   launch_check(ctx, "k_sel_scan1");
   k_sel_hist<2><<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
@@ -1309,6 +1328,18 @@ static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa
   launch_check(ctx, "k_sel_hist3");
   k_sel_scan<3><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
   launch_check(ctx, "k_sel_scan3");
+}
+
+static void prep_rays(Context& ctx, PairDev* dev_pairs, int n, int max_hwa) {
+  const int ppb = 1024;
+  k_prep<<<dim3((max_hwa + ppb - 1) / ppb, n), 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_prep");
+}
+
+// Ray maps + median threshold of the pairs (single-pair entry points).
+static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
+  select_median(ctx, dev_pairs, n, max_hwa, fraction);
+  prep_rays(ctx, dev_pairs, n, max_hwa);
 }
 
 // Batched match(+refine).  All pointers in `pairs` are device pointers.
@@ -1323,12 +1354,13 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     max_hwa = std::max(max_hwa, p.Ha * p.Wa);
     max_hwb = std::max(max_hwb, p.Hb * p.Wb);
   }
-  // chunk so that a chunk's FP64 ray maps + int8 descriptors + norm keys
-  // (60 B per a-pixel) stay L2-resident between k_prep and k_match/k_refine
-  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2) + sizeof(uint32_t);
+  // chunk so that a chunk's FP64 ray maps + int8 descriptors (56 B per
+  // a-pixel) stay L2-resident between k_prep and k_match / k_refine
+  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   const int chunk = std::max(1, std::min(npairs, (int)((64u << 20) / std::max<size_t>(pair_bytes, 1))));
   DevBuf scratch(pair_bytes * chunk, ctx.stream);
+  DevBuf keybuf(sizeof(uint32_t) * (size_t)max_hwa * npairs, ctx.stream);
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
   DevBuf sel(sizeof(SelState) * npairs, ctx.stream);
   DevBuf dpairs(sizeof(PairDev) * npairs, ctx.stream);
@@ -1338,11 +1370,10 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   double4* rays = reinterpret_cast<double4*>(base);
   uint4* q8a = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
   uint2* q8b = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
-  uint32_t* keys = reinterpret_cast<uint32_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(uint2)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
-    hp[i].keys = keys + (size_t)slot * max_hwa;
+    hp[i].keys = keybuf.as<uint32_t>() + (size_t)i * max_hwa;
     hp[i].hist = hist.as<uint32_t>() + (size_t)kHistTotal * i;
     hp[i].sel = sel.as<SelState>() + i;
     hp[i].dnorm = nullptr;
@@ -1355,12 +1386,16 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(sel.p, 0, sel.bytes, ctx.stream));
+  {
+    ProfScope ps(ctx, "k_select");
+    select_median(ctx, dpairs.as<PairDev>(), npairs, max_hwa, lp.median_fraction);
+  }
   for (int c0 = 0; c0 < npairs; c0 += chunk) {
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
     {
       ProfScope ps(ctx, "k_prep");
-      prep_and_select(ctx, dp, cn, max_hwa, lp.median_fraction);
+      prep_rays(ctx, dp, cn, max_hwa);
     }
     int max_tiles = 0;
     for (int i = c0; i < c0 + cn; ++i)
