@@ -37,7 +37,25 @@ namespace cg = cooperative_groups;
 
 namespace pmx {
 
+// Device-resident state of global_optimize's control loop (backend.cpp:
+// 192-256): every kernel of an iteration reads `stop` first, so the host
+// enqueues max_iterations iterations and synchronises once.
+struct GNState {
+  double cost;       // cost at the current poses
+  int cur;           // terms buffer holding the current poses' terms
+  int stop;          // loop finished (converged, reverted, or solve failure)
+  int solved;        // this iteration's damped solve succeeded
+  int failed;        // all damping attempts failed (state intact, not converged)
+  int converged;
+  int iterations;
+  int trace_len;
+  double trace[PMX_MAX_TRACE];
+};
+
+__device__ __forceinline__ bool gn_stopped(const GNState* st) { return st && st->stop; }
+
 struct EdgeArgs {
+  const GNState* st;          // nullable: skip everything once the loop stopped
   const CloudDev* clouds;     // [N]
   const MatchesDev* matches;  // [E]  (pixel_a in i, pixel_b in j)
   const int2* edges;          // [E]
@@ -58,6 +76,7 @@ struct EdgeArgs {
 };
 
 __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
+  if (gn_stopped(A.st)) return;
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
@@ -205,6 +224,7 @@ __device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<d
 // Both directed constraints of an edge from one read of its compacted matches
 // (two matches in flight per thread).
 __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
+  if (gn_stopped(A.st)) return;
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
@@ -238,7 +258,16 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
 }
 
 // Sum the closed-form partials of an edge and expand to {H 28, g 7, cost} x 2.
-__global__ void k_edge_sum_ray(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ terms) {
+// terms buffer written by an edge pass: `base` itself without a loop state,
+// else the current (which = 0) or the trial (which = 1) half.
+__device__ __forceinline__ double* terms_out(double* base, int64_t half, const GNState* st, int which) {
+  return st ? base + (which ? 1 - st->cur : st->cur) * half : base;
+}
+
+__global__ void k_edge_sum_ray(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ tbase,
+                               int64_t half, const GNState* st, int which) {
+  if (gn_stopped(st)) return;
+  double* terms = terms_out(tbase, half, st, which);
   const int e = e0 + blockIdx.x;
   __shared__ double s[2 * kRayAcc];
   for (int t = threadIdx.x; t < 2 * kRayAcc; t += blockDim.x) {
@@ -259,7 +288,10 @@ __global__ void k_edge_sum_ray(const double* __restrict__ partials, int bpe, int
 }
 
 // terms[e] = {H1 (28), g1 (7), cost1, H2 (28), g2 (7), cost2}
-__global__ void k_edge_sum(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ terms) {
+__global__ void k_edge_sum(const double* __restrict__ partials, int bpe, int e0, double* __restrict__ tbase,
+                           int64_t half, const GNState* st, int which) {
+  if (gn_stopped(st)) return;
+  double* terms = terms_out(tbase, half, st, which);
   const int e = e0 + blockIdx.x;
   for (int t = threadIdx.x; t < 2 * 36; t += blockDim.x) {
     const int dir = t / 36, i = t % 36;
@@ -279,9 +311,11 @@ __device__ __forceinline__ double tri(const double* h28, int a, int b) {  // upp
 }
 
 // K8: per edge S (49) and g (7) in the global frame.  adj[k] = Ad(T_wk^-1).
-__global__ void k_edge_blocks(const double* __restrict__ terms, const int2* __restrict__ edges,
-                              const double* __restrict__ adj, int N, int E, double* __restrict__ S,
-                              double* __restrict__ G) {
+__global__ void k_edge_blocks(const double* __restrict__ tbase, int64_t half, const GNState* st,
+                              const int2* __restrict__ edges, const double* __restrict__ adj, int N, int E,
+                              double* __restrict__ S, double* __restrict__ G) {
+  if (gn_stopped(st)) return;
+  const double* terms = st ? tbase + st->cur * half : tbase;
   const int e = blockIdx.x;
   if (e >= E) return;
   const int2 ij = edges[e];
@@ -519,150 +553,328 @@ __global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
   }
 }
 
-// ------------------------------------------------------- K9, envelope form
-// The gauge-fixed system is block-sparse (edges) and LDL^T in natural order
-// fills in only inside the envelope [first[i], i] of every row i.  Panel p
-// (NB columns) updates only the rows whose envelope reaches into it
-// (R_p = {i >= p_end : first[i] < p_end}, precomputed on the host), so a
-// banded graph with a few loop closures costs O(n (b + border)^2) instead of
-// O(n^3).  Same factorisation as the dense path (no pivoting, exact-zero
-// pivot -> failure); zero blocks are skipped, fill-in can only appear where
-// the dense algorithm would write it.  One CTA of 1024 threads.
-constexpr int kEnvRows = 320;  // max active rows per panel held in shared memory
+// ------------------------------------------------------- K9, skyline form
+// The gauge-fixed system is block-sparse (edges); LDL^T fills in only inside
+// the envelope [first[i], i] of every row i, so the lower triangle is stored
+// as a skyline (row i: columns first[i]..i contiguous at rowptr[i]).  The
+// factorisation runs over 7-column panels (one keyframe); panel k updates only
+// its active rows R_k = {i > panel : first[i] <= panel end} (precomputed), so
+// a banded graph with loop closures costs O(n (b + border)^2) instead of
+// O(n^3).  No pivoting, failure iff a pivot is exactly zero (SimplicialLDLT
+// factorisation semantics; the reference's AMD ordering only changes
+// rounding).  The forward substitution is fused into the factorisation.  One
+// CTA: the whole solve is latency-bound (~10^6 flops at N = 100).
+constexpr int kSkyRows = 512;   // max active rows of a panel
+constexpr int kSkyMaxN = 8192;  // rhs + row offsets kept in shared memory
+constexpr int kSkyThreads = 1024;
 
-struct EnvArgs {
-  double* A;         // work matrix (n x n row-major; envelope entries valid)
-  int n;
-  const int* first;  // first[i]: first column of row i's envelope
-  const int* rp_ptr; // panel p: active rows rp_rows[rp_ptr[p] .. rp_ptr[p+1])
+struct SkyArgs {
+  const double* H;          // assembled skyline (undamped)
+  double* A;                // work skyline
+  const int* rowptr;        // [n]
+  const int* first;         // [n]
+  const int* rp_ptr;        // [N+1] 7-column panels
   const int* rp_rows;
-  const double* b;
-  double* x;
-  int* status;
+  const double* grad;       // rhs = -grad
+  double* x;                // tau
+  long long nnz;
+  int n;
+  int attempt;              // damping attempt (backend.cpp:208-227)
+  double damping_init;
+  GNState* st;
 };
 
-__global__ void k_env_copy(const double* __restrict__ H, double* __restrict__ A, int n, const int* __restrict__ first,
-                           double lambda) {
-  const int i = blockIdx.x;
-  for (int j = first[i] + (int)threadIdx.x; j <= i; j += blockDim.x)
-    A[(size_t)i * n + j] = H[(size_t)i * n + j] + (i == j ? lambda : 0.0);
+// lane -> (row, col) of the 28 lower-triangle entries of a 7x7 block
+__constant__ int c_row[28] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5, 6, 6, 6, 6, 6, 6, 6};
+__constant__ int c_col[28] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5, 0, 1, 2, 3, 4, 5, 6};
+
+__device__ __forceinline__ int sky_at(const int* rowptr, const int* first, int i, int j) {
+  return rowptr[i] + (j - first[i]);
 }
 
-__global__ void __launch_bounds__(1024) k_ldlt_env(EnvArgs P) {
+__global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
+  if (P.st->stop || P.st->solved) return;
   extern __shared__ double smem[];
-  double(*sD)[NB + 1] = reinterpret_cast<double(*)[NB + 1]>(smem);
-  double* sW = smem + NB * (NB + 1);  // [kEnvRows][NB]
-  double* sL = sW + kEnvRows * NB;    // [kEnvRows][NB]
-  const int n = P.n;
+  double* y = smem;                   // [n]
+  double* sL = y + P.n;               // [kSkyRows][7]  L of the active rows
+  double* sW = sL + kSkyRows * 7;     // [kSkyRows][7]  L D
+  int* rp = reinterpret_cast<int*>(sW + kSkyRows * 7);  // [n] row offsets
+  int* first = rp + P.n;                                // [n] envelope starts
+  __shared__ double sD[7][8];         // panel block: D on the diagonal, unit L below
+  __shared__ int ok;
+  const int n = P.n, tid = threadIdx.x, nth = blockDim.x;
   double* A = P.A;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
-  if (tid == 0) *P.status = 1;
-  const int npanel = (n + NB - 1) / NB;
-  for (int pi = 0; pi < npanel; ++pi) {
-    const int p = pi * NB, nb = min(NB, n - p);
-    // (a) diagonal block
-    for (int i = tid; i < nb * nb; i += nth) {
-      const int r = i / nb, c = i % nb;
-      sD[r][c] = (c <= r && c + p >= P.first[p + r]) ? A[(size_t)(p + r) * n + p + c] : 0.0;
+  for (int i = tid; i < n; i += nth) {
+    rp[i] = P.rowptr[i];
+    first[i] = P.first[i];
+  }
+  double lambda = 0.0;
+  if (P.attempt > 0) {
+    lambda = P.damping_init;
+    for (int a = 1; a < P.attempt; ++a) lambda *= 10.0;
+  }
+  for (long long e = tid; e < P.nnz; e += nth) A[e] = P.H[e];
+  for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
+  if (tid == 0) ok = 1;
+  __syncthreads();
+  if (lambda != 0.0)  // backend.cpp:210-213: lambda on every diagonal entry
+    for (int i = tid; i < n; i += nth) A[sky_at(rp, first, i, i)] += lambda;
+  __syncthreads();
+  const int npanel = (n + 6) / 7;
+  for (int k = 0; k < npanel; ++k) {
+    const int c0 = 7 * k, nb = min(7, n - c0);
+    // (a) panel block, warp 0: LDL^T of the (already updated) 7x7 block in
+    // shared memory (lane (r, s) owns entry r >= s), then the panel's forward solve
+    if (tid < 32) {
+      const int r = tid < 28 ? c_row[tid] : 0, c = tid < 28 ? c_col[tid] : 0;
+      const bool own = tid < 28 && r < nb;
+      if (own) sD[r][c] = (c0 + c >= first[c0 + r]) ? A[sky_at(rp, first, c0 + r, c0 + c)] : 0.0;
+      __syncwarp();
+      for (int k2 = 0; k2 < nb; ++k2) {
+        const double D = sD[k2][k2];
+        if (tid == 0 && D == 0.0) ok = 0;
+        // trailing entries (r, c) with c > k2: a_rc -= a_r,k2 a_c,k2 / D (a_*,k2 not yet scaled)
+        const double upd = (own && c > k2) ? sD[r][k2] * sD[c][k2] / D : 0.0;
+        __syncwarp();
+        if (own && c > k2) sD[r][c] -= upd;
+        if (own && c == k2 && r > k2) sD[r][c] /= D;
+        __syncwarp();
+      }
+      if (own && c0 + c >= first[c0 + r]) A[sky_at(rp, first, c0 + r, c0 + c)] = sD[r][c];
+      // L y = b inside the panel: lane t < nb holds y_t
+      double yv = tid < nb ? y[c0 + tid] : 0.0;
+      for (int k2 = 0; k2 < nb; ++k2) {
+        const double yk = __shfl_sync(0xffffffffu, yv, k2);
+        if (tid > k2 && tid < nb) yv -= sD[tid][k2] * yk;
+      }
+      if (tid < nb) y[c0 + tid] = yv;
     }
     __syncthreads();
-    for (int c = 0; c < nb; ++c) {
-      const double d = sD[c][c];
-      if (tid == 0 && d == 0.0) *P.status = 0;  // SimplicialLDLT: exact zero pivot fails
-      const int m = nb - c - 1;
-      for (int i = tid; i < m * m; i += nth) {
-        const int r = c + 1 + i / m, s = c + 1 + i % m;
-        if (s <= r) sD[r][s] -= sD[r][c] * sD[s][c] / d;
-      }
-      __syncthreads();
-      for (int r = c + 1 + tid; r < nb; r += nth) sD[r][c] /= d;
-      __syncthreads();
-    }
-    for (int i = tid; i < nb * nb; i += nth) {
-      const int r = i / nb, c = i % nb;
-      if (c <= r && c + p >= P.first[p + r]) A[(size_t)(p + r) * n + p + c] = sD[r][c];
-    }
-    // (b) panel rows: W = A_R,panel L11^-T (one warp per row), L21 = W / D
-    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
-    for (int q = warp; q < ns; q += nth / 32) {
+    // (b) active rows: W = A_i,panel L^-T, L_i = W D^-1; forward update of y_i
+    const int r0 = P.rp_ptr[k], ns = P.rp_ptr[k + 1] - r0;
+    for (int q = tid; q < ns; q += nth) {
       const int i = P.rp_rows[r0 + q];
-      double a = (lane < nb && p + lane >= P.first[i]) ? A[(size_t)i * n + p + lane] : 0.0;
-      for (int m = 0; m < nb; ++m) {
-        const double wm = __shfl_sync(0xffffffffu, a, m);
-        if (lane > m && lane < nb) a -= wm * sD[lane][m];
+      double w[7];
+      const int c1 = max(0, first[i] - c0);
+      const int base = rp[i] + (c0 - first[i]);
+#pragma unroll
+      for (int t = 0; t < 7; ++t) w[t] = (t >= c1 && t < nb) ? A[base + t] : 0.0;
+#pragma unroll
+      for (int t = 1; t < 7; ++t)
+#pragma unroll
+        for (int u = 0; u < t; ++u) w[t] -= w[u] * sD[t][u];
+      double yi = 0.0;
+#pragma unroll
+      for (int t = 0; t < 7; ++t) {
+        if (t >= nb) break;
+        const double l = w[t] / sD[t][t];
+        if (t >= c1) A[base + t] = l;
+        sL[q * 7 + t] = l;
+        sW[q * 7 + t] = w[t];
+        yi += l * y[c0 + t];
       }
-      if (lane < nb) {
-        const double l = a / sD[lane][lane];
-        sW[q * NB + lane] = a;
-        sL[q * NB + lane] = l;
-        A[(size_t)i * n + p + lane] = l;
-      }
+      y[i] -= yi;
     }
     __syncthreads();
     // (c) trailing update over active pairs (j <= i, inside row i's envelope)
     const int npair = ns * (ns + 1) / 2;
     for (int t = tid; t < npair; t += nth) {
-      int qi = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+      int qi = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
       while ((qi + 1) * (qi + 2) / 2 <= t) ++qi;
       while (qi * (qi + 1) / 2 > t) --qi;
       const int qj = t - qi * (qi + 1) / 2;
       const int i = P.rp_rows[r0 + qi], j = P.rp_rows[r0 + qj];
-      if (j < P.first[i]) continue;
-      double s = 0.0;
-      for (int k = 0; k < nb; ++k) s += sW[qi * NB + k] * sL[qj * NB + k];
-      A[(size_t)i * n + j] -= s;
+      if (j < first[i]) continue;
+      double sacc = 0.0;
+#pragma unroll
+      for (int u = 0; u < 7; ++u) sacc += sW[qi * 7 + u] * sL[qj * 7 + u];
+      A[sky_at(rp, first, i, j)] -= sacc;
     }
     __syncthreads();
   }
-  // forward: L y = b
-  for (int i = tid; i < n; i += nth) P.x[i] = P.b[i];
+  // D z = y
+  for (int i = tid; i < n; i += nth) y[i] /= A[sky_at(rp, first, i, i)];
   __syncthreads();
-  for (int pi = 0; pi < npanel; ++pi) {
-    const int p = pi * NB, nb = min(NB, n - p);
-    if (warp == 0) {
-      double y = lane < nb ? P.x[p + lane] : 0.0;
-      for (int m = 0; m < nb; ++m) {
-        const double ym = __shfl_sync(0xffffffffu, y, m);
-        if (lane > m && lane < nb && p + m >= P.first[p + lane]) y -= A[(size_t)(p + lane) * n + p + m] * ym;
-      }
-      if (lane < nb) P.x[p + lane] = y;
-    }
-    __syncthreads();
-    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
-    for (int q = tid; q < ns; q += nth) {
-      const int i = P.rp_rows[r0 + q];
-      double s = 0.0;
-      for (int k = max(0, P.first[i] - p); k < nb; ++k) s += A[(size_t)i * n + p + k] * P.x[p + k];
-      P.x[i] -= s;
-    }
-    __syncthreads();
-  }
-  for (int i = tid; i < n; i += nth) P.x[i] /= A[(size_t)i * n + i];
-  __syncthreads();
-  // backward: L^T x = z
-  for (int pi = npanel - 1; pi >= 0; --pi) {
-    const int p = pi * NB, nb = min(NB, n - p);
-    const int r0 = P.rp_ptr[pi], ns = P.rp_ptr[pi + 1] - r0;
+  // L^T x = z, panel by panel from the end
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int k = npanel - 1; k >= 0; --k) {
+    const int c0 = 7 * k, nb = min(7, n - c0);
+    const int r0 = P.rp_ptr[k], ns = P.rp_ptr[k + 1] - r0;
     if (warp < nb) {
-      const int k = p + warp;
-      double s = 0.0;
+      double sacc = 0.0;
       for (int q = lane; q < ns; q += 32) {
         const int i = P.rp_rows[r0 + q];
-        if (k >= P.first[i]) s += A[(size_t)i * n + k] * P.x[i];
+        if (c0 + warp >= first[i]) sacc += A[sky_at(rp, first, i, c0 + warp)] * y[i];
       }
-      s = warp_sum(s);
-      if (lane == 0) P.x[k] -= s;
+      sacc = warp_sum(sacc);
+      if (lane == 0) y[c0 + warp] -= sacc;
     }
     __syncthreads();
-    if (warp == 0) {
-      double xv = lane < nb ? P.x[p + lane] : 0.0;
-      for (int m = nb - 1; m >= 0; --m) {
-        const double xm = __shfl_sync(0xffffffffu, xv, m);
-        if (lane < m && p + lane >= P.first[p + m]) xv -= A[(size_t)(p + m) * n + p + lane] * xm;
+    if (tid < 32) {  // L_panel^T x = z inside the panel: lane t < nb holds x_t
+      double xv = tid < nb ? y[c0 + tid] : 0.0;
+      double lrow[7];
+#pragma unroll
+      for (int c = 0; c < 7; ++c)  // column tid of L below the diagonal: L[c][tid], c > tid
+        lrow[c] = (tid < nb && c < nb && c > tid && c0 + tid >= first[c0 + c]) ? A[sky_at(rp, first, c0 + c, c0 + tid)]
+                                                                              : 0.0;
+      for (int c = nb - 1; c >= 0; --c) {
+        const double xc = __shfl_sync(0xffffffffu, xv, c);
+#pragma unroll
+        for (int q = 0; q < 7; ++q)
+          if (q == c && tid < c) xv -= lrow[q] * xc;
       }
-      if (lane < nb) P.x[p + lane] = xv;
+      if (tid < nb) y[c0 + tid] = xv;
     }
     __syncthreads();
+  }
+  // accept iff factorised, finite and ||tau||_inf < 1e3 (backend.cpp:220-223)
+  __shared__ int good;
+  if (tid == 0) good = ok;
+  __syncthreads();
+  for (int i = tid; i < n; i += nth) {
+    const double v = y[i];
+    P.x[i] = v;
+    if (!isfinite(v) || !(fabs(v) < 1e3)) good = 0;
+  }
+  __syncthreads();
+  if (tid == 0 && good) P.st->solved = 1;
+}
+
+// ----------------------------------------------------- device control loop
+// Ad(T_k^-1) of every keyframe (backend.cpp:114).
+__global__ void k_adjoint(const DSim3* __restrict__ P, int N, double* __restrict__ adj, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) sim3_adjoint(sim3_inv(P[k]), adj + 49 * (size_t)k);
+}
+
+// Lower-triangle blocks into the skyline; anchor gauge (backend.cpp:144-155).
+__global__ void k_sky_assemble(const int* __restrict__ blk_rc, const int* __restrict__ blk_ptr,
+                               const int* __restrict__ contrib, const double* __restrict__ S,
+                               const int* __restrict__ rowptr, const int* __restrict__ first,
+                               double* __restrict__ H, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const int k = blk_rc[2 * b], l = blk_rc[2 * b + 1];
+  if (tid >= 49 || l > k) return;
+  const int r = tid / 7, c = tid % 7;
+  if (k == l && c > r) return;
+  double sacc = 0.0;
+  for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; ++q) {
+    const int cc = contrib[q];
+    const double v = S[(size_t)(cc >> 1) * 49 + tid];
+    sacc += (cc & 1) ? -v : v;
+  }
+  H[sky_at(rowptr, first, 7 * k + r, 7 * l + c)] = sacc;
+}
+
+__global__ void k_sky_grad(const int* __restrict__ g_ptr, const int* __restrict__ g_contrib,
+                           const double* __restrict__ G, int N, int anchor, double* __restrict__ grad,
+                           const int* __restrict__ rowptr, const int* __restrict__ first,
+                           double* __restrict__ H, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int k = blockIdx.x, r = threadIdx.x;
+  if (k >= N || r >= 7) return;
+  double sacc = 0.0;
+  for (int q = g_ptr[k]; q < g_ptr[k + 1]; ++q) {
+    const int c = g_contrib[q];
+    const double v = G[(size_t)(c >> 1) * 7 + r];
+    sacc += (c & 1) ? -v : v;
+  }
+  if (k == anchor) {  // (a, a) = I, g_a = 0
+    sacc = 0.0;
+    for (int c = 0; c <= r; ++c) H[sky_at(rowptr, first, 7 * k + r, 7 * k + c)] = (c == r) ? 1.0 : 0.0;
+  }
+  grad[7 * k + r] = sacc;
+}
+
+// Deterministic block sum (fixed tree; blockDim a power of two <= 1024).
+__device__ double block_sum_fixed(double v) {
+  __shared__ double red[1024];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Cost of a terms buffer: sum of both directed constraints of every edge.
+__device__ double terms_cost(const double* __restrict__ terms, int E) {
+  double c = 0.0;
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    c += terms[(size_t)e * PMX_EDGE_TERMS + 35] + terms[(size_t)e * PMX_EDGE_TERMS + 71];
+  return block_sum_fixed(c);
+}
+
+// Initial cost (backend.cpp:201).
+__global__ void k_gn_init(const double* __restrict__ terms, int E, GNState* st) {
+  const double c = terms_cost(terms, E);
+  if (threadIdx.x == 0) {
+    st->cost = c;
+    st->trace[0] = c;
+    st->trace_len = 1;
+  }
+}
+
+// Start of an iteration: count it, clear the solve flag (backend.cpp:203-204).
+__global__ void k_gn_begin(GNState* st) {
+  if (st->stop) return;
+  st->iterations++;
+  st->solved = 0;
+}
+
+// After the damping attempts: failure leaves the state intact (228-230);
+// else retract the non-anchor poses, T <- exp(tau) T (235-239).
+__global__ void k_gn_retract(const DSim3* __restrict__ P, DSim3* __restrict__ Pt, const double* __restrict__ tau,
+                             int N, int anchor, GNState* st) {
+  if (st->stop) return;
+  if (!st->solved) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      st->failed = 1;
+      st->stop = 1;
+    }
+    return;
+  }
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) Pt[k] = k == anchor ? P[k] : sim3_mul(sim3_exp(tau + 7 * k), P[k]);
+}
+
+// Accept / revert (backend.cpp:240-252) and the pose trace of the iteration.
+__global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int E, DSim3* __restrict__ P,
+                            const DSim3* __restrict__ Pt, const double* __restrict__ tau, int N, double tol,
+                            pmx_sim3* trace, GNState* st) {
+  __shared__ int accept, it;
+  if (st->stop) return;  // uniform: st is only written below, after the barriers
+  const double c = terms_cost(tbase + (1 - st->cur) * half, E);
+  double t2 = 0.0;
+  for (int i = threadIdx.x; i < 7 * N; i += blockDim.x) t2 += tau[i] * tau[i];
+  const double n2 = block_sum_fixed(t2);
+  if (threadIdx.x == 0) {
+    accept = !(c > st->cost * (1.0 + 1e-12) + 1e-300);
+    it = st->iterations - 1;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {
+    if (accept) P[k] = Pt[k];
+    if (trace) trace[(size_t)it * N + k] = to_pmx(accept ? Pt[k] : P[k]);
+  }
+  if (threadIdx.x == 0) {
+    if (!accept) {
+      st->stop = 1;
+      st->converged = 1;
+    } else {
+      st->cost = c;
+      st->cur = 1 - st->cur;
+      if (st->trace_len < PMX_MAX_TRACE) st->trace[st->trace_len++] = c;
+      if (sqrt(n2) < tol) {
+        st->stop = 1;
+        st->converged = 1;
+      }
+    }
   }
 }
 
@@ -804,80 +1016,114 @@ static std::vector<DSim3> host_poses(const pmx_graph* g) {
   return P;
 }
 
-// Edge terms for edges [e0, e1) at poses P -> terms (device, indexed by absolute edge).
-static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, const std::vector<DSim3>& P, int e0,
-                       int e1, double* terms) {
-  if (e1 <= e0) return;
-  std::vector<PoseR<float>> rel(2 * (size_t)G.E);
-  std::vector<PoseR<double>> rel64(2 * (size_t)G.E);
-  for (int e = e0; e < e1; ++e) {
-    const int i = G.edges[e].x, j = G.edges[e].y;
-    if (i < 0 || j < 0 || i >= G.N || j >= G.N) continue;
-    const DSim3 a = sim3_mul(sim3_inv(P[i]), P[j]);  // relative_pose(ref=i, src=j)
-    const DSim3 b = sim3_mul(sim3_inv(P[j]), P[i]);  // relative_pose(ref=j, src=i)
-    rel[2 * e] = make_pose<float>(a);
-    rel[2 * e + 1] = make_pose<float>(b);
-    rel64[2 * e] = make_pose<double>(a);
-    rel64[2 * e + 1] = make_pose<double>(b);
-  }
-  DevBuf drel(sizeof(PoseR<float>) * rel.size(), ctx.stream);
-  PMX_CUDA(cudaMemcpyAsync(drel.p, rel.data(), drel.bytes, cudaMemcpyHostToDevice, ctx.stream));
-  DevBuf drel64(sizeof(PoseR<double>) * rel64.size(), ctx.stream);
-  PMX_CUDA(cudaMemcpyAsync(drel64.p, rel64.data(), drel64.bytes, cudaMemcpyHostToDevice, ctx.stream));
+// Relative poses of both directed constraints of every edge (backend.cpp:
+// 101-110, relative_pose = T_ref^-1 T_src) from device-resident poses.
+__global__ void k_rel_poses(const DSim3* __restrict__ P, const int2* __restrict__ edges, int N, int e0, int e1,
+                            PoseR<float>* rel, PoseR<double>* rel64, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int e = e0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= e1) return;
+  const int2 ij = edges[e];
+  if (ij.x < 0 || ij.y < 0 || ij.x >= N || ij.y >= N) return;
+  const DSim3 a = sim3_mul(sim3_inv(P[ij.x]), P[ij.y]);  // ref = i, src = j
+  const DSim3 b = sim3_mul(sim3_inv(P[ij.y]), P[ij.x]);  // ref = j, src = i
+  rel[2 * e] = make_pose<float>(a);
+  rel[2 * e + 1] = make_pose<float>(b);
+  rel64[2 * e] = make_pose<double>(a);
+  rel64[2 * e + 1] = make_pose<double>(b);
+}
+
+// Buffers of one edge pass, allocated once per API call.
+struct EdgeWork {
+  DevBuf rel, rel64, partials;
+  int bpe = 1;
+  EdgeArgs A;
+};
+
+static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& p, EdgeWork& W) {
+  const int E = std::max(G.E, 1);
+  W.rel = DevBuf(sizeof(PoseR<float>) * 2 * (size_t)E, ctx.stream);
+  W.rel64 = DevBuf(sizeof(PoseR<double>) * 2 * (size_t)E, ctx.stream);
   // about two waves of 2 resident blocks per SM, >= 16 matches per thread
   const int64_t want = (2LL * 2 * ctx.num_sms + G.E - 1) / std::max(1, G.E);
-  const int bpe = (int)std::max<int64_t>(1, std::min<int64_t>(want, (G.max_count + 4095) / 4096));
-  DevBuf partials(sizeof(double) * (size_t)G.E * bpe * 2 * kAcc, ctx.stream);
-  EdgeArgs A;
+  W.bpe = (int)std::max<int64_t>(1, std::min<int64_t>(want, (G.max_count + 4095) / 4096));
+  const bool ray = p.mode == PMX_TRACK_RAY;
+  require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
+  W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);
+  EdgeArgs& A = W.A;
+  A.st = nullptr;
   A.clouds = G.clouds.as<CloudDev>();
   A.matches = G.matches.as<MatchesDev>();
   A.edges = G.edges_dev.as<int2>();
-  A.rel = drel.as<PoseR<float>>();
-  A.rel64 = drel64.as<PoseR<double>>();
+  A.rel = W.rel.as<PoseR<float>>();
+  A.rel64 = W.rel64.as<PoseR<double>>();
   A.qmin = G.qmin.as<double>();
   A.wp = backend_weights(p);
   A.K = p.has_intrinsics ? IntrDev{p.intrinsics.fx, p.intrinsics.fy, p.intrinsics.cx, p.intrinsics.cy, 1}
                          : IntrDev{0, 0, 0, 0, 0};
   A.mode = p.mode;
   A.N = G.N;
-  A.bpe = bpe;
-  A.partials = partials.as<double>();
-  const bool ray = p.mode == PMX_TRACK_RAY;
-  require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
+  A.bpe = W.bpe;
+  A.partials = W.partials.as<double>();
   A.c4 = ray ? G.c4ptrs.as<const float4*>() : nullptr;
   A.packed = ray ? G.pk.as<int4>() : nullptr;
   A.pk_total = ray ? G.pk_total.as<int>() : nullptr;
   A.seg = G.seg;
-  if (ray) {  // closed-form partials are 2 x 29 per block
-    partials = DevBuf(sizeof(double) * (size_t)G.E * bpe * 2 * kRayAcc, ctx.stream);
-    A.partials = partials.as<double>();
-  }
+}
+
+// Edge terms for edges [e0, e1) at the device poses dP -> terms (indexed by
+// absolute edge; with a loop state: the current / trial half of `terms`).
+static void edge_terms_dev(Context& ctx, const DevGraph& G, const pmx_backend_params& p, EdgeWork& W,
+                           const DSim3* dP, int e0, int e1, double* terms, const GNState* st = nullptr,
+                           int which = 0) {
+  if (e1 <= e0) return;
+  const bool ray = p.mode == PMX_TRACK_RAY;
+  const int64_t half = (int64_t)PMX_EDGE_TERMS * std::max(G.E, 1);
+  k_rel_poses<<<(e1 - e0 + 127) / 128, 128, 0, ctx.stream>>>(dP, G.edges_dev.as<int2>(), G.N, e0, e1,
+                                                                W.rel.as<PoseR<float>>(), W.rel64.as<PoseR<double>>(),
+                                                                st);
+  launch_check(ctx, "k_rel_poses");
+  EdgeArgs A = W.A;
+  A.st = st;
   for (int c0 = e0; c0 < e1; c0 += 65535) {
     const int cn = std::min(65535, e1 - c0);
     {
       ProfScope ps(ctx, "k_edge_terms");
       if (ray)
-        k_edge_terms_ray<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+        k_edge_terms_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(A, c0);
       else
-        k_edge_terms<<<dim3(bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+        k_edge_terms<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(A, c0);
     }
     launch_check(ctx, "k_edge_terms");
     if (ray)
-      k_edge_sum_ray<<<cn, 64, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
+      k_edge_sum_ray<<<cn, 64, 0, ctx.stream>>>(W.partials.as<double>(), W.bpe, c0, terms, half, st, which);
     else
-      k_edge_sum<<<cn, 128, 0, ctx.stream>>>(partials.as<double>(), bpe, c0, terms);
+      k_edge_sum<<<cn, 128, 0, ctx.stream>>>(W.partials.as<double>(), W.bpe, c0, terms, half, st, which);
     launch_check(ctx, "k_edge_sum");
   }
-  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // rel host vector lifetime
+}
+
+// Host-pose variant (edge_terms / backend_cost / assemble_system entry points).
+static void edge_terms(Context& ctx, DevGraph& G, const pmx_backend_params& p, const std::vector<DSim3>& P, int e0,
+                       int e1, double* terms) {
+  if (e1 <= e0) return;
+  EdgeWork W;
+  make_edge_work(ctx, G, p, W);
+  DevBuf dP(sizeof(DSim3) * std::max<size_t>(P.size(), 1), ctx.stream);
+  if (!P.empty()) PMX_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(DSim3) * P.size(), cudaMemcpyHostToDevice, ctx.stream));
+  edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), e0, e1, terms);
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // P host vector lifetime
 }
 
 struct Assembly {
   int dim = 0;
   DevBuf blk_rc, blk_ptr, contrib, g_ptr, g_contrib, adj, S, G, H, grad;
   int nblocks = 0;
-  // envelope structure for k_ldlt_env (env_ok = every panel fits in shared memory)
-  bool env_ok = false;
-  DevBuf first, rp_ptr, rp_rows;
+  // skyline of the gauge-fixed system for k_ldlt_sky (sky_ok: every panel's
+  // active rows and the rhs fit the kernel's shared memory)
+  bool sky_ok = false;
+  long long nnz = 0;
+  DevBuf first, rowptr, rp_ptr, rp_rows, skyH, skyA;
 };
 
 // Contribution lists (edge order) for every non-zero block, gauge-fixed.
@@ -925,30 +1171,38 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
     for (int k = 0; k < N; ++k) fb[k] = k;
     for (auto& kv : blocks)
       if (kv.first.second <= kv.first.first) fb[kv.first.first] = std::min(fb[kv.first.first], kv.first.second);
-    std::vector<int> first(7 * N), rptr{0}, rrows;
-    for (int k = 0; k < N; ++k)
-      for (int r = 0; r < 7; ++r) first[7 * k + r] = 7 * fb[k];
-    const int n = 7 * N, npanel = (n + NB - 1) / NB;
-    bool fits = true;
-    for (int pi = 0; pi < npanel && fits; ++pi) {
-      const int pend = std::min(n, (pi + 1) * NB);
+    const int n = 7 * N;
+    std::vector<int> first(n), rptr{0}, rrows, rowptr(n);
+    long long nnz = 0;
+    for (int i = 0; i < n; ++i) {
+      first[i] = 7 * fb[i / 7];
+      rowptr[i] = (int)std::min<long long>(nnz, INT32_MAX);
+      nnz += i - first[i] + 1;
+    }
+    bool fits = n <= kSkyMaxN && nnz < INT32_MAX;
+    for (int k = 0; k < N && fits; ++k) {  // 7-column panels
+      const int pend = 7 * k + 7;
       for (int i = pend; i < n; ++i)
         if (first[i] < pend) rrows.push_back(i);
-      if ((int)rrows.size() - rptr.back() > kEnvRows) fits = false;
+      if ((int)rrows.size() - rptr.back() > kSkyRows) fits = false;
       rptr.push_back((int)rrows.size());
     }
-    As.env_ok = fits && N > 0;
-    if (As.env_ok) {
+    As.sky_ok = fits && N > 0;
+    if (As.sky_ok) {
+      As.nnz = nnz;
       up(As.first, first);
       up(As.rp_ptr, rptr);
       up(As.rp_rows, rrows);
+      up(As.rowptr, rowptr);
+      As.skyH = DevBuf(sizeof(double) * nnz, ctx.stream);
+      As.skyA = DevBuf(sizeof(double) * nnz, ctx.stream);
       PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     }
   }
   As.adj =DevBuf(sizeof(double) * 49 * std::max(N, 1), ctx.stream);
   As.S = DevBuf(sizeof(double) * 49 * std::max(G.E, 1), ctx.stream);
   As.G = DevBuf(sizeof(double) * 7 * std::max(G.E, 1), ctx.stream);
-  As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);
+  if (!As.sky_ok) As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);  // dense path
   As.grad = DevBuf(sizeof(double) * std::max(As.dim, 1), ctx.stream);
   PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // host vectors lifetime
 }
@@ -958,9 +1212,10 @@ static void assemble(Context& ctx, const DevGraph& G, Assembly& As, const std::v
   std::vector<double> adj(49 * (size_t)G.N);
   for (int k = 0; k < G.N; ++k) sim3_adjoint(sim3_inv(P[k]), adj.data() + 49 * (size_t)k);  // backend.cpp:114
   PMX_CUDA(cudaMemcpyAsync(As.adj.p, adj.data(), sizeof(double) * adj.size(), cudaMemcpyHostToDevice, ctx.stream));
+  if (!As.H.p) As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);
   if (G.E) {
-    k_edge_blocks<<<G.E, 64, 0, ctx.stream>>>(terms, G.edges_dev.as<int2>(), As.adj.as<double>(), G.N, G.E,
-                                             As.S.as<double>(), As.G.as<double>());
+    k_edge_blocks<<<G.E, 64, 0, ctx.stream>>>(terms, 0, nullptr, G.edges_dev.as<int2>(), As.adj.as<double>(), G.N,
+                                             G.E, As.S.as<double>(), As.G.as<double>());
     launch_check(ctx, "k_edge_blocks");
   }
   PMX_CUDA(cudaMemsetAsync(As.H.p, 0, As.H.bytes, ctx.stream));
@@ -982,39 +1237,27 @@ __global__ void k_negate(const double* a, double* b, int n) {
   if (i < n) b[i] = -a[i];
 }
 
-// Damped solve attempts (backend.cpp:208-230).  Returns solved; tau on host.
+// Dense damped solve attempts (backend.cpp:208-230) for graphs whose skyline
+// does not fit k_ldlt_sky.  Returns solved; tau on host.
 static bool damped_solve(Context& ctx, const pmx_backend_params& p, Assembly& As, std::vector<double>& tau) {
   const int n = As.dim;
   DevBuf work(sizeof(double) * (size_t)n * n, ctx.stream), rhs(sizeof(double) * n, ctx.stream),
-      x(sizeof(double) * n, ctx.stream), status(sizeof(int), ctx.stream), W;
+      x(sizeof(double) * n, ctx.stream), status(sizeof(int), ctx.stream);
   k_negate<<<(n + 255) / 256, 256, 0, ctx.stream>>>(As.grad.as<double>(), rhs.as<double>(), n);
   launch_check(ctx, "k_negate");
-  int nb = 0;
-  const size_t env_smem = sizeof(double) * (NB * (NB + 1) + 2 * kEnvRows * NB);
-  if (As.env_ok) {
-    PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_env, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)env_smem));
-  } else {
-    W = DevBuf(sizeof(double) * (size_t)n * NB, ctx.stream);
-    int per_sm = 0;
-    PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
-    nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
-  }
+  DevBuf W(sizeof(double) * (size_t)n * NB, ctx.stream);
+  int per_sm = 0;
+  PMX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)k_ldlt, 256, 0));
+  const int nb = std::max(1, std::min(per_sm, 2)) * ctx.num_sms;
   double lambda = 0.0;
   tau.assign(n, 0.0);
   for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
     {
       ProfScope ps(ctx, "k_ldlt");
-      if (As.env_ok) {
-        k_env_copy<<<n, 128, 0, ctx.stream>>>(As.H.as<double>(), work.as<double>(), n, As.first.as<int>(), lambda);
-        EnvArgs E{work.as<double>(), n, As.first.as<int>(), As.rp_ptr.as<int>(), As.rp_rows.as<int>(),
-                  rhs.as<double>(), x.as<double>(), status.as<int>()};
-        k_ldlt_env<<<1, 1024, env_smem, ctx.stream>>>(E);
-      } else {
-        LdltArgs L{work.as<double>(), As.H.as<double>(), lambda, rhs.as<double>(), x.as<double>(), W.as<double>(), n,
-                   status.as<int>()};
-        void* args[] = {&L};
-        PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
-      }
+      LdltArgs L{work.as<double>(), As.H.as<double>(), lambda, rhs.as<double>(), x.as<double>(), W.as<double>(), n,
+                 status.as<int>()};
+      void* args[] = {&L};
+      PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_ldlt, dim3(nb), dim3(256), args, 0, ctx.stream));
     }
     launch_check(ctx, "k_ldlt");
     int ok = 0;
@@ -1033,6 +1276,48 @@ static bool damped_solve(Context& ctx, const pmx_backend_params& p, Assembly& As
     lambda = lambda == 0.0 ? p.damping_init : lambda * 10.0;
   }
   return false;
+}
+
+// Skyline assembly at the device poses dP from the current terms (loop state
+// `st`, or `terms` itself when st is null).
+static void assemble_sky(Context& ctx, const DevGraph& G, Assembly& As, const DSim3* dP, const double* tbase,
+                         int64_t half, const GNState* st) {
+  k_adjoint<<<(G.N + 127) / 128, 128, 0, ctx.stream>>>(dP, G.N, As.adj.as<double>(), st);
+  launch_check(ctx, "k_adjoint");
+  if (G.E) {
+    k_edge_blocks<<<G.E, 64, 0, ctx.stream>>>(tbase, half, st, G.edges_dev.as<int2>(), As.adj.as<double>(), G.N, G.E,
+                                             As.S.as<double>(), As.G.as<double>());
+    launch_check(ctx, "k_edge_blocks");
+  }
+  PMX_CUDA(cudaMemsetAsync(As.skyH.p, 0, As.skyH.bytes, ctx.stream));
+  if (As.nblocks) {
+    k_sky_assemble<<<As.nblocks, 64, 0, ctx.stream>>>(As.blk_rc.as<int>(), As.blk_ptr.as<int>(), As.contrib.as<int>(),
+                                                      As.S.as<double>(), As.rowptr.as<int>(), As.first.as<int>(),
+                                                      As.skyH.as<double>(), st);
+    launch_check(ctx, "k_sky_assemble");
+  }
+  k_sky_grad<<<G.N, 32, 0, ctx.stream>>>(As.g_ptr.as<int>(), As.g_contrib.as<int>(), As.G.as<double>(), G.N, G.anchor,
+                                         As.grad.as<double>(), As.rowptr.as<int>(), As.first.as<int>(),
+                                         As.skyH.as<double>(), st);
+  launch_check(ctx, "k_sky_grad");
+}
+
+// Damping attempts (backend.cpp:208-227) on the device: attempt a runs only
+// while no earlier one succeeded (st->solved).
+static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, GNState* st, double* tau) {
+  const int n = As.dim;
+  const size_t smem = sizeof(double) * ((size_t)n + 2 * kSkyRows * 7) + 2 * sizeof(int) * n;
+  PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
+    SkyArgs a{As.skyH.as<double>(), As.skyA.as<double>(), As.rowptr.as<int>(), As.first.as<int>(),
+              As.rp_ptr.as<int>(), As.rp_rows.as<int>(), As.grad.as<double>(), tau, As.nnz, n, attempt,
+              p.damping_init, st};
+    {
+      ProfScope ps(ctx, "k_ldlt");
+      k_ldlt_sky<<<1, kSkyThreads, smem, ctx.stream>>>(a);
+    }
+    launch_check(ctx, "k_ldlt_sky");
+  }
 }
 
 static double read_cost(Context& ctx, const DevGraph& G, const double* terms) {
@@ -1131,9 +1416,24 @@ extern "C" int pmx_impl_backend_solve_terms(pmx_context* c, pmx_memory mem, cons
   *cost = read_cost(ctx, G, dterms);
   Assembly As;
   build_assembly(ctx, G, As);
-  assemble(ctx, G, As, P, dterms);
   std::vector<double> t;
-  *solved = damped_solve(ctx, p, As, t) ? 1 : 0;
+  if (As.sky_ok) {
+    DevBuf dP(sizeof(DSim3) * std::max<size_t>(P.size(), 1), ctx.stream), dst(sizeof(GNState), ctx.stream),
+        dtau(sizeof(double) * std::max(As.dim, 1), ctx.stream);
+    PMX_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(DSim3) * P.size(), cudaMemcpyHostToDevice, ctx.stream));
+    PMX_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(GNState), ctx.stream));
+    assemble_sky(ctx, G, As, dP.as<DSim3>(), dterms, 0, nullptr);
+    solve_sky(ctx, p, As, dst.as<GNState>(), dtau.as<double>());
+    GNState hs;
+    t.resize(As.dim);
+    PMX_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaMemcpyAsync(t.data(), dtau.p, sizeof(double) * As.dim, cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    *solved = hs.solved;
+  } else {
+    assemble(ctx, G, As, P, dterms);
+    *solved = damped_solve(ctx, p, As, t) ? 1 : 0;
+  }
   if (mem == PMX_MEM_HOST)
     std::memcpy(tau, t.data(), sizeof(double) * t.size());
   else
@@ -1158,6 +1458,50 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
   std::vector<DSim3> P = host_poses(g);
   Assembly As;
   build_assembly(ctx, G, As);
+  if (As.sky_ok) {  // the whole GN loop on the device, one synchronisation
+    const int64_t half = (int64_t)PMX_EDGE_TERMS * G.E;
+    EdgeWork W;
+    make_edge_work(ctx, G, p, W);
+    DevBuf terms(sizeof(double) * 2 * half, ctx.stream), dP(sizeof(DSim3) * n, ctx.stream),
+        dPt(sizeof(DSim3) * n, ctx.stream), dst(sizeof(GNState), ctx.stream),
+        dtau(sizeof(double) * As.dim, ctx.stream);
+    DevBuf dtrace(pose_trace ? sizeof(pmx_sim3) * (size_t)std::max(p.max_iterations, 1) * n : 0, ctx.stream);
+    PMX_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(DSim3) * n, cudaMemcpyHostToDevice, ctx.stream));
+    PMX_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(GNState), ctx.stream));
+    GNState* S = dst.as<GNState>();
+    edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), 0, G.E, terms.as<double>(), S, 0);
+    k_gn_init<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), G.E, S);
+    launch_check(ctx, "k_gn_init");
+    for (int iter = 0; iter < p.max_iterations; ++iter) {
+      k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
+      assemble_sky(ctx, G, As, dP.as<DSim3>(), terms.as<double>(), half, S);
+      solve_sky(ctx, p, As, S, dtau.as<double>());
+      k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
+                                                            G.anchor, S);
+      edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
+      k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
+                                              dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
+      launch_check(ctx, "k_gn_iteration");
+    }
+    GNState hs;
+    PMX_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaMemcpyAsync(P.data(), dP.p, sizeof(DSim3) * n, cudaMemcpyDeviceToHost, ctx.stream));
+    if (pose_trace && hs.iterations >= 0) {
+      PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+      const int rec = hs.failed ? hs.iterations - 1 : hs.iterations;  // the failed iteration records nothing
+      if (rec > 0)
+        PMX_CUDA(cudaMemcpyAsync(pose_trace, dtrace.p, sizeof(pmx_sim3) * (size_t)rec * n, cudaMemcpyDeviceToHost,
+                                 ctx.stream));
+    }
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    result->iterations = hs.iterations;
+    result->converged = hs.failed ? 0 : 1;  // backend.cpp:228-230 vs 244, 250, 254
+    result->cost_trace_len = hs.trace_len;
+    for (int i = 0; i < hs.trace_len && i < PMX_MAX_TRACE; ++i) result->cost_trace[i] = hs.trace[i];
+    for (int k = 0; k < n; ++k) g->poses[k] = to_pmx(P[k]);
+    return PMX_OK;
+  }
+  // dense fallback: host-driven loop
   DevBuf terms(sizeof(double) * PMX_EDGE_TERMS * G.E, ctx.stream);
   edge_terms(ctx, G, p, P, 0, G.E, terms.as<double>());
   double cost = read_cost(ctx, G, terms.as<double>());

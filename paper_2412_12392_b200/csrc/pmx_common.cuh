@@ -259,7 +259,7 @@ __host__ __device__ inline void sim3_adjoint(const DSim3& T, double* ad) {
   ad[48] = 1.0;
 }
 
-inline pmx_sim3 to_pmx(const DSim3& d) {
+__host__ __device__ inline pmx_sim3 to_pmx(const DSim3& d) {
   pmx_sim3 T;
   for (int i = 0; i < 9; ++i) T.R[i] = d.R[i];
   for (int i = 0; i < 3; ++i) T.t[i] = d.t[i];
