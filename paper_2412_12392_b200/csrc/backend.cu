@@ -553,177 +553,259 @@ __global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
   }
 }
 
-// ------------------------------------------------------- K9, skyline form
-// The gauge-fixed system is block-sparse (edges); LDL^T fills in only inside
-// the envelope [first[i], i] of every row i, so the lower triangle is stored
-// as a skyline (row i: columns first[i]..i contiguous at rowptr[i]).  The
-// factorisation runs over 7-column panels (one keyframe); panel k updates only
-// its active rows R_k = {i > panel : first[i] <= panel end} (precomputed), so
-// a banded graph with loop closures costs O(n (b + border)^2) instead of
-// O(n^3).  No pivoting, failure iff a pivot is exactly zero (SimplicialLDLT
-// factorisation semantics; the reference's AMD ordering only changes
-// rounding).  The forward substitution is fused into the factorisation.  One
-// CTA: the whole solve is latency-bound (~10^6 flops at N = 100).
-constexpr int kSkyRows = 512;   // max active rows of a panel
-constexpr int kSkyMaxN = 8192;  // rhs + row offsets kept in shared memory
+// ------------------------------------------------------- K9, frontal form
+// The gauge-fixed system is block-sparse (edges) and LDL^T fills in only
+// inside the envelope [first[i], i] of every row (stored as a skyline by the
+// assembly).  The factorisation walks 7-column panels (one keyframe) with a
+// dense FRONT in shared memory: index m is live from panel(first[m]) to
+// panel(m); when it enters, its row of the original matrix against the live
+// indices is scattered into the front (host-precomputed (slot, slot, skyline
+// index) triples, one global round trip per panel), the panel's 7x7 pivot
+// block is factorised in registers by one warp, the live rows below it get
+// their L (forward substitution) and the Schur update is applied inside the
+// front.  Nothing but the entering values and the written-out L travels
+// through global memory, so a panel costs four barriers.  Banded graphs with
+// loop closures keep the front small (band + border rows).  No pivoting,
+// failure iff a pivot is exactly zero (SimplicialLDLT factorisation
+// semantics; the reference's AMD ordering only changes rounding).  The
+// forward substitution is fused; the backward one reads the compact L.
+constexpr int kPW = 7;           // panel width (one keyframe)
+constexpr int kFront = 96;       // max live indices
+constexpr int kSkyMaxN = 8192;   // rhs + panel table kept in shared memory
 constexpr int kSkyThreads = 1024;
 
 struct SkyArgs {
   const double* H;          // assembled skyline (undamped)
-  double* A;                // work skyline
-  const int* rowptr;        // [n]
-  const int* first;         // [n]
-  const int* rp_ptr;        // [N+1] 7-column panels
-  const int* rp_rows;
+  const int4* trip;         // entering triples {slot a, slot b, skyline index or -1, diag}
+  const int4* pinfo;        // [npanel] {trip begin, trip end, live-row begin, live-row end}
+  const int2* rinfo;        // live non-pivot rows of each panel {index, slot}
+  const int* slot;          // [n] front slot of every index
+  const int* lofs;          // [npanel] offset of the panel's L rows in Lst
+  double* Lst;              // compact L: per panel ns x 7 rows, then 49 for the pivot block
+  double* Dst;              // [n] pivots
   const double* grad;       // rhs = -grad
   double* x;                // tau
-  long long nnz;
   int n;
   int attempt;              // damping attempt (backend.cpp:208-227)
   double damping_init;
   GNState* st;
 };
 
-// lane -> (row, col) of the 28 lower-triangle entries of a 7x7 block
-__constant__ int c_row[28] = {0, 1, 1, 2, 2, 2, 3, 3, 3, 3, 4, 4, 4, 4, 4, 5, 5, 5, 5, 5, 5, 6, 6, 6, 6, 6, 6, 6};
-__constant__ int c_col[28] = {0, 0, 1, 0, 1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 4, 0, 1, 2, 3, 4, 5, 0, 1, 2, 3, 4, 5, 6};
-
 __device__ __forceinline__ int sky_at(const int* rowptr, const int* first, int i, int j) {
   return rowptr[i] + (j - first[i]);
 }
 
+// 1/d to ~1 ulp without the long IEEE division sequence: fp32 seed and Newton
+// steps (pivots are not the reference's rounding either way: its AMD-ordered
+// SimplicialLDLT differs at this level).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r = (double)__frcp_rn((float)d);
+  if (!isfinite(r) || r == 0.0) return 1.0 / d;  // outside fp32 range
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+
+// Prefetched data of the next panel, one item per thread (registers), so the
+// global round trips overlap the current panel's barriers.
+struct PanelPrefetch {
+  int4 t;      // entering triple (tid < ntrip)
+  double v;    // its value
+  int2 r;      // live row (tid < ns)
+  int ps;      // pivot slot (tid < 7)
+  bool ht, hr;
+};
+
 __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   if (P.st->stop || P.st->solved) return;
   extern __shared__ double smem[];
-  double* y = smem;                   // [n]
-  double* sL = y + P.n;               // [kSkyRows][7]  L of the active rows
-  double* sW = sL + kSkyRows * 7;     // [kSkyRows][7]  L D
-  int* rp = reinterpret_cast<int*>(sW + kSkyRows * 7);  // [n] row offsets
-  int* first = rp + P.n;                                // [n] envelope starts
-  __shared__ double sD[7][8];         // panel block: D on the diagonal, unit L below
+  const int npanel = (P.n + kPW - 1) / kPW;
+  int4* pin = reinterpret_cast<int4*>(smem);            // [npanel] panel info
+  double* F = smem + 2 * npanel;                        // [kFront][kFront] front (symmetric)
+  double* y = F + kFront * kFront;                      // [n]
+  double* sL = y + P.n;                                 // [kFront][kPW]
+  double* sW = sL + kFront * kPW;                       // [kFront][kPW]
+  __shared__ double sD[kPW][kPW + 1], sIv[kPW];
+  __shared__ int2 rows[2][kFront];
+  __shared__ int psl[2][kPW];
   __shared__ int ok;
-  const int n = P.n, tid = threadIdx.x, nth = blockDim.x;
-  double* A = P.A;
-  for (int i = tid; i < n; i += nth) {
-    rp[i] = P.rowptr[i];
-    first[i] = P.first[i];
-  }
+  const int n = P.n, tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
   double lambda = 0.0;
   if (P.attempt > 0) {
     lambda = P.damping_init;
     for (int a = 1; a < P.attempt; ++a) lambda *= 10.0;
   }
-  for (long long e = tid; e < P.nnz; e += nth) A[e] = P.H[e];
   for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
+  for (int k = tid; k < npanel; k += nth) pin[k] = P.pinfo[k];
   if (tid == 0) ok = 1;
   __syncthreads();
-  if (lambda != 0.0)  // backend.cpp:210-213: lambda on every diagonal entry
-    for (int i = tid; i < n; i += nth) A[sky_at(rp, first, i, i)] += lambda;
+  PanelPrefetch pf;
+  auto issue = [&](int k) {  // structure of panel k (values: issue_values)
+    const int4 pi = pin[k];
+    pf.ht = pi.x + tid < pi.y;
+    pf.hr = pi.z + tid < pi.w;
+    if (pf.ht) pf.t = P.trip[pi.x + tid];
+    if (pf.hr) pf.r = P.rinfo[pi.z + tid];
+    if (tid < min(kPW, n - kPW * k)) pf.ps = P.slot[kPW * k + tid];
+  };
+  auto issue_values = [&]() {
+    if (pf.ht) pf.v = (pf.t.z >= 0 ? P.H[pf.t.z] : 0.0) + (pf.t.w ? lambda : 0.0);  // backend.cpp:210-213
+  };
+  auto land = [&](int k, int buf) {  // entering rows of panel k into the front
+    const int4 pi = pin[k];
+    if (pf.ht) {
+      F[pf.t.x * kFront + pf.t.y] = pf.v;
+      F[pf.t.y * kFront + pf.t.x] = pf.v;
+    }
+    for (int t = pi.x + nth + tid; t < pi.y; t += nth) {  // rare: more triples than threads
+      const int4 q = P.trip[t];
+      const double v = (q.z >= 0 ? P.H[q.z] : 0.0) + (q.w ? lambda : 0.0);
+      F[q.x * kFront + q.y] = v;
+      F[q.y * kFront + q.x] = v;
+    }
+    if (pf.hr) rows[buf][tid] = pf.r;
+    if (tid < min(kPW, n - kPW * k)) psl[buf][tid] = pf.ps;
+  };
+  issue(0);
+  issue_values();
+  land(0, 0);
   __syncthreads();
-  const int npanel = (n + 6) / 7;
   for (int k = 0; k < npanel; ++k) {
-    const int c0 = 7 * k, nb = min(7, n - c0);
-    // (a) panel block, warp 0: LDL^T of the (already updated) 7x7 block in
-    // shared memory (lane (r, s) owns entry r >= s), then the panel's forward solve
-    if (tid < 32) {
-      const int r = tid < 28 ? c_row[tid] : 0, c = tid < 28 ? c_col[tid] : 0;
-      const bool own = tid < 28 && r < nb;
-      if (own) sD[r][c] = (c0 + c >= first[c0 + r]) ? A[sky_at(rp, first, c0 + r, c0 + c)] : 0.0;
-      __syncwarp();
-      for (int k2 = 0; k2 < nb; ++k2) {
-        const double D = sD[k2][k2];
-        if (tid == 0 && D == 0.0) ok = 0;
-        // trailing entries (r, c) with c > k2: a_rc -= a_r,k2 a_c,k2 / D (a_*,k2 not yet scaled)
-        const double upd = (own && c > k2) ? sD[r][k2] * sD[c][k2] / D : 0.0;
-        __syncwarp();
-        if (own && c > k2) sD[r][c] -= upd;
-        if (own && c == k2 && r > k2) sD[r][c] /= D;
-        __syncwarp();
+    const int c0 = kPW * k, nb = min(kPW, n - c0), buf = k & 1;
+    const int4 pi = pin[k];
+    const int ns = pi.w - pi.z;
+    double* Lp = P.Lst + P.lofs[k];
+    if (k + 1 < npanel) issue(k + 1);
+    // (a) pivot block on warp 0, in registers (lane r holds row r)
+    if (warp == 0) {
+      double a[kPW];
+      const int sr = lane < nb ? psl[buf][lane] : 0;
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFront + psl[buf][c]] : 0.0;
+#pragma unroll
+      for (int p = 0; p < kPW; ++p) {
+        if (p < nb) {
+          const double D = __shfl_sync(0xffffffffu, a[p], p);
+          if (lane == 0 && D == 0.0) ok = 0;  // SimplicialLDLT: exact zero pivot fails
+          const double iD = fast_rcp(D);
+          const double w = a[p];  // this row's unscaled entry in column p
+#pragma unroll
+          for (int c = p + 1; c < kPW; ++c) {
+            const double wc = __shfl_sync(0xffffffffu, w, c);  // row c's unscaled entry
+            if (lane >= c) a[c] -= w * (wc * iD);
+          }
+          if (lane > p) a[p] = w * iD;
+          if (lane == p) sIv[p] = iD;
+        }
       }
-      if (own && c0 + c >= first[c0 + r]) A[sky_at(rp, first, c0 + r, c0 + c)] = sD[r][c];
-      // L y = b inside the panel: lane t < nb holds y_t
-      double yv = tid < nb ? y[c0 + tid] : 0.0;
-      for (int k2 = 0; k2 < nb; ++k2) {
-        const double yk = __shfl_sync(0xffffffffu, yv, k2);
-        if (tid > k2 && tid < nb) yv -= sD[tid][k2] * yk;
+      if (lane < nb) {
+#pragma unroll
+        for (int c = 0; c < kPW; ++c) {
+          if (c <= lane) sD[lane][c] = a[c];
+          Lp[ns * kPW + lane * kPW + c] = c < lane ? a[c] : 0.0;  // unit L of the pivot block
+        }
+        P.Dst[c0 + lane] = a[lane];
       }
-      if (tid < nb) y[c0 + tid] = yv;
+      double yv = lane < nb ? y[c0 + lane] : 0.0;  // L y = b inside the panel
+#pragma unroll
+      for (int p = 0; p < kPW; ++p) {
+        const double yp = __shfl_sync(0xffffffffu, yv, p);
+        if (lane > p && lane < nb) yv -= a[p] * yp;
+      }
+      if (lane < nb) y[c0 + lane] = yv;
     }
     __syncthreads();
-    // (b) active rows: W = A_i,panel L^-T, L_i = W D^-1; forward update of y_i
-    const int r0 = P.rp_ptr[k], ns = P.rp_ptr[k + 1] - r0;
+    if (k + 1 < npanel) issue_values();
+    // (b) live rows below the panel: W = F_r,panel L^-T, L_r = W D^-1; forward update of y_r
     for (int q = tid; q < ns; q += nth) {
-      const int i = P.rp_rows[r0 + q];
-      double w[7];
-      const int c1 = max(0, first[i] - c0);
-      const int base = rp[i] + (c0 - first[i]);
+      const int2 ri = rows[buf][q];
+      double w[kPW];
 #pragma unroll
-      for (int t = 0; t < 7; ++t) w[t] = (t >= c1 && t < nb) ? A[base + t] : 0.0;
+      for (int t = 0; t < kPW; ++t) w[t] = t < nb ? F[ri.y * kFront + psl[buf][t]] : 0.0;
 #pragma unroll
-      for (int t = 1; t < 7; ++t)
+      for (int t = 1; t < kPW; ++t)
 #pragma unroll
         for (int u = 0; u < t; ++u) w[t] -= w[u] * sD[t][u];
       double yi = 0.0;
 #pragma unroll
-      for (int t = 0; t < 7; ++t) {
-        if (t >= nb) break;
-        const double l = w[t] / sD[t][t];
-        if (t >= c1) A[base + t] = l;
-        sL[q * 7 + t] = l;
-        sW[q * 7 + t] = w[t];
-        yi += l * y[c0 + t];
+      for (int t = 0; t < kPW; ++t) {
+        const double l = t < nb ? w[t] * sIv[t] : 0.0;
+        Lp[q * kPW + t] = l;
+        sL[q * kPW + t] = l;
+        sW[q * kPW + t] = t < nb ? w[t] : 0.0;
+        yi += t < nb ? l * y[c0 + t] : 0.0;
       }
-      y[i] -= yi;
+      y[ri.x] -= yi;
     }
     __syncthreads();
-    // (c) trailing update over active pairs (j <= i, inside row i's envelope)
+    // (c) Schur update of the live rows inside the front
     const int npair = ns * (ns + 1) / 2;
     for (int t = tid; t < npair; t += nth) {
       int qi = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
       while ((qi + 1) * (qi + 2) / 2 <= t) ++qi;
       while (qi * (qi + 1) / 2 > t) --qi;
       const int qj = t - qi * (qi + 1) / 2;
-      const int i = P.rp_rows[r0 + qi], j = P.rp_rows[r0 + qj];
-      if (j < first[i]) continue;
+      const int si = rows[buf][qi].y, sj = rows[buf][qj].y;
       double sacc = 0.0;
 #pragma unroll
-      for (int u = 0; u < 7; ++u) sacc += sW[qi * 7 + u] * sL[qj * 7 + u];
-      A[sky_at(rp, first, i, j)] -= sacc;
+      for (int u = 0; u < kPW; ++u) sacc += sW[qi * kPW + u] * sL[qj * kPW + u];
+      const double v = F[si * kFront + sj] - sacc;
+      F[si * kFront + sj] = v;
+      F[sj * kFront + si] = v;
     }
     __syncthreads();
+    if (k + 1 < npanel) {
+      land(k + 1, buf ^ 1);
+      __syncthreads();
+    }
   }
   // D z = y
-  for (int i = tid; i < n; i += nth) y[i] /= A[sky_at(rp, first, i, i)];
+  for (int i = tid; i < n; i += nth) y[i] *= fast_rcp(P.Dst[i]);
   __syncthreads();
-  // L^T x = z, panel by panel from the end
-  const int warp = tid >> 5, lane = tid & 31;
+  // L^T x = z, panel by panel from the end.  Every thread holds one L entry
+  // of the panel (prefetched one panel ahead) and forms its product with x;
+  // warp c sums column c.
+  __shared__ double colsum[kPW];
+  double lv = 0.0;
+  int lrow = -1;
+  auto bissue = [&](int k) {
+    const int4 pi = pin[k];
+    const int ns = pi.w - pi.z;
+    lrow = -1;
+    if (tid < ns * kPW) {
+      lv = P.Lst[P.lofs[k] + tid];
+      lrow = P.rinfo[pi.z + tid / kPW].x;
+    }
+  };
+  bissue(npanel - 1);
   for (int k = npanel - 1; k >= 0; --k) {
-    const int c0 = 7 * k, nb = min(7, n - c0);
-    const int r0 = P.rp_ptr[k], ns = P.rp_ptr[k + 1] - r0;
-    if (warp < nb) {
-      double sacc = 0.0;
-      for (int q = lane; q < ns; q += 32) {
-        const int i = P.rp_rows[r0 + q];
-        if (c0 + warp >= first[i]) sacc += A[sky_at(rp, first, i, c0 + warp)] * y[i];
-      }
-      sacc = warp_sum(sacc);
-      if (lane == 0) y[c0 + warp] -= sacc;
+    const int c0 = kPW * k, nb = min(kPW, n - c0);
+    const int4 pi = pin[k];
+    const int ns = pi.w - pi.z;
+    const double* Lp = P.Lst + P.lofs[k];
+    if (tid < ns * kPW) sW[tid] = lv * y[lrow];
+    double lc[kPW];  // warp 0: column `lane` of the pivot block's unit L
+    if (warp == 0) {
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) lc[c] = (lane < nb && c < nb) ? Lp[ns * kPW + c * kPW + lane] : 0.0;
     }
     __syncthreads();
-    if (tid < 32) {  // L_panel^T x = z inside the panel: lane t < nb holds x_t
-      double xv = tid < nb ? y[c0 + tid] : 0.0;
-      double lrow[7];
+    if (k > 0) bissue(k - 1);
+    if (warp < nb) {
+      double sacc = 0.0;
+      for (int q = lane; q < ns; q += 32) sacc += sW[q * kPW + warp];
+      sacc = warp_sum(sacc);
+      if (lane == 0) colsum[warp] = sacc;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double xv = lane < nb ? y[c0 + lane] - colsum[lane] : 0.0;
 #pragma unroll
-      for (int c = 0; c < 7; ++c)  // column tid of L below the diagonal: L[c][tid], c > tid
-        lrow[c] = (tid < nb && c < nb && c > tid && c0 + tid >= first[c0 + c]) ? A[sky_at(rp, first, c0 + c, c0 + tid)]
-                                                                              : 0.0;
-      for (int c = nb - 1; c >= 0; --c) {
+      for (int c = kPW - 1; c >= 0; --c) {
         const double xc = __shfl_sync(0xffffffffu, xv, c);
-#pragma unroll
-        for (int q = 0; q < 7; ++q)
-          if (q == c && tid < c) xv -= lrow[q] * xc;
+        xv -= lc[c] * xc;
       }
-      if (tid < nb) y[c0 + tid] = xv;
+      if (lane < nb) y[c0 + lane] = xv;
     }
     __syncthreads();
   }
@@ -1123,7 +1205,8 @@ struct Assembly {
   // active rows and the rhs fit the kernel's shared memory)
   bool sky_ok = false;
   long long nnz = 0;
-  DevBuf first, rowptr, rp_ptr, rp_rows, skyH, skyA;
+  DevBuf first, rowptr, rp_ptr, rp_rows, skyH;
+  DevBuf trip, pinfo, rinfo, slot, lofs, Lst, Dst;  // frontal factorisation plan
 };
 
 // Contribution lists (edge order) for every non-zero block, gauge-fixed.
@@ -1179,23 +1262,72 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
       rowptr[i] = (int)std::min<long long>(nnz, INT32_MAX);
       nnz += i - first[i] + 1;
     }
+    // frontal plan: index m is live for panels [panel(first[m]), panel(m)]
     bool fits = n <= kSkyMaxN && nnz < INT32_MAX;
-    for (int k = 0; k < N && fits; ++k) {  // 7-column panels
-      const int pend = 7 * k + 7;
-      for (int i = pend; i < n; ++i)
-        if (first[i] < pend) rrows.push_back(i);
-      if ((int)rrows.size() - rptr.back() > kSkyRows) fits = false;
+    const int npanel = (n + kPW - 1) / kPW;
+    std::vector<std::vector<int>> enter(npanel);
+    for (int m = 0; m < n; ++m) enter[first[m] / kPW].push_back(m);
+    std::vector<int> slot(n, -1), freel, live, tptr{0}, lofs(npanel);
+    std::vector<int4> trip;
+    for (int s2 = kFront - 1; s2 >= 0; --s2) freel.push_back(s2);
+    long long lsize = 0;
+    for (int k = 0; k < npanel && fits; ++k) {
+      for (int m : enter[k]) {
+        if (freel.empty()) {
+          fits = false;
+          break;
+        }
+        slot[m] = freel.back();
+        freel.pop_back();
+        live.push_back(m);
+      }
+      if (!fits) break;
+      for (int m : enter[k])  // m's row against every live index (itself included)
+        for (int x : live) {
+          const int r = std::max(m, x), c = std::min(m, x);
+          if (x > m && std::find(enter[k].begin(), enter[k].end(), x) != enter[k].end()) continue;  // pair once
+          const int idx = c >= first[r] ? rowptr[r] + (c - first[r]) : -1;
+          trip.push_back(make_int4(slot[m], slot[x], idx, m == x ? 1 : 0));
+        }
+      tptr.push_back((int)trip.size());
+      const int pend = std::min(n, kPW * k + kPW);
+      for (int m : live)
+        if (m >= pend) rrows.push_back(m);
       rptr.push_back((int)rrows.size());
+      lofs[k] = (int)lsize;
+      lsize += (long long)(rptr[k + 1] - rptr[k]) * kPW + kPW * kPW;
+      std::vector<int> keep;  // the panel's pivots leave the front
+      for (int m : live) {
+        if (m < pend)
+          freel.push_back(slot[m]);
+        else
+          keep.push_back(m);
+      }
+      live.swap(keep);
     }
+    fits = fits && lsize < INT32_MAX;
     As.sky_ok = fits && N > 0;
     if (As.sky_ok) {
       As.nnz = nnz;
       up(As.first, first);
-      up(As.rp_ptr, rptr);
-      up(As.rp_rows, rrows);
       up(As.rowptr, rowptr);
+      std::vector<int4> pinfo(npanel);
+      std::vector<int2> rinfo(rrows.size());
+      for (int k = 0; k < npanel; ++k) pinfo[k] = make_int4(tptr[k], tptr[k + 1], rptr[k], rptr[k + 1]);
+      for (size_t q = 0; q < rrows.size(); ++q) rinfo[q] = make_int2(rrows[q], slot[rrows[q]]);
+      As.pinfo = DevBuf(sizeof(int4) * npanel, ctx.stream);
+      PMX_CUDA(cudaMemcpyAsync(As.pinfo.p, pinfo.data(), sizeof(int4) * npanel, cudaMemcpyHostToDevice, ctx.stream));
+      As.rinfo = DevBuf(sizeof(int2) * std::max<size_t>(rinfo.size(), 1), ctx.stream);
+      if (!rinfo.empty())
+        PMX_CUDA(cudaMemcpyAsync(As.rinfo.p, rinfo.data(), sizeof(int2) * rinfo.size(), cudaMemcpyHostToDevice, ctx.stream));
+      up(As.slot, slot);
+      up(As.lofs, lofs);
+      As.trip = DevBuf(sizeof(int4) * std::max<size_t>(trip.size(), 1), ctx.stream);
+      if (!trip.empty())
+        PMX_CUDA(cudaMemcpyAsync(As.trip.p, trip.data(), sizeof(int4) * trip.size(), cudaMemcpyHostToDevice, ctx.stream));
       As.skyH = DevBuf(sizeof(double) * nnz, ctx.stream);
-      As.skyA = DevBuf(sizeof(double) * nnz, ctx.stream);
+      As.Lst = DevBuf(sizeof(double) * lsize, ctx.stream);
+      As.Dst = DevBuf(sizeof(double) * n, ctx.stream);
       PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     }
   }
@@ -1306,11 +1438,12 @@ static void assemble_sky(Context& ctx, const DevGraph& G, Assembly& As, const DS
 // while no earlier one succeeded (st->solved).
 static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, GNState* st, double* tau) {
   const int n = As.dim;
-  const size_t smem = sizeof(double) * ((size_t)n + 2 * kSkyRows * 7) + 2 * sizeof(int) * n;
+  const size_t smem = sizeof(double) * ((size_t)kFront * kFront + n + 2 * kFront * kPW) +
+                      sizeof(int4) * (size_t)((n + kPW - 1) / kPW);
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
-    SkyArgs a{As.skyH.as<double>(), As.skyA.as<double>(), As.rowptr.as<int>(), As.first.as<int>(),
-              As.rp_ptr.as<int>(), As.rp_rows.as<int>(), As.grad.as<double>(), tau, As.nnz, n, attempt,
+    SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.rinfo.as<int2>(), As.slot.as<int>(),
+              As.lofs.as<int>(), As.Lst.as<double>(), As.Dst.as<double>(), As.grad.as<double>(), tau, n, attempt,
               p.damping_init, st};
     {
       ProfScope ps(ctx, "k_ldlt");
