@@ -48,6 +48,9 @@ __device__ void eval_pass(const PoseR<float>& T, const MatchesDev& M, const Clou
 // partials per block (stride kAcc).  Same skips as eval_match.
 __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const CloudDev& Xref,
                               const CloudDev& Xsrc, const WeightsDev& wp, double* __restrict__ partials) {
+  const PoseR<float> Tf = {{(float)T.sR[0], (float)T.sR[1], (float)T.sR[2], (float)T.sR[3], (float)T.sR[4],
+                            (float)T.sR[5], (float)T.sR[6], (float)T.sR[7], (float)T.sR[8]},
+                           {(float)T.t[0], (float)T.t[1], (float)T.t[2]}};
   float acc[kRayAcc];
 #pragma unroll
   for (int i = 0; i < kRayAcc; ++i) acc[i] = 0.0f;
@@ -68,7 +71,7 @@ __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const
     if (!(rr >= 1e-24)) continue;  // |ref| < 1e-12 (tracking.cpp:78)
     const float rrf = (float)rr;
     const float ir = rsqrt_nr(rrf);
-    ray_accumulate(T, rd, rr, rrf * ir, ir, rf, sd, info, c, acc);
+    ray_accumulate(T, Tf, rd, rr, rrf * ir, ir, rf, sd, sf, info, c, acc);
   }
   block_reduce_n<kRayAcc>(acc, partials + (size_t)blockIdx.x * kAcc);
 }
