@@ -574,7 +574,8 @@ __global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
 constexpr int kPW = 7;           // panel width (one keyframe)
 constexpr int kFront = 96;       // max live indices
 constexpr int kSkyMaxN = 8192;   // rhs + panel table kept in shared memory
-constexpr int kSkyThreads = 1024;
+constexpr int kSkyThreads = 768;  // >= kFront * kPW (one L entry per thread in the backward pass)
+static_assert(kSkyThreads >= kFront * kPW, "backward pass holds one L entry per thread");
 
 struct SkyArgs {
   const double* H;          // assembled skyline (undamped)
@@ -623,7 +624,8 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   extern __shared__ double smem[];
   const int npanel = (P.n + kPW - 1) / kPW;
   int4* pin = reinterpret_cast<int4*>(smem);            // [npanel] panel info
-  double* F = smem + 2 * npanel;                        // [kFront][kFront] front (symmetric)
+  int* plofs = reinterpret_cast<int*>(pin + npanel);    // [npanel] L offsets
+  double* F = smem + 2 * npanel + (npanel + 1) / 2;     // [kFront][kFront] front (symmetric)
   double* y = F + kFront * kFront;                      // [n]
   double* sL = y + P.n;                                 // [kFront][kPW]
   double* sW = sL + kFront * kPW;                       // [kFront][kPW]
@@ -638,7 +640,10 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
     for (int a = 1; a < P.attempt; ++a) lambda *= 10.0;
   }
   for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
-  for (int k = tid; k < npanel; k += nth) pin[k] = P.pinfo[k];
+  for (int k = tid; k < npanel; k += nth) {
+    pin[k] = P.pinfo[k];
+    plofs[k] = P.lofs[k];
+  }
   if (tid == 0) ok = 1;
   __syncthreads();
   PanelPrefetch pf;
@@ -676,7 +681,7 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
     const int c0 = kPW * k, nb = min(kPW, n - c0), buf = k & 1;
     const int4 pi = pin[k];
     const int ns = pi.w - pi.z;
-    double* Lp = P.Lst + P.lofs[k];
+    double* Lp = P.Lst + plofs[k];
     if (k + 1 < npanel) issue(k + 1);
     // (a) pivot block on warp 0, in registers (lane r holds row r)
     if (warp == 0) {
@@ -701,12 +706,14 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
         }
       }
       if (lane < nb) {
+        double dl = 0.0;  // a[lane] without a dynamic register index
 #pragma unroll
         for (int c = 0; c < kPW; ++c) {
           if (c <= lane) sD[lane][c] = a[c];
+          if (c == lane) dl = a[c];
           Lp[ns * kPW + lane * kPW + c] = c < lane ? a[c] : 0.0;  // unit L of the pivot block
         }
-        P.Dst[c0 + lane] = a[lane];
+        P.Dst[c0 + lane] = dl;
       }
       double yv = lane < nb ? y[c0 + lane] : 0.0;  // L y = b inside the panel
 #pragma unroll
@@ -775,7 +782,7 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
     const int ns = pi.w - pi.z;
     lrow = -1;
     if (tid < ns * kPW) {
-      lv = P.Lst[P.lofs[k] + tid];
+      lv = P.Lst[plofs[k] + tid];
       lrow = P.rinfo[pi.z + tid / kPW].x;
     }
   };
@@ -784,7 +791,7 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
     const int c0 = kPW * k, nb = min(kPW, n - c0);
     const int4 pi = pin[k];
     const int ns = pi.w - pi.z;
-    const double* Lp = P.Lst + P.lofs[k];
+    const double* Lp = P.Lst + plofs[k];
     if (tid < ns * kPW) sW[tid] = lv * y[lrow];
     double lc[kPW];  // warp 0: column `lane` of the pivot block's unit L
     if (warp == 0) {
@@ -1440,8 +1447,9 @@ static void assemble_sky(Context& ctx, const DevGraph& G, Assembly& As, const DS
 // while no earlier one succeeded (st->solved).
 static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, GNState* st, double* tau) {
   const int n = As.dim;
+  const int npanel = (n + kPW - 1) / kPW;
   const size_t smem = sizeof(double) * ((size_t)kFront * kFront + n + 2 * kFront * kPW) +
-                      sizeof(int4) * (size_t)((n + kPW - 1) / kPW);
+                      sizeof(int4) * (size_t)npanel + sizeof(double) * (size_t)((npanel + 1) / 2);
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
     SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.rinfo.as<int2>(), As.slot.as<int>(),
@@ -1604,19 +1612,22 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
     PMX_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(DSim3) * n, cudaMemcpyHostToDevice, ctx.stream));
     PMX_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(GNState), ctx.stream));
     GNState* S = dst.as<GNState>();
-    edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), 0, G.E, terms.as<double>(), S, 0);
-    k_gn_init<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), G.E, S);
-    launch_check(ctx, "k_gn_init");
-    for (int iter = 0; iter < p.max_iterations; ++iter) {
-      k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
-      assemble_sky(ctx, G, As, dP.as<DSim3>(), terms.as<double>(), half, S);
-      solve_sky(ctx, p, As, S, dtau.as<double>());
-      k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
-                                                            G.anchor, S);
-      edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
-      k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
-                                              dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
-      launch_check(ctx, "k_gn_iteration");
+    {
+      ProfScope loop_scope(ctx, "gn_loop");  // the device loop (staging / planning excluded)
+      edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), 0, G.E, terms.as<double>(), S, 0);
+      k_gn_init<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), G.E, S);
+      launch_check(ctx, "k_gn_init");
+      for (int iter = 0; iter < p.max_iterations; ++iter) {
+        k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
+        assemble_sky(ctx, G, As, dP.as<DSim3>(), terms.as<double>(), half, S);
+        solve_sky(ctx, p, As, S, dtau.as<double>());
+        k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
+                                                              G.anchor, S);
+        edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
+        k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
+                                                dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
+        launch_check(ctx, "k_gn_iteration");
+      }
     }
     GNState hs;
     PMX_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));

@@ -49,10 +49,12 @@ for rep in range(2):
     dt = time.perf_counter() - t0
     et, en = ctx.profile_get("k_edge_terms")
     lt, ln = ctx.profile_get("k_ldlt")
+    gl, _ = ctx.profile_get("gn_loop")
     ctx.profile_enable(False)
     err0 = max(np.abs(P.t - Q.t).max() for P, Q in zip(g["init"], g["gt"]))
     err = max(np.abs(np.array(P.t[:]) - Q.t).max() for P, Q in zip(G.poses, g["gt"]))
     nm = sum(m["valid"].size for m in g["matches"])
     print(f"rep {rep}: {r.iterations} it, {dt * 1e3:.1f} ms total, {dt * 1e3 / max(1, r.iterations):.2f} ms/it; "
           f"k_edge_terms {et / max(1, en):.3f} ms x{en} ({32 * nm / (et / max(1, en) * 1e-3) / 1e9:.0f} GB/s alg), "
-          f"k_ldlt {lt / max(1, ln):.3f} ms x{ln}; |dt| {err0:.3f} -> {err:.4f}; converged {r.converged}")
+          f"k_ldlt {lt / max(1, r.iterations):.3f} ms/it; loop {gl:.2f} ms = {gl / max(1, r.iterations):.3f} ms/it; "
+          f"|dt| {err0:.3f} -> {err:.4f}; converged {r.converged}")
