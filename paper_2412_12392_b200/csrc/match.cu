@@ -389,6 +389,8 @@ struct Interp {
   double4 c00, c10, c01, c11;
 };
 
+// All four supports are loaded before any test (no load -> branch -> load
+// round trips); the validity and |g| tests are applied to the result.
 __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, int W, int H, double u, double v,
                                             Interp& I) {
   if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
@@ -396,22 +398,22 @@ __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, in
   int v0 = (int)floor(v);
   u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
   v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
-  const int u1 = min(u0 + 1, W - 1);
-  const int v1 = min(v0 + 1, H - 1);
+  const int du = min(u0 + 1, W - 1) - u0, dv = (min(v0 + 1, H - 1) - v0) * W;
+  const double4* p = rays + (v0 * W + u0);
   I.fu = u - u0;
   I.fv = v - v0;
-  I.c00 = ld_ray(rays, v0 * W + u0);
-  I.c10 = ld_ray(rays, v0 * W + u1);
-  I.c01 = ld_ray(rays, v1 * W + u0);
-  I.c11 = ld_ray(rays, v1 * W + u1);
-  if (I.c00.w == 0.0 || I.c10.w == 0.0 || I.c01.w == 0.0 || I.c11.w == 0.0) return false;
+  I.c00 = ld_ray(p, 0);
+  I.c10 = ld_ray(p, du);
+  I.c01 = ld_ray(p, dv);
+  I.c11 = ld_ray(p, dv + du);
   const double fu = I.fu, fv = I.fv;
   const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
   const double g0 = w00 * I.c00.x + w10 * I.c10.x + w01 * I.c01.x + w11 * I.c11.x;
   const double g1 = w00 * I.c00.y + w10 * I.c10.y + w01 * I.c01.y + w11 * I.c11.y;
   const double g2 = w00 * I.c00.z + w10 * I.c10.z + w01 * I.c01.z + w11 * I.c11.z;
   const double gg = g0 * g0 + g1 * g1 + g2 * g2;
-  if (gg < 1e-24) return false;  // |g| < 1e-12
+  const bool valid = I.c00.w != 0.0 && I.c10.w != 0.0 && I.c01.w != 0.0 && I.c11.w != 0.0;
+  if (!valid || gg < 1e-24) return false;  // an invalid support / |g| < 1e-12
   I.rs = rsqrt(gg);
   I.r0 = g0 * I.rs;
   I.r1 = g1 * I.rs;
@@ -532,8 +534,10 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     ldlt2_solve(h00, a01, h11, g0, g1, &s0, &s1);
     const double d0 = -s0, d1 = -s1;
     if (!isfinite(d0) || !isfinite(d1)) break;
-    const double tu = fmin(fmax(pu + d0, 0.0), (double)(W - 1));
-    const double tv = fmin(fmax(pv + d1, 0.0), (double)(H - 1));
+    // clamp_to_image (camera.cpp:104-107); pu + d0 is finite here
+    const double xu = pu + d0, xv = pv + d1;
+    const double tu = xu < 0.0 ? 0.0 : (xu > (double)(W - 1) ? (double)(W - 1) : xu);
+    const double tv = xv < 0.0 ? 0.0 : (xv > (double)(H - 1) ? (double)(H - 1) : xv);
     if (interp_eval(rays, W, H, tu, tv, I)) {
       const double e0 = I.r0 - t0, e1 = I.r1 - t1, e2 = I.r2 - t2;
       const double ct = e0 * e0 + e1 * e1 + e2 * e2;
@@ -903,15 +907,9 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 
 // ---------------------------------------------------------------- K3 + K4
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair.
-__global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
-  const PairDev& P = pairs[blockIdx.y];
-  const int tiles_x = (P.Wb + 31) / 32;
-  const int tiles = tiles_x * ((P.Hb + 7) / 8);
-  if ((int)blockIdx.x >= tiles) return;
-  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
-  const int v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
-  if (u >= P.Wb || v >= P.Hb) return;
-  const int n = v * P.Wb + u;
+// match_pointmaps for b-pixel n (camera.cpp:213-236): LM from the seed,
+// lround + clamp, validity, q.  Writes the outputs; returns (pa, valid).
+__device__ __forceinline__ int2 match_pixel(const PairDev& P, const LMParams& lp, int n) {
   if (P.out_pb) P.out_pb[n] = n;
   int32_t pa_out = -1;
   float q_out = 0.0f;
@@ -948,6 +946,19 @@ __global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pa
   P.out_pa[n] = pa_out;
   P.out_q[n] = q_out;
   P.out_valid[n] = valid_out;
+  return make_int2(pa_out, valid_out);
+}
+
+// One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair (no refinement).
+__global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int tiles_x = (P.Wb + 31) / 32;
+  const int tiles = tiles_x * ((P.Hb + 7) / 8);
+  if ((int)blockIdx.x >= tiles) return;
+  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
+  const int v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+  if (u >= P.Wb || v >= P.Hb) return;
+  match_pixel(P, lp, v * P.Wb + u);
 }
 
 // K4: feature_refine of the valid matches just written by k_match, in place.
@@ -1142,11 +1153,13 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
   return refine_dispatch(P, pa, n, L);
 }
 
-// One thread per b-pixel of a 32x8 tile (blockIdx.x = tile, blockIdx.y =
-// pair); the int8 a-image (L2-resident chunk scratch) is read through L1,
-// where a tile's windows overlap: no staging, no block barriers.
-__global__ void __launch_bounds__(256, 4) k_refine_q8(const PairDev* __restrict__ pairs, RefineLevels L,
-                                                       unsigned long long* __restrict__ exact_px) {
+// K3 + K4 fused: one thread per b-pixel of a 32x8 tile (blockIdx.x = tile,
+// blockIdx.y = pair) runs the LM, then (warp-collectively) the refinement of
+// the valid matches; the int8 a-image (L2-resident chunk scratch) is read
+// through L1, where a tile's windows overlap.  Fusing lets the FP64-bound LM
+// of some warps overlap the integer-bound refinement of others on every SM.
+__global__ void __launch_bounds__(256, 3) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
+                                                         RefineLevels L, unsigned long long* __restrict__ exact_px) {
   const PairDev& P = pairs[blockIdx.y];
   const int tiles_x = (P.Wb + 31) / 32;
   if ((int)blockIdx.x >= tiles_x * ((P.Hb + 7) / 8)) return;
@@ -1154,8 +1167,9 @@ __global__ void __launch_bounds__(256, 4) k_refine_q8(const PairDev* __restrict_
   const int m = v * P.Wb + u;
   int n = -1, pa = 0;
   if (u < P.Wb && v < P.Hb) {
-    pa = P.out_pa[m];
-    if (P.out_valid[m]) n = m;
+    const int2 r = match_pixel(P, lp, m);
+    pa = r.x;
+    if (r.y) n = m;
   }
   const bool fast_pair = P.q8a != nullptr && P.sel->qbad == 0;
   QB B;
@@ -1184,8 +1198,10 @@ __global__ void __launch_bounds__(256, 4) k_refine_q8(const PairDev* __restrict_
   }
   if (q.st != 2) {
     const int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
-    P.out_pa[n] = out;
-    P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
+    if (out != pa) {
+      P.out_pa[n] = out;
+      P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
+    }
   }
 }
 
@@ -1400,16 +1416,15 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     int max_tiles = 0;
     for (int i = c0; i < c0 + cn; ++i)
       max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
-    {
+    if (refine && L.n > 0) {
+      ProfScope ps(ctx, "k_match_refine");
+      unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
+      k_match_refine<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp, L, exact_px);
+      launch_check(ctx, "k_match_refine");
+    } else {
       ProfScope ps(ctx, "k_match");
       k_match<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp);
-    }
-    launch_check(ctx, "k_match");
-    if (refine && L.n > 0) {
-      ProfScope ps(ctx, "k_refine");
-      unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
-      k_refine_q8<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, L, exact_px);
-      launch_check(ctx, "k_refine_q8");
+      launch_check(ctx, "k_match");
     }
   }
   // Device-memory calls on a caller-adopted stream (pmx_set_stream) stay

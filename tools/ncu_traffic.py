@@ -16,7 +16,7 @@ h = rows[0]
 col = {k: h.index(k) for k in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum")}
 units = rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
-names = {"k_refine_q8": "k_refine", "k_match": "k_match", "k_prep": "k_prep"}
+names = {"k_match_refine": "k_match_refine", "k_prep": "k_prep"}
 res = {}
 for r in rows[2:]:
     kname = r[col["Kernel Name"]]
