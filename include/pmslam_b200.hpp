@@ -12,6 +12,7 @@
 #include <array>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -200,6 +201,34 @@ inline MatchSet feature_refine(Context& c, const MatchSet& matches, const Featur
   const auto fa = F_a.view(), fb = F_b.view();
   check(c.get(), pmx_feature_refine(c.get(), PMX_MEM_HOST, &i, &fa, &fb, &params, &o));
   return out.to_matchset();
+}
+
+// ------------------------------------------------------ retrieval.hpp API
+// accept_loop_edge, retrieval.cpp:226-251 (std::optional<Edge> as in the reference).
+inline std::optional<Edge> accept_loop_edge(Context& c, int kf_i, int kf_j, const Pointmap& X_i_i,
+                                            const Pointmap& X_j_in_i, const FeatureMap& F_i, const FeatureMap& F_j,
+                                            double omega_l, const pmx_match_params& match_params = default_match_params(),
+                                            const pmx_refine_params& refine_params = default_refine_params()) {
+  detail::SoA out((size_t)X_j_in_i.size());
+  auto o = out.view();
+  const pmx_pair p{X_i_i.view(), X_j_in_i.view(), F_i.view(), F_j.view(), nullptr};
+  int32_t accepted = 0;
+  check(c.get(), pmx_accept_loop_edges(c.get(), PMX_MEM_HOST, 1, &p, omega_l, &match_params, &refine_params, &o,
+                                       &accepted));
+  if (!accepted) return std::nullopt;
+  Edge e;
+  e.i = kf_i;
+  e.j = kf_j;
+  e.matches = out.to_matchset();
+  return e;
+}
+
+// ------------------------------------------------------- pipeline.cpp API
+// constrain_to_rays, pipeline.cpp:32-46 (calibrated mode), in place.
+inline void constrain_to_rays(Context& c, Pointmap& pm, const pmx_intrinsics& K) {
+  if (pm.valid.empty()) pm.valid.assign((size_t)pm.size(), 1);
+  check(c.get(), pmx_constrain_to_rays(c.get(), PMX_MEM_HOST, pm.height, pm.width, pm.xyz.data(), pm.valid.data(),
+                                       &K));
 }
 
 // ------------------------------------------------------- tracking.hpp API

@@ -254,6 +254,16 @@ int pmx_match_batch(pmx_context* ctx, pmx_memory mem, int32_t num_pairs,
                     const pmx_pair* pairs, const pmx_match_params* params,
                     const pmx_refine_params* refine, pmx_matchset* outs);
 
+/* accept_loop_edge, retrieval.cpp:226-251, for a batch of candidate loop
+ * edges (X_a = X_i_i, X_b_in_a = X_j_in_i, F_a = F_i, F_b = F_j): match +
+ * refine, then the descriptor-agreement gate (exact FP64 dot of the two
+ * endpoints' descriptors < 0.5 invalidates a match, retrieval.cpp:238-244),
+ * then accepted[e] = valid_fraction() >= omega_l (else the reference's
+ * nullopt).  outs[e] receives the gated matches (Edge::matches). */
+int pmx_accept_loop_edges(pmx_context* ctx, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
+                          double omega_l, const pmx_match_params* params, const pmx_refine_params* refine,
+                          pmx_matchset* outs, int32_t* accepted);
+
 /* MatchSet::valid_count / unique_pixel_fraction, camera.cpp:10-28, and
  * keyframe_decision, tracking.cpp:249-257. */
 int pmx_match_stats(pmx_context* ctx, pmx_memory mem, const pmx_matchset* m,
@@ -262,6 +272,37 @@ int pmx_match_stats(pmx_context* ctx, pmx_memory mem, const pmx_matchset* m,
 int pmx_keyframe_decision(pmx_context* ctx, pmx_memory mem, const pmx_matchset* m,
                           int32_t height, int32_t width, double omega_k,
                           int32_t* new_keyframe);
+
+/* ------------------------------------- inputs of the path (pipeline.cpp) */
+
+/* One PMPAIR01 pair record (StreamPredictor::predict, pipeline.cpp:642-676):
+ * 8-byte magic, then float32 X_i_in_i [HW*3], X_j_in_i [HW*3], C_i [HW],
+ * C_j [HW], D_i [HW*dim] (pixel-major), D_j, Q_i [HW], Q_j [HW].  Unpacked
+ * into the layouts above: valid = allFinite(point) (pipeline.cpp:536-543),
+ * descriptors converted to fp16 (inexact_descriptors counts values that are
+ * not exactly representable: parity with the reference needs 0).  All
+ * output arrays are caller-allocated (host or device per mem, like record). */
+typedef struct pmx_pair_record {
+  float* X_i;
+  uint8_t* valid_i;
+  float* X_j;
+  uint8_t* valid_j;
+  float* C_i;
+  float* C_j;
+  uint16_t* D_i;
+  uint16_t* D_j;
+  float* Q_i;
+  float* Q_j;
+} pmx_pair_record;
+int pmx_ingest_pair_record(pmx_context* ctx, pmx_memory mem, const void* record, int64_t nbytes,
+                           int32_t height, int32_t width, int32_t dim, pmx_pair_record* out,
+                           int64_t* inexact_descriptors);
+
+/* constrain_to_rays, pipeline.cpp:32-46 (calibrated mode), in place:
+ * valid points with z > 0 become z * ((u - cx) / fx, (v - cy) / fy, 1),
+ * z <= 0 invalidates. */
+int pmx_constrain_to_rays(pmx_context* ctx, pmx_memory mem, int32_t height, int32_t width, float* xyz,
+                          uint8_t* valid, const pmx_intrinsics* K);
 
 /* ------------------------------------------------- tracking (tracking.cpp) */
 

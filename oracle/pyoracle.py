@@ -325,3 +325,74 @@ def sim3_adjoint(a):
     out = np.zeros((7, 7))
     _check(lib().orc_sim3_adjoint(C.byref(a), ptr(out)))
     return out
+
+
+# --------------------------------------------------------------------------
+# Neighbours of the path, restated in numpy (FP64).
+
+def accept_loop_edge(pair, omega_l, params=None, refine=None):
+    """accept_loop_edge, reference src/retrieval.cpp:226-251: match + refine,
+    then every valid match whose endpoint descriptors have dot < 0.5
+    (FP64, retrieval.cpp:238-244) is invalidated; accepted iff
+    valid_fraction() >= omega_l (camera.cpp:16-19).  Returns (accepted, MatchSet)."""
+    m = feature_refine(match_pointmaps(pair, params), pair, refine or abi.default_refine_params())
+    Da = np.asarray(pair["D_a"], np.uint16).view(np.float16).astype(np.float64)
+    Db = np.asarray(pair["D_b"], np.uint16).view(np.float16).astype(np.float64)
+    valid = m.valid.astype(bool)
+    idx = np.nonzero(valid)[0]
+    dots = np.einsum("ij,ij->i", Da[m.pixel_a[idx]], Db[m.pixel_b[idx]])  # exact: fp16 products in FP64
+    valid[idx[dots < 0.5]] = False
+    m.valid = valid.astype(np.uint8)
+    frac = valid.sum() / len(valid) if len(valid) else 0.0
+    return bool(frac >= omega_l), m
+
+
+def constrain_to_rays(xyz, valid, h, w, K):
+    """constrain_to_rays, reference src/pipeline.cpp:32-46 (z <= 0 invalidates)."""
+    xyz = np.array(xyz, np.float32).reshape(-1, 3)
+    valid = np.array(valid, np.uint8)
+    u = np.tile(np.arange(w), h)
+    v = np.repeat(np.arange(h), w)
+    z = xyz[:, 2].astype(np.float64)
+    keep = (valid != 0) & (z > 0.0)
+    valid[(valid != 0) & ~(z > 0.0)] = 0
+    x = z * ((u - K.cx) / K.fx)
+    y = z * ((v - K.cy) / K.fy)
+    out = xyz.copy()
+    out[keep, 0] = x[keep].astype(np.float32)
+    out[keep, 1] = y[keep].astype(np.float32)
+    out[keep, 2] = z[keep].astype(np.float32)
+    return out, valid
+
+
+PAIR_MAGIC = b"PMPAIR01"
+
+
+def write_pair_record(X_i, X_j, C_i, C_j, D_i, D_j, Q_i, Q_j) -> bytes:
+    """RecordingPredictor::predict's record, reference src/pipeline.cpp:582-594:
+    magic, then float32 X_i, X_j (HW x 3), C_i, C_j, D_i, D_j (HW x dim,
+    pixel-major = Eigen column order), Q_i, Q_j."""
+    parts = [np.ascontiguousarray(a, np.float32).ravel() for a in (X_i, X_j, C_i, C_j, D_i, D_j, Q_i, Q_j)]
+    return PAIR_MAGIC + b"".join(p.tobytes() for p in parts)
+
+
+def read_pair_record(buf: bytes, h, w, dim):
+    """StreamPredictor::predict, reference src/pipeline.cpp:642-676."""
+    if buf[:8] != PAIR_MAGIC:
+        raise ValueError("StreamPredictor: bad magic")
+    hw = h * w
+    sizes = [3 * hw, 3 * hw, hw, hw, dim * hw, dim * hw, hw, hw]
+    if len(buf) < 8 + 4 * sum(sizes):
+        raise ValueError("StreamPredictor: truncated record")
+    a = np.frombuffer(buf, np.float32, count=sum(sizes), offset=8)
+    out, o = {}, 0
+    for name, n in zip(("X_i", "X_j", "C_i", "C_j", "D_i", "D_j", "Q_i", "Q_j"), sizes):
+        out[name] = a[o:o + n].copy()
+        o += n
+    out["X_i"] = out["X_i"].reshape(hw, 3)
+    out["X_j"] = out["X_j"].reshape(hw, 3)
+    out["D_i"] = out["D_i"].reshape(hw, dim)
+    out["D_j"] = out["D_j"].reshape(hw, dim)
+    out["valid_i"] = np.isfinite(out["X_i"]).all(axis=1).astype(np.uint8)  # allFinite (pipeline.cpp:541)
+    out["valid_j"] = np.isfinite(out["X_j"]).all(axis=1).astype(np.uint8)
+    return out

@@ -130,6 +130,12 @@ class pmx_pair(C.Structure):
                 ("init", C.POINTER(pmx_matchset))]
 
 
+class pmx_pair_record(C.Structure):  # PMPAIR01 record unpacked (pipeline.cpp:642-676)
+    _fields_ = [("X_i", C.c_void_p), ("valid_i", C.c_void_p), ("X_j", C.c_void_p), ("valid_j", C.c_void_p),
+                ("C_i", C.c_void_p), ("C_j", C.c_void_p), ("D_i", C.c_void_p), ("D_j", C.c_void_p),
+                ("Q_i", C.c_void_p), ("Q_j", C.c_void_p)]
+
+
 # Every symbol include/pmx.h declares (checked by tests/test_abi.py).
 PMX_SYMBOLS = [
     "pmx_default_match_params", "pmx_default_refine_params",
@@ -143,7 +149,8 @@ PMX_SYMBOLS = [
     "pmx_solve_pose", "pmx_fuse_canonical", "pmx_assemble_system", "pmx_backend_cost",
     "pmx_global_optimize", "pmx_backend_edge_terms", "pmx_backend_solve_terms",
     "pmx_ldlt_solve", "pmx_profile_enable", "pmx_profile_reset", "pmx_profile_get",
-    "pmx_sim3_retract", "pmx_sim3_relative",
+    "pmx_sim3_retract", "pmx_sim3_relative", "pmx_accept_loop_edges", "pmx_ingest_pair_record",
+    "pmx_constrain_to_rays",
 ]
 
 _lib = None
@@ -163,6 +170,12 @@ def load_library(path: str = LIB_PATH):
     lib.pmx_get_stream.restype = C.c_void_p
     lib.pmx_kernel_launch_count.restype = C.c_int64
     lib.pmx_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    lib.pmx_accept_loop_edges.argtypes = [C.c_void_p, C.c_int, C.c_int32, C.c_void_p, C.c_double, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.pmx_ingest_pair_record.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
+                                           C.c_int32, C.c_void_p, C.POINTER(C.c_int64)]
+    lib.pmx_constrain_to_rays.argtypes = [C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]
     for name in PMX_SYMBOLS:
         fn = getattr(lib, name)
         if name not in ("pmx_last_error", "pmx_get_stream", "pmx_kernel_launch_count",

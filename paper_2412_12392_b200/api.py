@@ -310,6 +310,66 @@ class Context:
                                              C.byref(params), C.byref(refine) if refine is not None else None, oarr))
         return outs
 
+    def accept_loop_edges(self, pairs, omega_l: float, params=None, refine=None, outs=None):
+        """accept_loop_edge (retrieval.cpp:226-251) over candidate edges
+        (X_i_i, X_j_in_i, F_i, F_j): match + refine + descriptor-agreement
+        gate + valid_fraction >= omega_l.  Returns (accepted bools, gated
+        MatchSets)."""
+        keep, structs, mem = [], [], None
+        for p in pairs:
+            X_a, X_b, F_a, F_b = p[:4]
+            m = self._mem(X_a.xyz, X_b.xyz, F_a.descriptors, F_b.descriptors)
+            if mem is not None and m != mem:
+                raise PmxInvalidArgument(abi.PMX_ERR_INVALID_ARGUMENT, "mixed host and device pairs")
+            mem = m
+            structs.append(abi.pmx_pair(X_a.struct(), X_b.struct(), F_a.struct(), F_b.struct(), None))
+        n = len(structs)
+        if outs is None:
+            outs = [MatchSet.empty(p[1].height * p[1].width, p[1].xyz.device if mem == abi.PMX_MEM_DEVICE else None)
+                    for p in pairs]
+        arr = (abi.pmx_pair * max(1, n))(*structs)
+        oarr = (abi.pmx_matchset * max(1, n))(*[o.struct() for o in outs])
+        acc = (C.c_int32 * max(1, n))()
+        params = params or abi.default_match_params()
+        refine = refine if refine is not None else abi.default_refine_params()
+        self._check(self.lib.pmx_accept_loop_edges(self.h, mem if mem is not None else abi.PMX_MEM_HOST, C.c_int32(n),
+                                                   arr, C.c_double(omega_l), C.byref(params), C.byref(refine), oarr,
+                                                   acc))
+        return [bool(acc[i]) for i in range(n)], outs
+
+    def ingest_pair_record(self, record, height: int, width: int, dim: int, device=None):
+        """Unpack one PMPAIR01 record (pipeline.cpp:642-676; bytes / uint8
+        array on the host, or a uint8 CUDA tensor) into the matcher's
+        layouts.  Returns (dict of arrays / tensors, inexact fp16 count)."""
+        import torch
+        hw = height * width
+        on_dev = isinstance(record, torch.Tensor) and record.is_cuda
+        if on_dev:
+            dev, rec_ptr, nbytes = record.device, record.data_ptr(), record.numel()
+            mk = lambda shape, dt: torch.empty(shape, dtype=dt, device=dev)
+        else:
+            buf = np.frombuffer(record, np.uint8) if isinstance(record, (bytes, bytearray)) else np.asarray(record)
+            rec_ptr, nbytes = buf.ctypes.data, buf.nbytes
+            npdt = {torch.float32: np.float32, torch.uint8: np.uint8, torch.int16: np.uint16}
+            mk = lambda shape, dt: np.empty(shape, npdt[dt])
+        out = {"X_i": mk((hw, 3), torch.float32), "valid_i": mk((hw,), torch.uint8),
+               "X_j": mk((hw, 3), torch.float32), "valid_j": mk((hw,), torch.uint8),
+               "C_i": mk((hw,), torch.float32), "C_j": mk((hw,), torch.float32),
+               "D_i": mk((hw, dim), torch.int16), "D_j": mk((hw, dim), torch.int16),
+               "Q_i": mk((hw,), torch.float32), "Q_j": mk((hw,), torch.float32)}
+        rec = abi.pmx_pair_record(*[ptr(out[k]) for k, _ in abi.pmx_pair_record._fields_])
+        bad = C.c_int64()
+        self._check(self.lib.pmx_ingest_pair_record(self.h, abi.PMX_MEM_DEVICE if on_dev else abi.PMX_MEM_HOST,
+                                                    C.c_void_p(rec_ptr), C.c_int64(nbytes), C.c_int32(height),
+                                                    C.c_int32(width), C.c_int32(dim), C.byref(rec), C.byref(bad)))
+        return out, int(bad.value)
+
+    def constrain_to_rays(self, xyz, valid, height: int, width: int, K):
+        """constrain_to_rays (pipeline.cpp:32-46) in place; K: pmx_intrinsics."""
+        mem = self._mem(xyz)
+        self._check(self.lib.pmx_constrain_to_rays(self.h, mem, C.c_int32(height), C.c_int32(width), ptr(xyz),
+                                                   ptr(valid), C.byref(K)))
+
     def match_stats(self, m: MatchSet, num_pixels_a: int):
         vc, uf = C.c_int64(), C.c_double()
         s = m.struct()

@@ -11,6 +11,11 @@ using pmx::Context;
 extern "C" {
 int pmx_impl_match_batch(pmx_context*, pmx_memory, int32_t, const pmx_pair*, const pmx_match_params*,
                          const pmx_refine_params*, pmx_matchset*);
+int pmx_impl_accept_loop_edges(pmx_context*, pmx_memory, int32_t, const pmx_pair*, double,
+                               const pmx_match_params*, const pmx_refine_params*, pmx_matchset*, int32_t*);
+int pmx_impl_ingest_pair_record(pmx_context*, pmx_memory, const void*, int64_t, int32_t, int32_t, int32_t,
+                                pmx_pair_record*, int64_t*);
+int pmx_impl_constrain_to_rays(pmx_context*, pmx_memory, int32_t, int32_t, float*, uint8_t*, const pmx_intrinsics*);
 int pmx_impl_feature_refine(pmx_context*, pmx_memory, const pmx_matchset*, const pmx_featuremap*,
                             const pmx_featuremap*, const pmx_refine_params*, pmx_matchset*);
 int pmx_impl_normalize_rays(pmx_context*, pmx_memory, const pmx_pointmap*, double*, double*, uint8_t*);
@@ -287,6 +292,26 @@ int pmx_feature_refine(pmx_context* c, pmx_memory mem, const pmx_matchset* in, c
 int pmx_match_batch(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
                     const pmx_match_params* params, const pmx_refine_params* refine, pmx_matchset* outs) {
   return guarded(c, [&] { return pmx_impl_match_batch(c, mem, num_pairs, pairs, params, refine, outs); });
+}
+
+int pmx_accept_loop_edges(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs, double omega_l,
+                          const pmx_match_params* params, const pmx_refine_params* refine, pmx_matchset* outs,
+                          int32_t* accepted) {
+  return guarded(c, [&] {
+    return pmx_impl_accept_loop_edges(c, mem, num_pairs, pairs, omega_l, params, refine, outs, accepted);
+  });
+}
+
+int pmx_ingest_pair_record(pmx_context* c, pmx_memory mem, const void* record, int64_t nbytes, int32_t height,
+                           int32_t width, int32_t dim, pmx_pair_record* out, int64_t* inexact_descriptors) {
+  return guarded(c, [&] {
+    return pmx_impl_ingest_pair_record(c, mem, record, nbytes, height, width, dim, out, inexact_descriptors);
+  });
+}
+
+int pmx_constrain_to_rays(pmx_context* c, pmx_memory mem, int32_t height, int32_t width, float* xyz,
+                          uint8_t* valid, const pmx_intrinsics* K) {
+  return guarded(c, [&] { return pmx_impl_constrain_to_rays(c, mem, height, width, xyz, valid, K); });
 }
 
 int pmx_match_stats(pmx_context* c, pmx_memory mem, const pmx_matchset* m, int32_t num_pixels_a,

@@ -1267,6 +1267,29 @@ __global__ void k_rays_out(const double4* __restrict__ rays, int HW, double* out
   }
 }
 
+// accept_loop_edge's descriptor-agreement gate (retrieval.cpp:238-244): a
+// valid match stays valid only if the exact dot of its endpoints'
+// descriptors is >= 0.5 (unit-norm descriptors; FP64 sum of the exact fp16
+// products, as the reference's double dot).  Counts the surviving matches
+// of every pair (valid_fraction, camera.cpp:16-19).
+__global__ void __launch_bounds__(256) k_loop_gate(const PairDev* __restrict__ pairs, double min_agreement,
+                                                   unsigned long long* __restrict__ valid_count) {
+  const PairDev& P = pairs[blockIdx.y];
+  const int hwb = P.Hb * P.Wb;
+  int cnt = 0;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < hwb; n += gridDim.x * blockDim.x) {
+    if (!P.out_valid[n]) continue;
+    const int pa = P.out_pa[n];
+    const double d = dot_exact(P.da + (size_t)pa * P.dim, P.db + (size_t)n * P.dim, P.dim);
+    if (d < min_agreement)
+      P.out_valid[n] = 0;
+    else
+      ++cnt;
+  }
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(valid_count + blockIdx.y, (unsigned long long)cnt);
+}
+
 // ------------------------------------------------------------------ host
 // Largest double d with acos(clamp(d, -1, 1)) >= tol, found on the host with
 // the same libm acos the reference uses; the device tests d >= cos_tol.
@@ -1479,10 +1502,11 @@ static PairDev stage_pair(Stager& st, const pmx_pair& p, DevBuf* seed_buf, Conte
 
 using namespace pmx;
 
-extern "C" int pmx_impl_match_batch(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
-                                    const pmx_match_params* params, const pmx_refine_params* refine,
-                                    pmx_matchset* outs) {
-  Context& ctx = *reinterpret_cast<Context*>(c);
+// Stage a batch of pairs + their outputs (PMX_MEM_HOST: H2D / scratch),
+// run the fused matcher, optionally the loop-edge gate, copy the outputs back.
+static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
+                            const pmx_match_params* params, const pmx_refine_params* refine, pmx_matchset* outs,
+                            double gate, std::vector<unsigned long long>* gate_counts) {
   require(num_pairs >= 0 && (num_pairs == 0 || (pairs && outs)), "match_batch: null arguments");
   pmx_match_params mp;
   pmx_default_match_params(&mp);
@@ -1501,6 +1525,17 @@ extern "C" int pmx_impl_match_batch(pmx_context* c, pmx_memory mem, int32_t num_
     hp[i].out_valid = st.out(outs[i].valid, hwb);
   }
   match_batch_device(ctx, hp, mp, refine);
+  if (gate_counts && num_pairs > 0) {
+    DevBuf dp(sizeof(PairDev) * num_pairs, ctx.stream), cnt(sizeof(unsigned long long) * num_pairs, ctx.stream);
+    PMX_CUDA(cudaMemcpyAsync(dp.p, hp.data(), dp.bytes, cudaMemcpyHostToDevice, ctx.stream));
+    PMX_CUDA(cudaMemsetAsync(cnt.p, 0, cnt.bytes, ctx.stream));
+    k_loop_gate<<<dim3(2 * ctx.num_sms, num_pairs), 256, 0, ctx.stream>>>(dp.as<PairDev>(), gate,
+                                                                           cnt.as<unsigned long long>());
+    launch_check(ctx, "k_loop_gate");
+    gate_counts->resize(num_pairs);
+    PMX_CUDA(cudaMemcpyAsync(gate_counts->data(), cnt.p, cnt.bytes, cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
   for (int i = 0; i < num_pairs; ++i) {
     const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
     st.back(outs[i].pixel_a, hp[i].out_pa, hwb);
@@ -1510,6 +1545,29 @@ extern "C" int pmx_impl_match_batch(pmx_context* c, pmx_memory mem, int32_t num_
     outs[i].count = (int64_t)hwb;
   }
   if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+}
+
+extern "C" int pmx_impl_match_batch(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
+                                    const pmx_match_params* params, const pmx_refine_params* refine,
+                                    pmx_matchset* outs) {
+  run_match_batch(*reinterpret_cast<Context*>(c), mem, num_pairs, pairs, params, refine, outs, 0.0, nullptr);
+  return PMX_OK;
+}
+
+// accept_loop_edge (retrieval.cpp:226-251) for a batch of candidate edges.
+extern "C" int pmx_impl_accept_loop_edges(pmx_context* c, pmx_memory mem, int32_t num_pairs, const pmx_pair* pairs,
+                                          double omega_l, const pmx_match_params* params,
+                                          const pmx_refine_params* refine, pmx_matchset* outs, int32_t* accepted) {
+  require(num_pairs == 0 || accepted, "accept_loop_edges: null accepted");
+  std::vector<unsigned long long> counts;
+  constexpr double kMinDescriptorAgreement = 0.5;  // retrieval.cpp:238
+  run_match_batch(*reinterpret_cast<Context*>(c), mem, num_pairs, pairs, params, refine, outs,
+                  kMinDescriptorAgreement, &counts);
+  for (int i = 0; i < num_pairs; ++i) {  // valid_fraction() < omega_l -> nullopt (camera.cpp:16-19)
+    const double size = (double)pairs[i].X_b_in_a.height * pairs[i].X_b_in_a.width;
+    const double frac = size > 0 ? (double)counts[i] / size : 0.0;
+    accepted[i] = frac < omega_l ? 0 : 1;
+  }
   return PMX_OK;
 }
 

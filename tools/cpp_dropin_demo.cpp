@@ -110,6 +110,18 @@ int main() {
   }
   CHECK(threw);
 
+  // retrieval.hpp: a self pair agrees in appearance everywhere -> accepted,
+  // all matches kept; omega_l above 1 can never be met -> nullopt
+  const auto edge = accept_loop_edge(ctx, 3, 7, X, X, F, F, 0.9);
+  CHECK(edge.has_value() && edge->i == 3 && edge->j == 7 && edge->matches.valid_count() == n);
+  CHECK(!accept_loop_edge(ctx, 3, 7, X, X, F, F, 1.01).has_value());
+  // pipeline.cpp: constrain_to_rays puts points back on their pixel rays
+  Pointmap Xc = X;
+  const pmx_intrinsics Kc{50.0, 50.0, 32.0, 24.0};
+  constrain_to_rays(ctx, Xc, Kc);
+  const int pc = Xc.index(10, 20);
+  CHECK(std::fabs(Xc.xyz[3 * pc] - (float)(Xc.xyz[3 * pc + 2] * ((10 - 32.0) / 50.0))) < 1e-6f);
+
   // tracking.hpp: exact Sim(3) recovery with scale (test_tracking.cpp:200-223)
   const Sim3Pose T_true = make_pose(0.1, -0.08, 0.12, 0.08, -0.12, 0.05, 1.3);
   Keyframe kf;
