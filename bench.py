@@ -410,7 +410,7 @@ def run_pmx(args):
                             "share_of_step": kms / prof_ms if prof_ms > 0 else None,
                             "alg_bytes_per_px": KERNEL_BYTES_PER_PX.get(k, 117),
                             "achieved_gbs": nbytes / (kms / 1e3) / 1e9 if kms > 0 else None}
-        breakdown["k_refine"]["exact_path_px_per_step"] = exact_px / args.steps
+        breakdown["k_match_refine"]["exact_path_px_per_step"] = exact_px / args.steps
         dom = max(breakdown, key=lambda k: breakdown[k]["ms_per_step"])
         achieved = breakdown[dom]["achieved_gbs"]
         traffic = None
@@ -443,7 +443,7 @@ def run_pmx(args):
                          / max(1, kern[dom][1]), "peak_kind": peak_kind,
                          "path": {"alg_bytes_per_px": ALG_BYTES_PER_PX,
                                   "achieved_gbs": ALG_BYTES_PER_PX * px_steps / (ms_local / 1e3) / 1e9},
-                         "note": "issue-bound (FP64 LM, fp16 FHFMA window search), not HBM-bound: see DESIGN.md"},
+                         "note": "issue-bound (FP64 LM + int8 DP4A window search), not HBM-bound: see DESIGN.md"},
             "kernels": breakdown,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

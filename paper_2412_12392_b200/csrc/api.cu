@@ -175,6 +175,11 @@ int pmx_destroy(pmx_context* c) {
     cudaStreamSynchronize(ctx->own_stream);
     cudaStreamDestroy(ctx->own_stream);
   }
+  for (cudaStream_t s : {ctx->copy_in, ctx->copy_out})
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
   for (auto& kv : ctx->dev_counters) cudaFree(kv.second);
   delete ctx;
   return (int)PMX_OK;

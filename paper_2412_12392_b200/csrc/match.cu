@@ -27,6 +27,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <type_traits>
 #include <vector>
 
@@ -1382,8 +1383,16 @@ static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa
 }
 
 // Batched match(+refine).  All pointers in `pairs` are device pointers.
+// Host-staging hooks of the pipelined PMX_MEM_HOST path (run_match_batch):
+// before_select makes the stream wait for the a-side points, before_chunk /
+// after_chunk bracket a chunk's compute with its input / output copies.
+struct MatchHooks {
+  std::function<void()> before_select;
+  std::function<void(int, int)> before_chunk, after_chunk;
+};
+
 void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, const pmx_match_params& mp,
-                        const pmx_refine_params* refine) {
+                        const pmx_refine_params* refine, const MatchHooks* hooks = nullptr) {
   const LMParams lp = make_lm(mp);
   const RefineLevels L = make_levels(refine);
   const int npairs = (int)host_pairs.size();
@@ -1425,6 +1434,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(sel.p, 0, sel.bytes, ctx.stream));
+  if (hooks) hooks->before_select();
   {
     ProfScope ps(ctx, "k_select");
     select_median(ctx, dpairs.as<PairDev>(), npairs, max_hwa, lp.median_fraction);
@@ -1432,6 +1442,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   for (int c0 = 0; c0 < npairs; c0 += chunk) {
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
+    if (hooks) hooks->before_chunk(c0, cn);
     {
       ProfScope ps(ctx, "k_prep");
       prep_rays(ctx, dp, cn, max_hwa);
@@ -1449,6 +1460,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
       k_match<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp);
       launch_check(ctx, "k_match");
     }
+    if (hooks) hooks->after_chunk(c0, cn);
   }
   // Device-memory calls on a caller-adopted stream (pmx_set_stream) stay
   // asynchronous like any CUDA library call (scratch is stream-ordered and
@@ -1511,11 +1523,16 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
   pmx_match_params mp;
   pmx_default_match_params(&mp);
   if (params) mp = *params;
-  Stager st(ctx, mem);
+  bool seeded = false;
+  for (int i = 0; i < num_pairs; ++i) seeded = seeded || (pairs[i].init && pairs[i].init->count > 0);
+  // Host buffers: pipelined staging (inputs of chunk c+1 copied while chunk c
+  // computes, outputs of chunk c copied back on a second copy stream).
+  const bool pipelined = mem == PMX_MEM_HOST && !seeded && num_pairs > 0;
+  Stager st(ctx, pipelined ? PMX_MEM_DEVICE : mem);
   std::vector<PairDev> hp(num_pairs);
-  std::vector<DevBuf> seeds(num_pairs);
+  std::vector<DevBuf> seeds(num_pairs), dbufs;
   for (int i = 0; i < num_pairs; ++i) {
-    hp[i] = stage_pair(st, pairs[i], &seeds[i], ctx);
+    hp[i] = stage_pair(st, pairs[i], &seeds[i], ctx);  // device path: pointers as given / staged
     const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
     require(outs[i].count >= (int64_t)hwb && outs[i].pixel_a && outs[i].confidence && outs[i].valid,
             "match_batch: output matchset too small or null");
@@ -1524,7 +1541,98 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     hp[i].out_q = st.out(outs[i].confidence, hwb);
     hp[i].out_valid = st.out(outs[i].valid, hwb);
   }
-  match_batch_device(ctx, hp, mp, refine);
+  MatchHooks hooks;
+  cudaEvent_t ev_a = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  if (pipelined) {  // device mirrors of every array (one allocation), copies issued by the hooks
+    if (!ctx.copy_in) {
+      PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_in, cudaStreamNonBlocking));
+      PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_out, cudaStreamNonBlocking));
+    }
+    size_t total = 0;
+    auto room = [&](size_t bytes) { total += (bytes + 255) & ~size_t(255); };
+    for (int i = 0; i < num_pairs; ++i) {
+      const pmx_pair& p = pairs[i];
+      const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa, hwb = (size_t)hp[i].Hb * hp[i].Wb;
+      room(12 * hwa); room(p.X_a.valid ? hwa : 0); room(12 * hwb); room(p.X_b_in_a.valid ? hwb : 0);
+      room(2 * hwa * hp[i].dim); room(2 * hwb * hp[i].dim); room(4 * hwa); room(4 * hwb);
+      room(4 * hwb); room(outs[i].pixel_b ? 4 * hwb : 0); room(4 * hwb); room(hwb);
+    }
+    dbufs.emplace_back(total, ctx.stream);
+    char* cur = dbufs.back().as<char>();
+    auto take = [&](size_t bytes) {
+      char* r = bytes ? cur : nullptr;
+      cur += (bytes + 255) & ~size_t(255);
+      return r;
+    };
+    for (int i = 0; i < num_pairs; ++i) {
+      const pmx_pair& p = pairs[i];
+      const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa, hwb = (size_t)hp[i].Hb * hp[i].Wb;
+      hp[i].xa = reinterpret_cast<const float*>(take(12 * hwa));
+      hp[i].va = reinterpret_cast<const uint8_t*>(take(p.X_a.valid ? hwa : 0));
+      hp[i].xb = reinterpret_cast<const float*>(take(12 * hwb));
+      hp[i].vb = reinterpret_cast<const uint8_t*>(take(p.X_b_in_a.valid ? hwb : 0));
+      hp[i].da = reinterpret_cast<const __half*>(take(2 * hwa * hp[i].dim));
+      hp[i].db = reinterpret_cast<const __half*>(take(2 * hwb * hp[i].dim));
+      hp[i].qa = reinterpret_cast<const float*>(take(4 * hwa));
+      hp[i].qb = reinterpret_cast<const float*>(take(4 * hwb));
+      hp[i].out_pa = reinterpret_cast<int32_t*>(take(4 * hwb));
+      hp[i].out_pb = reinterpret_cast<int32_t*>(take(outs[i].pixel_b ? 4 * hwb : 0));
+      hp[i].out_q = reinterpret_cast<float*>(take(4 * hwb));
+      hp[i].out_valid = reinterpret_cast<uint8_t*>(take(hwb));
+    }
+    PMX_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
+    PMX_CUDA(cudaEventRecord(ev_a, ctx.stream));  // device buffers allocated (stream-ordered)
+    PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in, ev_a, 0));
+    auto h2d = [&](const void* d, const void* h, size_t bytes) {
+      if (bytes) PMX_CUDA(cudaMemcpyAsync(const_cast<void*>(d), h, bytes, cudaMemcpyHostToDevice, ctx.copy_in));
+    };
+    auto d2h = [&](void* h, const void* d, size_t bytes) {
+      if (bytes && h) PMX_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, ctx.copy_out));
+    };
+    hooks.before_select = [&]() {  // the median needs every pair's a-side points
+      for (int i = 0; i < num_pairs; ++i) {
+        const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa;
+        h2d(hp[i].xa, pairs[i].X_a.xyz, 12 * hwa);
+        if (pairs[i].X_a.valid) h2d(hp[i].va, pairs[i].X_a.valid, hwa);
+      }
+      PMX_CUDA(cudaEventRecord(ev_a, ctx.copy_in));
+      PMX_CUDA(cudaStreamWaitEvent(ctx.stream, ev_a, 0));
+    };
+    hooks.before_chunk = [&](int c0, int cn) {
+      for (int i = c0; i < c0 + cn; ++i) {
+        const pmx_pair& p = pairs[i];
+        const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa, hwb = (size_t)hp[i].Hb * hp[i].Wb;
+        h2d(hp[i].xb, p.X_b_in_a.xyz, 12 * hwb);
+        if (p.X_b_in_a.valid) h2d(hp[i].vb, p.X_b_in_a.valid, hwb);
+        h2d(hp[i].da, p.F_a.descriptors, 2 * hwa * hp[i].dim);
+        h2d(hp[i].db, p.F_b.descriptors, 2 * hwb * hp[i].dim);
+        h2d(hp[i].qa, p.F_a.match_confidence, 4 * hwa);
+        h2d(hp[i].qb, p.F_b.match_confidence, 4 * hwb);
+      }
+      cudaEvent_t e;
+      PMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev_in.push_back(e);
+      PMX_CUDA(cudaEventRecord(e, ctx.copy_in));
+      PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
+    };
+    hooks.after_chunk = [&](int c0, int cn) {
+      if (gate_counts) return;  // the gate still rewrites valid: copied back at the end
+      cudaEvent_t e;
+      PMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev_out.push_back(e);
+      PMX_CUDA(cudaEventRecord(e, ctx.stream));
+      PMX_CUDA(cudaStreamWaitEvent(ctx.copy_out, e, 0));
+      for (int i = c0; i < c0 + cn; ++i) {
+        const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
+        d2h(outs[i].pixel_a, hp[i].out_pa, 4 * hwb);
+        d2h(outs[i].pixel_b, hp[i].out_pb, 4 * hwb);
+        d2h(outs[i].confidence, hp[i].out_q, 4 * hwb);
+        d2h(outs[i].valid, hp[i].out_valid, hwb);
+      }
+    };
+  }
+  match_batch_device(ctx, hp, mp, refine, pipelined ? &hooks : nullptr);
   if (gate_counts && num_pairs > 0) {
     DevBuf dp(sizeof(PairDev) * num_pairs, ctx.stream), cnt(sizeof(unsigned long long) * num_pairs, ctx.stream);
     PMX_CUDA(cudaMemcpyAsync(dp.p, hp.data(), dp.bytes, cudaMemcpyHostToDevice, ctx.stream));
@@ -1535,6 +1643,26 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     gate_counts->resize(num_pairs);
     PMX_CUDA(cudaMemcpyAsync(gate_counts->data(), cnt.p, cnt.bytes, cudaMemcpyDeviceToHost, ctx.stream));
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  }
+  if (pipelined) {
+    if (gate_counts) {  // outputs after the gate
+      for (int i = 0; i < num_pairs; ++i) {
+        const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;
+        PMX_CUDA(cudaMemcpyAsync(outs[i].pixel_a, hp[i].out_pa, 4 * hwb, cudaMemcpyDeviceToHost, ctx.stream));
+        if (outs[i].pixel_b)
+          PMX_CUDA(cudaMemcpyAsync(outs[i].pixel_b, hp[i].out_pb, 4 * hwb, cudaMemcpyDeviceToHost, ctx.stream));
+        PMX_CUDA(cudaMemcpyAsync(outs[i].confidence, hp[i].out_q, 4 * hwb, cudaMemcpyDeviceToHost, ctx.stream));
+        PMX_CUDA(cudaMemcpyAsync(outs[i].valid, hp[i].out_valid, hwb, cudaMemcpyDeviceToHost, ctx.stream));
+      }
+    }
+    PMX_CUDA(cudaStreamSynchronize(ctx.copy_out));
+    PMX_CUDA(cudaStreamSynchronize(ctx.copy_in));
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaEventDestroy(ev_a);
+    for (auto e : ev_in) cudaEventDestroy(e);
+    for (auto e : ev_out) cudaEventDestroy(e);
+    for (int i = 0; i < num_pairs; ++i) outs[i].count = (int64_t)hp[i].Hb * hp[i].Wb;
+    return;
   }
   for (int i = 0; i < num_pairs; ++i) {
     const size_t hwb = (size_t)hp[i].Hb * hp[i].Wb;

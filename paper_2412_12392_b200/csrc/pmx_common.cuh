@@ -48,6 +48,7 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // pipelined host staging (created on first use)
   std::string err;
   int64_t launches = 0;
   int num_sms = 148;
