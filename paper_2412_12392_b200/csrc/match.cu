@@ -10,7 +10,7 @@
 //                    fp32 keys of the FP64 point norms, then an exact
 //                    rank-floor(n/2) radix select (12+12+8 bits): the upper
 //                    median of median_scene_distance's nth_element.
-//   then per chunk of pairs (sized so a chunk's scratch stays L2-resident):
+//   then per chunk of pairs (all pairs of a device-memory batch at once):
 //   K1 k_prep        one thread per a-pixel: FP64 unit ray + validity into a
 //                    32-byte ray map, and the int8 image of the descriptor
 //                    (24 B) for the refinement.
@@ -1383,12 +1383,20 @@ static void prep_and_select(Context& ctx, PairDev* dev_pairs, int n, int max_hwa
 }
 
 // Batched match(+refine).  All pointers in `pairs` are device pointers.
+// Scratch budget of one chunk of pairs (FP64 ray maps + int8 descriptors,
+// 56 B per a-pixel).  Measured on B200: one chunk over all 64 config-2 pairs
+// (704 MB, HBM-resident) beats L2-sized chunks of 5 pairs: the matcher is
+// issue-bound (its DRAM traffic is ~10% of peak either way) and one launch
+// per kernel removes 12 tails and launch gaps.
+constexpr size_t kChunkBytes = size_t(4) << 30;
+
 // Host-staging hooks of the pipelined PMX_MEM_HOST path (run_match_batch):
 // before_select makes the stream wait for the a-side points, before_chunk /
 // after_chunk bracket a chunk's compute with its input / output copies.
 struct MatchHooks {
   std::function<void()> before_select;
   std::function<void(int, int)> before_chunk, after_chunk;
+  int chunk_pairs;  // pairs per chunk (small: the copies of chunk c+1 overlap chunk c)
 };
 
 void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, const pmx_match_params& mp,
@@ -1402,11 +1410,12 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     max_hwa = std::max(max_hwa, p.Ha * p.Wa);
     max_hwb = std::max(max_hwb, p.Hb * p.Wb);
   }
-  // chunk so that a chunk's FP64 ray maps + int8 descriptors (56 B per
-  // a-pixel) stay L2-resident between k_prep and k_match / k_refine
+  // chunks of pairs sharing one scratch allocation: FP64 ray maps + int8
+  // descriptors (56 B per a-pixel), see kChunkBytes
   const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
-  const int chunk = std::max(1, std::min(npairs, (int)((64u << 20) / std::max<size_t>(pair_bytes, 1))));
+  int chunk = std::max(1, std::min(npairs, (int)((size_t(kChunkBytes)) / std::max<size_t>(pair_bytes, 1))));
+  if (hooks) chunk = std::max(1, std::min(chunk, hooks->chunk_pairs));
   DevBuf scratch(pair_bytes * chunk, ctx.stream);
   DevBuf keybuf(sizeof(uint32_t) * (size_t)max_hwa * npairs, ctx.stream);
   DevBuf hist(sizeof(uint32_t) * (size_t)kHistTotal * npairs, ctx.stream);
@@ -1542,6 +1551,7 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     hp[i].out_valid = st.out(outs[i].valid, hwb);
   }
   MatchHooks hooks;
+  hooks.chunk_pairs = 8;  // ~190 MB of inputs per chunk: ~3.5 ms of H2D against ~0.3 ms of compute
   cudaEvent_t ev_a = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   if (pipelined) {  // device mirrors of every array (one allocation), copies issued by the hooks
