@@ -390,6 +390,23 @@ int pmx_backend_solve_terms(pmx_context* ctx, pmx_memory mem, const pmx_graph* g
                             const pmx_backend_params* params, const double* terms,
                             double* tau, double* cost, int32_t* solved);
 
+/* Prepared graph: a graph staged once (canonicals packed, the frozen matches
+ * of edges [edge_begin, edge_end) compacted, the solver's frontal plan built)
+ * for repeated per-iteration calls at changing poses — the building blocks
+ * of the edge-sharded backend without per-iteration re-staging.  Edges
+ * outside the range may carry empty match sets.  poses are host memory;
+ * terms / tau are device memory (float64, layouts as above). */
+typedef struct pmx_prepared_graph pmx_prepared_graph;
+int pmx_graph_prepare(pmx_context* ctx, pmx_memory mem, const pmx_graph* graph,
+                      const pmx_backend_params* params, int32_t edge_begin, int32_t edge_end,
+                      pmx_prepared_graph** out);
+/* terms of the prepared edge range: out double[(edge_end-edge_begin)*PMX_EDGE_TERMS] */
+int pmx_graph_edge_terms(pmx_context* ctx, pmx_prepared_graph* pg, const pmx_sim3* poses, double* out);
+/* all edges' terms (double[num_edges*PMX_EDGE_TERMS]) -> cost, damped solve, tau double[7N] */
+int pmx_graph_solve(pmx_context* ctx, pmx_prepared_graph* pg, const pmx_sim3* poses, const double* terms,
+                    double* tau, double* cost, int32_t* solved);
+int pmx_graph_release(pmx_context* ctx, pmx_prepared_graph* pg);
+
 /* Dense symmetric LDL^T solve of A x = b (n x n, row-major, FP64) on the
  * device, no pivoting, fails (status field 0) on an exactly zero pivot —
  * the factorisation semantics of SimplicialLDLT (backend.cpp:216-218). */

@@ -150,7 +150,8 @@ PMX_SYMBOLS = [
     "pmx_global_optimize", "pmx_backend_edge_terms", "pmx_backend_solve_terms",
     "pmx_ldlt_solve", "pmx_profile_enable", "pmx_profile_reset", "pmx_profile_get",
     "pmx_sim3_retract", "pmx_sim3_relative", "pmx_accept_loop_edges", "pmx_ingest_pair_record",
-    "pmx_constrain_to_rays",
+    "pmx_constrain_to_rays", "pmx_graph_prepare", "pmx_graph_edge_terms", "pmx_graph_solve",
+    "pmx_graph_release",
 ]
 
 _lib = None
@@ -174,6 +175,12 @@ def load_library(path: str = LIB_PATH):
                                           C.c_void_p, C.c_void_p, C.c_void_p]
     lib.pmx_ingest_pair_record.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_int32, C.c_int32,
                                            C.c_int32, C.c_void_p, C.POINTER(C.c_int64)]
+    lib.pmx_graph_prepare.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_void_p)]
+    lib.pmx_graph_edge_terms.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.pmx_graph_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+    lib.pmx_graph_release.argtypes = [C.c_void_p, C.c_void_p]
     lib.pmx_constrain_to_rays.argtypes = [C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
     for name in PMX_SYMBOLS:

@@ -513,6 +513,12 @@ class Context:
                                                          ptr(terms), ptr(tau), C.byref(cost), C.byref(solved)))
         return tau, cost.value, bool(solved.value)
 
+    def prepare_graph(self, g: Graph, params=None, begin: int = 0, end: Optional[int] = None) -> "PreparedGraph":
+        """Stage g once for repeated edge-term / solve calls at changing poses
+        (edges [begin, end) compacted; the edge-sharded backend's handle)."""
+        return PreparedGraph(self, g, params or abi.default_backend_params(), begin,
+                             len(g.edges) if end is None else end)
+
     def global_optimize(self, g: Graph, params=None, trace: bool = False) -> OptimizeResult:
         keep = []
         gs = g.struct(keep)
@@ -579,3 +585,52 @@ class PreparedBatch:
         self.pairs, self.outs = list(pairs), outs
         self.arr = (abi.pmx_pair * max(1, self.n))(*structs)
         self.oarr = (abi.pmx_matchset * max(1, self.n))(*[o.struct() for o in outs])
+
+
+class PreparedGraph:
+    """pmx_graph_prepare handle: device-resident graph of one edge range.
+    edge_terms(poses) -> (end-begin, 72) float64 CUDA tensor;
+    solve(poses, terms) -> (tau (7N,) float64 CUDA tensor, cost, solved)."""
+
+    def __init__(self, ctx: "Context", g: Graph, params, begin: int, end: int):
+        import torch
+        self.ctx, self.begin, self.end, self.n = ctx, begin, end, len(g.canonicals)
+        self._keep = []
+        gs = g.struct(self._keep)
+        self._g = g
+        self.device = g.canonicals[0].xyz.device if _is_dev(g.canonicals[0].xyz) else torch.device("cuda")
+        h = C.c_void_p()
+        ctx._check(ctx.lib.pmx_graph_prepare(ctx.h, ctx._graph_mem(g), C.byref(gs), C.byref(params), C.c_int32(begin),
+                                             C.c_int32(end), C.byref(h)))
+        self.h = h
+
+    def _poses(self, poses):
+        arr = (abi.pmx_sim3 * max(1, self.n))(*poses)
+        self._keep_p = arr
+        return arr
+
+    def edge_terms(self, poses):
+        import torch
+        out = torch.empty((self.end - self.begin, abi.PMX_EDGE_TERMS), dtype=torch.float64, device=self.device)
+        self.ctx._check(self.ctx.lib.pmx_graph_edge_terms(self.ctx.h, self.h, self._poses(poses), ptr(out)))
+        self.ctx.synchronize()
+        return out
+
+    def solve(self, poses, terms):
+        import torch
+        tau = torch.empty(7 * self.n, dtype=torch.float64, device=self.device)
+        cost, solved = C.c_double(), C.c_int32()
+        self.ctx._check(self.ctx.lib.pmx_graph_solve(self.ctx.h, self.h, self._poses(poses), ptr(terms), ptr(tau),
+                                                     C.byref(cost), C.byref(solved)))
+        return tau, cost.value, bool(solved.value)
+
+    def release(self):
+        if getattr(self, "h", None):
+            self.ctx._check(self.ctx.lib.pmx_graph_release(self.ctx.h, self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass

@@ -16,6 +16,11 @@ int pmx_impl_accept_loop_edges(pmx_context*, pmx_memory, int32_t, const pmx_pair
 int pmx_impl_ingest_pair_record(pmx_context*, pmx_memory, const void*, int64_t, int32_t, int32_t, int32_t,
                                 pmx_pair_record*, int64_t*);
 int pmx_impl_constrain_to_rays(pmx_context*, pmx_memory, int32_t, int32_t, float*, uint8_t*, const pmx_intrinsics*);
+int pmx_impl_graph_prepare(pmx_context*, pmx_memory, const pmx_graph*, const pmx_backend_params*, int32_t, int32_t,
+                           pmx_prepared_graph**);
+int pmx_impl_graph_edge_terms(pmx_context*, pmx_prepared_graph*, const pmx_sim3*, double*);
+int pmx_impl_graph_solve(pmx_context*, pmx_prepared_graph*, const pmx_sim3*, const double*, double*, double*, int32_t*);
+int pmx_impl_graph_release(pmx_context*, pmx_prepared_graph*);
 int pmx_impl_feature_refine(pmx_context*, pmx_memory, const pmx_matchset*, const pmx_featuremap*,
                             const pmx_featuremap*, const pmx_refine_params*, pmx_matchset*);
 int pmx_impl_normalize_rays(pmx_context*, pmx_memory, const pmx_pointmap*, double*, double*, uint8_t*);
@@ -317,6 +322,21 @@ int pmx_ingest_pair_record(pmx_context* c, pmx_memory mem, const void* record, i
 int pmx_constrain_to_rays(pmx_context* c, pmx_memory mem, int32_t height, int32_t width, float* xyz,
                           uint8_t* valid, const pmx_intrinsics* K) {
   return guarded(c, [&] { return pmx_impl_constrain_to_rays(c, mem, height, width, xyz, valid, K); });
+}
+
+int pmx_graph_prepare(pmx_context* c, pmx_memory mem, const pmx_graph* g, const pmx_backend_params* p, int32_t e0,
+                      int32_t e1, pmx_prepared_graph** out) {
+  return guarded(c, [&] { return pmx_impl_graph_prepare(c, mem, g, p, e0, e1, out); });
+}
+int pmx_graph_edge_terms(pmx_context* c, pmx_prepared_graph* pg, const pmx_sim3* poses, double* out) {
+  return guarded(c, [&] { return pmx_impl_graph_edge_terms(c, pg, poses, out); });
+}
+int pmx_graph_solve(pmx_context* c, pmx_prepared_graph* pg, const pmx_sim3* poses, const double* terms, double* tau,
+                    double* cost, int32_t* solved) {
+  return guarded(c, [&] { return pmx_impl_graph_solve(c, pg, poses, terms, tau, cost, solved); });
+}
+int pmx_graph_release(pmx_context* c, pmx_prepared_graph* pg) {
+  return guarded(c, [&] { return pmx_impl_graph_release(c, pg); });
 }
 
 int pmx_match_stats(pmx_context* c, pmx_memory mem, const pmx_matchset* m, int32_t num_pixels_a,

@@ -977,6 +977,7 @@ struct DevGraph {
   std::vector<CloudDev> hclouds;
   std::vector<MatchesDev> hmatches;
   int64_t max_count = 0;
+  std::vector<DevBuf> staged;  // host-staged inputs kept alive by a prepared graph
   // ray mode: frozen-match preprocessing
   bool packed = false;
   DevBuf c4buf, c4ptrs, pk, pk_cnt, pk_total;
@@ -1689,6 +1690,111 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
   }
   result->converged = 1;  // backend.cpp:244, 250, 254
   for (int k = 0; k < n; ++k) g->poses[k] = to_pmx(P[k]);
+  return PMX_OK;
+}
+
+// ------------------------------------------------------- prepared graph
+// A graph staged once (canonicals packed, the edge range's frozen matches
+// compacted, the solver's frontal plan built) for repeated per-iteration
+// calls at changing poses: the building blocks of the edge-sharded backend
+// (one process per GPU: edge terms of the rank's edges -> NCCL reduce ->
+// rank 0 solve -> broadcast of tau), without re-staging every iteration.
+namespace pmx {
+struct PreparedGraph {
+  DevGraph G;
+  pmx_backend_params p;
+  EdgeWork W;
+  Assembly As;
+  int e0 = 0, e1 = 0;
+  DevBuf terms, dP, dst;
+};
+}  // namespace pmx
+
+extern "C" int pmx_impl_graph_prepare(pmx_context* c, pmx_memory mem, const pmx_graph* g,
+                                      const pmx_backend_params* pp, int32_t e0, int32_t e1,
+                                      pmx_prepared_graph** out) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(g && out && e0 >= 0 && e1 >= e0 && e1 <= g->num_edges, "graph_prepare: bad arguments");
+  auto* pg = new PreparedGraph();
+  try {
+    pg->p = backend_params(pp);
+    pg->e0 = e0;
+    pg->e1 = e1;
+    Stager st(ctx, mem);
+    stage_graph(ctx, st, g, pg->p, pg->G);
+    // host-staged inputs must outlive the handle: keep the staging buffers
+    pg->G.staged = std::move(st.bufs);
+    make_edge_work(ctx, pg->G, pg->p, pg->W);
+    build_assembly(ctx, pg->G, pg->As);
+    const int E = std::max(pg->G.E, 1), N = std::max(pg->G.N, 1);
+    pg->terms = DevBuf(sizeof(double) * PMX_EDGE_TERMS * (size_t)E, ctx.stream);
+    pg->dP = DevBuf(sizeof(DSim3) * N, ctx.stream);
+    pg->dst = DevBuf(sizeof(GNState), ctx.stream);
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  } catch (...) {
+    delete pg;
+    throw;
+  }
+  *out = reinterpret_cast<pmx_prepared_graph*>(pg);
+  return PMX_OK;
+}
+
+static void upload_poses(Context& ctx, pmx::PreparedGraph& pg, const pmx_sim3* poses) {
+  std::vector<DSim3> P(pg.G.N);
+  for (int k = 0; k < pg.G.N; ++k) {
+    require(poses[k].s > 0.0, "Sim3Pose: scale must be positive");
+    P[k] = to_dsim3(poses[k]);
+  }
+  if (pg.G.N)
+    PMX_CUDA(cudaMemcpyAsync(pg.dP.p, P.data(), sizeof(DSim3) * pg.G.N, cudaMemcpyHostToDevice, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // P host vector lifetime
+}
+
+extern "C" int pmx_impl_graph_edge_terms(pmx_context* c, pmx_prepared_graph* h, const pmx_sim3* poses, double* out) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(h && poses && out, "graph_edge_terms: null arguments");
+  PreparedGraph& pg = *reinterpret_cast<PreparedGraph*>(h);
+  upload_poses(ctx, pg, poses);
+  edge_terms_dev(ctx, pg.G, pg.p, pg.W, pg.dP.as<DSim3>(), pg.e0, pg.e1, pg.terms.as<double>());
+  const size_t cnt = (size_t)(pg.e1 - pg.e0) * PMX_EDGE_TERMS;
+  if (cnt)
+    PMX_CUDA(cudaMemcpyAsync(out, pg.terms.as<double>() + (size_t)pg.e0 * PMX_EDGE_TERMS, sizeof(double) * cnt,
+                             cudaMemcpyDeviceToDevice, ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_graph_solve(pmx_context* c, pmx_prepared_graph* h, const pmx_sim3* poses,
+                                    const double* terms, double* tau, double* cost, int32_t* solved) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(h && poses && terms && tau && cost && solved, "graph_solve: null arguments");
+  PreparedGraph& pg = *reinterpret_cast<PreparedGraph*>(h);
+  upload_poses(ctx, pg, poses);
+  *cost = read_cost(ctx, pg.G, terms);
+  if (pg.As.sky_ok) {
+    PMX_CUDA(cudaMemsetAsync(pg.dst.p, 0, sizeof(GNState), ctx.stream));
+    assemble_sky(ctx, pg.G, pg.As, pg.dP.as<DSim3>(), terms, 0, nullptr);
+    solve_sky(ctx, pg.p, pg.As, pg.dst.as<GNState>(), tau);
+    GNState hs;
+    PMX_CUDA(cudaMemcpyAsync(&hs, pg.dst.p, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    *solved = hs.solved;
+  } else {
+    std::vector<DSim3> P(pg.G.N);
+    for (int k = 0; k < pg.G.N; ++k) P[k] = to_dsim3(poses[k]);
+    assemble(ctx, pg.G, pg.As, P, terms);
+    std::vector<double> t;
+    *solved = damped_solve(ctx, pg.p, pg.As, t) ? 1 : 0;
+    PMX_CUDA(cudaMemcpy(tau, t.data(), sizeof(double) * t.size(), cudaMemcpyHostToDevice));
+  }
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_graph_release(pmx_context* c, pmx_prepared_graph* h) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  if (h) {
+    PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    delete reinterpret_cast<PreparedGraph*>(h);
+  }
   return PMX_OK;
 }
 

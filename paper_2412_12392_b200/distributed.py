@@ -150,3 +150,26 @@ def gpu_callbacks(ctx, graph, params):
         return c
 
     return terms_fn, solve_fn, cost_fn
+
+
+def gpu_prepared_callbacks(ctx, graph, params, begin: int, end: int, rank: int = 0):
+    """Bind the sharded driver to a prepared graph (pmx_graph_prepare): the
+    rank's edges [begin, end) are staged and compacted once; every iteration
+    is then edge terms on the device -> NCCL reduce -> rank 0 solve on the
+    device (frontal plan built once) -> broadcast, with no re-staging.
+    Rank 0 needs the full topology (all edges, any match sets)."""
+    pg = ctx.prepare_graph(graph, params, begin, end)
+
+    def terms_fn(e0, e1, P):
+        assert (e0, e1) == (begin, end), "prepared range mismatch"
+        return pg.edge_terms(list(P))
+
+    def solve_fn(terms, P):
+        tau, _cost, solved = pg.solve(list(P), terms.contiguous())
+        return tau.cpu().numpy(), solved
+
+    def cost_fn(terms):
+        t = terms.detach().cpu().numpy()
+        return float(np.sum(t[:, 35]) + np.sum(t[:, 71])) if t.size else 0.0
+
+    return terms_fn, solve_fn, cost_fn, pg

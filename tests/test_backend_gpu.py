@@ -147,3 +147,50 @@ def test_solve_terms_equals_global_step(ctx):
     H, grad = ctx.assemble_system(G, p)
     np.testing.assert_allclose(tau, np.linalg.solve(H, -grad), rtol=1e-6, atol=1e-10)
     assert abs(cost - ctx.backend_cost(G, p)) <= 1e-12 * cost
+
+
+def test_prepared_graph_matches_stateless_entry_points(ctx):
+    # pmx_graph_prepare: staged once, then terms / solve at changing poses
+    import torch
+    g, G, O = _graph()
+    p = _params()
+    pg = ctx.prepare_graph(G, p)
+    t_pg = pg.edge_terms(G.poses).cpu().numpy()
+    np.testing.assert_allclose(t_pg, ctx.backend_edge_terms(G, p), rtol=0, atol=0)
+    tau, cost, solved = pg.solve(G.poses, torch.from_numpy(t_pg).cuda())
+    tau_ref, cost_ref, solved_ref = ctx.backend_solve_terms(G, t_pg, p)
+    assert solved and solved_ref and cost == cost_ref
+    np.testing.assert_allclose(tau.cpu().numpy(), tau_ref, rtol=1e-9, atol=1e-12)
+    # a sub-range of edges only stages / compacts its own edges
+    half = len(g["edges"]) // 2
+    pg2 = ctx.prepare_graph(G, p, half, len(g["edges"]))
+    np.testing.assert_array_equal(pg2.edge_terms(G.poses).cpu().numpy(), t_pg[half:])
+    pg.release()
+    pg2.release()
+
+
+def test_sharded_driver_single_rank_nccl_matches_global_optimize(ctx):
+    # the edge-sharded loop (distributed.py) on one rank over NCCL, with the
+    # prepared-graph callbacks, converges to the device loop's poses
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2412_12392_b200 import distributed
+    g, G, O = _graph(n_kf=10, reach=3)
+    p = _params()
+    init = [abi.pmx_sim3.from_buffer_copy(T) for T in G.poses]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        terms_fn, solve_fn, cost_fn, pg = distributed.gpu_prepared_callbacks(ctx, G, p, 0, len(g["edges"]))
+        res = distributed.global_optimize_sharded(init, len(g["edges"]), 0, p, terms_fn, solve_fn, cost_fn,
+                                                  torch_device=torch.device("cuda", 0))
+        pg.release()
+    finally:
+        dist.destroy_process_group()
+    r = ctx.global_optimize(G, p)
+    assert res.converged == r.converged
+    for a, b in zip(res.poses, G.poses):
+        assert np.abs(np.array(a.t[:]) - np.array(b.t[:])).max() < 1e-7
+        assert np.abs(np.array(a.R[:]) - np.array(b.R[:])).max() < 1e-7
