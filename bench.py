@@ -237,6 +237,53 @@ def bench_backend(ctx, dev, cpu: bool, n_kf=100, reach=4, loops=1, iters=10, con
     return out
 
 
+def bench_backend_sharded(ctx, dev, rank, world, iters=5):
+    """BASELINE config 4 sharded across the job's GPUs (--backend-sharded):
+    each rank generates and stages only its edges' matches (prepared graph),
+    every GN iteration is edge terms -> one NCCL reduce of the E x 72 terms
+    -> rank 0 solve -> broadcast.  Per-iteration time split into
+    accumulation / communication / solve, max over ranks."""
+    import torch
+    import torch.distributed as tdist
+    import pmxgen
+    from paper_2412_12392_b200 import Graph, MatchSet, Pointmap, abi, distributed
+    n_kf, reach, loops = 1000, 5, 3
+    E = len(pmxgen.loop_edges(n_kf, reach))
+    e0, e1 = distributed.shard_range(E, rank, world)
+    g = pmxgen.backend_graph(n_kf, reach, 3, loops=loops, edge_range=(e0, e1))
+    T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    cans = [Pointmap(T(x), T(v), H, W) for x, v in g["canonicals"]]
+    ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["matches"]]
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    p.max_iterations = iters
+    init = [P.to_struct(abi.pmx_sim3) for P in g["init"]]
+    G = Graph(cans, list(init), g["edges"], ms)
+    terms_fn, solve_fn, cost_fn, pg = distributed.gpu_prepared_callbacks(ctx, G, p, e0, e1)
+    distributed.global_optimize_sharded(init, E, 0, p, terms_fn, solve_fn, cost_fn, torch_device=dev)  # warm-up
+    tdist.barrier()
+    timers = {}
+    t0 = time.perf_counter()
+    res = distributed.global_optimize_sharded(init, E, 0, p, terms_fn, solve_fn, cost_fn, torch_device=dev,
+                                              timers=timers)
+    torch.cuda.synchronize()
+    total = time.perf_counter() - t0
+    pg.release()
+    vals = torch.tensor([total, timers.get("accumulate", 0.0), timers.get("communication", 0.0),
+                         timers.get("solve", 0.0)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(vals, op=tdist.ReduceOp.MAX)
+    total, acc, comm, solve = (float(v) for v in vals.cpu())
+    it = max(1, res.iterations)
+    err = max(float(np.abs(np.array(P.t[:]) - Q.t).max()) for P, Q in zip(res.poses, g["gt"]))
+    return {"metric": f"global GN iteration ms at N={n_kf} (edge-sharded)", "value": 1e3 * total / it, "unit": "ms",
+            "higher_is_better": False, "n_gpus": world, "scaling": "strong",
+            "config": {"workload": f"config4: {n_kf} keyframes, loop x{loops}, {E} edges, {iters} GN iterations, "
+                                   f"edges sharded {e1 - e0} per rank, NCCL reduce + broadcast per iteration",
+                       "iterations_run": res.iterations, "converged": res.converged, "max_translation_error_m": err},
+            "breakdown_ms_per_iteration": {"accumulate": 1e3 * acc / (it + 1), "communication": 1e3 * comm / it,
+                                           "solve_rank0": 1e3 * solve / it}}
+
+
 def bench_tracking(ctx, dev):
     """BASELINE config 1: 10 GN iterations on one Sim(3) over 196,608 matches
     (10% outliers) + confidence-weighted fusion."""
@@ -301,9 +348,11 @@ def run_pmx(args):
     rank, world, local = _dist()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or args.backend_sharded:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29511")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", local))
     mine = edge_shard(rank, world)
     sc, poses, edges, make_pair = pmxgen.config2(seed=2)
     host_pairs = [make_pair(e) for e in mine]
@@ -371,6 +420,12 @@ def run_pmx(args):
         ms_max = ms_local
     px_total = N_EDGES * H * W  # all ranks
     value = px_total * args.steps / (ms_max / 1e3)
+
+    sharded = None
+    if args.backend_sharded and dist:  # every rank takes part (collectives)
+        del dev_pairs, batch
+        torch.cuda.empty_cache()
+        sharded = bench_backend_sharded(ctx, dev, rank, world)
 
     # e2e through the public API with host (pinned) buffers: H2D inputs, D2H results
     host_structs = [structs(p, lambda a: to_dev(a, pinned=True)) for p in host_pairs]
@@ -451,6 +506,8 @@ def run_pmx(args):
             "gpu_launches": gpu_launches,
             "clocks": clocks,
         }
+        if sharded is not None:
+            line["secondary"] = [sharded]
         if world == 1 and not args.no_secondary:
             line["secondary"] = [bench_backend(ctx, dev, cpu=not args.no_cpu), bench_tracking(ctx, dev)]
             torch.cuda.empty_cache()
@@ -470,6 +527,8 @@ def main():
     ap.add_argument("--impl", choices=["pmx", "reference"], default="pmx")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
     ap.add_argument("--no-secondary", action="store_true", help="skip the config-3 / config-1 secondary lines")
+    ap.add_argument("--backend-sharded", action="store_true",
+                    help="also run config 4 edge-sharded over the job's GPUs (NCCL reduce + broadcast)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -293,7 +293,7 @@ def gt_from_cameras(ca: "Camera", cb: "Camera"):
 
 def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: int = 1,
                   radius: float = 5.0, rot_deg=2.0, trans=0.05, scale_frac=0.03,
-                  edges=None):
+                  edges=None, edge_range=None):
     """Configs 3/4: GT loop poses, canonical pointmaps (own view + noise),
     edges with ground-truth matches (pixel_a in i, pixel_b in j, dense), and
     perturbed initial poses (anchor = keyframe 0, unperturbed)."""
@@ -302,7 +302,10 @@ def backend_graph(n_kf: int, reach: int, seed: int, height=H, width=W, loops: in
     cams = [Camera(sc, k, gt[k]) for k in range(n_kf)]
     canon = [(c.express(c.T, 1000 + k), c.valid) for k, c in enumerate(cams)]
     edges = edges if edges is not None else loop_edges(n_kf, reach)
-    matches = [gt_from_cameras(cams[i], cams[j]) for (i, j) in edges]
+    e0, e1 = edge_range if edge_range is not None else (0, len(edges))
+    empty = {"pixel_a": np.empty(0, np.int32), "confidence": np.empty(0, np.float32), "valid": np.empty(0, np.uint8)}
+    # edge_range: only these edges' matches (one rank's shard); the others are empty
+    matches = [gt_from_cameras(cams[i], cams[j]) if e0 <= e < e1 else empty for e, (i, j) in enumerate(edges)]
     init = [gt[0]] + [perturb_pose(gt[k], seed, 5000 + 3 * k, rot_deg, trans, scale_frac)
                       for k in range(1, n_kf)]
     return {"scene": sc, "gt": gt, "init": init, "canonicals": canon, "edges": edges,

@@ -58,13 +58,16 @@ class ShardedResult:
 
 def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params: abi.pmx_backend_params,
                             terms_fn: Callable, solve_fn: Callable, cost_fn: Callable, torch_device=None,
-                            group=None) -> ShardedResult:
+                            group=None, timers: dict | None = None) -> ShardedResult:
     """global_optimize (backend.cpp:192-256) with edge-sharded accumulation.
 
     terms_fn(e0, e1, poses) -> (e1-e0, 72) FP64 tensor/array of this rank's edges
     solve_fn(terms, poses)  -> (tau[7N] np.ndarray, solved: bool)      (rank 0)
     cost_fn(terms)          -> float, directed-constraint costs summed in edge order (rank 0)
+    timers                  -> optional dict accumulating seconds per phase ("accumulate",
+                               "communication", "solve"), device-synchronised at phase ends
     """
+    import time as _time
     import torch
     import torch.distributed as dist
 
@@ -78,18 +81,34 @@ def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params
     dev = torch_device if torch_device is not None else torch.device("cpu")
     e0, e1 = shard_range(num_edges, rank, world)
 
+    def sync():
+        if dev.type == "cuda":
+            torch.cuda.synchronize(dev)
+
+    def tick(phase, t0):
+        if timers is not None:
+            sync()
+            timers[phase] = timers.get(phase, 0.0) + _time.perf_counter() - t0
+        return _time.perf_counter()
+
     def reduce_terms(P):
+        t0 = _time.perf_counter()
         full = torch.zeros((num_edges, TERMS), dtype=torch.float64, device=dev)
         if e1 > e0:
             local = terms_fn(e0, e1, P)
             full[e0:e1] = torch.as_tensor(local, dtype=torch.float64, device=dev)
+        t0 = tick("accumulate", t0)
         dist.reduce(full, dst=0, group=group)
+        tick("communication", t0)
         return full
 
     def bcast(vec: np.ndarray) -> np.ndarray:
+        t0 = _time.perf_counter()
         t = torch.as_tensor(vec, dtype=torch.float64, device=dev).clone()
         dist.broadcast(t, src=0, group=group)
-        return t.cpu().numpy()
+        out = t.cpu().numpy()
+        tick("communication", t0)
+        return out
 
     terms = reduce_terms(P)
     cost = cost_fn(terms) if rank == 0 else 0.0
@@ -98,7 +117,9 @@ def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params
         res.iterations += 1
         msg = np.zeros(1 + 7 * n)
         if rank == 0:
+            t0 = _time.perf_counter()
             tau, solved = solve_fn(terms, P)
+            tick("solve", t0)
             msg[0] = 1.0 if solved else 0.0
             msg[1:] = tau
         msg = bcast(msg)
