@@ -831,6 +831,8 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   if (tid == 0 && good) P.st->solved = 1;
 }
 
+#include "band.cuh"
+
 // ----------------------------------------------------- device control loop
 // Ad(T_k^-1) of every keyframe (backend.cpp:114).
 __global__ void k_adjoint(const DSim3* __restrict__ P, int N, double* __restrict__ adj, const GNState* st) {
@@ -874,9 +876,47 @@ __global__ void k_sky_grad(const int* __restrict__ g_ptr, const int* __restrict_
   }
   if (k == anchor) {  // (a, a) = I, g_a = 0
     sacc = 0.0;
-    for (int c = 0; c <= r; ++c) H[sky_at(rowptr, first, 7 * k + r, 7 * k + c)] = (c == r) ? 1.0 : 0.0;
+    if (H)
+      for (int c = 0; c <= r; ++c) H[sky_at(rowptr, first, 7 * k + r, 7 * k + c)] = (c == r) ? 1.0 : 0.0;
   }
   grad[7 * k + r] = sacc;
+}
+
+// Band (block-tridiagonal) assembly: lower-triangle 7x7 blocks of the gauge-
+// fixed system into the super-blocks of the RCM order (kf_pos: keyframe ->
+// position, m keyframes per super-block of w = 7m unknowns).
+__global__ void k_band_assemble(const int* __restrict__ blk_rc, const int* __restrict__ blk_ptr,
+                                const int* __restrict__ contrib, const double* __restrict__ S,
+                                const int* __restrict__ kf_pos, int m, double* __restrict__ D0,
+                                double* __restrict__ L0, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int b = blockIdx.x, tid = threadIdx.x;
+  if (tid >= 49) return;
+  const int pk = kf_pos[blk_rc[2 * b]], pl = kf_pos[blk_rc[2 * b + 1]];
+  const int sk = pk / m, sl = pl / m, w = 7 * m;
+  double* dst;
+  if (sk == sl)
+    dst = D0 + (size_t)sk * w * w;
+  else if (sk == sl + 1)
+    dst = L0 + (size_t)sk * w * w;  // L0[s] = A(s, s-1)
+  else
+    return;  // the upper coupling (transpose of a stored one)
+  double sacc = 0.0;
+  for (int q = blk_ptr[b]; q < blk_ptr[b + 1]; ++q) {
+    const int cc = contrib[q];
+    const double v = S[(size_t)(cc >> 1) * 49 + tid];
+    sacc += (cc & 1) ? -v : v;
+  }
+  dst[(size_t)((pk % m) * 7 + tid / 7) * w + (pl % m) * 7 + tid % 7] = sacc;
+}
+
+__global__ void k_band_rhs(const double* __restrict__ grad, const int* __restrict__ kf_pos, int N,
+                           double* __restrict__ b0, const GNState* st) {
+  if (gn_stopped(st)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 7 * N) return;
+  const int pos = kf_pos[i / 7];
+  if (pos >= 0) b0[(size_t)pos * 7 + i % 7] = -grad[i];
 }
 
 // Deterministic block sum (fixed tree; blockDim a power of two <= 1024).
@@ -1217,6 +1257,10 @@ struct Assembly {
   long long nnz = 0;
   DevBuf first, rowptr, rp_ptr, rp_rows, skyH;
   DevBuf trip, pinfo, rinfo, slot, lofs, Lst, Dst;  // frontal factorisation plan
+  // band plan (preferred when the RCM bandwidth is small): block cyclic reduction
+  bool band_ok = false;
+  int band_m = 0, band_w = 0, band_S = 0, band_npad = 0;
+  DevBuf kf_pos, bD0, bL0, bb0, bD, bL, bb, bY, by, bx, bstatus;
 };
 
 // Contribution lists (edge order) for every non-zero block, gauge-fixed.
@@ -1259,7 +1303,96 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
   up(As.contrib, con);
   up(As.g_ptr, gp);
   up(As.g_contrib, gc);
-  {  // envelope of the gauge-fixed system: first non-zero block column of every block row
+  {  // band plan: reverse Cuthill-McKee order of the non-anchor keyframes
+    std::vector<std::vector<int>> adj(N);
+    for (auto& kv : blocks)
+      if (kv.first.first != kv.first.second) adj[kv.first.first].push_back(kv.first.second);
+    std::vector<int> order, deg(N), pos(N, -1);
+    for (int k = 0; k < N; ++k) deg[k] = (int)adj[k].size();
+    for (int k = 0; k < N; ++k) std::sort(adj[k].begin(), adj[k].end(), [&](int a, int c) { return deg[a] < deg[c]; });
+    std::vector<char> seen(N, 0);
+    auto bfs = [&](int s0, std::vector<int>& out) {  // Cuthill-McKee from s0 (one component)
+      std::vector<int> q{s0};
+      seen[s0] = 1;
+      for (size_t h = 0; h < q.size(); ++h)
+        for (int v : adj[q[h]])
+          if (!seen[v]) {
+            seen[v] = 1;
+            q.push_back(v);
+          }
+      out.insert(out.end(), q.begin(), q.end());
+      return q.back();
+    };
+    for (;;) {  // every component, from a pseudo-peripheral node
+      int s0 = -1;
+      for (int k = 0; k < N; ++k)
+        if (k != G.anchor && !seen[k] && (s0 < 0 || deg[k] < deg[s0])) s0 = k;
+      if (s0 < 0) break;
+      std::vector<int> probe;
+      std::vector<char> keep = seen;
+      const int far = bfs(s0, probe);  // restart from the far end of the first sweep
+      seen = keep;
+      bfs(far, order);
+    }
+    std::reverse(order.begin(), order.end());
+    // candidates: RCM, the keyframe order, and the keyframe order folded from
+    // both ends (a trajectory closing a loop on its start: bandwidth 2 x reach);
+    // the smallest bandwidth wins
+    std::vector<int> natural, folded;
+    for (int k = 0; k < N; ++k)
+      if (k != G.anchor) natural.push_back(k);
+    for (size_t lo = 0, hi = natural.size(); lo < hi;) {
+      folded.push_back(natural[lo++]);
+      if (lo < hi) folded.push_back(natural[--hi]);
+    }
+    auto bandwidth = [&](const std::vector<int>& ord) {
+      std::vector<int> ps(N, -1);
+      for (size_t i = 0; i < ord.size(); ++i) ps[ord[i]] = (int)i;
+      int bwv = 1;
+      for (auto& kv : blocks)
+        if (ps[kv.first.first] >= 0 && ps[kv.first.second] >= 0)
+          bwv = std::max(bwv, std::abs(ps[kv.first.first] - ps[kv.first.second]));
+      return bwv;
+    };
+    int bw = bandwidth(order);
+    for (const auto* cand : {&natural, &folded})
+      if (cand->size() == order.size()) {
+        const int bc = bandwidth(*cand);
+        if (bc < bw) {
+          bw = bc;
+          order = *cand;
+        }
+      }
+    for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
+    const int nf = (int)order.size(), m = bw, w = 7 * m;
+    const int S = nf > 0 ? (nf + m - 1) / m : 0;
+    // cost model (measured on B200): the frontal form walks ~7 us per keyframe
+    // panel; the cyclic reduction ~250 us per level (latency of the per-block
+    // dense kernels) + 200 us
+    int levels = 0;
+    while ((1 << levels) < S) ++levels;
+    As.band_ok = nf > 0 && w <= kBandMaxW && S >= 2 && 7.0 * nf > 250.0 * levels + 200.0;
+    if (As.band_ok) {
+      As.band_m = m;
+      As.band_w = w;
+      As.band_S = S;
+      As.band_npad = 7 * (S * m - nf);
+      up(As.kf_pos, pos);
+      const size_t bb = sizeof(double) * (size_t)S * w * w, bv = sizeof(double) * (size_t)S * w;
+      As.bD0 = DevBuf(bb, ctx.stream);
+      As.bL0 = DevBuf(bb, ctx.stream);
+      As.bD = DevBuf(bb, ctx.stream);
+      As.bL = DevBuf(bb, ctx.stream);
+      As.bY = DevBuf(2 * bb, ctx.stream);
+      As.bb0 = DevBuf(bv, ctx.stream);
+      As.bb = DevBuf(bv, ctx.stream);
+      As.by = DevBuf(bv, ctx.stream);
+      As.bx = DevBuf(bv, ctx.stream);
+      As.bstatus = DevBuf(sizeof(int), ctx.stream);
+      PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+    }
+  }
+  if (!As.band_ok) {  // envelope of the gauge-fixed system: first non-zero block column of every block row
     std::vector<int> fb(N);
     for (int k = 0; k < N; ++k) fb[k] = k;
     for (auto& kv : blocks)
@@ -1316,7 +1449,7 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
       live.swap(keep);
     }
     fits = fits && lsize < INT32_MAX;
-    As.sky_ok = fits && N > 0;
+    As.sky_ok = fits && N > 0;  // device path: band plan, else the frontal one
     if (As.sky_ok) {
       As.nnz = nnz;
       up(As.first, first);
@@ -1344,6 +1477,7 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
   As.adj =DevBuf(sizeof(double) * 49 * std::max(N, 1), ctx.stream);
   As.S = DevBuf(sizeof(double) * 49 * std::max(G.E, 1), ctx.stream);
   As.G = DevBuf(sizeof(double) * 7 * std::max(G.E, 1), ctx.stream);
+  if (As.band_ok) As.sky_ok = true;
   if (!As.sky_ok) As.H = DevBuf(sizeof(double) * (size_t)As.dim * As.dim, ctx.stream);  // dense path
   As.grad = DevBuf(sizeof(double) * std::max(As.dim, 1), ctx.stream);
   PMX_CUDA(cudaStreamSynchronize(ctx.stream));  // host vectors lifetime
@@ -1431,6 +1565,24 @@ static void assemble_sky(Context& ctx, const DevGraph& G, Assembly& As, const DS
                                              As.S.as<double>(), As.G.as<double>());
     launch_check(ctx, "k_edge_blocks");
   }
+  if (As.band_ok) {
+    PMX_CUDA(cudaMemsetAsync(As.bD0.p, 0, As.bD0.bytes, ctx.stream));
+    PMX_CUDA(cudaMemsetAsync(As.bL0.p, 0, As.bL0.bytes, ctx.stream));
+    PMX_CUDA(cudaMemsetAsync(As.bb0.p, 0, As.bb0.bytes, ctx.stream));
+    if (As.nblocks) {
+      k_band_assemble<<<As.nblocks, 64, 0, ctx.stream>>>(As.blk_rc.as<int>(), As.blk_ptr.as<int>(), As.contrib.as<int>(),
+                                                         As.S.as<double>(), As.kf_pos.as<int>(), As.band_m,
+                                                         As.bD0.as<double>(), As.bL0.as<double>(), st);
+      launch_check(ctx, "k_band_assemble");
+    }
+    k_sky_grad<<<G.N, 32, 0, ctx.stream>>>(As.g_ptr.as<int>(), As.g_contrib.as<int>(), As.G.as<double>(), G.N,
+                                           G.anchor, As.grad.as<double>(), nullptr, nullptr, nullptr, st);
+    launch_check(ctx, "k_sky_grad");
+    k_band_rhs<<<(7 * G.N + 255) / 256, 256, 0, ctx.stream>>>(As.grad.as<double>(), As.kf_pos.as<int>(), G.N,
+                                                              As.bb0.as<double>(), st);
+    launch_check(ctx, "k_band_rhs");
+    return;
+  }
   PMX_CUDA(cudaMemsetAsync(As.skyH.p, 0, As.skyH.bytes, ctx.stream));
   if (As.nblocks) {
     k_sky_assemble<<<As.nblocks, 64, 0, ctx.stream>>>(As.blk_rc.as<int>(), As.blk_ptr.as<int>(), As.contrib.as<int>(),
@@ -1446,7 +1598,43 @@ static void assemble_sky(Context& ctx, const DevGraph& G, Assembly& As, const DS
 
 // Damping attempts (backend.cpp:208-227) on the device: attempt a runs only
 // while no earlier one succeeded (st->solved).
+// Block cyclic reduction (band plan), attempts on the device.
+static void solve_band(Context& ctx, const pmx_backend_params& p, Assembly& As, GNState* st, double* tau) {
+  const int S = As.band_S, w = As.band_w;
+  BandArgs a{As.bD0.as<double>(), As.bL0.as<double>(), As.bb0.as<double>(), As.bD.as<double>(), As.bL.as<double>(),
+             As.bb.as<double>(), As.bY.as<double>(), As.by.as<double>(), As.bx.as<double>(), S, w, As.band_npad,
+             As.bstatus.as<int>(), st};
+  const size_t sm_elim = sizeof(double) * ((size_t)w * w + (size_t)w * (2 * w + 1) + 8 * w);
+  const size_t sm_upd = sizeof(double) * 4 * (size_t)w * w;
+  const size_t sm_top = sizeof(double) * ((size_t)w * w + 9 * w);
+  PMX_CUDA(cudaFuncSetAttribute((const void*)k_bcr_eliminate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sm_elim));
+  PMX_CUDA(cudaFuncSetAttribute((const void*)k_bcr_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_upd));
+  PMX_CUDA(cudaFuncSetAttribute((const void*)k_bcr_top, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_top));
+  for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
+    ProfScope ps(ctx, "k_ldlt");
+    k_bcr_init<<<2 * ctx.num_sms, 256, 0, ctx.stream>>>(a, attempt, p.damping_init);
+    int s = 1;
+    for (; s < S; s *= 2) {
+      const int nodd = (S - s + 2 * s - 1) / (2 * s), neven = (S + 2 * s - 1) / (2 * s);
+      if (nodd > 0) k_bcr_eliminate<<<nodd, kBandThreads, sm_elim, ctx.stream>>>(a, s);
+      k_bcr_update<<<neven, kBandThreads, sm_upd, ctx.stream>>>(a, s);
+    }
+    k_bcr_top<<<1, kBandThreads, sm_top, ctx.stream>>>(a);
+    for (s /= 2; s >= 1; s /= 2) {
+      const int nodd = (S - s + 2 * s - 1) / (2 * s);
+      if (nodd > 0) k_bcr_back<<<nodd, kBandThreads, 0, ctx.stream>>>(a, s);
+    }
+    k_bcr_finish<<<1, 1024, 0, ctx.stream>>>(a, As.kf_pos.as<int>(), As.dim / 7, tau);
+    launch_check(ctx, "k_bcr");
+  }
+}
+
 static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, GNState* st, double* tau) {
+  if (As.band_ok) {
+    solve_band(ctx, p, As, st, tau);
+    return;
+  }
   const int n = As.dim;
   const int npanel = (n + kPW - 1) / kPW;
   const size_t smem = sizeof(double) * ((size_t)kFront * kFront + n + 2 * kFront * kPW) +
