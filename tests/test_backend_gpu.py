@@ -194,3 +194,18 @@ def test_sharded_driver_single_rank_nccl_matches_global_optimize(ctx):
     for a, b in zip(res.poses, G.poses):
         assert np.abs(np.array(a.t[:]) - np.array(b.t[:])).max() < 1e-7
         assert np.abs(np.array(a.R[:]) - np.array(b.R[:])).max() < 1e-7
+
+
+def test_banded_solver_matches_dense_solve(ctx):
+    # a long ring of keyframes takes the banded form of K9 (folded order +
+    # block cyclic reduction): its step equals the dense solve of the system
+    g, G, O = _graph(n_kf=400, reach=2, h=12, w=16)
+    p = _params()
+    terms = ctx.backend_edge_terms(G, p)
+    tau, cost, solved = ctx.backend_solve_terms(G, terms, p)
+    assert solved
+    H, grad = ctx.assemble_system(G, p)
+    ref = np.linalg.solve(H, -grad)
+    np.testing.assert_allclose(tau, ref, rtol=1e-6, atol=1e-9 * np.abs(ref).max())
+    r = ctx.global_optimize(G, p)
+    assert r.converged and r.iterations >= 1
