@@ -203,8 +203,7 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
 }
 
 // Both directed constraints of one compacted match.
-__device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<double>& T2,
-                                          const PoseR<float>& T1f, const PoseR<float>& T2f, const int4 m,
+__device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<double>& T2, const int4 m,
                                           const float4 Pi, const float4 Pj, float inv_s2, const RayW& c,
                                           float* acc) {
   const float pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
@@ -212,13 +211,11 @@ __device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<d
   const float info = __int_as_float(m.z) * inv_s2;
   if (Pi.w >= 1e-24f) {  // ref = i; |ref| < 1e-12 (or NaN) skips the row (tracking.cpp:78)
     const float ii = rsqrt_nr(Pi.w);
-    const double rr = fma(di[0], di[0], fma(di[1], di[1], di[2] * di[2]));
-    ray_accumulate(T1, T1f, di, rr, Pi.w * ii, ii, pi, dj, pj, info, c, acc);  // ref = i, src = j (swapped)
+    ray_accumulate(T1, di, Pi.w * ii, ii, pi, dj, info, c, acc);  // ref = i, src = j (swapped)
   }
   if (Pj.w >= 1e-24f) {
     const float ij = rsqrt_nr(Pj.w);
-    const double rr = fma(dj[0], dj[0], fma(dj[1], dj[1], dj[2] * dj[2]));
-    ray_accumulate(T2, T2f, dj, rr, Pj.w * ij, ij, pj, di, pi, info, c, acc + kRayAcc);  // ref = j, src = i
+    ray_accumulate(T2, dj, Pj.w * ij, ij, pj, di, info, c, acc + kRayAcc);  // ref = j, src = i
   }
 }
 
@@ -238,7 +235,6 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
     const int4* __restrict__ P = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
     const PoseR<double> T1 = A.rel64[2 * e], T2 = A.rel64[2 * e + 1];
-    const PoseR<float> T1f = A.rel[2 * e], T2f = A.rel[2 * e + 1];
     const float inv_s2 = (float)(1.0 / A.wp.sigma2);
     const RayW c{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta),
                  (float)A.wp.distance_weight};
@@ -248,12 +244,12 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
       const int4 m0 = __ldg(P + k), m1 = __ldg(P + k + stride);
       const float4 a0 = __ldg(Ci + m0.x), b0 = __ldg(Cj + m0.y);
       const float4 a1 = __ldg(Ci + m1.x), b1 = __ldg(Cj + m1.y);
-      ray_match(T1, T2, T1f, T2f, m0, a0, b0, inv_s2, c, acc);
-      ray_match(T1, T2, T1f, T2f, m1, a1, b1, inv_s2, c, acc);
+      ray_match(T1, T2, m0, a0, b0, inv_s2, c, acc);
+      ray_match(T1, T2, m1, a1, b1, inv_s2, c, acc);
     }
     if (k < cnt) {
       const int4 m0 = __ldg(P + k);
-      ray_match(T1, T2, T1f, T2f, m0, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
+      ray_match(T1, T2, m0, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
     }
   }
   block_reduce_n<2 * kRayAcc>(acc, A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
@@ -1176,9 +1172,11 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   const int E = std::max(G.E, 1);
   W.rel = DevBuf(sizeof(PoseR<float>) * 2 * (size_t)E, ctx.stream);
   W.rel64 = DevBuf(sizeof(PoseR<double>) * 2 * (size_t)E, ctx.stream);
-  // about two waves of 2 resident blocks per SM, >= 16 matches per thread
-  const int64_t want = (2LL * 2 * ctx.num_sms + G.E - 1) / std::max(1, G.E);
-  W.bpe = (int)std::max<int64_t>(1, std::min<int64_t>(want, (G.max_count + 4095) / 4096));
+  // Few edges (< 4 waves of one block each): ~8192 matches per block, so the
+  // resident blocks cover a few edges at a time (their keyframes' clouds stay
+  // L2-resident) and the last wave is short; many edges: one block per edge.
+  const int64_t resident = 2LL * ctx.num_sms;
+  W.bpe = G.E < 4 * resident ? (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 8191) / 8192)) : 1;
   const bool ray = p.mode == PMX_TRACK_RAY;
   require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
   W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);

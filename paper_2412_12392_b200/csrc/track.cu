@@ -48,9 +48,6 @@ __device__ void eval_pass(const PoseR<float>& T, const MatchesDev& M, const Clou
 // partials per block (stride kAcc).  Same skips as eval_match.
 __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const CloudDev& Xref,
                               const CloudDev& Xsrc, const WeightsDev& wp, double* __restrict__ partials) {
-  const PoseR<float> Tf = {{(float)T.sR[0], (float)T.sR[1], (float)T.sR[2], (float)T.sR[3], (float)T.sR[4],
-                            (float)T.sR[5], (float)T.sR[6], (float)T.sR[7], (float)T.sR[8]},
-                           {(float)T.t[0], (float)T.t[1], (float)T.t[2]}};
   float acc[kRayAcc];
 #pragma unroll
   for (int i = 0; i < kRayAcc; ++i) acc[i] = 0.0f;
@@ -67,11 +64,10 @@ __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const
     if (!(q > wp.q_min)) continue;  // robust_weight: infinite denom -> excluded
     const float info = (float)(1.0 / (wp.sigma2 / q));
     const double rd[3] = {rf[0], rf[1], rf[2]}, sd[3] = {sf[0], sf[1], sf[2]};
-    const double rr = fma(rd[0], rd[0], fma(rd[1], rd[1], rd[2] * rd[2]));
-    if (!(rr >= 1e-24)) continue;  // |ref| < 1e-12 (tracking.cpp:78)
-    const float rrf = (float)rr;
+    const float rrf = fmaf(rf[0], rf[0], fmaf(rf[1], rf[1], rf[2] * rf[2]));
+    if (!(rrf >= 1e-24f)) continue;  // |ref| < 1e-12 (tracking.cpp:78)
     const float ir = rsqrt_nr(rrf);
-    ray_accumulate(T, Tf, rd, rr, rrf * ir, ir, rf, sd, sf, info, c, acc);
+    ray_accumulate(T, rd, rrf * ir, ir, rf, sd, info, c, acc);
   }
   block_reduce_n<kRayAcc>(acc, partials + (size_t)blockIdx.x * kAcc);
 }

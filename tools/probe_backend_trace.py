@@ -17,7 +17,10 @@ import pmxgen  # noqa: E402
 from paper_2412_12392_b200 import Context, Graph, MatchSet, Pointmap, abi  # noqa: E402
 
 H, W = 384, 512
-g = pmxgen.backend_graph(100, 4, 3)
+kf = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+reach = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+loops = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+g = pmxgen.backend_graph(kf, reach, 3, loops=loops)
 dev = torch.device("cuda")
 T = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)
 cans = [Pointmap(T(x), T(v), H, W) for x, v in g["canonicals"]]
@@ -25,7 +28,7 @@ ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["m
 ctx = Context(0)
 p = abi.default_backend_params()
 p.weights.distance_weight = 0.1
-p.max_iterations = 10
+p.max_iterations = int(sys.argv[4]) if len(sys.argv) > 4 else 10
 init = [P.to_struct(abi.pmx_sim3) for P in g["init"]]
 for _ in range(2):
     ctx.global_optimize(Graph(cans, list(init), g["edges"], ms), p)
