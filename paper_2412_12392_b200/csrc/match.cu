@@ -14,15 +14,15 @@
 //   K1 k_prep        one thread per a-pixel: FP64 unit ray + validity into a
 //                    32-byte ray map, and the int8 image of the descriptor
 //                    (24 B) for the refinement.
-//   K3 k_match       one thread per b-pixel: FP64 Levenberg-Marquardt on the
-//                    ray-angle error, lround + clamp, q = sqrt(Q_a Q_b), the 3D
-//                    invalidation test.
-//   K4 k_refine_q8   one thread per valid b-pixel: coarse-to-fine descriptor
-//                    refinement on exact int8 scores with a rigorous
-//                    uniqueness gap; undecided pixels (near ties) take the
-//                    exact path, so the argmax equals the reference's
-//                    exact-arithmetic argmax (strict '>' scan, ties keep the
-//                    centre / first raster).
+//   K3+K4 k_match_refine  one thread per b-pixel: FP64 Levenberg-Marquardt on
+//                    the ray-angle error, lround + clamp, q = sqrt(Q_a Q_b),
+//                    the 3D invalidation test (K3; k_match alone when no
+//                    refinement is asked), then the coarse-to-fine descriptor
+//                    refinement of the valid matches on exact int8 scores with
+//                    a rigorous uniqueness gap (K4); undecided pixels (near
+//                    ties) take the exact path, so the argmax equals the
+//                    reference's exact-arithmetic argmax (strict '>' scan,
+//                    ties keep the centre / first raster).
 #include <cfloat>
 #include <climits>
 #include <cmath>
