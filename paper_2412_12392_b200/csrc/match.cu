@@ -1159,7 +1159,7 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
 // the valid matches; the int8 a-image (L2-resident chunk scratch) is read
 // through L1, where a tile's windows overlap.  Fusing lets the FP64-bound LM
 // of some warps overlap the integer-bound refinement of others on every SM.
-__global__ void __launch_bounds__(256, 3) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
+__global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
                                                          RefineLevels L, unsigned long long* __restrict__ exact_px) {
   const PairDev& P = pairs[blockIdx.y];
   const int tiles_x = (P.Wb + 31) / 32;
