@@ -224,3 +224,82 @@ def test_match_stats_and_keyframe_decision(ctx):
     vc, uf = ctx.match_stats(m, 100)
     vo, uo = pyoracle.match_stats(pyoracle.MatchSet(pa, np.arange(500), np.ones(500), v), 100)
     assert vc == vo and uf == uo
+
+
+def _fused_vs_oracle(ctx, pairs, levels=BASELINE_REFINE, exact=True):
+    params = baseline_match_params()
+    rp = abi.refine_params(levels)
+    gpu = ctx.match_batch([pmx_pair(p) for p in pairs], params=params, refine=rp)
+    for p, g in zip(pairs, gpu):
+        orc = pyoracle.feature_refine(pyoracle.match_pointmaps(p, params), p, rp)
+        st = compare_matches(g, orc, p["width"])
+        _check(st)
+        if exact:
+            assert st["all_index_equal"], st
+
+
+def test_fused_refine_descriptor_overflow_takes_exact_path(ctx):
+    # |descriptor| > 1 + 2^-8 has no exact int8 image: the whole pair takes the
+    # exact path of the fused kernel (qbad), same results
+    pair = pmxgen.config0(seed=31, height=48, width=64)
+    big = dict(pair)
+    big["D_a"] = (pair["D_a"].view(np.float16) * np.float16(3.0)).view(np.uint16)
+    big["D_b"] = (pair["D_b"].view(np.float16) * np.float16(3.0)).view(np.uint16)
+    _fused_vs_oracle(ctx, [big, pair])
+
+
+def test_fused_refine_flat_descriptors_all_ties(ctx):
+    # every candidate ties: no pixel is decided by the integer scores; the
+    # exact path keeps the centre (strict '>' scan, camera.cpp:250-263)
+    pair = pmxgen.config0(seed=32, height=48, width=64)
+    flat = dict(pair)
+    one = np.zeros_like(pair["D_a"].view(np.float16))
+    one[:, 0] = np.float16(1.0)
+    flat["D_a"] = one.view(np.uint16)
+    flat["D_b"] = one.copy().view(np.uint16)
+    _fused_vs_oracle(ctx, [flat])
+
+
+@pytest.mark.parametrize("dim", [16, 32])
+def test_fused_refine_other_descriptor_dims(ctx, dim):
+    # no int8 fast path for dim != 24: per-pixel exact refinement in the same kernel
+    pair = pmxgen.config0(seed=33, height=48, width=64)
+    rng = np.random.default_rng(dim)
+    for k in ("D_a", "D_b"):
+        d = rng.normal(size=(48 * 64, dim))
+        d /= np.linalg.norm(d, axis=1, keepdims=True)
+        pair[k] = d.astype(np.float16).view(np.uint16)
+    pair["D_b"] = pair["D_a"].copy()  # b descriptors equal the a ones at the same pixel
+    _fused_vs_oracle(ctx, [pair])
+
+
+def test_ragged_batch_mixed_sizes(ctx):
+    # pairs of different sizes (and a < b grids) in one batch: scratch and tiles by the largest
+    pairs = [pmxgen.config0(seed=34, height=48, width=64), pmxgen.config0(seed=35, height=96, width=128),
+             pmxgen.config0(seed=36, height=24, width=32)]
+    a = pmxgen.config0(seed=37, height=48, width=64)
+    b = pmxgen.config0(seed=37, height=40, width=56)
+    mixed = dict(a)  # X_b / F_b on a smaller grid than X_a / F_a
+    for k in ("X_b", "valid_b", "D_b", "Q_b"):
+        mixed[k] = b[k]
+    mixed["height_b"], mixed["width_b"] = 40, 56
+    _fused_vs_oracle(ctx, pairs)
+    params = baseline_match_params()
+    rp = abi.refine_params(BASELINE_REFINE)
+    from paper_2412_12392_b200 import FeatureMap, Pointmap
+    Xa = Pointmap(mixed["X_a"], mixed["valid_a"], 48, 64)
+    Xb = Pointmap(mixed["X_b"], mixed["valid_b"], 40, 56)
+    Fa = FeatureMap(mixed["D_a"], mixed["Q_a"], 48, 64)
+    Fb = FeatureMap(mixed["D_b"], mixed["Q_b"], 40, 56)
+    g = ctx.match_batch([(Xa, Xb, Fa, Fb)] + [pmx_pair(p) for p in pairs[:1]], params=params, refine=rp)
+    assert len(g[0].pixel_a) == 40 * 56 and np.asarray(g[0].pixel_a).max() < 48 * 64
+    ok = np.asarray(g[0].valid).astype(bool)
+    assert ok.mean() > 0.2  # an unrelated view still matches its geometric neighbourhood
+
+
+def test_empty_batch_and_all_invalid_pair(ctx):
+    assert ctx.match_batch([], params=baseline_match_params()) == []
+    pair = pmxgen.config0(seed=38, height=24, width=32)
+    dead = dict(pair, valid_a=np.zeros_like(pair["valid_a"]), valid_b=np.zeros_like(pair["valid_b"]))
+    g = ctx.match_batch([pmx_pair(dead)], params=baseline_match_params(), refine=abi.refine_params(BASELINE_REFINE))[0]
+    assert not np.asarray(g.valid).any() and (np.asarray(g.pixel_a) == -1).all()
