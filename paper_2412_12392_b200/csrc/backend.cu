@@ -73,6 +73,8 @@ struct EdgeArgs {
   const int4* packed;       // [E][seg]
   const int* pk_total;      // [E]
   int64_t seg;
+  float inv_s2;  // 1 / sigma^2 and the Huber / distance constants in fp32 (host-converted)
+  RayW rw;
 };
 
 __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
@@ -202,21 +204,50 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
     if (keep & (1u << j)) *out++ = rec[j];
 }
 
-// Both directed constraints of one compacted match.
-__device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<double>& T2, const int4 m,
-                                          const float4 Pi, const float4 Pj, float inv_s2, const RayW& c,
-                                          float* acc) {
+// Both directed constraints of one compacted match, packed as a float2 pair
+// (.x: ref = i, src = j, swapped; .y: ref = j, src = i).  The FP64 offsets
+// delta = T src - ref are per direction; everything after them runs as packed
+// fp32 (ray_accumulate_pair); irregular matches take the scalar path.
+__device__ __forceinline__ void ray_match_scalar(const PoseR<double>& T1, const PoseR<double>& T2, const float4 Pi,
+                                              const float4 Pj, float info, const RayW& c, float* acc) {
   const float pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
   const double di[3] = {Pi.x, Pi.y, Pi.z}, dj[3] = {Pj.x, Pj.y, Pj.z};
-  const float info = __int_as_float(m.z) * inv_s2;
   if (Pi.w >= 1e-24f) {  // ref = i; |ref| < 1e-12 (or NaN) skips the row (tracking.cpp:78)
     const float ii = rsqrt_nr(Pi.w);
-    ray_accumulate(T1, di, Pi.w * ii, ii, pi, dj, info, c, acc);  // ref = i, src = j (swapped)
+    ray_accumulate<2>(T1, di, Pi.w * ii, ii, pi, dj, info, c, acc);  // ref = i, src = j (swapped)
   }
   if (Pj.w >= 1e-24f) {
     const float ij = rsqrt_nr(Pj.w);
-    ray_accumulate(T2, dj, Pj.w * ij, ij, pj, di, info, c, acc + kRayAcc);  // ref = j, src = i
+    ray_accumulate<2>(T2, dj, Pj.w * ij, ij, pj, di, info, c, acc + 1);  // ref = j, src = i
   }
+}
+
+// delta_r = (T src - ref)_r in FP64, rounded once to fp32: the translation
+// and the reference enter first (t - ref), so every DFMA of the chain takes
+// one warp-uniform pose operand (no register copies of the pose).
+__device__ __forceinline__ float offset64(const PoseR<double>& T, int r, const double* src, double ref) {
+  return (float)fma(T.sR[3 * r], src[0], fma(T.sR[3 * r + 1], src[1], fma(T.sR[3 * r + 2], src[2], T.t[r] - ref)));
+}
+
+__device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<double>& T2, const int4 m,
+                                          const float4* __restrict__ Ci, const float4* __restrict__ Cj,
+                                          const float4 Pi, const float4 Pj, float inv_s2, const RayW& c,
+                                          float2* acc) {
+  const float info = __int_as_float(m.z) * inv_s2;
+  if (Pi.w >= 1e-24f && Pj.w >= 1e-24f) {
+    const float2 r0 = pack2(Pi.x, Pj.x), r1 = pack2(Pi.y, Pj.y), r2 = pack2(Pi.z, Pj.z);
+    const double di[3] = {Pi.x, Pi.y, Pi.z}, dj[3] = {Pj.x, Pj.y, Pj.z};
+    const float2 rw = make_float2(Pi.w, Pj.w);
+    const float2 y = make_float2(rsqrt_n(Pi.w), rsqrt_n(Pj.w));
+    const float2 ir = mul2(y, fma2(mul2(mul2(p2(-0.5f), rw), y), y, p2(1.5f)));  // rsqrt_nr
+    const float2 e0 = make_float2(offset64(T1, 0, dj, di[0]), offset64(T2, 0, di, dj[0]));
+    const float2 e1 = make_float2(offset64(T1, 1, dj, di[1]), offset64(T2, 1, di, dj[1]));
+    const float2 e2 = make_float2(offset64(T1, 2, dj, di[2]), offset64(T2, 2, di, dj[2]));
+    if (ray_accumulate_pair(e0, e1, e2, r0, r1, r2, mul2(rw, ir), ir, info, c, acc)) return;
+  }
+  // irregular (rare): the points are read again so that the packed path
+  // above need not keep their scalar copies alive
+  ray_match_scalar(T1, T2, __ldg(Ci + m.x), __ldg(Cj + m.y), info, c, reinterpret_cast<float*>(acc));
 }
 
 // Both directed constraints of an edge from one read of its compacted matches
@@ -226,33 +257,33 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
-  float acc[2 * kRayAcc];
+  float2 acc[kRayAcc];
 #pragma unroll
-  for (int i = 0; i < 2 * kRayAcc; ++i) acc[i] = 0.0f;
+  for (int i = 0; i < kRayAcc; ++i) acc[i] = make_float2(0.0f, 0.0f);
   if (ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N) {
     const float4* __restrict__ Ci = A.c4[ij.x];
     const float4* __restrict__ Cj = A.c4[ij.y];
     const int4* __restrict__ P = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
     const PoseR<double> T1 = A.rel64[2 * e], T2 = A.rel64[2 * e + 1];
-    const float inv_s2 = (float)(1.0 / A.wp.sigma2);
-    const RayW c{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta),
-                 (float)A.wp.distance_weight};
+    const float inv_s2 = A.inv_s2;
+    const RayW c = A.rw;
     const int64_t stride = (int64_t)A.bpe * blockDim.x;
     int64_t k = (int64_t)b * blockDim.x + threadIdx.x;
     for (; k + stride < cnt; k += 2 * stride) {
       const int4 m0 = __ldg(P + k), m1 = __ldg(P + k + stride);
       const float4 a0 = __ldg(Ci + m0.x), b0 = __ldg(Cj + m0.y);
       const float4 a1 = __ldg(Ci + m1.x), b1 = __ldg(Cj + m1.y);
-      ray_match(T1, T2, m0, a0, b0, inv_s2, c, acc);
-      ray_match(T1, T2, m1, a1, b1, inv_s2, c, acc);
+      ray_match(T1, T2, m0, Ci, Cj, a0, b0, inv_s2, c, acc);
+      ray_match(T1, T2, m1, Ci, Cj, a1, b1, inv_s2, c, acc);
     }
     if (k < cnt) {
       const int4 m0 = __ldg(P + k);
-      ray_match(T1, T2, m0, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
+      ray_match(T1, T2, m0, Ci, Cj, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
     }
   }
-  block_reduce_n<2 * kRayAcc>(acc, A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
+  block_reduce_n<2 * kRayAcc, true>(reinterpret_cast<const float*>(acc),
+                                    A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
 }
 
 // Sum the closed-form partials of an edge and expand to {H 28, g 7, cost} x 2.
@@ -1199,6 +1230,8 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   A.packed = ray ? G.pk.as<int4>() : nullptr;
   A.pk_total = ray ? G.pk_total.as<int>() : nullptr;
   A.seg = G.seg;
+  A.inv_s2 = (float)(1.0 / A.wp.sigma2);
+  A.rw = RayW{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta), (float)A.wp.distance_weight};
 }
 
 // Edge terms for edges [e0, e1) at the device poses dP -> terms (indexed by
