@@ -600,6 +600,7 @@ __global__ void __launch_bounds__(256) k_ldlt(LdltArgs P) {
 // forward substitution is fused; the backward one reads the compact L.
 constexpr int kPW = 7;           // panel width (one keyframe)
 constexpr int kFront = 96;       // max live indices
+constexpr int kFS = kFront + 1;  // front row stride (odd: a column of the front spreads over the banks)
 constexpr int kSkyMaxN = 8192;   // rhs + panel table kept in shared memory
 constexpr int kSkyThreads = 768;  // >= kFront * kPW (one L entry per thread in the backward pass)
 static_assert(kSkyThreads >= kFront * kPW, "backward pass holds one L entry per thread");
@@ -608,6 +609,7 @@ struct SkyArgs {
   const double* H;          // assembled skyline (undamped)
   const int4* trip;         // entering triples {slot a, slot b, skyline index or -1, diag}
   const int4* pinfo;        // [npanel] {trip begin, trip end, live-row begin, live-row end}
+  const int2* pextra;       // [npanel] {live rows that are the next panel's pivots (lead), pivot-block triples (lead)}
   const int2* rinfo;        // live non-pivot rows of each panel {index, slot}
   const int* slot;          // [n] front slot of every index
   const int* lofs;          // [npanel] offset of the panel's L rows in Lst
@@ -625,38 +627,47 @@ __device__ __forceinline__ int sky_at(const int* rowptr, const int* first, int i
   return rowptr[i] + (j - first[i]);
 }
 
-// 1/d to ~1 ulp without the long IEEE division sequence: fp32 seed and Newton
-// steps (pivots are not the reference's rounding either way: its AMD-ordered
-// SimplicialLDLT differs at this level).
+// 1/d to ~1 ulp without the long IEEE division sequence: the MUFU FP64
+// seed and two correction steps (pivots are not the reference's rounding
+// either way: its AMD-ordered SimplicialLDLT differs at this level).
 __device__ __forceinline__ double fast_rcp(double d) {
-  double r = (double)__frcp_rn((float)d);
-  if (!isfinite(r) || r == 0.0) return 1.0 / d;  // outside fp32 range
-  r = fma(r, fma(-d, r, 1.0), r);
-  r = fma(r, fma(-d, r, 1.0), r);
-  return fma(r, fma(-d, r, 1.0), r);
+  const double ad = fabs(d);
+  if (!(ad > 1e-300 && ad < 1e300)) return 1.0 / d;  // zero, non-finite, extreme
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  e = fma(e, e, e);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  return fma(r, e, r);
 }
 
-// Prefetched data of the next panel, one item per thread (registers), so the
-// global round trips overlap the current panel's barriers.
-struct PanelPrefetch {
-  int4 t;      // entering triple (tid < ntrip)
-  double v;    // its value
-  int2 r;      // live row (tid < ns)
-  int ps;      // pivot slot (tid < 7)
-  bool ht, hr;
-};
+// Asynchronous global -> shared copies (cp.async): the next panel's structure
+// and entering values travel while the current panel is factorised, without
+// holding registers (a register prefetch here was spilled to local memory,
+// which made every panel wait for its loads).
+template <int B>
+__device__ __forceinline__ void cp_async_n(void* sdst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   if (P.st->stop || P.st->solved) return;
   extern __shared__ double smem[];
   const int npanel = (P.n + kPW - 1) / kPW;
-  int4* pin = reinterpret_cast<int4*>(smem);            // [npanel] panel info
-  int* plofs = reinterpret_cast<int*>(pin + npanel);    // [npanel] L offsets
-  double* F = smem + 2 * npanel + (npanel + 1) / 2;     // [kFront][kFront] front (symmetric)
-  double* y = F + kFront * kFront;                      // [n]
-  double* sL = y + P.n;                                 // [kFront][kPW]
-  double* sW = sL + kFront * kPW;                       // [kFront][kPW]
-  __shared__ double sD[kPW][kPW + 1], sIv[kPW];
+  int4* pin = reinterpret_cast<int4*>(smem);             // [npanel] panel info
+  int2* pex = reinterpret_cast<int2*>(pin + npanel);     // [npanel] {next-pivot rows, pivot triples}
+  int* plofs = reinterpret_cast<int*>(pex + npanel);     // [npanel] L offsets
+  double* F = smem + 3 * npanel + (npanel + 1) / 2;      // [kFront][kFS] front (symmetric)
+  double* y = F + kFront * kFS;                          // [n]
+  double* sL = y + P.n;                                  // [kFront][kPW]
+  double* sW = sL + kFront * kPW;                        // [kFront][kPW]
+  __shared__ double sD[2][kPW][kPW + 1], sIv[2][kPW];    // pivot block of the current / next panel
   __shared__ int2 rows[2][kFront];
   __shared__ int psl[2][kPW];
   __shared__ int ok;
@@ -669,103 +680,160 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
   for (int k = tid; k < npanel; k += nth) {
     pin[k] = P.pinfo[k];
+    pex[k] = P.pextra[k];
     plofs[k] = P.lofs[k];
   }
   if (tid == 0) ok = 1;
   __syncthreads();
-  PanelPrefetch pf;
-  auto issue = [&](int k) {  // structure of panel k (values: issue_values)
+  // Prefetch pipeline (cp.async, one item per thread): entering triples two
+  // panels ahead, their values and pivot slots one panel ahead, live rows one
+  // panel ahead; every panel ends with all copies landed.
+  __shared__ int4 stri[2][kSkyThreads];   // entering triples of a panel (slot of panel k: k & 1)
+  __shared__ double sval[2][kSkyThreads];  // their skyline values
+  auto issue_struct = [&](int k) {
     const int4 pi = pin[k];
-    pf.ht = pi.x + tid < pi.y;
-    pf.hr = pi.z + tid < pi.w;
-    if (pf.ht) pf.t = P.trip[pi.x + tid];
-    if (pf.hr) pf.r = P.rinfo[pi.z + tid];
-    if (tid < min(kPW, n - kPW * k)) pf.ps = P.slot[kPW * k + tid];
+    if (pi.x + tid < pi.y) cp_async_n<16>(&stri[k & 1][tid], P.trip + pi.x + tid);
   };
-  auto issue_values = [&]() {
-    if (pf.ht) pf.v = (pf.t.z >= 0 ? P.H[pf.t.z] : 0.0) + (pf.t.w ? lambda : 0.0);  // backend.cpp:210-213
-  };
-  auto land = [&](int k, int buf) {  // entering rows of panel k into the front
+  auto issue_rows = [&](int k) {
     const int4 pi = pin[k];
-    if (pf.ht) {
-      F[pf.t.x * kFront + pf.t.y] = pf.v;
-      F[pf.t.y * kFront + pf.t.x] = pf.v;
+    if (pi.z + tid < pi.w) cp_async_n<8>(&rows[k & 1][tid], P.rinfo + pi.z + tid);
+  };
+  auto issue_vals = [&](int k) {  // needs panel k's triples landed
+    const int4 pi = pin[k];
+    if (pi.x + tid < pi.y) {
+      const int z = stri[k & 1][tid].z;
+      if (z >= 0) cp_async_n<8>(&sval[k & 1][tid], P.H + z);
     }
-    for (int t = pi.x + nth + tid; t < pi.y; t += nth) {  // rare: more triples than threads
+    if (tid < min(kPW, n - kPW * k)) cp_async_n<4>(&psl[k & 1][tid], P.slot + kPW * k + tid);
+  };
+  auto land = [&](int k) {  // this thread's entering triple of panel k (+ the rare overflow) into the front
+    const int4 pi = pin[k];
+    if (pi.x + tid < pi.y) {
+      const int4 t = stri[k & 1][tid];
+      const double v = (t.z >= 0 ? sval[k & 1][tid] : 0.0) + (t.w ? lambda : 0.0);  // backend.cpp:210-213
+      F[t.x * kFS + t.y] = v;
+      F[t.y * kFS + t.x] = v;
+    }
+    for (int t = pi.x + nth + tid; t < pi.y; t += nth) {  // rare: more triples than threads (never pivot ones)
       const int4 q = P.trip[t];
       const double v = (q.z >= 0 ? P.H[q.z] : 0.0) + (q.w ? lambda : 0.0);
-      F[q.x * kFront + q.y] = v;
-      F[q.y * kFront + q.x] = v;
+      F[q.x * kFS + q.y] = v;
+      F[q.y * kFS + q.x] = v;
     }
-    if (pf.hr) rows[buf][tid] = pf.r;
-    if (tid < min(kPW, n - kPW * k)) psl[buf][tid] = pf.ps;
   };
-  issue(0);
-  issue_values();
-  land(0, 0);
+  // Warp 0: the 7x7 pivot block of panel k from the front, in registers
+  // (lane r holds row r) -> sD/sIv[fb], the block's unit L and D, and the
+  // forward substitution L y = b inside the panel.
+  auto factor = [&](int k, int fb) {
+    const int c0 = kPW * k, nb = min(kPW, n - c0);
+    const int ns = pin[k].w - pin[k].z;
+    double* Lp = P.Lst + plofs[k];
+    double a[kPW];
+    const int sr = lane < nb ? psl[fb][lane] : 0;
+#pragma unroll
+    for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFS + psl[fb][c]] : 0.0;
+#pragma unroll
+    for (int p = 0; p < kPW; ++p) {
+      if (p < nb) {
+        // column p of every row first (the pivot is lane p's entry), so the
+        // exchanges overlap the reciprocal instead of following it
+        const double w = a[p];  // this row's unscaled entry in column p
+        double wc[kPW];
+#pragma unroll
+        for (int c = p; c < kPW; ++c) wc[c] = __shfl_sync(0xffffffffu, w, c);
+        const double D = wc[p];
+        if (lane == 0 && D == 0.0) ok = 0;  // SimplicialLDLT: exact zero pivot fails
+        const double iD = fast_rcp(D);
+#pragma unroll
+        for (int c = p + 1; c < kPW; ++c)
+          if (lane >= c) a[c] -= w * (wc[c] * iD);
+        if (lane > p) a[p] = w * iD;
+        if (lane == p) sIv[fb][p] = iD;
+      }
+    }
+    if (lane < nb) {
+      double dl = 0.0;  // a[lane] without a dynamic register index
+#pragma unroll
+      for (int c = 0; c < kPW; ++c) {
+        if (c <= lane) sD[fb][lane][c] = a[c];
+        if (c == lane) dl = a[c];
+        Lp[ns * kPW + lane * kPW + c] = c < lane ? a[c] : 0.0;  // unit L of the pivot block
+      }
+      P.Dst[c0 + lane] = dl;
+    }
+    double yv = lane < nb ? y[c0 + lane] : 0.0;  // L y = b inside the panel
+#pragma unroll
+    for (int p = 0; p < kPW; ++p) {
+      const double yp = __shfl_sync(0xffffffffu, yv, p);
+      if (lane > p && lane < nb) yv -= a[p] * yp;
+    }
+    if (lane < nb) y[c0 + lane] = yv;
+  };
+  // Schur update of live-row pair t (row-major lower triangle) inside the front
+  auto schur = [&](int t, int buf) {
+    int qi = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((qi + 1) * (qi + 2) / 2 <= t) ++qi;
+    while (qi * (qi + 1) / 2 > t) --qi;
+    const int qj = t - qi * (qi + 1) / 2;
+    const int si = rows[buf][qi].y, sj = rows[buf][qj].y;
+    double sacc = 0.0;
+#pragma unroll
+    for (int u = 0; u < kPW; ++u) sacc += sW[qi * kPW + u] * sL[qj * kPW + u];
+    const double v = F[si * kFS + sj] - sacc;
+    F[si * kFS + sj] = v;
+    F[sj * kFS + si] = v;
+  };
+  issue_struct(0);
+  cp_async_commit();
+  cp_async_wait_all();
+  issue_vals(0);
+  issue_rows(0);
+  if (npanel > 1) issue_struct(1);
+  cp_async_commit();
+  cp_async_wait_all();
+  land(0);
   __syncthreads();
+  if (warp == 0) factor(0, 0);
+  __syncthreads();
+#ifdef PMX_SKY_TIMING
+  long long tph[4] = {0, 0, 0, 0}, tt = clock64();
+#define SKY_T(i) { const long long t2 = clock64(); tph[i] += t2 - tt; tt = t2; }
+#else
+#define SKY_T(i)
+#endif
+  // Look-ahead: the next panel's pivot rows lead its live-row list and its
+  // pivot-block triples lead its entering list (host plan), so while the
+  // other warps apply panel k's Schur update to the rest of the front, warp 0
+  // updates and lands the next pivot block and factorises it.  Per panel:
+  // (b) rows -> barrier -> [warp 0: next pivot block | others: Schur + land]
+  // -> barrier.
   for (int k = 0; k < npanel; ++k) {
     const int c0 = kPW * k, nb = min(kPW, n - c0), buf = k & 1;
     const int4 pi = pin[k];
     const int ns = pi.w - pi.z;
     double* Lp = P.Lst + plofs[k];
-    if (k + 1 < npanel) issue(k + 1);
-    // (a) pivot block on warp 0, in registers (lane r holds row r)
-    if (warp == 0) {
-      double a[kPW];
-      const int sr = lane < nb ? psl[buf][lane] : 0;
-#pragma unroll
-      for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFront + psl[buf][c]] : 0.0;
-#pragma unroll
-      for (int p = 0; p < kPW; ++p) {
-        if (p < nb) {
-          const double D = __shfl_sync(0xffffffffu, a[p], p);
-          if (lane == 0 && D == 0.0) ok = 0;  // SimplicialLDLT: exact zero pivot fails
-          const double iD = fast_rcp(D);
-          const double w = a[p];  // this row's unscaled entry in column p
-#pragma unroll
-          for (int c = p + 1; c < kPW; ++c) {
-            const double wc = __shfl_sync(0xffffffffu, w, c);  // row c's unscaled entry
-            if (lane >= c) a[c] -= w * (wc * iD);
-          }
-          if (lane > p) a[p] = w * iD;
-          if (lane == p) sIv[p] = iD;
-        }
-      }
-      if (lane < nb) {
-        double dl = 0.0;  // a[lane] without a dynamic register index
-#pragma unroll
-        for (int c = 0; c < kPW; ++c) {
-          if (c <= lane) sD[lane][c] = a[c];
-          if (c == lane) dl = a[c];
-          Lp[ns * kPW + lane * kPW + c] = c < lane ? a[c] : 0.0;  // unit L of the pivot block
-        }
-        P.Dst[c0 + lane] = dl;
-      }
-      double yv = lane < nb ? y[c0 + lane] : 0.0;  // L y = b inside the panel
-#pragma unroll
-      for (int p = 0; p < kPW; ++p) {
-        const double yp = __shfl_sync(0xffffffffu, yv, p);
-        if (lane > p && lane < nb) yv -= a[p] * yp;
-      }
-      if (lane < nb) y[c0 + lane] = yv;
+    const bool next = k + 1 < npanel;
+    if (next) {
+      issue_vals(k + 1);  // group A: what the look-ahead needs
+      cp_async_commit();
+      if (k + 2 < npanel) issue_struct(k + 2);  // group B
+      issue_rows(k + 1);
+      cp_async_commit();
     }
-    __syncthreads();
-    if (k + 1 < npanel) issue_values();
     // (b) live rows below the panel: W = F_r,panel L^-T, L_r = W D^-1; forward update of y_r
     for (int q = tid; q < ns; q += nth) {
       const int2 ri = rows[buf][q];
       double w[kPW];
 #pragma unroll
-      for (int t = 0; t < kPW; ++t) w[t] = t < nb ? F[ri.y * kFront + psl[buf][t]] : 0.0;
+      for (int t = 0; t < kPW; ++t) w[t] = t < nb ? F[ri.y * kFS + psl[buf][t]] : 0.0;
 #pragma unroll
       for (int t = 1; t < kPW; ++t)
 #pragma unroll
-        for (int u = 0; u < t; ++u) w[t] -= w[u] * sD[t][u];
+        for (int u = 0; u < t; ++u) w[t] -= w[u] * sD[buf][t][u];
       double yi = 0.0;
 #pragma unroll
       for (int t = 0; t < kPW; ++t) {
-        const double l = t < nb ? w[t] * sIv[t] : 0.0;
+        const double l = t < nb ? w[t] * sIv[buf][t] : 0.0;
         Lp[q * kPW + t] = l;
         sL[q * kPW + t] = l;
         sW[q * kPW + t] = t < nb ? w[t] : 0.0;
@@ -773,28 +841,37 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
       }
       y[ri.x] -= yi;
     }
+    SKY_T(0)
     __syncthreads();
-    // (c) Schur update of the live rows inside the front
-    const int npair = ns * (ns + 1) / 2;
-    for (int t = tid; t < npair; t += nth) {
-      int qi = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while ((qi + 1) * (qi + 2) / 2 <= t) ++qi;
-      while (qi * (qi + 1) / 2 > t) --qi;
-      const int qj = t - qi * (qi + 1) / 2;
-      const int si = rows[buf][qi].y, sj = rows[buf][qj].y;
-      double sacc = 0.0;
-#pragma unroll
-      for (int u = 0; u < kPW; ++u) sacc += sW[qi * kPW + u] * sL[qj * kPW + u];
-      const double v = F[si * kFront + sj] - sacc;
-      F[si * kFront + sj] = v;
-      F[sj * kFront + si] = v;
+    SKY_T(1)
+    // (c) Schur update; warp 0 takes the pairs inside the next pivot block
+    const int npair = ns * (ns + 1) / 2, nv = pex[k].x, nlead = nv * (nv + 1) / 2;
+    if (warp == 0) {
+      if (next) {
+        cp_async_wait_group<1>();  // group A of this thread
+        __syncwarp();
+        land(k + 1);
+        for (int t = lane; t < nlead; t += 32) schur(t, buf);
+        __syncwarp();
+        factor(k + 1, buf ^ 1);
+      }
+    } else {
+      for (int t = nlead + tid - 32; t < npair; t += nth - 32) schur(t, buf);
+      if (next) {
+        cp_async_wait_group<1>();
+        land(k + 1);
+      }
     }
+    cp_async_wait_all();  // the next panel's rows / pivot slots, visible after the barrier
+    SKY_T(2)
     __syncthreads();
-    if (k + 1 < npanel) {
-      land(k + 1, buf ^ 1);
-      __syncthreads();
-    }
+    SKY_T(3)
   }
+#ifdef PMX_SKY_TIMING
+  if (lane == 0 && (warp == 0 || warp == 1 || warp == 5))
+    printf("sky warp %d: b %lld | bar %lld | c/lookahead %lld | bar %lld (cycles per panel)\n", warp, tph[0] / npanel,
+           tph[1] / npanel, tph[2] / npanel, tph[3] / npanel);
+#endif
   // D z = y
   for (int i = tid; i < n; i += nth) y[i] *= fast_rcp(P.Dst[i]);
   __syncthreads();
@@ -1287,7 +1364,7 @@ struct Assembly {
   bool sky_ok = false;
   long long nnz = 0;
   DevBuf first, rowptr, rp_ptr, rp_rows, skyH;
-  DevBuf trip, pinfo, rinfo, slot, lofs, Lst, Dst;  // frontal factorisation plan
+  DevBuf trip, pinfo, pextra, rinfo, slot, lofs, Lst, Dst;  // frontal factorisation plan
   // band plan (preferred when the RCM bandwidth is small): block cyclic reduction
   bool band_ok = false;
   int band_m = 0, band_w = 0, band_S = 0, band_npad = 0;
@@ -1443,6 +1520,7 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
     for (int m = 0; m < n; ++m) enter[first[m] / kPW].push_back(m);
     std::vector<int> slot(n, -1), freel, live, tptr{0}, lofs(npanel);
     std::vector<int4> trip;
+    std::vector<int2> pext;
     for (int s2 = kFront - 1; s2 >= 0; --s2) freel.push_back(s2);
     long long lsize = 0;
     for (int k = 0; k < npanel && fits; ++k) {
@@ -1456,18 +1534,27 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
         live.push_back(m);
       }
       if (!fits) break;
+      const int pbeg = kPW * k, pend = std::min(n, kPW * k + kPW);
+      std::vector<int4> tpiv, trest;  // pivot-block triples lead (look-ahead, k_ldlt_sky)
       for (int m : enter[k])  // m's row against every live index (itself included)
         for (int x : live) {
           const int r = std::max(m, x), c = std::min(m, x);
           if (x > m && std::find(enter[k].begin(), enter[k].end(), x) != enter[k].end()) continue;  // pair once
           const int idx = c >= first[r] ? rowptr[r] + (c - first[r]) : -1;
-          trip.push_back(make_int4(slot[m], slot[x], idx, m == x ? 1 : 0));
+          (c >= pbeg && r < pend ? tpiv : trest).push_back(make_int4(slot[m], slot[x], idx, m == x ? 1 : 0));
         }
+      trip.insert(trip.end(), tpiv.begin(), tpiv.end());
+      trip.insert(trip.end(), trest.begin(), trest.end());
       tptr.push_back((int)trip.size());
-      const int pend = std::min(n, kPW * k + kPW);
+      std::vector<int> rnext;  // live rows that are the next panel's pivots lead, in index order
       for (int m : live)
-        if (m >= pend) rrows.push_back(m);
+        if (m >= pend && m < pend + kPW) rnext.push_back(m);
+      std::sort(rnext.begin(), rnext.end());
+      rrows.insert(rrows.end(), rnext.begin(), rnext.end());
+      for (int m : live)
+        if (m >= pend + kPW) rrows.push_back(m);
       rptr.push_back((int)rrows.size());
+      pext.push_back(make_int2((int)rnext.size(), (int)tpiv.size()));
       lofs[k] = (int)lsize;
       lsize += (long long)(rptr[k + 1] - rptr[k]) * kPW + kPW * kPW;
       std::vector<int> keep;  // the panel's pivots leave the front
@@ -1496,6 +1583,8 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
         PMX_CUDA(cudaMemcpyAsync(As.rinfo.p, rinfo.data(), sizeof(int2) * rinfo.size(), cudaMemcpyHostToDevice, ctx.stream));
       up(As.slot, slot);
       up(As.lofs, lofs);
+      As.pextra = DevBuf(sizeof(int2) * npanel, ctx.stream);
+      PMX_CUDA(cudaMemcpyAsync(As.pextra.p, pext.data(), sizeof(int2) * npanel, cudaMemcpyHostToDevice, ctx.stream));
       As.trip = DevBuf(sizeof(int4) * std::max<size_t>(trip.size(), 1), ctx.stream);
       if (!trip.empty())
         PMX_CUDA(cudaMemcpyAsync(As.trip.p, trip.data(), sizeof(int4) * trip.size(), cudaMemcpyHostToDevice, ctx.stream));
@@ -1668,11 +1757,11 @@ static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, G
   }
   const int n = As.dim;
   const int npanel = (n + kPW - 1) / kPW;
-  const size_t smem = sizeof(double) * ((size_t)kFront * kFront + n + 2 * kFront * kPW) +
-                      sizeof(int4) * (size_t)npanel + sizeof(double) * (size_t)((npanel + 1) / 2);
+  const size_t smem = sizeof(double) * ((size_t)kFront * kFS + n + 2 * kFront * kPW) +
+                      (sizeof(int4) + sizeof(int2)) * (size_t)npanel + sizeof(double) * (size_t)((npanel + 1) / 2);
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
-    SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.rinfo.as<int2>(), As.slot.as<int>(),
+    SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.pextra.as<int2>(), As.rinfo.as<int2>(), As.slot.as<int>(),
               As.lofs.as<int>(), As.Lst.as<double>(), As.Dst.as<double>(), As.grad.as<double>(), tau, n, attempt,
               p.damping_init, st};
     {

@@ -47,7 +47,7 @@ struct BandArgs {
 __device__ bool band_ldlt(double* A, int w, double* tmp) {
   constexpr int P = 8;
   __shared__ int bad;
-  __shared__ double piv[P];
+  __shared__ double piv[P];  // 1 / pivot
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) bad = 0;
   for (int p0 = 0; p0 < w; p0 += P) {
@@ -61,7 +61,7 @@ __device__ bool band_ldlt(double* A, int w, double* tmp) {
         if (p < nb) {
           const double D = __shfl_sync(0xffffffffu, a[p], p);
           if (lane == 0 && D == 0.0) bad = 1;
-          const double iD = 1.0 / D;
+          const double iD = fast_rcp(D);
           const double wv = a[p];
 #pragma unroll
           for (int c = p + 1; c < P; ++c) {
@@ -69,7 +69,7 @@ __device__ bool band_ldlt(double* A, int w, double* tmp) {
             if (lane >= c) a[c] -= wv * (wc * iD);
           }
           if (lane > p) a[p] = wv * iD;
-          if (lane == p) piv[p] = D;
+          if (lane == p) piv[p] = iD;
         }
       }
       if (lane < nb) {
@@ -93,7 +93,7 @@ __device__ bool band_ldlt(double* A, int w, double* tmp) {
       for (int t = 0; t < P; ++t) {
         if (t < nb) {
           tmp[t * w + r] = wv[t];
-          A[r * w + p0 + t] = wv[t] / piv[t];
+          A[r * w + p0 + t] = wv[t] * piv[t];
         }
       }
     }
@@ -125,44 +125,94 @@ __device__ bool band_ldlt(double* A, int w, double* tmp) {
 }
 
 // In place: X (w x n, row-major, leading dimension n) <- (L D L^T)^-1 X.
-// Blocked substitution: an 8-row diagonal block is solved per column (one
-// thread per column), then the remaining rows are updated in parallel.
+// Blocked substitution by 8-row blocks: the diagonal block is solved per
+// column (one thread per column, the block's column in registers), then the
+// rows below (forward) / above (backward) take a rank-8 update in 4 x 4
+// register tiles (columns strided across the threads: conflict-free X rows,
+// broadcast L loads) - two FMAs per shared load instead of one per two.
 __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
   constexpr int B = 8;
+  __shared__ double rdiag[kBandMaxW];
+  for (int r = threadIdx.x; r < w; r += blockDim.x) rdiag[r] = fast_rcp(A[r * w + r]);
+  const int ct = (n + 3) / 4;  // column tiles: thread column tc takes tc, tc + ct, tc + 2 ct, tc + 3 ct
+  auto col = [&](int tc, int j) { return tc + j * ct; };
   for (int r0 = 0; r0 < w; r0 += B) {  // L z = x
-    const int r1 = min(w, r0 + B);
-    for (int c = threadIdx.x; c < n; c += blockDim.x)
-      for (int r = r0 + 1; r < r1; ++r) {
-        double s = X[r * n + c];
-        for (int k = r0; k < r; ++k) s -= A[r * w + k] * X[k * n + c];
-        X[r * n + c] = s;
-      }
+    const int r1 = min(w, r0 + B), nb = r1 - r0;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      double z[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * n + c] : 0.0;
+#pragma unroll
+      for (int r = 1; r < B; ++r)
+#pragma unroll
+        for (int k = 0; k < r; ++k)
+          if (r < nb) z[r] -= A[(r0 + r) * w + r0 + k] * z[k];
+#pragma unroll
+      for (int i = 1; i < B; ++i)
+        if (i < nb) X[(r0 + i) * n + c] = z[i];
+    }
     __syncthreads();
-    const int rows = w - r1;
-    for (int t = threadIdx.x; t < rows * n; t += blockDim.x) {
-      const int r = r1 + t / n, c = t % n;
-      double s = X[r * n + c];
-      for (int k = r0; k < r1; ++k) s -= A[r * w + k] * X[k * n + c];
-      X[r * n + c] = s;
+    const int rt = (w - r1 + 3) / 4;
+    for (int t = threadIdx.x; t < rt * ct; t += blockDim.x) {
+      const int ra = r1 + 4 * (t / ct), tc = t % ct;
+      double acc[4][4] = {};
+      for (int k = 0; k < nb; ++k) {
+        double av[4], zv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = A[min(ra + i, w - 1) * w + r0 + k];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * n + min(col(tc, j), n - 1)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], zv[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ra + i < w && col(tc, j) < n) X[(ra + i) * n + col(tc, j)] -= acc[i][j];
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < w * n; t += blockDim.x) X[t] /= A[(t / n) * w + t / n];  // D
+  for (int t = threadIdx.x; t < w * n; t += blockDim.x) X[t] *= rdiag[t / n];  // D
   __syncthreads();
   for (int r1 = w; r1 > 0; r1 -= B) {  // L^T x = z, from the bottom
-    const int r0 = max(0, r1 - B);
-    for (int c = threadIdx.x; c < n; c += blockDim.x)
-      for (int r = r1 - 2; r >= r0; --r) {
-        double s = X[r * n + c];
-        for (int k = r + 1; k < r1; ++k) s -= A[k * w + r] * X[k * n + c];
-        X[r * n + c] = s;
-      }
+    const int r0 = max(0, r1 - B), nb = r1 - r0;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      double z[B];
+#pragma unroll
+      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * n + c] : 0.0;
+#pragma unroll
+      for (int r = B - 2; r >= 0; --r)
+#pragma unroll
+        for (int k = r + 1; k < B; ++k)
+          if (k < nb) z[r] -= A[(r0 + k) * w + r0 + r] * z[k];
+#pragma unroll
+      for (int i = 0; i < B - 1; ++i)
+        if (i < nb) X[(r0 + i) * n + c] = z[i];
+    }
     __syncthreads();
-    for (int t = threadIdx.x; t < r0 * n; t += blockDim.x) {
-      const int r = t / n, c = t % n;
-      double s = X[r * n + c];
-      for (int k = r0; k < r1; ++k) s -= A[k * w + r] * X[k * n + c];
-      X[r * n + c] = s;
+    const int rt = (r0 + 3) / 4;
+    for (int t = threadIdx.x; t < rt * ct; t += blockDim.x) {
+      const int ra = 4 * (t / ct), tc = t % ct;
+      double acc[4][4] = {};
+      for (int k = 0; k < nb; ++k) {
+        double av[4], zv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = A[(r0 + k) * w + min(ra + i, w - 1)];  // L^T
+#pragma unroll
+        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * n + min(col(tc, j), n - 1)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], zv[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (ra + i < r0 && col(tc, j) < n) X[(ra + i) * n + col(tc, j)] -= acc[i][j];
     }
     __syncthreads();
   }
