@@ -52,6 +52,7 @@ __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const
 #pragma unroll
   for (int i = 0; i < kRayAcc; ++i) acc[i] = 0.0f;
   const RayW c{(float)wp.huber_delta, (float)(wp.huber_delta * wp.huber_delta), (float)wp.distance_weight};
+  double cost64 = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M.count; k += stride) {
     const int pa = M.pa ? __ldg(M.pa + k) : (int)k;
@@ -68,8 +69,20 @@ __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const
     if (!(rrf >= 1e-24f)) continue;  // |ref| < 1e-12 (tracking.cpp:78)
     const float ir = rsqrt_nr(rrf);
     ray_accumulate(T, rd, rrf * ir, ir, rf, sd, info, c, acc);
+    cost64 += ray_cost64(T, rd, sd, 1.0 / (wp.sigma2 / q), wp.distance_weight, wp.huber_delta);
   }
   block_reduce_n<kRayAcc>(acc, partials + (size_t)blockIdx.x * kAcc);
+  // the cost slot takes the FP64 sum (deterministic: warp sums in lane order, warps in order)
+  __shared__ double wc[32];
+  cost64 = warp_sum(cost64);
+  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = cost64;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wc[w];
+    partials[(size_t)blockIdx.x * kAcc + kRayAcc - 1] = t;
+  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(256) k_normal_eq(PoseR<float> T, MatchesDev M, CloudDev Xref, CloudDev Xsrc,

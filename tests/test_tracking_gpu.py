@@ -208,3 +208,29 @@ def test_fusion_is_idempotent_and_first_is_exact(ctx):
     ctx.fuse_canonical(gx, gv, gc, Pointmap(X, None, H_, W_), c["canonical_conf"], sim3(), H_, W_)
     np.testing.assert_allclose(gx, before, rtol=1e-6, atol=1e-6)
     np.testing.assert_allclose(gc, 2 * c["canonical_conf"], rtol=1e-6)
+
+
+def test_track_decisions_match_oracle_at_full_size(ctx):
+    """Config-1 size (384 x 512): the accept / stop decisions of the LM loop
+    (tracking.cpp:206-223) compare costs a few 1e-12 apart near convergence;
+    the loop's FP64 cost sum (ray_cost64) must reproduce the oracle's
+    iteration count and cost trace, not just the final pose."""
+    h, w = 384, 512
+    c = pmxgen.config1(seed=1)
+    pa = np.arange(h * w, dtype=np.int32)
+    pa, v = pmxgen.inject_outliers(pa, c["valid_k"].copy(), 0.1, 1, h * w)
+    q = np.sqrt(c["C_f"][np.clip(pa, 0, None)].astype(np.float64) * c["C_k"].astype(np.float64)).astype(np.float32)
+    p = abi.default_solve_pose_params()
+    p.max_iterations = 10
+    p.weights.distance_weight = 0.1
+    rg = ctx.track_given_matches(Pointmap(c["canonical"], c["canonical_valid"], h, w),
+                                 Pointmap(c["X_f_f"], c["valid_f"], h, w), MatchSet(pa, q, v), sim3(), params=p)
+    om = pyoracle.MatchSet(pa, np.arange(h * w), q.astype(np.float64), v)
+    ro = pyoracle.track_given_matches(c["canonical"], c["canonical_valid"], c["X_f_f"], c["valid_f"], h, w, om,
+                                      sim3(), params=p)
+    assert rg.iterations == ro.iterations
+    n = len(rg.cost_trace)
+    assert n >= 3
+    np.testing.assert_allclose(rg.cost_trace, np.asarray(ro.cost_trace)[:n], rtol=1e-9)
+    et, er, es = _pose_err(rg.T_kf, ro.T_kf)
+    assert et < 1e-6 and er < 1e-6 and es < 1e-6, (et, er, es)
