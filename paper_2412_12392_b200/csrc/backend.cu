@@ -842,11 +842,16 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
       y[ri.x] -= yi;
     }
     SKY_T(0)
-    __syncthreads();
-    SKY_T(1)
-    // (c) Schur update; warp 0 takes the pairs inside the next pivot block
+    // (c) Schur update; warp 0 takes the pairs inside the next pivot block and
+    // goes on without waiting for the other rows of (b): the next pivot rows
+    // lead the live list (its own rows), its land writes only slots that
+    // (b) does not read (no slot is reused by the panel right after), and
+    // its pivot-block pairs are disjoint from the others' pairs
     const int npair = ns * (ns + 1) / 2, nv = pex[k].x, nlead = nv * (nv + 1) / 2;
     if (warp == 0) {
+      __threadfence_block();  // this warp's rows of (b) before the others' Schur update
+      asm volatile("bar.arrive 1, %0;" ::"r"(nth) : "memory");
+      SKY_T(1)
       if (next) {
         cp_async_wait_group<1>();  // group A of this thread
         __syncwarp();
@@ -856,6 +861,8 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
         factor(k + 1, buf ^ 1);
       }
     } else {
+      asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");  // every row of (b) is in
+      SKY_T(1)
       for (int t = nlead + tid - 32; t < npair; t += nth - 32) schur(t, buf);
       if (next) {
         cp_async_wait_group<1>();
@@ -1521,6 +1528,7 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
     std::vector<int> slot(n, -1), freel, live, tptr{0}, lofs(npanel);
     std::vector<int4> trip;
     std::vector<int2> pext;
+    std::vector<int> retiring;
     for (int s2 = kFront - 1; s2 >= 0; --s2) freel.push_back(s2);
     long long lsize = 0;
     for (int k = 0; k < npanel && fits; ++k) {
@@ -1557,10 +1565,15 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
       pext.push_back(make_int2((int)rnext.size(), (int)tpiv.size()));
       lofs[k] = (int)lsize;
       lsize += (long long)(rptr[k + 1] - rptr[k]) * kPW + kPW * kPW;
-      std::vector<int> keep;  // the panel's pivots leave the front
+      // the panel's pivots leave the front; their slots are reused from panel
+      // k + 2 on (k_ldlt_sky lands panel k+1 while panel k's pivot columns
+      // may still be read)
+      std::vector<int> keep;
+      freel.insert(freel.end(), retiring.begin(), retiring.end());
+      retiring.clear();
       for (int m : live) {
         if (m < pend)
-          freel.push_back(slot[m]);
+          retiring.push_back(slot[m]);
         else
           keep.push_back(m);
       }
