@@ -216,6 +216,12 @@ int64_t pmx_kernel_launch_count(const pmx_context* ctx);
 int pmx_profile_enable(pmx_context* ctx, int on);
 int pmx_profile_reset(pmx_context* ctx);
 int pmx_profile_get(pmx_context* ctx, const char* kernel, double* total_ms, int64_t* launches);
+/* Device-side loops (the global_optimize GN loop) run as one CUDA graph with
+ * a conditional WHILE node (default on): the loop stops on the device when it
+ * converges, without enqueueing max_iterations iterations.  Off: the loop is
+ * enqueued kernel by kernel (every kernel checks the stop flag), which is what
+ * the per-kernel profile brackets need. */
+int pmx_set_device_graphs(pmx_context* ctx, int on);
 
 /* -------------------------------------------------- matching (camera.cpp) */
 

@@ -196,6 +196,10 @@ class Context:
     def profile_enable(self, on: bool = True):
         self._check(self.lib.pmx_profile_enable(self.h, int(on)))
 
+    def set_device_graphs(self, on: bool = True):
+        """Device loops as one CUDA graph with a conditional WHILE node (default)."""
+        self._check(self.lib.pmx_set_device_graphs(self.h, int(on)))
+
     def profile_reset(self):
         self._check(self.lib.pmx_profile_reset(self.h))
 

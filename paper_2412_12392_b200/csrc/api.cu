@@ -231,6 +231,13 @@ int pmx_profile_enable(pmx_context* c, int on) {
   });
 }
 
+int pmx_set_device_graphs(pmx_context* c, int on) {
+  return guarded(c, [&] {
+    reinterpret_cast<Context*>(c)->graphs = on != 0;
+    return (int)PMX_OK;
+  });
+}
+
 int pmx_profile_reset(pmx_context* c) {
   return guarded(c, [&] {
     Context& ctx = *reinterpret_cast<Context*>(c);

@@ -618,7 +618,7 @@ struct SkyArgs {
   const double* grad;       // rhs = -grad
   double* x;                // tau
   int n;
-  int attempt;              // damping attempt (backend.cpp:208-227)
+  int retries;              // damping attempts after the first (backend.cpp:208-227)
   double damping_init;
   GNState* st;
 };
@@ -656,8 +656,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-__global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
-  if (P.st->stop || P.st->solved) return;
+// One damping attempt (lambda on every diagonal entry, backend.cpp:208-227);
+// sets st->solved when the factorisation and tau pass the accept test.
+__device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   extern __shared__ double smem[];
   const int npanel = (P.n + kPW - 1) / kPW;
   int4* pin = reinterpret_cast<int4*>(smem);             // [npanel] panel info
@@ -672,11 +673,6 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   __shared__ int psl[2][kPW];
   __shared__ int ok;
   const int n = P.n, tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
-  double lambda = 0.0;
-  if (P.attempt > 0) {
-    lambda = P.damping_init;
-    for (int a = 1; a < P.attempt; ++a) lambda *= 10.0;
-  }
   for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
   for (int k = tid; k < npanel; k += nth) {
     pin[k] = P.pinfo[k];
@@ -940,6 +936,19 @@ __global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
   }
   __syncthreads();
   if (tid == 0 && good) P.st->solved = 1;
+}
+
+// All damping attempts in one launch: attempt a runs only while no earlier one
+// succeeded (the reference's retry loop, without a launch per attempt).
+__global__ void __launch_bounds__(kSkyThreads) k_ldlt_sky(SkyArgs P) {
+  double lambda = 0.0;
+  for (int attempt = 0; attempt <= P.retries; ++attempt) {
+    if (P.st->stop || P.st->solved) return;  // uniform: written before the barrier that ends an attempt
+    if (attempt == 1) lambda = P.damping_init;
+    if (attempt > 1) lambda *= 10.0;
+    sky_attempt(P, lambda);
+    __syncthreads();
+  }
 }
 
 #include "band.cuh"
@@ -1773,16 +1782,14 @@ static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, G
   const size_t smem = sizeof(double) * ((size_t)kFront * kFS + n + 2 * kFront * kPW) +
                       (sizeof(int4) + sizeof(int2)) * (size_t)npanel + sizeof(double) * (size_t)((npanel + 1) / 2);
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  for (int attempt = 0; attempt <= p.damping_retries; ++attempt) {
-    SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.pextra.as<int2>(), As.rinfo.as<int2>(), As.slot.as<int>(),
-              As.lofs.as<int>(), As.Lst.as<double>(), As.Dst.as<double>(), As.grad.as<double>(), tau, n, attempt,
-              p.damping_init, st};
-    {
-      ProfScope ps(ctx, "k_ldlt");
-      k_ldlt_sky<<<1, kSkyThreads, smem, ctx.stream>>>(a);
-    }
-    launch_check(ctx, "k_ldlt_sky");
+  SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.pextra.as<int2>(), As.rinfo.as<int2>(),
+            As.slot.as<int>(), As.lofs.as<int>(), As.Lst.as<double>(), As.Dst.as<double>(), As.grad.as<double>(), tau,
+            n, std::max(p.damping_retries, 0), p.damping_init, st};
+  {
+    ProfScope ps(ctx, "k_ldlt");
+    k_ldlt_sky<<<1, kSkyThreads, smem, ctx.stream>>>(a);
   }
+  launch_check(ctx, "k_ldlt_sky");
 }
 
 static double read_cost(Context& ctx, const DevGraph& G, const double* terms) {
@@ -1906,6 +1913,54 @@ extern "C" int pmx_impl_backend_solve_terms(pmx_context* c, pmx_memory mem, cons
   return PMX_OK;
 }
 
+// Continue the loop graph's WHILE node while the GN loop runs (device side).
+__global__ void k_gn_continue(const GNState* st, cudaGraphConditionalHandle h, int max_iterations) {
+  cudaGraphSetConditional(h, (!st->stop && st->iterations < max_iterations) ? 1u : 0u);
+}
+
+namespace pmx {
+// A device loop captured once per call: graph = { WHILE(handle) { body } }.
+struct LoopGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle handle = 0;
+  template <class Body>
+  void build(Context& ctx, Body body) {
+    PMX_CUDA(cudaGraphCreate(&graph, 0));
+    PMX_CUDA(cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams np = {};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = handle;
+    np.conditional.type = cudaGraphCondTypeWhile;
+    np.conditional.size = 1;
+    cudaGraphNode_t node;
+    PMX_CUDA(cudaGraphAddNode(&node, graph, nullptr, 0, &np));
+    cudaGraph_t bodyg = np.conditional.phGraph_out[0];
+    PMX_CUDA(cudaStreamBeginCaptureToGraph(ctx.stream, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    ctx.capturing = true;
+    try {
+      body();
+    } catch (...) {
+      ctx.capturing = false;
+      cudaGraph_t dummy;
+      cudaStreamEndCapture(ctx.stream, &dummy);
+      throw;
+    }
+    ctx.capturing = false;
+    PMX_CUDA(cudaStreamEndCapture(ctx.stream, &bodyg));
+    PMX_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  void launch(Context& ctx) {
+    PMX_CUDA(cudaGraphLaunch(exec, ctx.stream));
+    ++ctx.launches;
+  }
+  ~LoopGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+  }
+};
+}  // namespace pmx
+
 extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_graph* g, const pmx_backend_params* pp,
                                         pmx_optimize_result* result, pmx_sim3* pose_trace) {
   Context& ctx = *reinterpret_cast<Context*>(c);
@@ -1934,22 +1989,34 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
     PMX_CUDA(cudaMemcpyAsync(dP.p, P.data(), sizeof(DSim3) * n, cudaMemcpyHostToDevice, ctx.stream));
     PMX_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(GNState), ctx.stream));
     GNState* S = dst.as<GNState>();
+    auto iteration = [&] {  // backend.cpp:200-252, every kernel a no-op once st->stop
+      k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
+      assemble_sky(ctx, G, As, dP.as<DSim3>(), terms.as<double>(), half, S);
+      solve_sky(ctx, p, As, S, dtau.as<double>());
+      k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
+                                                            G.anchor, S);
+      edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
+      k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
+                                              dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
+      launch_check(ctx, "k_gn_iteration");
+    };
+    // The loop as one CUDA graph: a conditional WHILE node whose body is one
+    // iteration, continued from the device (k_gn_continue) until the loop
+    // stops or max_iterations ran - nothing is enqueued past convergence.
+    LoopGraph lg;
+    if (ctx.graphs && p.max_iterations > 0) lg.build(ctx, [&] {
+        iteration();
+        k_gn_continue<<<1, 1, 0, ctx.stream>>>(S, lg.handle, p.max_iterations);
+      });
     {
       ProfScope loop_scope(ctx, "gn_loop");  // the device loop (staging / planning excluded)
       edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), 0, G.E, terms.as<double>(), S, 0);
       k_gn_init<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), G.E, S);
       launch_check(ctx, "k_gn_init");
-      for (int iter = 0; iter < p.max_iterations; ++iter) {
-        k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
-        assemble_sky(ctx, G, As, dP.as<DSim3>(), terms.as<double>(), half, S);
-        solve_sky(ctx, p, As, S, dtau.as<double>());
-        k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
-                                                              G.anchor, S);
-        edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
-        k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
-                                                dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
-        launch_check(ctx, "k_gn_iteration");
-      }
+      if (lg.exec)
+        lg.launch(ctx);
+      else
+        for (int iter = 0; iter < p.max_iterations; ++iter) iteration();
     }
     GNState hs;
     PMX_CUDA(cudaMemcpyAsync(&hs, dst.p, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));

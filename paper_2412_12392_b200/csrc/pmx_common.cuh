@@ -53,6 +53,8 @@ struct Context {
   int64_t launches = 0;
   int num_sms = 148;
   bool profiling = false;
+  bool graphs = true;      // device-side loops as CUDA graphs (pmx_set_device_graphs)
+  bool capturing = false;  // a graph body is being captured: no per-kernel event brackets
   std::vector<ProfEvent> prof;  // unresolved event pairs (pmx_profile_*)
   std::map<std::string, int64_t> counters;  // profiling counters (pmx_profile_get, total_ms = 0)
   std::map<std::string, unsigned long long*> dev_counters;  // device-side counters, read at pmx_profile_get
@@ -73,15 +75,16 @@ inline unsigned long long* dev_counter(Context& ctx, const char* name) {
 struct ProfScope {
   Context& c;
   ProfEvent ev{nullptr, nullptr, nullptr};
-  ProfScope(Context& ctx, const char* name) : c(ctx) {
-    if (!c.profiling) return;
+  bool on;
+  ProfScope(Context& ctx, const char* name) : c(ctx), on(ctx.profiling && !ctx.capturing) {
+    if (!on) return;
     ev.name = name;
     cudaEventCreate(&ev.start);
     cudaEventCreate(&ev.stop);
     cudaEventRecord(ev.start, c.stream);
   }
   ~ProfScope() {
-    if (!c.profiling) return;
+    if (!on) return;
     cudaEventRecord(ev.stop, c.stream);
     c.prof.push_back(ev);
   }

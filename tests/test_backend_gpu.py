@@ -209,3 +209,26 @@ def test_banded_solver_matches_dense_solve(ctx):
     np.testing.assert_allclose(tau, ref, rtol=1e-6, atol=1e-9 * np.abs(ref).max())
     r = ctx.global_optimize(G, p)
     assert r.converged and r.iterations >= 1
+
+
+@pytest.mark.parametrize("n_kf,reach", [(20, 4), (400, 2)])
+def test_graph_loop_equals_enqueued_loop(ctx, n_kf, reach):
+    # the GN loop as one CUDA graph (conditional WHILE node, stops on the
+    # device) runs exactly the kernels of the enqueued loop: identical poses,
+    # iterations and cost trace, for the frontal (20 kf) and banded (400 kf) solvers
+    h, w = (48, 64) if n_kf < 100 else (12, 16)
+    p = _params()
+    p.damping_retries = 3
+    out = []
+    for graphs in (True, False):
+        ctx.set_device_graphs(graphs)
+        _, G, _ = _graph(n_kf=n_kf, reach=reach, h=h, w=w)
+        r = ctx.global_optimize(G, p, trace=True)
+        out.append((r, [(list(P.R), list(P.t), P.s) for P in G.poses]))
+    ctx.set_device_graphs(True)
+    (ra, pa), (rb, pb) = out
+    assert ra.iterations == rb.iterations and ra.converged == rb.converged
+    assert list(ra.cost_trace) == list(rb.cost_trace)
+    assert pa == pb
+    if n_kf < 100:
+        assert ra.iterations < p.max_iterations  # converged before the cap: the graph stopped early

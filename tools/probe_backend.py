@@ -22,6 +22,7 @@ ap.add_argument("--kf", type=int, default=100)
 ap.add_argument("--reach", type=int, default=4)
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--loops", type=int, default=1)
+ap.add_argument("--no-graphs", action="store_true")
 a = ap.parse_args()
 H, W = 384, 512
 t0 = time.time()
@@ -34,6 +35,8 @@ ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["m
 s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 ctx = Context(0, stream=s)
+if a.no_graphs:
+    ctx.set_device_graphs(False)
 p = abi.default_backend_params()
 p.weights.distance_weight = 0.1
 p.max_iterations = a.iters
