@@ -686,36 +686,42 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   // panel ahead; every panel ends with all copies landed.
   __shared__ int4 stri[2][kSkyThreads];   // entering triples of a panel (slot of panel k: k & 1)
   __shared__ double sval[2][kSkyThreads];  // their skyline values
+  // Copy roles: warps 1.. (ti = tid - 32) issue every copy and land every
+  // triple, so warp 0 - the look-ahead's critical path - issues none; the
+  // pivot-block triples (first in the list) and the next pivot slots belong to
+  // warp 1, which hands them to warp 0 through named barrier 2.
+  const int ti = tid - 32, ntc = nth - 32;
   auto issue_struct = [&](int k) {
     const int4 pi = pin[k];
-    if (pi.x + tid < pi.y) cp_async_n<16>(&stri[k & 1][tid], P.trip + pi.x + tid);
+    if (ti >= 0 && pi.x + ti < pi.y) cp_async_n<16>(&stri[k & 1][ti], P.trip + pi.x + ti);
   };
   auto issue_rows = [&](int k) {
     const int4 pi = pin[k];
-    if (pi.z + tid < pi.w) cp_async_n<8>(&rows[k & 1][tid], P.rinfo + pi.z + tid);
+    if (ti >= 0 && pi.z + ti < pi.w) cp_async_n<8>(&rows[k & 1][ti], P.rinfo + pi.z + ti);
   };
   auto issue_vals = [&](int k) {  // needs panel k's triples landed
     const int4 pi = pin[k];
-    if (pi.x + tid < pi.y) {
-      const int z = stri[k & 1][tid].z;
-      if (z >= 0) cp_async_n<8>(&sval[k & 1][tid], P.H + z);
+    if (ti >= 0 && pi.x + ti < pi.y) {
+      const int z = stri[k & 1][ti].z;
+      if (z >= 0) cp_async_n<8>(&sval[k & 1][ti], P.H + z);
     }
-    if (tid < min(kPW, n - kPW * k)) cp_async_n<4>(&psl[k & 1][tid], P.slot + kPW * k + tid);
+    if (ti >= 0 && ti < min(kPW, n - kPW * k)) cp_async_n<4>(&psl[k & 1][ti], P.slot + kPW * k + ti);
   };
   auto land = [&](int k) {  // this thread's entering triple of panel k (+ the rare overflow) into the front
     const int4 pi = pin[k];
-    if (pi.x + tid < pi.y) {
-      const int4 t = stri[k & 1][tid];
-      const double v = (t.z >= 0 ? sval[k & 1][tid] : 0.0) + (t.w ? lambda : 0.0);  // backend.cpp:210-213
+    if (ti >= 0 && pi.x + ti < pi.y) {
+      const int4 t = stri[k & 1][ti];
+      const double v = (t.z >= 0 ? sval[k & 1][ti] : 0.0) + (t.w ? lambda : 0.0);  // backend.cpp:210-213
       F[t.x * kFS + t.y] = v;
       F[t.y * kFS + t.x] = v;
     }
-    for (int t = pi.x + nth + tid; t < pi.y; t += nth) {  // rare: more triples than threads (never pivot ones)
-      const int4 q = P.trip[t];
-      const double v = (q.z >= 0 ? P.H[q.z] : 0.0) + (q.w ? lambda : 0.0);
-      F[q.x * kFS + q.y] = v;
-      F[q.y * kFS + q.x] = v;
-    }
+    if (ti >= 0)
+      for (int t = pi.x + ntc + ti; t < pi.y; t += ntc) {  // rare: more triples than threads (never pivot ones)
+        const int4 q = P.trip[t];
+        const double v = (q.z >= 0 ? P.H[q.z] : 0.0) + (q.w ? lambda : 0.0);
+        F[q.x * kFS + q.y] = v;
+        F[q.y * kFS + q.x] = v;
+      }
   };
   // Warp 0: the 7x7 pivot block of panel k from the front, in registers
   // (lane r holds row r) -> sD/sIv[fb], the block's unit L and D, and the
@@ -849,18 +855,21 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
       asm volatile("bar.arrive 1, %0;" ::"r"(nth) : "memory");
       SKY_T(1)
       if (next) {
-        cp_async_wait_group<1>();  // group A of this thread
-        __syncwarp();
-        land(k + 1);
         for (int t = lane; t < nlead; t += 32) schur(t, buf);
-        __syncwarp();
+        asm volatile("bar.sync 2, 64;" ::: "memory");  // warp 1 landed the pivot triples and slots
         factor(k + 1, buf ^ 1);
       }
     } else {
+      if (warp == 1 && next) {
+        cp_async_wait_group<1>();  // group A of this thread
+        land(k + 1);
+        __threadfence_block();
+        asm volatile("bar.arrive 2, 64;" ::: "memory");
+      }
       asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");  // every row of (b) is in
       SKY_T(1)
       for (int t = nlead + tid - 32; t < npair; t += nth - 32) schur(t, buf);
-      if (next) {
+      if (next && warp != 1) {
         cp_async_wait_group<1>();
         land(k + 1);
       }
