@@ -204,6 +204,20 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
     if (keep & (1u << j)) *out++ = rec[j];
 }
 
+// Asynchronous global -> shared copies (cp.async): the next panel's structure
+// and entering values travel while the current panel is factorised, without
+// holding registers (a register prefetch here was spilled to local memory,
+// which made every panel wait for its loads).
+template <int B>
+__device__ __forceinline__ void cp_async_n(void* sdst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(B) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Both directed constraints of one compacted match, packed as a float2 pair
 // (.x: ref = i, src = j, swapped; .y: ref = j, src = i).  The FP64 offsets
 // delta = T src - ref are per direction; everything after them runs as packed
@@ -250,10 +264,13 @@ __device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<d
   ray_match_scalar(T1, T2, __ldg(Ci + m.x), __ldg(Cj + m.y), info, c, reinterpret_cast<float*>(acc));
 }
 
-// Both directed constraints of an edge from one read of its compacted matches
-// (two matches in flight per thread).
+constexpr int kEdgeSmem = (6 * 256 + 8 * 256) * 16;  // cp.async stages of k_edge_terms_ray (56 KB)
+static_assert(kEdgeSmem >= block_reduce_scratch_bytes<2 * kRayAcc>(), "reduction scratch aliases the stages");
+
+// Both directed constraints of an edge from one read of its compacted matches.
 __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
   if (gn_stopped(A.st)) return;
+  extern __shared__ int4 edge_sm[];
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
@@ -269,21 +286,56 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
     const float inv_s2 = A.inv_s2;
     const RayW c = A.rw;
     const int64_t stride = (int64_t)A.bpe * blockDim.x;
-    int64_t k = (int64_t)b * blockDim.x + threadIdx.x;
-    for (; k + stride < cnt; k += 2 * stride) {
-      const int4 m0 = __ldg(P + k), m1 = __ldg(P + k + stride);
-      const float4 a0 = __ldg(Ci + m0.x), b0 = __ldg(Cj + m0.y);
-      const float4 a1 = __ldg(Ci + m1.x), b1 = __ldg(Cj + m1.y);
-      ray_match(T1, T2, m0, Ci, Cj, a0, b0, inv_s2, c, acc);
-      ray_match(T1, T2, m1, Ci, Cj, a1, b1, inv_s2, c, acc);
+    const int64_t k0 = (int64_t)b * blockDim.x + threadIdx.x;
+    // Per-thread cp.async pipeline (no block barriers: every thread consumes
+    // only what it copied): while tile t (this thread's matches 2t, 2t+1) is
+    // evaluated, the records of tile t+2 and the two points of each match of
+    // tile t+1 travel into shared memory, holding no registers.
+    int4* R = edge_sm;                                        // [3 stages][2][256] records
+    float4* PT = reinterpret_cast<float4*>(edge_sm + 6 * 256);  // [2 stages][2][2 (Pi, Pj)][256]
+    const int tid = threadIdx.x;
+    auto rslot = [&](int t, int j) { return R + ((t % 3) * 2 + j) * 256 + tid; };
+    auto pslot = [&](int t, int j, int side) { return PT + (((t & 1) * 2 + j) * 2 + side) * 256 + tid; };
+    const int64_t nmine = k0 < cnt ? (cnt - k0 + stride - 1) / stride : 0;
+    const int ntile = (int)((nmine + 1) / 2);
+    auto kof = [&](int t, int j) { return k0 + (int64_t)(2 * t + j) * stride; };
+    auto issue_rec = [&](int t) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (2 * t + j < nmine) cp_async_n<16>(rslot(t, j), P + kof(t, j));
+    };
+    auto issue_pts = [&](int t) {  // needs tile t's records landed
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (2 * t + j < nmine) {
+          const int4 m = *rslot(t, j);
+          cp_async_n<16>(pslot(t, j, 0), Ci + m.x);
+          cp_async_n<16>(pslot(t, j, 1), Cj + m.y);
+        }
+    };
+    if (ntile > 0) {
+      issue_rec(0);
+      issue_rec(1);
+      cp_async_commit();
+      cp_async_wait_all();
+      issue_pts(0);
+      cp_async_commit();
     }
-    if (k < cnt) {
-      const int4 m0 = __ldg(P + k);
-      ray_match(T1, T2, m0, Ci, Cj, __ldg(Ci + m0.x), __ldg(Cj + m0.y), inv_s2, c, acc);
+    for (int t = 0; t < ntile; ++t) {
+      cp_async_wait_all();  // points of tile t, records of tile t+1
+      issue_pts(t + 1);
+      issue_rec(t + 2);
+      cp_async_commit();
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (2 * t + j < nmine)
+          ray_match(T1, T2, *rslot(t, j), Ci, Cj, *pslot(t, j, 0), *pslot(t, j, 1), inv_s2, c, acc);
     }
   }
-  block_reduce_n<2 * kRayAcc, true>(reinterpret_cast<const float*>(acc),
-                                    A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc));
+  cp_async_wait_all();
+  __syncthreads();  // the pipeline's shared memory becomes the reduction scratch
+  block_reduce_n_ext<2 * kRayAcc, true>(reinterpret_cast<const float*>(acc),
+                                        A.partials + ((size_t)e * A.bpe + b) * (2 * kRayAcc), edge_sm);
 }
 
 // Sum the closed-form partials of an edge and expand to {H 28, g 7, cost} x 2.
@@ -641,20 +693,6 @@ __device__ __forceinline__ double fast_rcp(double d) {
   e = fma(-d, r, 1.0);
   return fma(r, e, r);
 }
-
-// Asynchronous global -> shared copies (cp.async): the next panel's structure
-// and entering values travel while the current panel is factorised, without
-// holding registers (a register prefetch here was spilled to local memory,
-// which made every panel wait for its loads).
-template <int B>
-__device__ __forceinline__ void cp_async_n(void* sdst, const void* gsrc) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(d), "l"(gsrc), "n"(B) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // One damping attempt (lambda on every diagonal entry, backend.cpp:208-227);
 // sets st->solved when the factorisation and tau pass the accept test.
@@ -1332,6 +1370,7 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   A.packed = ray ? G.pk.as<int4>() : nullptr;
   A.pk_total = ray ? G.pk_total.as<int>() : nullptr;
   A.seg = G.seg;
+  PMX_CUDA(cudaFuncSetAttribute((const void*)k_edge_terms_ray, cudaFuncAttributeMaxDynamicSharedMemorySize, kEdgeSmem));
   A.inv_s2 = (float)(1.0 / A.wp.sigma2);
   A.rw = RayW{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta), (float)A.wp.distance_weight};
 }
@@ -1355,7 +1394,7 @@ static void edge_terms_dev(Context& ctx, const DevGraph& G, const pmx_backend_pa
     {
       ProfScope ps(ctx, "k_edge_terms");
       if (ray)
-        k_edge_terms_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(A, c0);
+        k_edge_terms_ray<<<dim3(W.bpe, cn), 256, kEdgeSmem, ctx.stream>>>(A, c0);
       else
         k_edge_terms<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(A, c0);
     }
