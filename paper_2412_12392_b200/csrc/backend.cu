@@ -2002,10 +2002,13 @@ struct LoopGraph {
     PMX_CUDA(cudaGraphLaunch(exec, ctx.stream));
     ++ctx.launches;
   }
-  ~LoopGraph() {
+  void reset() {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
   }
+  ~LoopGraph() { reset(); }
 };
 }  // namespace pmx
 
@@ -2052,10 +2055,17 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
     // iteration, continued from the device (k_gn_continue) until the loop
     // stops or max_iterations ran - nothing is enqueued past convergence.
     LoopGraph lg;
-    if (ctx.graphs && p.max_iterations > 0) lg.build(ctx, [&] {
-        iteration();
-        k_gn_continue<<<1, 1, 0, ctx.stream>>>(S, lg.handle, p.max_iterations);
-      });
+    if (ctx.graphs && p.max_iterations > 0) {
+      try {
+        lg.build(ctx, [&] {
+          iteration();
+          k_gn_continue<<<1, 1, 0, ctx.stream>>>(S, lg.handle, p.max_iterations);
+        });
+      } catch (const Error&) {  // no conditional graph nodes here: enqueue the loop instead
+        lg.reset();
+        cudaGetLastError();
+      }
+    }
     {
       ProfScope loop_scope(ctx, "gn_loop");  // the device loop (staging / planning excluded)
       edge_terms_dev(ctx, G, p, W, dP.as<DSim3>(), 0, G.E, terms.as<double>(), S, 0);
