@@ -910,29 +910,39 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair.
 // match_pointmaps for b-pixel n (camera.cpp:213-236): LM from the seed,
 // lround + clamp, validity, q.  Writes the outputs; returns (pa, valid).
-__device__ __forceinline__ int2 match_pixel(const PairDev& P, const LMParams& lp, int n) {
+// (u, v): the b-pixel's column / row (n = v W_b + u).  Returns {pixel_a,
+// valid, column, row of pixel_a} (pixel_a = -1: skipped pixel).
+__device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp, int n, int u, int v) {
   if (P.out_pb) P.out_pb[n] = n;
   int32_t pa_out = -1;
   float q_out = 0.0f;
   uint8_t valid_out = 0;
+  int cu = 0, cv = 0;
   const bool vb = P.vb ? P.vb[n] != 0 : true;
   const double x0 = P.xb[3 * n], x1 = P.xb[3 * n + 1], x2 = P.xb[3 * n + 2];
   // camera.cpp:217-219 (norm < 1e-12 skips; a NaN norm does not)
   const double xnorm = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
   if (vb && !(xnorm < 1e-12)) {
-    int seed_pixel = n;
+    // seed = pixel n of the a-grid (camera.cpp:221), or the init match
+    int su = u, sv = v;
+    if (P.Wa != P.Wb) {
+      su = n % P.Wa;
+      sv = n / P.Wa;
+    }
     if (P.seed_last) {
       const int k = P.seed_last[n];
       if (k >= 0) {
         const int s = P.init_pa[k];
-        if (s >= 0) seed_pixel = s;
+        if (s >= 0) {
+          su = s % P.Wa;
+          sv = s / P.Wa;
+        }
       }
     }
-    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)(seed_pixel % P.Wa),
-                                             (double)(seed_pixel / P.Wa), lp);
-    const int pu = (int)round(pr.pu);  // std::lround: half away from zero
-    const int pv = (int)round(pr.pv);
-    int pa = min(max(pv, 0), P.Ha - 1) * P.Wa + min(max(pu, 0), P.Wa - 1);
+    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp);
+    cu = min(max((int)round(pr.pu), 0), P.Wa - 1);  // std::lround: half away from zero
+    cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
+    int pa = cv * P.Wa + cu;
     bool valid = pr.converged && (P.va ? P.va[pa] != 0 : true);
     if (valid) {
       const double a0 = P.xa[3 * pa], a1 = P.xa[3 * pa + 1], a2 = P.xa[3 * pa + 2];
@@ -947,19 +957,15 @@ __device__ __forceinline__ int2 match_pixel(const PairDev& P, const LMParams& lp
   P.out_pa[n] = pa_out;
   P.out_q[n] = q_out;
   P.out_valid[n] = valid_out;
-  return make_int2(pa_out, valid_out);
+  return make_int4(pa_out, valid_out, cu, cv);
 }
 
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair (no refinement).
 __global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
-  const PairDev& P = pairs[blockIdx.y];
-  const int tiles_x = (P.Wb + 31) / 32;
-  const int tiles = tiles_x * ((P.Hb + 7) / 8);
-  if ((int)blockIdx.x >= tiles) return;
-  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31);
-  const int v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+  const PairDev& P = pairs[blockIdx.z];
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (u >= P.Wb || v >= P.Hb) return;
-  match_pixel(P, lp, v * P.Wb + u);
+  match_pixel(P, lp, v * P.Wb + u, u, v);
 }
 
 // K4: feature_refine of the valid matches just written by k_match, in place.
@@ -1161,15 +1167,16 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
 // of some warps overlap the integer-bound refinement of others on every SM.
 __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
                                                          RefineLevels L, unsigned long long* __restrict__ exact_px) {
-  const PairDev& P = pairs[blockIdx.y];
-  const int tiles_x = (P.Wb + 31) / 32;
-  if ((int)blockIdx.x >= tiles_x * ((P.Hb + 7) / 8)) return;
-  const int u = (blockIdx.x % tiles_x) * 32 + (threadIdx.x & 31), v = (blockIdx.x / tiles_x) * 8 + (threadIdx.x >> 5);
+  const PairDev& P = pairs[blockIdx.z];
+  if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * 8 >= P.Hb) return;
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
   const int m = v * P.Wb + u;
-  int n = -1, pa = 0;
+  int n = -1, pa = 0, pcu = 0, pcv = 0;
   if (u < P.Wb && v < P.Hb) {
-    const int2 r = match_pixel(P, lp, m);
+    const int4 r = match_pixel(P, lp, m, u, v);
     pa = r.x;
+    pcu = r.z;
+    pcv = r.w;
     if (r.y) n = m;
   }
   const bool fast_pair = P.q8a != nullptr && P.sel->qbad == 0;
@@ -1188,7 +1195,7 @@ __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restri
     tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
     fast = !q.bad;
   }
-  QState q{pa % P.Wa, pa / P.Wa, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
+  QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
   if (__any_sync(0xffffffffu, fast)) {
     const QGlob T{P.q8a, P.q8b, P.Wa};
     q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
@@ -1456,17 +1463,19 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
       ProfScope ps(ctx, "k_prep");
       prep_rays(ctx, dp, cn, max_hwa);
     }
-    int max_tiles = 0;
-    for (int i = c0; i < c0 + cn; ++i)
-      max_tiles = std::max(max_tiles, ((hp[i].Wb + 31) / 32) * ((hp[i].Hb + 7) / 8));
+    int max_tx = 0, max_ty = 0;  // grid (x tiles, y tiles, pairs) of 32x8 b-pixel tiles
+    for (int i = c0; i < c0 + cn; ++i) {
+      max_tx = std::max(max_tx, (hp[i].Wb + 31) / 32);
+      max_ty = std::max(max_ty, (hp[i].Hb + 7) / 8);
+    }
     if (refine && L.n > 0) {
       ProfScope ps(ctx, "k_match_refine");
       unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
-      k_match_refine<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp, L, exact_px);
+      k_match_refine<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp, L, exact_px);
       launch_check(ctx, "k_match_refine");
     } else {
       ProfScope ps(ctx, "k_match");
-      k_match<<<dim3(max_tiles, cn), 256, 0, ctx.stream>>>(dp, lp);
+      k_match<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp);
       launch_check(ctx, "k_match");
     }
     if (hooks) hooks->after_chunk(c0, cn);
