@@ -38,11 +38,11 @@ H, W = 384, 512
 N_EDGES = 64
 ALG_BYTES_PER_PX = 133  # X_b 12 + X_a 12 + Q_a 4 + Q_b 4 + D_a 48 + D_b 48 + idx 4 + valid 1
 # Algorithmic bytes per b-pixel of each matching kernel:
-#  k_select X_a 12 + valid_a 1 (norm keys + 3 radix-select rounds)        = 13
-#  k_prep   X_a 12 + valid_a 1 + D_a 48                               = 61
+#  k_select 3 radix-select rounds over the 4-B norm keys                  = 12
+#  k_prep   X_a 12 + valid_a 1 + D_a 48 (rays, int8 image, norm keys)   = 61
 #  k_match_refine  X_b 12 + valid_b 1 + X_a (one ray per pixel) 12 + D_b 48 + Q_a 4 + Q_b 4
 #                  + pa/valid/q out 9                                  = 90
-KERNEL_BYTES_PER_PX = {"k_select": 13, "k_prep": 61, "k_match_refine": 90}
+KERNEL_BYTES_PER_PX = {"k_select": 12, "k_prep": 61, "k_match_refine": 90}
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
 
 

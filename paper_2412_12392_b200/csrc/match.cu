@@ -232,16 +232,31 @@ __global__ void __launch_bounds__(256) k_keys(const PairDev* __restrict__ pairs,
 // exact division as the reference), the int8 descriptor image for the
 // refinement (+ its per-pair error-bound statistics), or the fp32 norm bounds
 // of the standalone refine.
-__global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block) {
+__global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs, int px_per_block, bool with_keys) {
   const PairDev& P = pairs[blockIdx.y];
   const int HW = P.Ha * P.Wa;
   const int begin = blockIdx.x * px_per_block;
   const int end = min(HW, begin + px_per_block);
+  // with_keys: also the median's norm keys and their first histogram level
+  // (k_keys folded in: one read of X_a instead of two)
+  __shared__ uint32_t sh[kHist1];
+  if (with_keys) {
+    for (int i = threadIdx.x; i < kHist1; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
   int a1max = 0, qbad = 0;
   for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
     const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
     const bool v = P.va ? P.va[i] != 0 : true;
     const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+    if (with_keys) {  // k_keys
+      uint32_t key = kNoKey;
+      if (v && nrm > 1e-12) {
+        key = __float_as_uint((float)nrm);
+        atomicAdd(&sh[key >> 20], 1u);
+      }
+      P.keys[i] = key;
+    }
     double4 r = make_double4(0.0, 0.0, 1.0, 0.0);
     if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
     P.rays[i] = r;
@@ -265,6 +280,11 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       if (a1max) atomicMax(&P.sel->a1max, a1max);
       if (qbad) atomicOr(&P.sel->qbad, qbad);
     }
+  }
+  if (with_keys) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHist1; i += blockDim.x)
+      if (sh[i]) atomicAdd(&P.hist[i], sh[i]);
   }
 }
 
@@ -1360,11 +1380,10 @@ static void check_pointmap(const pmx_pointmap& p) {
 // Median threshold (camera.cpp:178-200) of every pair of `dev_pairs[0..n)`
 // (keys / hist / sel set), enqueued on ctx.stream: one key pass and three
 // radix-select rounds over all pairs at once.
-static void select_median(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
+// The three radix rounds after the keys and the first histogram level.
+static void select_rounds(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
   const int ppb = 4096;
   dim3 g1((max_hwa + ppb - 1) / ppb, n);
-  k_keys<<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
-  launch_check(ctx, "k_keys");
   k_sel_scan<1><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
   launch_check(ctx, "k_sel_scan1");
   k_sel_hist<2><<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
@@ -1377,9 +1396,16 @@ static void select_median(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, 
   launch_check(ctx, "k_sel_scan3");
 }
 
-static void prep_rays(Context& ctx, PairDev* dev_pairs, int n, int max_hwa) {
+static void select_median(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
+  const int ppb = 4096;
+  k_keys<<<dim3((max_hwa + ppb - 1) / ppb, n), 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_keys");
+  select_rounds(ctx, dev_pairs, n, max_hwa, fraction);
+}
+
+static void prep_rays(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, bool with_keys = false) {
   const int ppb = 1024;
-  k_prep<<<dim3((max_hwa + ppb - 1) / ppb, n), 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  k_prep<<<dim3((max_hwa + ppb - 1) / ppb, n), 256, 0, ctx.stream>>>(dev_pairs, ppb, with_keys);
   launch_check(ctx, "k_prep");
 }
 
@@ -1451,17 +1477,17 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
   PMX_CUDA(cudaMemsetAsync(sel.p, 0, sel.bytes, ctx.stream));
   if (hooks) hooks->before_select();
-  {
-    ProfScope ps(ctx, "k_select");
-    select_median(ctx, dpairs.as<PairDev>(), npairs, max_hwa, lp.median_fraction);
-  }
   for (int c0 = 0; c0 < npairs; c0 += chunk) {
     const int cn = std::min(chunk, npairs - c0);
     PairDev* dp = dpairs.as<PairDev>() + c0;
     if (hooks) hooks->before_chunk(c0, cn);
     {
-      ProfScope ps(ctx, "k_prep");
-      prep_rays(ctx, dp, cn, max_hwa);
+      ProfScope ps(ctx, "k_prep");  // rays, int8 image, norm keys + first histogram level
+      prep_rays(ctx, dp, cn, max_hwa, true);
+    }
+    {
+      ProfScope ps(ctx, "k_select");
+      select_rounds(ctx, dp, cn, max_hwa, lp.median_fraction);
     }
     int max_tx = 0, max_ty = 0;  // grid (x tiles, y tiles, pairs) of 32x8 b-pixel tiles
     for (int i = c0; i < c0 + cn; ++i) {
