@@ -153,12 +153,23 @@ struct TrackArgs {
 
 __device__ void load_sums(const double* __restrict__ partials, int nblocks, bool ray, double* H, double* g,
                           double* cost) {
-  // block 0, all threads: deterministic ordered sum; results into shared
+  // block 0, all threads: fixed-order sum (deterministic), columns x 8 row
+  // groups in parallel, then the groups in order; results into shared
   __shared__ double s[kAcc];
+  __shared__ double grp[8][kAcc];
   const int n = ray ? kRayAcc : kAcc;
+  for (int t = threadIdx.x; t < 8 * n; t += blockDim.x) {
+    const int i = t % n, q = t / n;
+    const int b0 = (int)((int64_t)nblocks * q / 8), b1 = (int)((int64_t)nblocks * (q + 1) / 8);
+    double a = 0.0;
+#pragma unroll 4
+    for (int b = b0; b < b1; ++b) a += partials[(size_t)b * kAcc + i];
+    grp[q][i] = a;
+  }
+  __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double a = 0.0;
-    for (int b = 0; b < nblocks; ++b) a += partials[(size_t)b * kAcc + i];
+    for (int q = 0; q < 8; ++q) a += grp[q][i];
     s[i] = a;
   }
   __syncthreads();
@@ -178,8 +189,103 @@ __device__ void load_sums(const double* __restrict__ partials, int nblocks, bool
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) k_track_gn(TrackArgs A) {
+// ldlt_pivoted_solve(7, ...) (pmx_common.cuh, Eigen's pivoted LDLT) on one
+// warp with the matrix in shared memory: the same operations in the same
+// order on every element (bit-identical), lanes over rows / columns where the
+// reference's loops are independent.  H, g: this warp's inputs; tau out.
+__device__ void ldlt7_solve_warp(const double* H, const double* mg, double* tau, double* M, double* tmp, int* tr) {
+  constexpr int n = 7;
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < n * n; i += 32) M[i] = H[i];
+  __syncwarp();
+  for (int k = 0; k < n; ++k) {
+    int big = k;
+    if (lane == 0) {  // first largest |diagonal| (strict '>', as the scan of the reference)
+      double bigv = fabs(M[k * n + k]);
+      for (int i = k + 1; i < n; ++i)
+        if (fabs(M[i * n + i]) > bigv) {
+          bigv = fabs(M[i * n + i]);
+          big = i;
+        }
+      tr[k] = big;
+    }
+    big = __shfl_sync(0xffffffffu, big, 0);
+    if (k != big) {
+      if (lane < k) {
+        const double t = M[k * n + lane];
+        M[k * n + lane] = M[big * n + lane];
+        M[big * n + lane] = t;
+      }
+      if (lane > big && lane < n) {
+        const double t = M[lane * n + k];
+        M[lane * n + k] = M[lane * n + big];
+        M[lane * n + big] = t;
+      }
+      if (lane == 0) {
+        const double t = M[k * n + k];
+        M[k * n + k] = M[big * n + big];
+        M[big * n + big] = t;
+      }
+      if (lane > k && lane < big) {
+        const double t = M[lane * n + k];
+        M[lane * n + k] = M[big * n + lane];
+        M[big * n + lane] = t;
+      }
+    }
+    __syncwarp();
+    if (k > 0) {
+      if (lane < k) tmp[lane] = M[lane * n + lane] * M[k * n + lane];
+      __syncwarp();
+      if (lane >= k && lane < n) {
+        double a = 0.0;
+        for (int c = 0; c < k; ++c) a += M[lane * n + c] * tmp[c];
+        M[lane * n + k] -= a;  // lane k: the diagonal (acc of the reference)
+      }
+      __syncwarp();
+    }
+    const double akk = M[k * n + k];
+    const bool ok = fabs(akk) > 0.0;
+    if (k == 0 && !ok) {
+      if (lane < n) tau[lane] = 0.0;
+      __syncwarp();
+      return;
+    }
+    if (ok && lane > k && lane < n) M[lane * n + k] /= akk;
+    __syncwarp();
+  }
+  if (lane == 0) {  // substitutions: sequential, as the reference
+    double d[n];
+    for (int i = 0; i < n; ++i) d[i] = mg[i];
+    for (int k = 0; k < n; ++k) {
+      const double t = d[k];
+      d[k] = d[tr[k]];
+      d[tr[k]] = t;
+    }
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < i; ++c) d[i] -= M[i * n + c] * d[c];
+    for (int i = 0; i < n; ++i) {
+      if (fabs(M[i * n + i]) > 2.2250738585072014e-308)
+        d[i] /= M[i * n + i];
+      else
+        d[i] = 0.0;
+    }
+    for (int i = n - 1; i >= 0; --i)
+      for (int r = i + 1; r < n; ++r) d[i] -= M[r * n + i] * d[r];
+    for (int k = n - 1; k >= 0; --k) {
+      const double t = d[k];
+      d[k] = d[tr[k]];
+      d[tr[k]] = t;
+    }
+    for (int i = 0; i < n; ++i) tau[i] = d[i];
+  }
+  __syncwarp();
+}
+
+template <bool RAY>
+__global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
   cg::grid_group grid = cg::this_grid();
+  __shared__ double s_Hd[49], s_mg[7], s_tau[7], s_M[49], s_tmp[7];  // block 0's 7x7 solve
+  __shared__ int s_tr[7];
   GNState* st = A.st;
   const int nb = gridDim.x;
   // valid_count (camera.cpp:10-14) for the lost test (tracking.cpp:165-168)
@@ -209,7 +315,7 @@ __global__ void __launch_bounds__(256) k_track_gn(TrackArgs A) {
   if (st->stop) return;
   WeightsDev wp = A.wp;
   wp.q_min = st->q_min;
-  const bool ray = A.mode == PMX_TRACK_RAY;
+  constexpr bool ray = RAY;  // ray mode gets its own instance (register budget)
   if (ray) {
     eval_pass_ray(make_pose<double>(st->T), A.M, A.Xref, A.Xsrc, wp, A.partials);
   } else {
@@ -229,14 +335,21 @@ __global__ void __launch_bounds__(256) k_track_gn(TrackArgs A) {
   }
   grid.sync();
   for (int it = 0; it < A.max_iterations; ++it) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+      // tracking.cpp:200-206 (the 7x7 pivoted LDLT on warp 0, bit-identical)
+      for (int i = threadIdx.x; i < 49; i += 32) s_Hd[i] = st->H[i];
+      __syncwarp();
+      if (threadIdx.x < 7) {
+        s_Hd[threadIdx.x * 8] += st->lambda * fmax(st->H[threadIdx.x * 8], 1e-12);
+        s_mg[threadIdx.x] = -st->g[threadIdx.x];
+      }
+      __syncwarp();
+      ldlt7_solve_warp(s_Hd, s_mg, s_tau, s_M, s_tmp, s_tr);
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      // tracking.cpp:200-206
       st->iterations++;
-      double Hd[49], mg[7], tau[7];
-      for (int i = 0; i < 49; ++i) Hd[i] = st->H[i];
-      for (int k = 0; k < 7; ++k) Hd[k * 8] += st->lambda * fmax(st->H[k * 8], 1e-12);
-      for (int k = 0; k < 7; ++k) mg[k] = -st->g[k];
-      ldlt_pivoted_solve(7, Hd, mg, tau);
+      double tau[7];
+      for (int k = 0; k < 7; ++k) tau[k] = s_tau[k];
       bool fin = true;
       double inf = 0.0;
       for (int k = 0; k < 7; ++k) {
@@ -494,7 +607,8 @@ extern "C" int pmx_impl_track_given_matches(pmx_context* c, pmx_memory mem, cons
   PMX_CUDA(cudaMemcpyAsync(segbuf.p, &seg, sizeof(seg), cudaMemcpyHostToDevice, ctx.stream));
   segmented_median(ctx, segbuf.as<SelSeg>(), 1, A.M.count, selscratch);
   A.median_dev = median.as<double>();
-  const int nb = grid_for(ctx, (const void*)k_track_gn, 256);
+  const void* kern = mode == PMX_TRACK_RAY ? (const void*)k_track_gn<true> : (const void*)k_track_gn<false>;
+  const int nb = grid_for(ctx, kern, 256);
   DevBuf partials(sizeof(double) * kAcc * nb, ctx.stream), state(sizeof(GNState), ctx.stream);
   GNState init_state;
   std::memset(&init_state, 0, sizeof(init_state));
@@ -515,7 +629,7 @@ extern "C" int pmx_impl_track_given_matches(pmx_context* c, pmx_memory mem, cons
   }
   {
     ProfScope ps(ctx, "k_track_gn");
-    PMX_CUDA(cudaLaunchCooperativeKernel((const void*)k_track_gn, dim3(nb), dim3(256), args, 0, ctx.stream));
+    PMX_CUDA(cudaLaunchCooperativeKernel(kern, dim3(nb), dim3(256), args, 0, ctx.stream));
   }
   launch_check(ctx, "k_track_gn");
   GNState out;
