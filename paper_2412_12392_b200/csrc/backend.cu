@@ -929,6 +929,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   // of the panel (prefetched one panel ahead) and forms its product with x;
   // warp c sums column c.
   __shared__ double colsum[kPW];
+  __shared__ double sLc[2][kPW * kPW];  // pivot blocks' unit L, one panel ahead (cp.async, warp 1)
   double lv = 0.0;
   int lrow = -1;
   auto bissue = [&](int k) {
@@ -939,20 +940,24 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
       lv = P.Lst[plofs[k] + tid];
       lrow = P.rinfo[pi.z + tid / kPW].x;
     }
+    if (warp == 1)
+      for (int i = lane; i < kPW * kPW; i += 32)
+        cp_async_n<8>(&sLc[k & 1][i], P.Lst + plofs[k] + ns * kPW + i);
+    cp_async_commit();
   };
   bissue(npanel - 1);
   for (int k = npanel - 1; k >= 0; --k) {
     const int c0 = kPW * k, nb = min(kPW, n - c0);
     const int4 pi = pin[k];
     const int ns = pi.w - pi.z;
-    const double* Lp = P.Lst + plofs[k];
     if (tid < ns * kPW) sW[tid] = lv * y[lrow];
+    cp_async_wait_all();  // warp 1: this panel's pivot block
+    __syncthreads();
     double lc[kPW];  // warp 0: column `lane` of the pivot block's unit L
     if (warp == 0) {
 #pragma unroll
-      for (int c = 0; c < kPW; ++c) lc[c] = (lane < nb && c < nb) ? Lp[ns * kPW + c * kPW + lane] : 0.0;
+      for (int c = 0; c < kPW; ++c) lc[c] = (lane < nb && c < nb) ? sLc[k & 1][c * kPW + lane] : 0.0;
     }
-    __syncthreads();
     if (k > 0) bissue(k - 1);
     if (warp < nb) {
       double sacc = 0.0;
