@@ -232,3 +232,36 @@ def test_graph_loop_equals_enqueued_loop(ctx, n_kf, reach):
     assert pa == pb
     if n_kf < 100:
         assert ra.iterations < p.max_iterations  # converged before the cap: the graph stopped early
+
+
+@pytest.mark.parametrize("n_kf,reach,h,w", [(8, 2, 48, 64), (400, 2, 12, 16)])
+def test_damping_retry_on_zero_pivot(ctx, n_kf, reach, h, w):
+    # a keyframe whose edges carry no valid match has an all-zero 7x7 block:
+    # the undamped factorisation meets an exact zero pivot and fails, the
+    # retry with lambda = damping_init on every diagonal succeeds
+    # (backend.cpp:208-227) - frontal (8 kf) and banded (400 kf) solvers
+    g = pmxgen.backend_graph(n_kf, reach, 3, height=h, width=w, radius=1.0)
+    lone = n_kf // 2
+    ms, oms = [], []
+    for (i, j), m in zip(g["edges"], g["matches"]):
+        valid = np.zeros_like(m["valid"]) if lone in (i, j) else m["valid"]
+        ms.append(MatchSet(m["pixel_a"], m["confidence"], valid))
+        oms.append(pyoracle.MatchSet(m["pixel_a"], np.arange(h * w), m["confidence"].astype(np.float64), valid))
+    poses = [T.to_struct(abi.pmx_sim3) for T in g["init"]]
+    G = Graph([Pointmap(x, v, h, w) for x, v in g["canonicals"]], poses, g["edges"], ms, anchor=0)
+    p = _params()
+    p.max_iterations = 2
+    terms = ctx.backend_edge_terms(G, p)
+    tau, cost, solved = ctx.backend_solve_terms(G, terms, p)
+    assert solved
+    np.testing.assert_array_equal(tau[7 * lone:7 * lone + 7], 0.0)  # g = 0 on the lone keyframe
+    r = ctx.global_optimize(G, p)
+    assert r.iterations >= 1
+    if n_kf < 100:  # the oracle at the small size: same retry semantics, same poses
+        O = pyoracle.Graph(g["canonicals"], [T.to_struct(abi.pmx_sim3) for T in g["init"]], g["edges"], oms, h, w)
+        pyoracle.global_optimize(O, p)
+        for a, b in zip(G.poses, O.poses):
+            et, er = _pose_err(a, b)
+            assert et < 1e-5 and er < 1e-5, (et, er)
+    assert list(G.poses[lone].t) == list(g["init"][lone].to_struct(abi.pmx_sim3).t) or \
+        np.abs(np.array(G.poses[lone].t[:]) - g["init"][lone].t).max() < 1e-12
