@@ -683,15 +683,16 @@ __device__ __forceinline__ int sky_at(const int* rowptr, const int* first, int i
 // seed and two correction steps (pivots are not the reference's rounding
 // either way: its AMD-ordered SimplicialLDLT differs at this level).
 __device__ __forceinline__ double fast_rcp(double d) {
-  const double ad = fabs(d);
-  if (!(ad > 1e-300 && ad < 1e300)) return 1.0 / d;  // zero, non-finite, extreme
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
   double e = fma(-d, r, 1.0);
   e = fma(e, e, e);
   r = fma(r, e, r);
   e = fma(-d, r, 1.0);
-  return fma(r, e, r);
+  r = fma(r, e, r);
+  const double ad = fabs(d);  // off the seed's dependency chain
+  if (!(ad > 1e-300 && ad < 1e300)) r = 1.0 / d;  // zero, non-finite, extreme
+  return r;
 }
 
 // One damping attempt (lambda on every diagonal entry, backend.cpp:208-227);
