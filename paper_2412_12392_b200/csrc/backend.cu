@@ -117,13 +117,23 @@ __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
 // = invalid pixel), and every edge's matches -> a compacted int4 list
 // {pa, pb, q bits, 0} of the matches that pass all the pose-independent skips
 // (valid flag, index range, both pointmaps valid, q > q_min), in match order.
-__global__ void k_pack_cloud(const float* __restrict__ xyz, const uint8_t* __restrict__ valid, int hw,
-                             float4* __restrict__ out) {
+// Every keyframe's cloud as float4 {x, y, z, |p|^2 or -1 if invalid} and a
+// validity bitmap (bit i of word i/32), one launch for all keyframes.
+__global__ void __launch_bounds__(256) k_pack_cloud(const CloudDev* __restrict__ clouds,
+                                                    float4* const* __restrict__ out,
+                                                    uint32_t* const* __restrict__ vbits) {
+  const CloudDev C = clouds[blockIdx.y];
+  const int hw = C.H * C.W;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= hw) return;
-  const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
-  const bool v = valid ? valid[i] != 0 : true;
-  out[i] = make_float4(x, y, z, v ? fmaf(x, x, fmaf(y, y, z * z)) : -1.0f);
+  if (blockIdx.x * blockDim.x >= hw) return;
+  bool v = false;
+  if (i < hw) {
+    const float x = C.xyz[3 * i], y = C.xyz[3 * i + 1], z = C.xyz[3 * i + 2];
+    v = C.valid ? C.valid[i] != 0 : true;
+    out[blockIdx.y][i] = make_float4(x, y, z, v ? fmaf(x, x, fmaf(y, y, z * z)) : -1.0f);
+  }
+  const unsigned word = __ballot_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && i < hw) vbits[blockIdx.y][i >> 5] = word;
 }
 
 constexpr int kCompactPer = 8;                     // consecutive matches per thread
@@ -132,12 +142,12 @@ constexpr int kCompactChunk = 256 * kCompactPer;   // matches per block
 struct CompactArgs {
   const MatchesDev* matches;
   const int2* edges;
-  const float4* const* c4;  // [N]
+  const uint32_t* const* vbits;  // [N] validity bitmaps of the packed clouds
   const CloudDev* clouds;
   const double* qmin;
   int N, chunks;
   int64_t seg;     // slots per edge in `packed`
-  int* cnt;        // [E][chunks]
+  int* cnt;        // [E][chunks]: kept per chunk, then (k_chunk_scan) exclusive offsets
   int* total;      // [E]
   int4* packed;    // [E][seg]
 };
@@ -150,7 +160,8 @@ __device__ __forceinline__ bool match_survives(const CompactArgs& A, const Match
   const CloudDev& Ci = A.clouds[ij.x];
   const CloudDev& Cj = A.clouds[ij.y];
   if (pa < 0 || pb < 0 || pa >= Ci.H * Ci.W || pb >= Cj.H * Cj.W) return false;
-  if (A.c4[ij.x][pa].w < 0.0f || A.c4[ij.y][pb].w < 0.0f) return false;  // tracking.cpp:62
+  if (!((A.vbits[ij.x][pa >> 5] >> (pa & 31)) & 1u) || !((A.vbits[ij.y][pb >> 5] >> (pb & 31)) & 1u))
+    return false;  // tracking.cpp:62
   const float q = M.q[k];
   if (!((double)q > qmin)) return false;  // robust_weight excludes (tracking.cpp:10-13)
   rec = make_int4(pa, pb, __float_as_int(q), 0);
@@ -164,44 +175,74 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
   const MatchesDev M = A.matches[e];
   const bool ok = ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N;  // backend.cpp:61
   const double qmin = A.qmin[e];
-  const int64_t k0 = (int64_t)c * kCompactChunk + (int64_t)threadIdx.x * kCompactPer;
+  // thread t takes matches c*chunk + j*256 + t (coalesced loads)
+  const int64_t k0 = (int64_t)c * kCompactChunk + threadIdx.x;
   unsigned keep = 0;
   int4 rec[kCompactPer];
 #pragma unroll
   for (int j = 0; j < kCompactPer; ++j)
-    if (ok && match_survives(A, M, ij, qmin, k0 + j, rec[j])) keep |= 1u << j;
-  const int n = __popc(keep);
-  // block exclusive scan of the per-thread counts
-  __shared__ int wsum[8];
+    if (ok && match_survives(A, M, ij, qmin, k0 + (int64_t)j * blockDim.x, rec[j])) keep |= 1u << j;
+  // output in increasing match order (j, thread): per j, a warp ballot and a
+  // block table of the warps' counts give every kept record its slot
+  __shared__ int wc[kCompactPer][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = n;
+  const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+  for (int j = 0; j < kCompactPer; ++j) {
+    const unsigned b = __ballot_sync(0xffffffffu, (keep >> j) & 1u);
+    if (lane == 0) wc[j][warp] = __popc(b);
   }
-  if (lane == 31) wsum[warp] = incl;
   __syncthreads();
-  int before = 0, block_total = 0;
-  for (int w = 0; w < 8; ++w) {
-    before += w < warp ? wsum[w] : 0;
-    block_total += wsum[w];
-  }
+  int block_total = 0;
+  for (int j = 0; j < kCompactPer; ++j)
+    for (int w = 0; w < 8; ++w) block_total += wc[j][w];
   if (!WRITE) {
     if (threadIdx.x == 0) A.cnt[(size_t)e * A.chunks + c] = block_total;
     return;
   }
-  int64_t off = 0;
-  for (int cc = 0; cc < c; ++cc) off += A.cnt[(size_t)e * A.chunks + cc];
-  if (c == 0 && threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int cc = 0; cc < A.chunks; ++cc) t += A.cnt[(size_t)e * A.chunks + cc];
-    A.total[e] = (int)t;
-  }
-  int4* out = A.packed + (size_t)e * A.seg + off + before + (incl - n);
+  int4* out = A.packed + (size_t)e * A.seg + A.cnt[(size_t)e * A.chunks + c];  // exclusive offset (k_chunk_scan)
+  int base = 0;
 #pragma unroll
-  for (int j = 0; j < kCompactPer; ++j)
-    if (keep & (1u << j)) *out++ = rec[j];
+  for (int j = 0; j < kCompactPer; ++j) {
+    const unsigned b = __ballot_sync(0xffffffffu, (keep >> j) & 1u);
+    int before = base;
+    for (int w = 0; w < warp; ++w) before += wc[j][w];
+    if ((keep >> j) & 1u) out[before + __popc(b & lt)] = rec[j];
+    for (int w = 0; w < 8; ++w) base += wc[j][w];
+  }
+}
+
+// Per edge: chunk counts -> exclusive offsets (in place) and the edge's total.
+__global__ void __launch_bounds__(256) k_chunk_scan(int* __restrict__ cnt, int chunks, int* __restrict__ total) {
+  int* c = cnt + (size_t)blockIdx.x * chunks;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int ws[8];
+  for (int b = 0; b < chunks; b += blockDim.x) {
+    const int i = b + threadIdx.x;
+    const int v = i < chunks ? c[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += ws[w];
+    if (i < chunks) c[i] = before + incl - v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+      carry += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[blockIdx.x] = carry;
 }
 
 // Asynchronous global -> shared copies (cp.async): the next panel's structure
@@ -1193,27 +1234,42 @@ struct DevGraph {
   std::vector<DevBuf> staged;  // host-staged inputs kept alive by a prepared graph
   // ray mode: frozen-match preprocessing
   bool packed = false;
-  DevBuf c4buf, c4ptrs, pk, pk_cnt, pk_total;
+  DevBuf c4buf, c4ptrs, vbbuf, vbptrs, pk, pk_cnt, pk_total;
   int64_t seg = 0;
 };
 
 // Pack clouds / compact the matches of every edge (ray mode, once per call).
 static void pack_graph(Context& ctx, DevGraph& G) {
-  size_t tot = 0;
-  for (const auto& c : G.hclouds) tot += (size_t)c.H * c.W;
+  size_t tot = 0, wtot = 0;
+  int max_hw = 1;
+  for (const auto& c : G.hclouds) {
+    tot += (size_t)c.H * c.W;
+    wtot += ((size_t)c.H * c.W + 31) / 32;
+    max_hw = std::max(max_hw, c.H * c.W);
+  }
   G.c4buf = DevBuf(sizeof(float4) * std::max<size_t>(tot, 1), ctx.stream);
+  G.vbbuf = DevBuf(sizeof(uint32_t) * std::max<size_t>(wtot, 1), ctx.stream);
   std::vector<const float4*> ptrs(std::max(G.N, 1), nullptr);
-  size_t off = 0;
+  std::vector<const uint32_t*> vptrs(std::max(G.N, 1), nullptr);
+  size_t off = 0, woff = 0;
   for (int k = 0; k < G.N; ++k) {
     const int hw = G.hclouds[k].H * G.hclouds[k].W;
-    float4* dst = G.c4buf.as<float4>() + off;
-    k_pack_cloud<<<(hw + 255) / 256, 256, 0, ctx.stream>>>(G.hclouds[k].xyz, G.hclouds[k].valid, hw, dst);
-    launch_check(ctx, "k_pack_cloud");
-    ptrs[k] = dst;
+    ptrs[k] = G.c4buf.as<float4>() + off;
+    vptrs[k] = G.vbbuf.as<uint32_t>() + woff;
     off += hw;
+    woff += ((size_t)hw + 31) / 32;
   }
   G.c4ptrs = DevBuf(sizeof(float4*) * ptrs.size(), ctx.stream);
   PMX_CUDA(cudaMemcpyAsync(G.c4ptrs.p, ptrs.data(), G.c4ptrs.bytes, cudaMemcpyHostToDevice, ctx.stream));
+  G.vbptrs = DevBuf(sizeof(uint32_t*) * vptrs.size(), ctx.stream);
+  PMX_CUDA(cudaMemcpyAsync(G.vbptrs.p, vptrs.data(), G.vbptrs.bytes, cudaMemcpyHostToDevice, ctx.stream));
+  for (int k0 = 0; k0 < G.N; k0 += 65535) {
+    const int kn = std::min(65535, G.N - k0);
+    k_pack_cloud<<<dim3((max_hw + 255) / 256, kn), 256, 0, ctx.stream>>>(
+        G.clouds.as<CloudDev>() + k0, const_cast<float4* const*>(G.c4ptrs.as<float4*>()) + k0,
+        const_cast<uint32_t* const*>(G.vbptrs.as<uint32_t*>()) + k0);
+    launch_check(ctx, "k_pack_cloud");
+  }
   G.seg = std::max<int64_t>(G.max_count, 1);
   const int chunks = (int)std::max<int64_t>(1, (G.max_count + kCompactChunk - 1) / kCompactChunk);
   G.pk = DevBuf(sizeof(int4) * (size_t)G.seg * std::max(G.E, 1), ctx.stream);
@@ -1223,7 +1279,7 @@ static void pack_graph(Context& ctx, DevGraph& G) {
   CompactArgs A;
   A.matches = G.matches.as<MatchesDev>();
   A.edges = G.edges_dev.as<int2>();
-  A.c4 = G.c4ptrs.as<const float4*>();
+  A.vbits = G.vbptrs.as<const uint32_t*>();
   A.clouds = G.clouds.as<CloudDev>();
   A.qmin = G.qmin.as<double>();
   A.N = G.N;
@@ -1243,6 +1299,8 @@ static void pack_graph(Context& ctx, DevGraph& G) {
     B.packed += (size_t)e0 * G.seg;
     k_compact<false><<<dim3(chunks, en), 256, 0, ctx.stream>>>(B);
     launch_check(ctx, "k_compact_count");
+    k_chunk_scan<<<en, 256, 0, ctx.stream>>>(B.cnt, chunks, B.total);
+    launch_check(ctx, "k_chunk_scan");
     k_compact<true><<<dim3(chunks, en), 256, 0, ctx.stream>>>(B);
     launch_check(ctx, "k_compact");
   }
