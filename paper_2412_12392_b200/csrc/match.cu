@@ -217,10 +217,8 @@ __global__ void __launch_bounds__(256) k_keys(const PairDev* __restrict__ pairs,
     const bool v = P.va ? P.va[i] != 0 : true;
     const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
     uint32_t key = kNoKey;
-    if (v && nrm > 1e-12) {
-      key = __float_as_uint((float)nrm);
-      atomicAdd(&sh[key >> 20], 1u);
-    }
+    if (v && nrm > 1e-12) key = __float_as_uint((float)nrm);
+    hist_add(sh, key >> 20, key != kNoKey);
     P.keys[i] = key;
   }
   __syncthreads();
@@ -251,10 +249,8 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     const double nrm = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
     if (with_keys) {  // k_keys
       uint32_t key = kNoKey;
-      if (v && nrm > 1e-12) {
-        key = __float_as_uint((float)nrm);
-        atomicAdd(&sh[key >> 20], 1u);
-      }
+      if (v && nrm > 1e-12) key = __float_as_uint((float)nrm);
+      hist_add(sh, key >> 20, key != kNoKey);
       P.keys[i] = key;
     }
     double4 r = make_double4(0.0, 0.0, 1.0, 0.0);
@@ -381,12 +377,8 @@ __global__ void __launch_bounds__(256) k_sel_hist(const PairDev* __restrict__ pa
   const int end = min(HW, begin + px_per_block);
   for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
     const uint32_t key = P.keys[i];
-    if (key == kNoKey) continue;
-    if (PASS == 2) {
-      if ((key >> 20) == prefix) atomicAdd(&sh[(key >> 8) & 0xfff], 1u);
-    } else {
-      if ((key >> 8) == prefix) atomicAdd(&sh[key & 0xff], 1u);
-    }
+    const bool take = key != kNoKey && (PASS == 2 ? (key >> 20) == prefix : (key >> 8) == prefix);
+    hist_add(sh, PASS == 2 ? (key >> 8) & 0xfff : key & 0xff, take);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += blockDim.x)

@@ -352,6 +352,18 @@ __host__ __device__ inline void ldlt_pivoted_solve(int n, const double* A_in, co
   for (int i = 0; i < n; ++i) x[i] = d[i];
 }
 
+// Shared-memory histogram increment aggregated over the warp's lanes that hit
+// the same bin (keys of one image cluster in a few bins: plain atomics would
+// serialise on them).  Call from every lane of the converged warp; `take` =
+// this lane has a key.
+__device__ __forceinline__ void hist_add(uint32_t* sh, uint32_t bin, bool take) {
+  const unsigned active = __activemask();
+  const unsigned with = __ballot_sync(active, take);
+  if (!take) return;
+  const unsigned peers = __match_any_sync(with, bin);
+  if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&sh[bin], (uint32_t)__popc(peers));
+}
+
 // --------------------------------------------------------- reductions
 __device__ inline double warp_sum(double v) {
 #pragma unroll

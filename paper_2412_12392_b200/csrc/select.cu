@@ -35,13 +35,13 @@ __global__ void __launch_bounds__(256) k_hist(const SelSeg* __restrict__ segs, u
   const int64_t b0 = (int64_t)blockIdx.x * per_block;
   const int64_t b1 = min(S.n, b0 + per_block);
   for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    if (S.valid && !S.valid[i]) continue;
+    const bool ok = !(S.valid && !S.valid[i]);
     const float v = S.vals[i];
-    if (v != v) continue;  // NaN never orders; std::nth_element is UB on it, we drop it
+    // NaN never orders; std::nth_element is UB on it, we drop it
     const uint32_t k = fkey(v);
-    if (PASS == 1) atomicAdd(&sh[k >> 20], 1u);
-    if (PASS == 2 && (k >> 20) == prefix) atomicAdd(&sh[(k >> 8) & 0xfff], 1u);
-    if (PASS == 3 && (k >> 8) == prefix) atomicAdd(&sh[k & 0xff], 1u);
+    const bool take = ok && v == v &&
+                      (PASS == 1 || (PASS == 2 ? (k >> 20) == prefix : (k >> 8) == prefix));
+    hist_add(sh, PASS == 1 ? k >> 20 : PASS == 2 ? (k >> 8) & 0xfff : k & 0xff, take);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += blockDim.x)
