@@ -1812,6 +1812,7 @@ static void build_raymap(Context& ctx, Stager& st, const pmx_pointmap* pm, DevBu
   P.hist = hist.as<uint32_t>();
   P.sel = sel.as<SelState>();
   PMX_CUDA(cudaMemsetAsync(hist.p, 0, hist.bytes, ctx.stream));
+  PMX_CUDA(cudaMemsetAsync(sel.p, 0, sel.bytes, ctx.stream));  // a1max / qbad start at 0
   PMX_CUDA(cudaMemcpyAsync(dpair.p, &P, sizeof(P), cudaMemcpyHostToDevice, ctx.stream));
   prep_and_select(ctx, dpair.as<PairDev>(), 1, (int)hw, 1.0);
 }
