@@ -543,7 +543,8 @@ def run_pmx(args):
         if sharded is not None:
             line["secondary"] = [sharded]
         if world == 1 and not args.no_secondary:
-            line["secondary"] = [bench_backend(ctx, dev, cpu=not args.no_cpu), bench_tracking(ctx, dev)]
+            line["secondary"] = ([sharded] if sharded is not None else []) + \
+                [bench_backend(ctx, dev, cpu=not args.no_cpu), bench_tracking(ctx, dev)]
             torch.cuda.empty_cache()
             line["secondary"].append(bench_backend(ctx, dev, cpu=not args.no_cpu, n_kf=1000, reach=5, loops=3,
                                                    iters=5, config="config4"))
