@@ -1871,7 +1871,9 @@ static void solve_band(Context& ctx, const pmx_backend_params& p, Assembly& As, 
     int s = 1;
     for (; s < S; s *= 2) {
       const int nodd = (S - s + 2 * s - 1) / (2 * s), neven = (S + 2 * s - 1) / (2 * s);
-      if (nodd > 0) k_bcr_eliminate<<<nodd, kBandThreads, sm_elim, ctx.stream>>>(a, s);
+      // few blocks at the deep levels: split their right-hand sides over CTAs
+      const int split = std::max(1, std::min(4, (2 * ctx.num_sms) / std::max(nodd, 1)));
+      if (nodd > 0) k_bcr_eliminate<<<dim3(nodd, split), kBandThreads, sm_elim, ctx.stream>>>(a, s);
       k_bcr_update<<<neven, kBandThreads, sm_upd, ctx.stream>>>(a, s);
     }
     k_bcr_top<<<1, kBandThreads, sm_top, ctx.stream>>>(a);

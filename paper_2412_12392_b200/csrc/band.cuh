@@ -124,13 +124,13 @@ __device__ bool band_ldlt(double* A, int w, double* tmp) {
   return true;
 }
 
-// In place: X (w x n, row-major, leading dimension n) <- (L D L^T)^-1 X.
+// In place: X (w x n, row-major, leading dimension ld) <- (L D L^T)^-1 X.
 // Blocked substitution by 8-row blocks: the diagonal block is solved per
 // column (one thread per column, the block's column in registers), then the
 // rows below (forward) / above (backward) take a rank-8 update in 4 x 4
 // register tiles (columns strided across the threads: conflict-free X rows,
 // broadcast L loads) - two FMAs per shared load instead of one per two.
-__device__ void band_solve_cols(const double* A, int w, double* X, int n) {
+__device__ void band_solve_cols(const double* A, int w, double* X, int n, int ld) {
   constexpr int B = 8;
   __shared__ double rdiag[kBandMaxW];
   for (int r = threadIdx.x; r < w; r += blockDim.x) rdiag[r] = fast_rcp(A[r * w + r]);
@@ -141,7 +141,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
       double z[B];
 #pragma unroll
-      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * n + c] : 0.0;
+      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * ld + c] : 0.0;
 #pragma unroll
       for (int r = 1; r < B; ++r)
 #pragma unroll
@@ -149,7 +149,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
           if (r < nb) z[r] -= A[(r0 + r) * w + r0 + k] * z[k];
 #pragma unroll
       for (int i = 1; i < B; ++i)
-        if (i < nb) X[(r0 + i) * n + c] = z[i];
+        if (i < nb) X[(r0 + i) * ld + c] = z[i];
     }
     __syncthreads();
     const int rt = (w - r1 + 3) / 4;
@@ -161,7 +161,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) av[i] = A[min(ra + i, w - 1) * w + r0 + k];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * n + min(col(tc, j), n - 1)];
+        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * ld + min(col(tc, j), n - 1)];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -171,18 +171,18 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (ra + i < w && col(tc, j) < n) X[(ra + i) * n + col(tc, j)] -= acc[i][j];
+          if (ra + i < w && col(tc, j) < n) X[(ra + i) * ld + col(tc, j)] -= acc[i][j];
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < w * n; t += blockDim.x) X[t] *= rdiag[t / n];  // D
+  for (int t = threadIdx.x; t < w * n; t += blockDim.x) X[(t / n) * ld + t % n] *= rdiag[t / n];  // D
   __syncthreads();
   for (int r1 = w; r1 > 0; r1 -= B) {  // L^T x = z, from the bottom
     const int r0 = max(0, r1 - B), nb = r1 - r0;
     for (int c = threadIdx.x; c < n; c += blockDim.x) {
       double z[B];
 #pragma unroll
-      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * n + c] : 0.0;
+      for (int i = 0; i < B; ++i) z[i] = i < nb ? X[(r0 + i) * ld + c] : 0.0;
 #pragma unroll
       for (int r = B - 2; r >= 0; --r)
 #pragma unroll
@@ -190,7 +190,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
           if (k < nb) z[r] -= A[(r0 + k) * w + r0 + r] * z[k];
 #pragma unroll
       for (int i = 0; i < B - 1; ++i)
-        if (i < nb) X[(r0 + i) * n + c] = z[i];
+        if (i < nb) X[(r0 + i) * ld + c] = z[i];
     }
     __syncthreads();
     const int rt = (r0 + 3) / 4;
@@ -202,7 +202,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) av[i] = A[(r0 + k) * w + min(ra + i, w - 1)];  // L^T
 #pragma unroll
-        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * n + min(col(tc, j), n - 1)];
+        for (int j = 0; j < 4; ++j) zv[j] = X[(r0 + k) * ld + min(col(tc, j), n - 1)];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -212,7 +212,7 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n) {
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          if (ra + i < r0 && col(tc, j) < n) X[(ra + i) * n + col(tc, j)] -= acc[i][j];
+          if (ra + i < r0 && col(tc, j) < n) X[(ra + i) * ld + col(tc, j)] -= acc[i][j];
     }
     __syncthreads();
   }
@@ -329,14 +329,22 @@ __global__ void __launch_bounds__(kBandThreads) k_bcr_eliminate(BandArgs A, int 
     if (threadIdx.x == 0) *A.status = 0;
     return;
   }
-  band_solve_cols(Dj, w, X, n);
+  // this CTA's share of the 2w+1 right-hand sides (blockIdx.y of gridDim.y;
+  // every CTA of the block factorises D_j itself)
+  const int cb = (int)(((int64_t)n * blockIdx.y) / gridDim.y), ce = (int)(((int64_t)n * (blockIdx.y + 1)) / gridDim.y);
+  band_solve_cols(Dj, w, X + cb, ce - cb, n);
   double* Y = A.Y + (size_t)j * 2 * w * w;
-  for (int i = threadIdx.x; i < w * w; i += blockDim.x) {
-    const int r = i / w, c = i % w;
-    Y[i] = X[r * n + c];
-    Y[w * w + i] = X[r * n + w + c];
+  const int nc = ce - cb;
+  for (int i = threadIdx.x; i < w * nc; i += blockDim.x) {
+    const int r = i / nc, c = cb + i % nc;
+    const double v = X[r * n + c];
+    if (c < w)
+      Y[r * w + c] = v;
+    else if (c < 2 * w)
+      Y[w * w + r * w + c - w] = v;
+    else
+      A.y[(size_t)j * w + r] = v;
   }
-  for (int r = threadIdx.x; r < w; r += blockDim.x) A.y[(size_t)j * w + r] = X[r * n + 2 * w];
 }
 
 // Level with stride s: even active block i = 2 s t absorbs its odd neighbours.
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(kBandThreads) k_bcr_top(BandArgs A) {
     if (threadIdx.x == 0) *A.status = 0;
     return;
   }
-  band_solve_cols(D, w, X, 1);
+  band_solve_cols(D, w, X, 1, 1);
   for (int r = threadIdx.x; r < w; r += blockDim.x) A.x[r] = X[r];
 }
 
