@@ -1874,7 +1874,8 @@ static void solve_band(Context& ctx, const pmx_backend_params& p, Assembly& As, 
       // few blocks at the deep levels: split their right-hand sides over CTAs
       const int split = std::max(1, std::min(4, (2 * ctx.num_sms) / std::max(nodd, 1)));
       if (nodd > 0) k_bcr_eliminate<<<dim3(nodd, split), kBandThreads, sm_elim, ctx.stream>>>(a, s);
-      k_bcr_update<<<neven, kBandThreads, sm_upd, ctx.stream>>>(a, s);
+      const int usplit = std::max(1, std::min(4, (2 * ctx.num_sms) / std::max(neven, 1)));
+      k_bcr_update<<<dim3(neven, usplit), kBandThreads, sm_upd, ctx.stream>>>(a, s);
     }
     k_bcr_top<<<1, kBandThreads, sm_top, ctx.stream>>>(a);
     for (s /= 2; s >= 1; s /= 2) {

@@ -220,10 +220,12 @@ __device__ void band_solve_cols(const double* A, int w, double* X, int n, int ld
 
 // C (w x w, smem) -= op(P) Q with P, Q in shared memory (row-major w x w);
 // transP: use P^T.  Each thread owns a 4 x 4 tile of C (register blocking).
-__device__ void band_gemm_sub(double* C, const double* P, const double* Q, int w, bool transP) {
-  const int tiles = (w + 3) / 4;
-  for (int t = threadIdx.x; t < tiles * tiles; t += blockDim.x) {
-    const int r0 = (t / tiles) * 4, c0 = (t % tiles) * 4;
+__device__ void band_gemm_sub(double* C, const double* P, const double* Q, int w, bool transP, int rb = 0,
+                              int re = -1) {
+  if (re < 0) re = w;  // output rows [rb, re) (rb a multiple of 4)
+  const int tiles = (w + 3) / 4, rtiles = (re - rb + 3) / 4;
+  for (int t = threadIdx.x; t < rtiles * tiles; t += blockDim.x) {
+    const int r0 = rb + (t / tiles) * 4, c0 = (t % tiles) * 4;
     double acc[4][4] = {};
     for (int q = 0; q < w; ++q) {
       double pv[4], qv[4];
@@ -242,7 +244,7 @@ __device__ void band_gemm_sub(double* C, const double* P, const double* Q, int w
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if (r0 + i < w && c0 + j < w) C[(r0 + i) * w + c0 + j] -= acc[i][j];
+        if (r0 + i < re && c0 + j < w) C[(r0 + i) * w + c0 + j] -= acc[i][j];
   }
   __syncthreads();
 }
@@ -381,24 +383,28 @@ __global__ void __launch_bounds__(kBandThreads) k_bcr_update(BandArgs A, int s) 
     yr[q] = right ? A.y[(size_t)(i + s) * w + q] : 0.0;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < w; r += blockDim.x) {
+  for (int r = threadIdx.x; r < (blockIdx.y == 0 ? w : 0); r += blockDim.x) {
     double acc = A.b[(size_t)i * w + r];
     for (int q = 0; q < w; ++q) acc -= Li[r * w + q] * yl[q] + Lr[q * w + r] * yr[q];
     A.b[(size_t)i * w + r] = acc;
   }
-  if (left) band_gemm_sub(Dn, Li, T, w, false);  // D_i -= A(i,i-s) Y_{i-s,R}
+  // this CTA's rows of the outputs (blockIdx.y of gridDim.y, multiples of 4)
+  const int rq = (((w + 3) / 4) + gridDim.y - 1) / gridDim.y;
+  const int rb = min(w, (int)blockIdx.y * rq * 4), re = min(w, rb + rq * 4);
+  if (left) band_gemm_sub(Dn, Li, T, w, false, rb, re);  // D_i -= A(i,i-s) Y_{i-s,R}
   if (right) {                                   // D_i -= A(i,i+s) Y_{i+s,L} = L_{i+s}^T Y_{i+s,L}
     band_copy_in(T, YrL, ww);
     __syncthreads();
-    band_gemm_sub(Dn, Lr, T, w, true);
+    band_gemm_sub(Dn, Lr, T, w, true, rb, re);
   }
-  for (int k = threadIdx.x; k < ww; k += blockDim.x) Di[k] = 0.5 * (Dn[k] + Dn[(k % w) * w + k / w]);
+  // the factorisations read the lower triangle only: rows written as computed
+  for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) Di[k] = Dn[k];
   if (left && i >= 2 * s) {  // coupling to the next active block on the left: -A(i,i-s) Y_{i-s,L}
     band_copy_in(T, YlL, ww);
     for (int k = threadIdx.x; k < ww; k += blockDim.x) Dn[k] = 0.0;
     __syncthreads();
-    band_gemm_sub(Dn, Li, T, w, false);
-    for (int k = threadIdx.x; k < ww; k += blockDim.x) A.L[(size_t)i * ww + k] = Dn[k];
+    band_gemm_sub(Dn, Li, T, w, false, rb, re);
+    for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) A.L[(size_t)i * ww + k] = Dn[k];
   }
 }
 
