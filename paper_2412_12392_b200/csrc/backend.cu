@@ -1602,12 +1602,12 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
     for (size_t i = 0; i < order.size(); ++i) pos[order[i]] = (int)i;
     const int nf = (int)order.size(), m = bw, w = 7 * m;
     const int S = nf > 0 ? (nf + m - 1) / m : 0;
-    // cost model (measured on B200): the frontal form walks ~7 us per keyframe
-    // panel; the cyclic reduction ~250 us per level (latency of the per-block
-    // dense kernels) + 200 us
+    // cost model (measured on B200): the frontal form walks ~4.3 us per
+    // keyframe panel (forward + backward); the cyclic reduction ~180 us per
+    // level (latency of the per-block dense kernels, damping no-ops included)
     int levels = 0;
     while ((1 << levels) < S) ++levels;
-    As.band_ok = nf > 0 && w <= kBandMaxW && S >= 2 && 7.0 * nf > 250.0 * levels + 200.0;
+    As.band_ok = nf > 0 && w <= kBandMaxW && S >= 2 && 4.3 * nf > 180.0 * levels;
     if (As.band_ok) {
       As.band_m = m;
       As.band_w = w;
