@@ -1407,11 +1407,11 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   const int E = std::max(G.E, 1);
   W.rel = DevBuf(sizeof(PoseR<float>) * 2 * (size_t)E, ctx.stream);
   W.rel64 = DevBuf(sizeof(PoseR<double>) * 2 * (size_t)E, ctx.stream);
-  // Few edges (< 4 waves of one block each): ~8192 matches per block, so the
+  // Few edges (< 4 waves of one block each): ~16384 matches per block, so the
   // resident blocks cover a few edges at a time (their keyframes' clouds stay
   // L2-resident) and the last wave is short; many edges: one block per edge.
   const int64_t resident = 2LL * ctx.num_sms;
-  W.bpe = G.E < 4 * resident ? (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 8191) / 8192)) : 1;
+  W.bpe = G.E < 4 * resident ? (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 16383) / 16384)) : 1;
   const bool ray = p.mode == PMX_TRACK_RAY;
   require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
   W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);
