@@ -265,3 +265,20 @@ def test_damping_retry_on_zero_pivot(ctx, n_kf, reach, h, w):
             assert et < 1e-5 and er < 1e-5, (et, er)
     assert list(G.poses[lone].t) == list(g["init"][lone].to_struct(abi.pmx_sim3).t) or \
         np.abs(np.array(G.poses[lone].t[:]) - g["init"][lone].t).max() < 1e-12
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_zero_iterations_leaves_poses(ctx, graphs):
+    # max_iterations = 0: the initial cost only, poses untouched (no loop graph is built)
+    ctx.set_device_graphs(graphs)
+    try:
+        g, G, O = _graph(n_kf=8, reach=2)
+        p = _params()
+        p.max_iterations = 0
+        before = [(list(P.R), list(P.t), P.s) for P in G.poses]
+        r = ctx.global_optimize(G, p)
+        assert r.iterations == 0
+        assert [(list(P.R), list(P.t), P.s) for P in G.poses] == before
+        assert len(r.cost_trace) == 1 and r.cost_trace[0] > 0
+    finally:
+        ctx.set_device_graphs(True)
