@@ -148,6 +148,7 @@ struct CompactArgs {
   int N, chunks;
   int64_t seg;     // slots per edge in `packed`
   int* cnt;        // [E][chunks]: kept per chunk, then (k_chunk_scan) exclusive offsets
+  uint8_t* keep;   // [E][chunks][256] survival bits of each thread's 8 matches (count pass -> write pass)
   int* total;      // [E]
   int4* packed;    // [E][seg]
 };
@@ -177,11 +178,23 @@ __global__ void __launch_bounds__(256) k_compact(CompactArgs A) {
   const double qmin = A.qmin[e];
   // thread t takes matches c*chunk + j*256 + t (coalesced loads)
   const int64_t k0 = (int64_t)c * kCompactChunk + threadIdx.x;
+  uint8_t* mask = A.keep + ((size_t)e * A.chunks + c) * blockDim.x + threadIdx.x;
   unsigned keep = 0;
   int4 rec[kCompactPer];
+  if (!WRITE) {  // the survival tests, remembered for the write pass (1 byte per 8 matches)
 #pragma unroll
-  for (int j = 0; j < kCompactPer; ++j)
-    if (ok && match_survives(A, M, ij, qmin, k0 + (int64_t)j * blockDim.x, rec[j])) keep |= 1u << j;
+    for (int j = 0; j < kCompactPer; ++j)
+      if (ok && match_survives(A, M, ij, qmin, k0 + (int64_t)j * blockDim.x, rec[j])) keep |= 1u << j;
+    *mask = (uint8_t)keep;
+  } else {
+    keep = *mask;
+#pragma unroll
+    for (int j = 0; j < kCompactPer; ++j)
+      if ((keep >> j) & 1u) {
+        const int64_t k = k0 + (int64_t)j * blockDim.x;
+        rec[j] = make_int4(M.pa[k], M.pb ? M.pb[k] : (int)k, __float_as_int(M.q[k]), 0);
+      }
+  }
   // output in increasing match order (j, thread): per j, a warp ballot and a
   // block table of the warps' counts give every kept record its slot
   __shared__ int wc[kCompactPer][8];
@@ -1274,6 +1287,7 @@ static void pack_graph(Context& ctx, DevGraph& G) {
   const int chunks = (int)std::max<int64_t>(1, (G.max_count + kCompactChunk - 1) / kCompactChunk);
   G.pk = DevBuf(sizeof(int4) * (size_t)G.seg * std::max(G.E, 1), ctx.stream);
   G.pk_cnt = DevBuf(sizeof(int) * (size_t)chunks * std::max(G.E, 1), ctx.stream);
+  DevBuf keepbuf((size_t)chunks * 256 * std::max(G.E, 1), ctx.stream);
   G.pk_total = DevBuf(sizeof(int) * std::max(G.E, 1), ctx.stream);
   PMX_CUDA(cudaMemsetAsync(G.pk_total.p, 0, G.pk_total.bytes, ctx.stream));
   CompactArgs A;
@@ -1286,6 +1300,7 @@ static void pack_graph(Context& ctx, DevGraph& G) {
   A.chunks = chunks;
   A.seg = G.seg;
   A.cnt = G.pk_cnt.as<int>();
+  A.keep = keepbuf.as<uint8_t>();
   A.total = G.pk_total.as<int>();
   A.packed = G.pk.as<int4>();
   for (int e0 = 0; e0 < G.E; e0 += 65535) {
@@ -1295,6 +1310,7 @@ static void pack_graph(Context& ctx, DevGraph& G) {
     B.edges += e0;
     B.qmin += e0;
     B.cnt += (size_t)e0 * chunks;
+    B.keep += (size_t)e0 * chunks * 256;
     B.total += e0;
     B.packed += (size_t)e0 * G.seg;
     k_compact<false><<<dim3(chunks, en), 256, 0, ctx.stream>>>(B);
