@@ -111,10 +111,10 @@ void segmented_median(Context& ctx, const SelSeg* dev_segs, int nseg, int64_t ma
   if (nseg == 0) return;
   scratch = DevBuf(sizeof(uint32_t) * (size_t)NT * nseg, ctx.stream);
   PMX_CUDA(cudaMemsetAsync(scratch.p, 0, scratch.bytes, ctx.stream));
-  // elements per block: 8 blocks per SM over all segments, 1024..8192 (one
+  // elements per block: 8 blocks per SM over all segments, 1024..32768 (one
   // 196,608-element segment - tracking's q_min median - gets 192 blocks, not 24)
   const int64_t want = (max_n * nseg + (int64_t)ctx.num_sms * 8 - 1) / ((int64_t)ctx.num_sms * 8);
-  const int64_t per_block = std::min<int64_t>(8192, std::max<int64_t>(1024, (want + 1023) / 1024 * 1024));
+  const int64_t per_block = std::min<int64_t>(32768, std::max<int64_t>(1024, (want + 1023) / 1024 * 1024));
   dim3 g((unsigned)std::max<int64_t>(1, (max_n + per_block - 1) / per_block), nseg);
   uint32_t* s = scratch.as<uint32_t>();
   k_hist<1><<<g, 256, 0, ctx.stream>>>(dev_segs, s, per_block);
