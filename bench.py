@@ -3,14 +3,18 @@
 
 Headline (BASELINE.json metric, config 2): batched iterative projective
 matching + descriptor refinement over 64 directed edges of 512x384
-pointmaps -> matched pixels/s, whole job over N GPUs (edges sharded, no
-collective: scaling "weak" per rank-share).  One "step" = one pass of the
+pointmaps -> matched pixels/s, whole job over N GPUs (the fixed 64-edge
+batch sharded by edge, no collective: scaling "strong").  One "step" = one pass of the
 hot path over the rank's edges.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pmx|reference]
 
-N > 1 is launched by torchrun (one process per GPU, NCCL only for the
-barrier / max-over-ranks timing).  ``--impl reference`` times the reference
+N > 1 runs one process per GPU: under torchrun as launched by the driver,
+or, when WORLD_SIZE is unset, bench.py re-executes itself under
+``torch.distributed.run --nproc-per-node N`` (and fails loudly when fewer
+than N GPUs are visible).  NCCL carries only the barrier / max-over-ranks
+timing for matching, and the reduce + broadcast of the edge-sharded
+backend line (config 4), which runs by default at N > 1.  ``--impl reference`` times the reference
 algorithm on the host cores (the FP64 C++ oracle restatement of
 src/camera.cpp, all threads, bounded sample) on the same metric.
 """
@@ -153,7 +157,7 @@ def run_reference(args):
     value = px / statistics.mean(times)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gen/pmx_gen.cpp, seed 2)",
             "config": {"workload": "config2: batched match+refine, 64 directed edges, 512x384, 24-d fp16",
                        "sample": f"{sample_edges} of 64 edges per step"},
@@ -438,7 +442,7 @@ def run_pmx(args):
     value = px_total * args.steps / (ms_max / 1e3)
 
     sharded = None
-    if args.backend_sharded and dist:  # every rank takes part (collectives)
+    if (args.backend_sharded or world > 1) and dist:  # every rank takes part (collectives)
         del dev_pairs, batch
         torch.cuda.empty_cache()
         sharded = bench_backend_sharded(ctx, dev, rank, world)
@@ -518,7 +522,7 @@ def run_pmx(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
             "data": "synthetic (gen/pmx_gen.cpp, seed 2; radial point noise sigma=0.005)",
             "config": {"workload": "config2: batched match+refine, 64 directed edges, 512x384, 24-d fp16, "
                                    "LM 10 it lambda 1e-8 tol 1e-6 rad, refine {(1,3),(1,3)}",
@@ -554,6 +558,26 @@ def run_pmx(args):
         dist.destroy_process_group()
 
 
+def _spawn(args) -> int:
+    """--gpus N without torchrun: one process per GPU via torch.distributed.run
+    (the driver's own launch line), after checking N devices exist."""
+    if args.impl != "reference":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} requested but only {have} CUDA device(s) visible"}),
+                  flush=True)
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {have} visible", file=sys.stderr)
+            return 2
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -565,6 +589,8 @@ def main():
     ap.add_argument("--backend-sharded", action="store_true",
                     help="also run config 4 edge-sharded over the job's GPUs (NCCL reduce + broadcast)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -535,7 +535,10 @@ class Context:
         g.poses = [abi.pmx_sim3.from_buffer_copy(gs.poses[k]) for k in range(n)]
         pt = []
         if trace:
-            pt = [[abi.pmx_sim3.from_buffer_copy(tr[it * n + k]) for k in range(n)] for it in range(res.iterations)]
+            # a failed iteration (no damped solve succeeded, backend.cpp:228-230)
+            # records no poses: the trace has iterations - 1 rows then
+            rows = res.iterations if res.converged else max(0, res.iterations - 1)
+            pt = [[abi.pmx_sim3.from_buffer_copy(tr[it * n + k]) for k in range(n)] for it in range(rows)]
         return OptimizeResult(res.iterations, bool(res.converged), list(res.cost_trace[:res.cost_trace_len]), pt)
 
     def ldlt_solve(self, A, b):

@@ -365,32 +365,35 @@ __global__ void __launch_bounds__(kBandThreads) k_bcr_update(BandArgs A, int s) 
   const double* YlL = A.Y + (size_t)(i - s) * 2 * ww;       // Y_{i-s,L}
   const double* YrL = A.Y + (size_t)(i + s) * 2 * ww;       // Y_{i+s,L}
   double* Di = A.D + (size_t)i * ww;
+  // this CTA's rows [rb, re) of every output of block i (blockIdx.y of
+  // gridDim.y, multiples of 4).  A CTA reads only its own rows of A(i,i-s),
+  // D_i and b_i -- the rows it overwrites itself below -- so the CTAs of one
+  // block never read what another one writes in this launch.
+  const int rq = (((w + 3) / 4) + gridDim.y - 1) / gridDim.y;
+  const int rb = min(w, (int)blockIdx.y * rq * 4), re = min(w, rb + rq * 4);
   if (left)
-    band_copy_in(Li, A.L + (size_t)i * ww, ww);
+    band_copy_in(Li + rb * w, A.L + (size_t)i * ww + rb * w, (re - rb) * w);
   else
-    for (int k = threadIdx.x; k < ww; k += blockDim.x) Li[k] = 0.0;
+    for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) Li[k] = 0.0;
   if (right)
-    band_copy_in(Lr, A.L + (size_t)(i + s) * ww, ww);
+    band_copy_in(Lr, A.L + (size_t)(i + s) * ww, ww);  // odd block: not written at this level
   else
     for (int k = threadIdx.x; k < ww; k += blockDim.x) Lr[k] = 0.0;
-  band_copy_in(Dn, Di, ww);
+  band_copy_in(Dn + rb * w, Di + rb * w, (re - rb) * w);
   if (left) band_copy_in(T, YlR, ww);
   __syncthreads();
-  // b_i -= A(i,i-s) y_{i-s} + A(i,i+s) y_{i+s}
+  // b_i -= A(i,i-s) y_{i-s} + A(i,i+s) y_{i+s}  (rows [rb, re))
   __shared__ double yl[kBandMaxW], yr[kBandMaxW];
   for (int q = threadIdx.x; q < w; q += blockDim.x) {
     yl[q] = left ? A.y[(size_t)(i - s) * w + q] : 0.0;
     yr[q] = right ? A.y[(size_t)(i + s) * w + q] : 0.0;
   }
   __syncthreads();
-  for (int r = threadIdx.x; r < (blockIdx.y == 0 ? w : 0); r += blockDim.x) {
+  for (int r = rb + threadIdx.x; r < re; r += blockDim.x) {
     double acc = A.b[(size_t)i * w + r];
     for (int q = 0; q < w; ++q) acc -= Li[r * w + q] * yl[q] + Lr[q * w + r] * yr[q];
     A.b[(size_t)i * w + r] = acc;
   }
-  // this CTA's rows of the outputs (blockIdx.y of gridDim.y, multiples of 4)
-  const int rq = (((w + 3) / 4) + gridDim.y - 1) / gridDim.y;
-  const int rb = min(w, (int)blockIdx.y * rq * 4), re = min(w, rb + rq * 4);
   if (left) band_gemm_sub(Dn, Li, T, w, false, rb, re);  // D_i -= A(i,i-s) Y_{i-s,R}
   if (right) {                                   // D_i -= A(i,i+s) Y_{i+s,L} = L_{i+s}^T Y_{i+s,L}
     band_copy_in(T, YrL, ww);
@@ -400,8 +403,9 @@ __global__ void __launch_bounds__(kBandThreads) k_bcr_update(BandArgs A, int s) 
   // the factorisations read the lower triangle only: rows written as computed
   for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) Di[k] = Dn[k];
   if (left && i >= 2 * s) {  // coupling to the next active block on the left: -A(i,i-s) Y_{i-s,L}
+    __syncthreads();         // every thread's Dn rows are in D_i before Dn is reused
     band_copy_in(T, YlL, ww);
-    for (int k = threadIdx.x; k < ww; k += blockDim.x) Dn[k] = 0.0;
+    for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) Dn[k] = 0.0;
     __syncthreads();
     band_gemm_sub(Dn, Li, T, w, false, rb, re);
     for (int k = rb * w + threadIdx.x; k < re * w; k += blockDim.x) A.L[(size_t)i * ww + k] = Dn[k];

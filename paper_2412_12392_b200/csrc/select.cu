@@ -18,9 +18,10 @@ __device__ __forceinline__ float unkey(uint32_t k) {
 
 template <int PASS>
 __global__ void __launch_bounds__(256) k_hist(const SelSeg* __restrict__ segs, uint32_t* __restrict__ scratch,
-                                              int64_t per_block) {
-  const SelSeg S = segs[blockIdx.y];
-  uint32_t* base = scratch + (size_t)NT * blockIdx.y;
+                                              int64_t per_block, int seg0) {
+  const int seg = seg0 + (int)blockIdx.y;
+  const SelSeg S = segs[seg];
+  uint32_t* base = scratch + (size_t)NT * seg;
   uint32_t* state = base + N1 + N2 + N3;  // [0]=n [1]=krem [2]=prefix
   constexpr int NB = PASS == 3 ? N3 : 4096;
   uint32_t* h = base + (PASS == 1 ? 0 : PASS == 2 ? N1 : N1 + N2);
@@ -51,13 +52,13 @@ __global__ void __launch_bounds__(256) k_hist(const SelSeg* __restrict__ segs, u
 template <int PASS>
 __global__ void __launch_bounds__(1024) k_scan(const SelSeg* __restrict__ segs, uint32_t* __restrict__ scratch) {
   const SelSeg S = segs[blockIdx.x];
-  uint32_t* base = scratch + (size_t)NT * blockIdx.x;
+  uint32_t* base = scratch + (size_t)NT * blockIdx.x;  // gridDim.x = nseg (no 65535 limit on x)
   uint32_t* state = base + N1 + N2 + N3;
   constexpr int NB = PASS == 3 ? N3 : 4096;
   const uint32_t* h = base + (PASS == 1 ? 0 : PASS == 2 ? N1 : N1 + N2);
   constexpr int PER = (NB + 1023) / 1024;
   __shared__ uint32_t wsum[32];
-  __shared__ uint32_t total;
+  __shared__ uint32_t total, krem_s, prefix_s;
   const int t = threadIdx.x;
   uint32_t local[PER], s = 0;
 #pragma unroll
@@ -89,17 +90,21 @@ __global__ void __launch_bounds__(1024) k_scan(const SelSeg* __restrict__ segs, 
     state[1] = total / 2;
     if (total == 0) *S.out = S.scale * 0.0;
   }
+  if (t == 0) {  // one read of the state before the matching thread rewrites it
+    krem_s = state[1];
+    prefix_s = state[2];
+  }
   __syncthreads();
   if (total == 0) return;
-  const uint32_t krem = state[1];
+  const uint32_t krem = krem_s;
   uint32_t excl = wsum[t >> 5] + incl - s;
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
     const int b = t * PER + j;
     if (b < NB && local[j] > 0 && excl <= krem && krem < excl + local[j]) {
       if (PASS == 1) state[2] = (uint32_t)b;
-      if (PASS == 2) state[2] = (state[2] << 12) | (uint32_t)b;
-      if (PASS == 3) *S.out = S.scale * (double)unkey((state[2] << 8) | (uint32_t)b);
+      if (PASS == 2) state[2] = (prefix_s << 12) | (uint32_t)b;
+      if (PASS == 3) *S.out = S.scale * (double)unkey((prefix_s << 8) | (uint32_t)b);
       state[1] = krem - excl;
     }
     excl += local[j];
@@ -115,18 +120,22 @@ void segmented_median(Context& ctx, const SelSeg* dev_segs, int nseg, int64_t ma
   // 196,608-element segment - tracking's q_min median - gets 192 blocks, not 24)
   const int64_t want = (max_n * nseg + (int64_t)ctx.num_sms * 8 - 1) / ((int64_t)ctx.num_sms * 8);
   const int64_t per_block = std::min<int64_t>(32768, std::max<int64_t>(1024, (want + 1023) / 1024 * 1024));
-  dim3 g((unsigned)std::max<int64_t>(1, (max_n + per_block - 1) / per_block), nseg);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, (max_n + per_block - 1) / per_block);
   uint32_t* s = scratch.as<uint32_t>();
-  k_hist<1><<<g, 256, 0, ctx.stream>>>(dev_segs, s, per_block);
-  launch_check(ctx, "sel k_hist1");
+  // gridDim.y is capped at 65535: the histogram passes run over segment chunks
+  auto hist = [&](auto kernel, const char* what) {
+    for (int s0 = 0; s0 < nseg; s0 += 65535) {
+      kernel<<<dim3(gx, std::min(65535, nseg - s0)), 256, 0, ctx.stream>>>(dev_segs, s, per_block, s0);
+      launch_check(ctx, what);
+    }
+  };
+  hist(k_hist<1>, "sel k_hist1");
   k_scan<1><<<nseg, 1024, 0, ctx.stream>>>(dev_segs, s);
   launch_check(ctx, "sel k_scan1");
-  k_hist<2><<<g, 256, 0, ctx.stream>>>(dev_segs, s, per_block);
-  launch_check(ctx, "sel k_hist2");
+  hist(k_hist<2>, "sel k_hist2");
   k_scan<2><<<nseg, 1024, 0, ctx.stream>>>(dev_segs, s);
   launch_check(ctx, "sel k_scan2");
-  k_hist<3><<<g, 256, 0, ctx.stream>>>(dev_segs, s, per_block);
-  launch_check(ctx, "sel k_hist3");
+  hist(k_hist<3>, "sel k_hist3");
   k_scan<3><<<nseg, 1024, 0, ctx.stream>>>(dev_segs, s);
   launch_check(ctx, "sel k_scan3");
 }
