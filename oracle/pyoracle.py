@@ -7,6 +7,7 @@ __graft_entry__.smoke() as the checker, and by bench.py's cpu_baseline /
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import os
 import subprocess
@@ -18,17 +19,48 @@ from paper_2412_12392_b200.abi import ptr
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "liborc.so")
-_lib = None
+# The genuine reference sources (src/{lie,camera,tracking,backend}.cpp)
+# compiled against the Eigen-API shim behind the same orc_* ABI
+# (oracle/Makefile target `ref`): the pin of the restatement.
+REF_LIB_PATH = os.path.join(_HERE, "_ref", "libpmslam_ref.so")
+_libs = {}
+_active = "restatement"
+
+
+def have_reference() -> bool:
+    """True when oracle/_ref/libpmslam_ref.so was built (it is built from
+    /root/reference, and travels to the GPU box with the snapshot)."""
+    return os.path.exists(REF_LIB_PATH)
 
 
 def lib():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            subprocess.check_call(["make", "-s", "-C", _HERE])
-        _lib = C.CDLL(LIB_PATH)
-        _lib.orc_last_error.restype = C.c_char_p
-    return _lib
+    if _active not in _libs:
+        if _active == "reference":
+            path = REF_LIB_PATH
+            if not os.path.exists(path):
+                raise FileNotFoundError(f"{path} not built (make -C oracle ref, needs /root/reference)")
+        else:
+            path = LIB_PATH
+            if not os.path.exists(path):
+                subprocess.check_call(["make", "-s", "-C", _HERE])
+        L = C.CDLL(path)
+        L.orc_last_error.restype = C.c_char_p
+        L.orc_robust_weight.restype = C.c_double
+        L.orc_robust_weight.argtypes = [C.c_double] * 3
+        _libs[_active] = L
+    return _libs[_active]
+
+
+@contextlib.contextmanager
+def reference():
+    """Route every pyoracle call inside the block to the genuine reference
+    build (oracle/_ref) instead of the restatement."""
+    global _active
+    prev, _active = _active, "reference"
+    try:
+        yield
+    finally:
+        _active = prev
 
 
 class OracleError(RuntimeError):
@@ -285,7 +317,8 @@ def global_optimize(g: Graph, params=None):
     _check(lib().orc_global_optimize(C.byref(gs), C.byref(params), C.byref(res), trace))
     poses = [gs.poses[k] for k in range(n)]
     g.poses = [abi.pmx_sim3.from_buffer_copy(p) for p in poses]
-    tr = [[abi.pmx_sim3.from_buffer_copy(trace[it * n + k]) for k in range(n)] for it in range(res.iterations)]
+    rows = res.iterations if res.converged else max(0, res.iterations - 1)  # a failed iteration records nothing
+    tr = [[abi.pmx_sim3.from_buffer_copy(trace[it * n + k]) for k in range(n)] for it in range(rows)]
     return res, tr
 
 
@@ -396,3 +429,24 @@ def read_pair_record(buf: bytes, h, w, dim):
     out["valid_i"] = np.isfinite(out["X_i"]).all(axis=1).astype(np.uint8)  # allFinite (pipeline.cpp:541)
     out["valid_j"] = np.isfinite(out["X_j"]).all(axis=1).astype(np.uint8)
     return out
+
+
+def solve_pose(canonical, valid_c, pred, h, w, init, mode=abi.PMX_TRACK_RAY, params=None,
+               seed: MatchSet | None = None):
+    """solve_pose, reference src/tracking.cpp:149-226: match the frame's own
+    pointmap (a = frame, b = keyframe image) + refine + LM-damped GN.
+    pred: X_f_f / valid_f / D_f / Q_f and X_k_f / valid_k / D_k / Q_k."""
+    res = abi.pmx_track_result()
+    pc = _pm(canonical, valid_c, h, w)
+    pf = _pm(pred["X_f_f"], pred.get("valid_f"), h, w)
+    pk = _pm(pred["X_k_f"], pred.get("valid_k"), h, w)
+    Ff = _fm(pred["D_f"], pred["Q_f"], h, w)
+    Fk = _fm(pred["D_k"], pred["Q_k"], h, w)
+    out = MatchSet.empty(h * w)
+    o = out.struct()
+    s = seed.struct() if seed is not None else None
+    params = params or abi.default_solve_pose_params()
+    _check(lib().orc_solve_pose(C.byref(pc), C.byref(pf), C.byref(pk), C.byref(Ff), C.byref(Fk), C.byref(init),
+                                C.c_int(mode), C.byref(params), C.byref(s) if s is not None else None,
+                                C.byref(res), C.byref(o)))
+    return res, out

@@ -1,7 +1,13 @@
-"""Generates tests/golden/*.npz: small seeded BASELINE-shaped cases run
-through the FP64 oracle (the reference itself cannot be built here — no
-Eigen3 — so these are oracle outputs, themselves pinned by
-tests/test_oracle_pins.py).  Regenerate with:  python tests/golden/make_golden.py
+"""Generates tests/golden/*.npz: small seeded BASELINE-shaped cases.
+
+Matching and backend outputs come from the GENUINE reference sources
+(oracle/_ref/libpmslam_ref.so: /root/reference/proj/src/*.cpp compiled
+against the Eigen-API shim) when that build exists, else from the FP64
+restatement; tests/test_ref_pins.py checks that both produce these fixtures
+bit for bit (matching) / within 1e-10 (backend).  The track fixture is the
+restatement's match-given GN (the reference has no such entry; its
+residuals are pinned to the reference in test_ref_pins).
+Regenerate with:  python tests/golden/make_golden.py
 """
 import os
 import sys
@@ -75,8 +81,11 @@ def backend_case(name, seed, n_kf, reach, h, w):
 
 
 if __name__ == "__main__":
-    match_case("match_radial_48x64.npz", 21, 48, 64, "radial")
-    match_case("match_isotropic_48x64.npz", 22, 48, 64, "isotropic")
+    import contextlib
+    src = pyoracle.reference() if pyoracle.have_reference() else contextlib.nullcontext()
+    with src:
+        match_case("match_radial_48x64.npz", 21, 48, 64, "radial")
+        match_case("match_isotropic_48x64.npz", 22, 48, 64, "isotropic")
+        backend_case("backend_6kf_24x32.npz", 24, 6, 2, 24, 32)
     track_case("track_48x64.npz", 23, 48, 64)
-    backend_case("backend_6kf_24x32.npz", 24, 6, 2, 24, 32)
-    print("golden fixtures written to", HERE)
+    print("golden fixtures written to", HERE, "(reference build)" if pyoracle.have_reference() else "(restatement)")

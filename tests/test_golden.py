@@ -115,7 +115,9 @@ def test_oracle_reproduces_backend_fixture():
     p.weights.distance_weight = 0.1
     res, _ = pyoracle.global_optimize(O, p)
     final = np.array([list(T.R) + list(T.t) + [T.s] for T in O.poses])
-    assert np.array_equal(final, z["final"]) and res.iterations == int(z["iterations"][0])
+    # the fixture is the reference build's output (make_golden.py); the
+    # restatement differs from it by rounding only (test_ref_pins.py)
+    assert np.abs(final - z["final"]).max() <= 1e-10 and res.iterations == int(z["iterations"][0])
 
 
 @pytest.mark.gpu
