@@ -231,6 +231,20 @@ int pmx_set_device_graphs(pmx_context* ctx, int on);
 int pmx_normalize_rays(pmx_context* ctx, pmx_memory mem, const pmx_pointmap* pm,
                        double* rays, double* distances, uint8_t* valid);
 
+/* interpolate_ray, camera.hpp:118-119 / camera.cpp:58-100, at n continuous
+ * pixels p (double[n*2], (u, v)) of the ray map of `pm`: ray (double[n*3]),
+ * jacobian (double[n*6], nullable; column-major 3x2: d/du then d/dv),
+ * ok (uint8[n]: 0 = std::nullopt, ray / jacobian then zero). */
+int pmx_interpolate_ray(pmx_context* ctx, pmx_memory mem, const pmx_pointmap* pm, int64_t n,
+                        const double* p, double* ray, double* jacobian, uint8_t* ok);
+
+/* median_scene_distance, camera.cpp:178-191 (the reference's file-local
+ * helper behind match_pointmaps' 3D invalidation threshold, exported as a
+ * test surface): the rank floor(n/2) FP64 norm over valid pixels with
+ * norm > 1e-12, 0 when there are none.  out: one double (host memory for
+ * PMX_MEM_HOST, device memory for PMX_MEM_DEVICE). */
+int pmx_median_scene_distance(pmx_context* ctx, pmx_memory mem, const pmx_pointmap* pm, double* out);
+
 /* iterative_project, camera.hpp:123-124 / camera.cpp:115-174, for a batch
  * of n query points x (float[n*3]) with seeds p0 (double[n*2]) against the
  * ray map of `pm`.  Outputs pixel (double[n*2]), converged (uint8[n]),

@@ -142,7 +142,8 @@ PMX_SYMBOLS = [
     "pmx_default_robust_weight_params", "pmx_default_solve_pose_params",
     "pmx_default_backend_params", "pmx_sim3_identity", "pmx_abi_version",
     "pmx_create", "pmx_destroy", "pmx_last_error", "pmx_set_stream", "pmx_get_stream",
-    "pmx_synchronize", "pmx_kernel_launch_count", "pmx_normalize_rays",
+    "pmx_synchronize", "pmx_kernel_launch_count", "pmx_normalize_rays", "pmx_interpolate_ray",
+    "pmx_median_scene_distance",
     "pmx_iterative_project", "pmx_match_pointmaps", "pmx_feature_refine",
     "pmx_match_batch", "pmx_match_stats", "pmx_keyframe_decision",
     "pmx_residual_blocks", "pmx_normal_equations", "pmx_track_given_matches",

@@ -242,6 +242,24 @@ class Context:
         self._check(self.lib.pmx_normalize_rays(self.h, mem, C.byref(s), ptr(rays), ptr(dist), ptr(valid)))
         return rays, dist, valid
 
+    def interpolate_ray(self, pm: Pointmap, p):
+        """interpolate_ray (camera.cpp:58-100) at continuous pixels p (n x 2):
+        (ray n x 3, jacobian n x 6 column-major 3x2, ok n)."""
+        p = np.ascontiguousarray(p, np.float64).reshape(-1, 2)
+        n = p.shape[0]
+        ray, jac, ok = np.empty((n, 3)), np.empty((n, 6)), np.empty(n, np.uint8)
+        s = pm.struct()
+        self._check(self.lib.pmx_interpolate_ray(self.h, abi.PMX_MEM_HOST, C.byref(s), C.c_int64(n), ptr(p), ptr(ray),
+                                                 ptr(jac), ptr(ok)))
+        return ray, jac, ok
+
+    def median_scene_distance(self, pm: Pointmap) -> float:
+        """median_scene_distance (camera.cpp:178-191), exact FP64."""
+        out = np.zeros(1)
+        s = pm.struct()
+        self._check(self.lib.pmx_median_scene_distance(self.h, abi.PMX_MEM_HOST, C.byref(s), ptr(out)))
+        return float(out[0])
+
     def iterative_project(self, pm: Pointmap, x, p0, params=None):
         x = np.ascontiguousarray(x, np.float32).reshape(-1, 3)
         p0 = np.ascontiguousarray(p0, np.float64).reshape(-1, 2)

@@ -24,6 +24,9 @@ int pmx_impl_graph_release(pmx_context*, pmx_prepared_graph*);
 int pmx_impl_feature_refine(pmx_context*, pmx_memory, const pmx_matchset*, const pmx_featuremap*,
                             const pmx_featuremap*, const pmx_refine_params*, pmx_matchset*);
 int pmx_impl_normalize_rays(pmx_context*, pmx_memory, const pmx_pointmap*, double*, double*, uint8_t*);
+int pmx_impl_interpolate_ray(pmx_context*, pmx_memory, const pmx_pointmap*, int64_t, const double*, double*, double*,
+                             uint8_t*);
+int pmx_impl_median_scene_distance(pmx_context*, pmx_memory, const pmx_pointmap*, double*);
 int pmx_impl_iterative_project(pmx_context*, pmx_memory, const pmx_pointmap*, int64_t, const float*,
                                const double*, const pmx_iter_proj_params*, double*, uint8_t*, int32_t*);
 int pmx_impl_match_stats(pmx_context*, pmx_memory, const pmx_matchset*, int32_t, int64_t*, double*);
@@ -281,6 +284,15 @@ int pmx_profile_get(pmx_context* c, const char* kernel, double* total_ms, int64_
 int pmx_normalize_rays(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, double* rays, double* dist,
                        uint8_t* valid) {
   return guarded(c, [&] { return pmx_impl_normalize_rays(c, mem, pm, rays, dist, valid); });
+}
+
+int pmx_interpolate_ray(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, int64_t n, const double* p,
+                        double* ray, double* jacobian, uint8_t* ok) {
+  return guarded(c, [&] { return pmx_impl_interpolate_ray(c, mem, pm, n, p, ray, jacobian, ok); });
+}
+
+int pmx_median_scene_distance(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, double* out) {
+  return guarded(c, [&] { return pmx_impl_median_scene_distance(c, mem, pm, out); });
 }
 
 int pmx_iterative_project(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, int64_t n, const float* x,

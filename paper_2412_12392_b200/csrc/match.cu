@@ -39,6 +39,8 @@ constexpr int kHist1 = 4096, kHist2 = 4096, kHist3 = 256;
 constexpr int kHistTotal = kHist1 + kHist2 + kHist3;
 constexpr uint32_t kNoKey = 0xffffffffu;
 
+constexpr int kSelCap = 64;  // FP64 candidates kept per pair for the exact tie resolution
+
 struct SelState {
   uint32_t n;       // number of keys
   uint32_t k;       // target rank (n / 2)
@@ -47,6 +49,11 @@ struct SelState {
   double threshold; // invalidation_median_fraction * median
   int a1max;        // max over a-pixels of sum q8(D_a)^2 (int8 refinement error bound)
   int qbad;         // some |D_a component| * 127 >= 127.5: no int8 fast path for this pair
+  // exact FP64 median: the fp32 key of the rank-k element, how many norms
+  // share that key, and their FP64 values (the rank-krem one is the median)
+  uint32_t key, ties, cnt, pad_;
+  double median;
+  double cand[kSelCap];
 };
 
 struct PairDev {
@@ -75,9 +82,11 @@ struct PairDev {
   // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
   // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
   float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (standalone refine)
-  // int8 descriptors of every a-pixel, round(127 x), dims 0-15 / 16-23 (batched refine)
-  uint4* q8a;
-  uint2* q8b;
+  // int8 descriptors of every a-pixel, round(127 x) (batched refine), 32 B per
+  // pixel as two words: q8[2i] = {dims 0-3, dims 4-7, nt, 0} with nt =
+  // ceil(sqrt(sum of the squares of dims 8-23)) (the Cauchy-Schwarz bound of
+  // the tail), q8[2i+1] = dims 8-23
+  uint4* q8;
 };
 
 struct LMParams {
@@ -163,7 +172,8 @@ __device__ __forceinline__ void desc_aux(const __half* row, float q, float4* nrm
 struct Q8 {
   uint4 a;  // dims 0-15
   uint2 b;  // dims 16-23
-  int l2;
+  int l2;   // sum of squares, all dims
+  int nt;   // ceil(sqrt(sum of squares of dims 8-23))
   int bad;
 };
 __device__ __forceinline__ uint32_t q8_word(uint32_t w0, uint32_t w1, __half2& amax) {
@@ -190,12 +200,15 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
   q.b.y = q8_word(d2.z, d2.w, amax);
   const float2 m = __half22float2(amax);
   q.bad = !(m.x <= 1.00390625f && m.y <= 1.00390625f);  // also NaN / inf
-  int l2 = __dp4a((int)q.a.x, (int)q.a.x, 0);
-  l2 = __dp4a((int)q.a.y, (int)q.a.y, l2);
-  l2 = __dp4a((int)q.a.z, (int)q.a.z, l2);
-  l2 = __dp4a((int)q.a.w, (int)q.a.w, l2);
-  l2 = __dp4a((int)q.b.x, (int)q.b.x, l2);
-  q.l2 = __dp4a((int)q.b.y, (int)q.b.y, l2);
+  const int l2h = __dp4a((int)q.a.y, (int)q.a.y, __dp4a((int)q.a.x, (int)q.a.x, 0));
+  int l2t = __dp4a((int)q.a.z, (int)q.a.z, 0);
+  l2t = __dp4a((int)q.a.w, (int)q.a.w, l2t);
+  l2t = __dp4a((int)q.b.x, (int)q.b.x, l2t);
+  l2t = __dp4a((int)q.b.y, (int)q.b.y, l2t);
+  q.l2 = l2h + l2t;
+  int nt = (int)ceilf(sqrtf((float)l2t));  // exact integer ceil(sqrt): l2t < 2^24
+  if (nt * nt < l2t) ++nt;
+  q.nt = nt;
   return q;
 }
 // Upper bound of sum |q_k| from sum q_k^2 (Cauchy-Schwarz over 24 dims).
@@ -257,16 +270,16 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
     P.rays[i] = r;
     if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
-    if (P.q8a) {
+    if (P.q8) {
       const uint4* row = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)i;
       const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
-      P.q8a[i] = q.a;
-      P.q8b[i] = q.b;
+      P.q8[2 * (size_t)i] = make_uint4(q.a.x, q.a.y, (uint32_t)q.nt, 0u);
+      P.q8[2 * (size_t)i + 1] = make_uint4(q.a.z, q.a.w, q.b.x, q.b.y);
       a1max = max(a1max, q.l2);
       qbad |= q.bad;
     }
   }
-  if (P.q8a) {
+  if (P.q8) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a1max = max(a1max, __shfl_xor_sync(0xffffffffu, a1max, o));
@@ -330,13 +343,17 @@ __global__ void __launch_bounds__(1024) k_sel_scan(const PairDev* __restrict__ p
   __syncthreads();
   uint32_t excl = wsum[t >> 5] + incl - s;
   SelState* st = P.sel;
-  if (PASS == 1 && t == 0) {
-    st->n = total;
-    st->k = total / 2;
-    st->krem = total / 2;
+  __shared__ uint32_t krem_s;
+  if (t == 0) {
+    if (PASS == 1) {
+      st->n = total;
+      st->k = total / 2;
+      st->krem = total / 2;
+    }
+    krem_s = st->krem;  // read once: the matching thread rewrites st->krem below
   }
   __syncthreads();
-  const uint32_t krem = st->krem;
+  const uint32_t krem = krem_s;
   if (total == 0) {
     if (t == 0) {
       st->prefix = 0;
@@ -353,7 +370,12 @@ __global__ void __launch_bounds__(1024) k_sel_scan(const PairDev* __restrict__ p
       } else if (PASS == 2) {
         st->prefix = (st->prefix << 12) | (uint32_t)b;
       } else {
+        // the fp32 key of the rank-k norm; k_sel_exact resolves it to the
+        // FP64 norm (the keys are fp32 roundings of FP64 norms: monotone, so
+        // the median is the krem-th smallest FP64 norm among those with this key)
         const uint32_t key = (st->prefix << 8) | (uint32_t)b;
+        st->key = key;
+        st->ties = local[j];
         st->threshold = fraction * (double)__uint_as_float(key);
       }
       st->krem = krem - excl;
@@ -385,11 +407,100 @@ __global__ void __launch_bounds__(256) k_sel_hist(const PairDev* __restrict__ pa
     if (sh[i]) atomicAdd(&h[i], sh[i]);
 }
 
+// FP64 norm of an a-pixel exactly as normalize_rays / median_scene_distance
+// compute it (camera.cpp:49, 183: x*x + y*y + z*z in order, no FMA, sqrt).
+__device__ __forceinline__ double norm64(const float* __restrict__ xa, int i) {
+  const double x = xa[3 * i], y = xa[3 * i + 1], z = xa[3 * i + 2];
+  return sqrt(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+// Exact median, step 1: the FP64 norms whose fp32 key equals the selected key
+// (st->ties of them; kept when there are at most kSelCap).
+__global__ void __launch_bounds__(256) k_sel_collect(const PairDev* __restrict__ pairs, int px_per_block) {
+  const PairDev& P = pairs[blockIdx.y];
+  SelState* st = P.sel;
+  if (st->n == 0 || st->ties > (uint32_t)kSelCap) return;
+  const uint32_t key = st->key;
+  const int HW = P.Ha * P.Wa;
+  const int begin = blockIdx.x * px_per_block;
+  const int end = min(HW, begin + px_per_block);
+  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
+    if (P.keys[i] != key) continue;
+    const uint32_t slot = atomicAdd(&st->cnt, 1u);
+    if (slot < (uint32_t)kSelCap) st->cand[slot] = norm64(P.xa, i);
+  }
+}
+
+// Exact median, step 2 (one block per pair): the krem-th smallest of the
+// tied FP64 norms -> median and threshold = fraction * median (camera.cpp:
+// 188-190, 199-200).  More than kSelCap ties (adversarial inputs): exact
+// bisection over the FP64 bit patterns of the tied norms (positive doubles
+// order as their bit patterns), one counting pass over the pair per step.
+__global__ void __launch_bounds__(256) k_sel_exact(const PairDev* __restrict__ pairs, double fraction) {
+  const PairDev& P = pairs[blockIdx.x];
+  SelState* st = P.sel;
+  if (st->n == 0) {
+    if (threadIdx.x == 0) st->median = 0.0;
+    return;
+  }
+  const uint32_t krem = st->krem, ties = st->ties;
+  if (ties <= (uint32_t)kSelCap) {
+    for (uint32_t t = threadIdx.x; t < ties; t += blockDim.x) {
+      const double v = st->cand[t];
+      uint32_t less = 0, eq = 0;
+      for (uint32_t o = 0; o < ties; ++o) {
+        less += st->cand[o] < v;
+        eq += st->cand[o] == v;
+      }
+      if (less <= krem && krem < less + eq) {  // equal values write the same result
+        st->median = v;
+        st->threshold = fraction * v;
+      }
+    }
+    return;
+  }
+  __shared__ unsigned long long lo_s, hi_s;
+  __shared__ uint32_t count_s;
+  const uint32_t key = st->key;
+  const int HW = P.Ha * P.Wa;
+  if (threadIdx.x == 0) {
+    lo_s = 0ull;
+    hi_s = 0x7ff0000000000000ull;  // +inf
+  }
+  __syncthreads();
+  for (int step = 0; step < 64; ++step) {
+    const unsigned long long lo = lo_s, hi = hi_s;
+    if (lo >= hi) break;
+    const unsigned long long mid = lo + (hi - lo) / 2;
+    if (threadIdx.x == 0) count_s = 0;
+    __syncthreads();
+    uint32_t c = 0;
+    for (int i = threadIdx.x; i < HW; i += blockDim.x)
+      if (P.keys[i] == key && (unsigned long long)__double_as_longlong(norm64(P.xa, i)) <= mid) ++c;
+    atomicAdd(&count_s, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (count_s >= krem + 1)
+        hi_s = mid;
+      else
+        lo_s = mid + 1;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double v = __longlong_as_double((long long)lo_s);
+    st->median = v;
+    st->threshold = fraction * v;
+  }
+}
+
 // ---------------------------------------------------------------- LM
-__device__ __forceinline__ double4 ld_ray(const double4* rays, int i) {
-  const double2* p = reinterpret_cast<const double2*>(rays + i);
-  const double2 a = __ldg(p), b = __ldg(p + 1);
-  return make_double4(a.x, a.y, b.x, b.y);
+// One 256-bit load per support (LDG.E.ENL2.256 on sm_100: 32-byte aligned
+// double4 through the read-only path).
+__device__ __forceinline__ double4 ld_ray(const double4* __restrict__ rays, int i) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(rays + i));
+  return v;
 }
 
 // interpolate_ray, camera.cpp:58-100, split so the 3x2 Jacobian is only
@@ -477,14 +588,17 @@ __device__ __forceinline__ void ldlt2_solve(double h00, double h01, double h11, 
     *x1 = 0.0;
     return;
   }
-  m10 /= m00;
+  // the quotients of Eigen's LDLT as products with reciprocals (within 1-2
+  // ulp of the IEEE quotients, like the rsqrt normalisation of interp_eval)
+  const double i00 = rcp64(m00);
+  m10 *= i00;
   const double temp0 = m00 * m10;
   m11 -= m10 * temp0;
   double d0 = sw ? b1 : b0, d1 = sw ? b0 : b1;
   d1 -= m10 * d0;
   const double tiny = 2.2250738585072014e-308;
-  d0 = fabs(m00) > tiny ? d0 / m00 : 0.0;
-  d1 = fabs(m11) > tiny ? d1 / m11 : 0.0;
+  d0 = fabs(m00) > tiny ? d0 * i00 : 0.0;
+  d1 = fabs(m11) > tiny ? d1 * rcp64(m11) : 0.0;
   d0 -= m10 * d1;
   *x0 = sw ? d1 : d0;
   *x1 = sw ? d0 : d1;
@@ -511,7 +625,8 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     res.pv = cv;
     return res;
   }
-  const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
+  const double ixn = rcp64(xn);
+  const double t0 = x0 * ixn, t1 = x1 * ixn, t2 = x2 * ixn;
   double pu = cu, pv = cv;
   Interp I;
   if (!interp_eval(rays, W, H, pu, pv, I)) {
@@ -1002,16 +1117,19 @@ __global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pa
 // previous window (those were all strictly below the moved-to centre); a level
 // whose window is unchanged is skipped (camera.cpp semantics, strict '>').
 struct QB {  // register-resident int8 target descriptor
-  uint32_t w[6];
+  uint32_t w[6];  // dims 0-3, 4-7 (head), 8-11, 12-15, 16-19, 20-23 (tail)
+  int nt;         // ceil(sqrt(sum of squares of the tail))
 };
 
-__device__ __forceinline__ int qdot(const uint4 a, const uint2 b, const QB& B) {
-  int s = __dp4a((int)a.x, (int)B.w[0], 0);
-  s = __dp4a((int)a.y, (int)B.w[1], s);
-  s = __dp4a((int)a.z, (int)B.w[2], s);
-  s = __dp4a((int)a.w, (int)B.w[3], s);
-  s = __dp4a((int)b.x, (int)B.w[4], s);
-  return __dp4a((int)b.y, (int)B.w[5], s);
+// Head (dims 0-7) and tail (dims 8-23) partial scores of one candidate.
+__device__ __forceinline__ int qdot_head(const uint4 h, const QB& B) {
+  return __dp4a((int)h.y, (int)B.w[1], __dp4a((int)h.x, (int)B.w[0], 0));
+}
+__device__ __forceinline__ int qdot_tail(const uint4 t, const QB& B, int s) {
+  s = __dp4a((int)t.x, (int)B.w[2], s);
+  s = __dp4a((int)t.y, (int)B.w[3], s);
+  s = __dp4a((int)t.z, (int)B.w[4], s);
+  return __dp4a((int)t.w, (int)B.w[5], s);
 }
 
 // Best and second-best candidate of a scan as packed keys score * 256 + rank
@@ -1032,24 +1150,41 @@ __device__ __forceinline__ void top2_add(Top2& T, int key) {
 // The int8 a-image read in place from the (L2-resident) chunk scratch
 // through the L1 cache: no staging, no block barriers.
 struct QGlob {
-  const uint4* __restrict__ a;
-  const uint2* __restrict__ b;
-  int bw;  // row pitch (= W)
+  const uint4* __restrict__ q;  // 2 words per pixel (see PairDev::q8)
+  int bw;                       // row pitch (= W)
   __device__ __forceinline__ int at(int u, int v) const { return v * bw + u; }
-  __device__ __forceinline__ int score(int i, const QB& B) const { return qdot(__ldg(a + i), __ldg(b + i), B); }
+  __device__ __forceinline__ uint4 head(int i) const { return __ldg(q + 2 * i); }
+  __device__ __forceinline__ uint4 tail(int i) const { return __ldg(q + 2 * i + 1); }
+  __device__ __forceinline__ int score(int i, const QB& B) const { return qdot_tail(tail(i), B, qdot_head(head(i), B)); }
 };
 
-// First level, compile-time radius / stride, window inside the image: all
-// (2R+1)^2 candidates, unrolled (LDS immediate offsets, 6 DP4A each).
+// First level, compile-time radius / stride, window inside the image,
+// unrolled (immediate load offsets).  The centre is scored first; every other
+// candidate costs its 8-dim head score plus the Cauchy-Schwarz bound of its
+// tail, |tail . b_tail| <= nt_a nt_b, and is skipped when even that upper
+// bound stays at or below best - tgap - 1: it can then neither become the
+// argmax nor come within the uniqueness gap of the final best (which is >=
+// the running best), so skipping it leaves the decision exact.  Survivors
+// (the true peak, near ties) get the full score (4 more DP4A).
 template <int R, int S, class Tile>
-__device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int cv) {
-  constexpr int D = 2 * R + 1;
-  Top2 t{INT_MIN, INT_MIN};
+__device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int cv, int tgap) {
+  constexpr int D = 2 * R + 1, C = R * D + R;
   const int base = T.at(cu - R * S, cv - R * S);
+  Top2 t{qkey(T.score(base + R * S * T.bw + R * S, B), C), INT_MIN};
+  int thr = t.score1() - tgap - 1;
 #pragma unroll
   for (int dv = 0; dv < D; ++dv) {
 #pragma unroll
-    for (int du = 0; du < D; ++du) top2_add(t, qkey(T.score(base + dv * S * T.bw + du * S, B), dv * D + du));
+    for (int du = 0; du < D; ++du) {
+      if (dv * D + du == C) continue;
+      const int i = base + dv * S * T.bw + du * S;
+      const uint4 h = T.head(i);
+      const int s8 = qdot_head(h, B);
+      if (s8 + (int)h.z * B.nt > thr) {
+        top2_add(t, qkey(qdot_tail(T.tail(i), B, s8), dv * D + du));
+        thr = t.score1() - tgap - 1;
+      }
+    }
   }
   return t;
 }
@@ -1123,9 +1258,9 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
                               q.cv + r * s < Ha;
         if (interior && s == 1 && r == 3) {
-          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv);
+          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
         } else if (interior && s == 2 && r == 2) {
-          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv);
+          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap);
         } else {
           if (q.best == INT_MIN) q.best = T.score(T.at(q.cu, q.cv), B);
           t = q_level_lane(T, B, q.cu, q.cv, s, r, Wa, Ha, q.best, q.pcu, q.pcv, q.ps, q.pr);
@@ -1143,6 +1278,7 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         QB Bs;
 #pragma unroll
         for (int w = 0; w < 6; ++w) Bs.w[w] = __shfl_sync(0xffffffffu, B.w[w], src);
+        Bs.nt = __shfl_sync(0xffffffffu, B.nt, src);
         Top2 t{lane == 0 ? qkey(centre, lim0) : INT_MIN, INT_MIN};
         const int lim = pr * ps;
         for (int k = lane; k < nc; k += 32) {
@@ -1191,7 +1327,7 @@ __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restri
     pcv = r.w;
     if (r.y) n = m;
   }
-  const bool fast_pair = P.q8a != nullptr && P.sel->qbad == 0;
+  const bool fast_pair = P.q8 != nullptr && P.sel->qbad == 0;
   QB B;
   int tgap = 0;
   bool fast = n >= 0 && fast_pair;
@@ -1204,12 +1340,13 @@ __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restri
     B.w[3] = q.a.w;
     B.w[4] = q.b.x;
     B.w[5] = q.b.y;
+    B.nt = q.nt;
     tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
     fast = !q.bad;
   }
   QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
   if (__any_sync(0xffffffffu, fast)) {
-    const QGlob T{P.q8a, P.q8b, P.Wa};
+    const QGlob T{P.q8, P.Wa};
     q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
   }
   if (exact_px) {
@@ -1386,6 +1523,10 @@ static void select_rounds(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, 
   launch_check(ctx, "k_sel_hist3");
   k_sel_scan<3><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
   launch_check(ctx, "k_sel_scan3");
+  k_sel_collect<<<g1, 256, 0, ctx.stream>>>(dev_pairs, ppb);
+  launch_check(ctx, "k_sel_collect");
+  k_sel_exact<<<n, 256, 0, ctx.stream>>>(dev_pairs, fraction);
+  launch_check(ctx, "k_sel_exact");
 }
 
 static void select_median(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
@@ -1437,7 +1578,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   }
   // chunks of pairs sharing one scratch allocation: FP64 ray maps + int8
   // descriptors (56 B per a-pixel), see kChunkBytes
-  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2);
+  const size_t per_px = sizeof(double4) + 2 * sizeof(uint4);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   int chunk = std::max(1, std::min(npairs, (int)((size_t(kChunkBytes)) / std::max<size_t>(pair_bytes, 1))));
   if (hooks) chunk = std::max(1, std::min(chunk, hooks->chunk_pairs));
@@ -1450,8 +1591,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   char* base = scratch.as<char>();
   const size_t nslot = (size_t)max_hwa * chunk;
   double4* rays = reinterpret_cast<double4*>(base);
-  uint4* q8a = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
-  uint2* q8b = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint4* q8 = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
@@ -1461,8 +1601,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     hp[i].dnorm = nullptr;
     const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
     if (refine && hp[i].dim == 24 && aligned) {
-      hp[i].q8a = q8a + (size_t)slot * max_hwa;
-      hp[i].q8b = q8b + (size_t)slot * max_hwa;
+      hp[i].q8 = q8 + 2 * (size_t)slot * max_hwa;
     }
   }
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
@@ -1835,6 +1974,57 @@ extern "C" int pmx_impl_normalize_rays(pmx_context* c, pmx_memory mem, const pmx
   st.back(rays, orays, 3 * hw);
   st.back(distances, odist, hw);
   st.back(valid, ov, hw);
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+__global__ void k_interp_points(const double4* __restrict__ rays, int W, int H, int64_t n, const double* __restrict__ p,
+                                double* ray, double* jac, uint8_t* ok) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double r[3] = {0.0, 0.0, 0.0}, J[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  const bool good = interp_ray(rays, W, H, p[2 * k], p[2 * k + 1], r, J);
+  if (!good) r[0] = r[1] = r[2] = J[0] = J[1] = J[2] = J[3] = J[4] = J[5] = 0.0;
+  for (int c = 0; c < 3; ++c) ray[3 * k + c] = r[c];
+  if (jac)
+    for (int c = 0; c < 6; ++c) jac[6 * k + c] = J[c];  // J[0..2] = d/du, J[3..5] = d/dv
+  ok[k] = good ? 1 : 0;
+}
+
+extern "C" int pmx_impl_interpolate_ray(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, int64_t n,
+                                        const double* p, double* ray, double* jacobian, uint8_t* ok) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(pm && p && ray && ok && n >= 0, "interpolate_ray: null arguments");
+  Stager st(ctx, mem);
+  DevBuf r, k, h, s, d;
+  const float* xyz = nullptr;
+  build_raymap(ctx, st, pm, r, k, h, s, d, &xyz);
+  const double* dp = st.in(p, 2 * (size_t)n);
+  double* dray = st.out(ray, 3 * (size_t)n);
+  double* djac = jacobian ? st.out(jacobian, 6 * (size_t)n) : nullptr;
+  uint8_t* dok = st.out(ok, (size_t)n);
+  if (n > 0) {
+    k_interp_points<<<(unsigned)((n + 127) / 128), 128, 0, ctx.stream>>>(r.as<double4>(), pm->width, pm->height, n,
+                                                                         dp, dray, djac, dok);
+    launch_check(ctx, "k_interp_points");
+  }
+  st.back(ray, dray, 3 * (size_t)n);
+  if (jacobian) st.back(jacobian, djac, 6 * (size_t)n);
+  st.back(ok, dok, (size_t)n);
+  if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_median_scene_distance(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, double* out) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(pm && out, "median_scene_distance: null arguments");
+  Stager st(ctx, mem);
+  DevBuf r, k, h, s, d;
+  const float* xyz = nullptr;
+  build_raymap(ctx, st, pm, r, k, h, s, d, &xyz);  // fraction 1.0: threshold = median
+  double* dout = st.out(out, 1);
+  PMX_CUDA(cudaMemcpyAsync(dout, &s.as<SelState>()->median, sizeof(double), cudaMemcpyDeviceToDevice, ctx.stream));
+  st.back(out, dout, 1);
   if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
   return PMX_OK;
 }

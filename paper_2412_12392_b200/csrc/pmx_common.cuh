@@ -356,6 +356,22 @@ __host__ __device__ inline void ldlt_pivoted_solve(int n, const double* A_in, co
 // the same bin (keys of one image cluster in a few bins: plain atomics would
 // serialise on them).  Call from every lane of the converged warp; `take` =
 // this lane has a key.
+// FP64 reciprocal from the MUFU seed + two Newton steps (within 1 ulp of the
+// correctly rounded 1/d; zero, non-finite and extreme inputs take the IEEE
+// division).
+__device__ __forceinline__ double rcp64(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  double e = fma(-d, r, 1.0);
+  e = fma(e, e, e);
+  r = fma(r, e, r);
+  e = fma(-d, r, 1.0);
+  r = fma(r, e, r);
+  const double ad = fabs(d);
+  if (!(ad > 1e-300 && ad < 1e300)) r = 1.0 / d;
+  return r;
+}
+
 __device__ __forceinline__ void hist_add(uint32_t* sh, uint32_t bin, bool take) {
   const unsigned active = __activemask();
   const unsigned with = __ballot_sync(active, take);

@@ -303,3 +303,57 @@ def test_empty_batch_and_all_invalid_pair(ctx):
     dead = dict(pair, valid_a=np.zeros_like(pair["valid_a"]), valid_b=np.zeros_like(pair["valid_b"]))
     g = ctx.match_batch([pmx_pair(dead)], params=baseline_match_params(), refine=abi.refine_params(BASELINE_REFINE))[0]
     assert not np.asarray(g.valid).any() and (np.asarray(g.pixel_a) == -1).all()
+
+
+def _sphere_points(n, radius, seed):
+    rng = np.random.default_rng(seed)
+    d = rng.normal(size=(n, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return (radius * d).astype(np.float32)
+
+
+@pytest.mark.parametrize("case", ["config0", "sphere_ties", "even_count", "with_invalid", "empty"])
+def test_median_scene_distance_exact(ctx, case):
+    """median_scene_distance (camera.cpp:178-191) is the FP64 rank-floor(n/2)
+    norm; the device selects it exactly, including many FP64 norms that share
+    one fp32 key (points on a sphere: > 64 ties, the bisection path)."""
+    h, w = 96, 128
+    valid = None
+    if case == "config0":
+        xyz = pmxgen.config0(seed=8, height=h, width=w)["X_a"]
+    elif case in ("sphere_ties", "even_count"):
+        xyz = _sphere_points(h * w, 2.0, 9)
+        if case == "even_count":
+            valid = np.ones(h * w, np.uint8)
+            valid[::97] = 0
+    elif case == "with_invalid":
+        xyz = pmxgen.config0(seed=10, height=h, width=w)["X_a"].copy()
+        valid = (np.arange(h * w) % 3 != 0).astype(np.uint8)
+        xyz[::5] = 0.0  # |p| < 1e-12 is excluded too
+    else:
+        xyz = np.zeros((h * w, 3), np.float32)
+    got = ctx.median_scene_distance(Pointmap(xyz, valid, h, w))
+    want = pyoracle.median_scene_distance(xyz, valid, h, w)
+    assert got == want, (got, want)
+
+
+def test_interpolate_ray_entry(ctx):
+    pair = pmxgen.config0(seed=12, height=96, width=128)
+    rng = np.random.default_rng(1)
+    p = np.c_[rng.uniform(-1, 128, 3000), rng.uniform(-1, 96, 3000)]
+    p[:20] = np.floor(p[:20])
+    p[20:30, 0] = 127.0
+    ray, J, ok = ctx.interpolate_ray(Pointmap(pair["X_a"], pair["valid_a"], 96, 128), p)
+    with (pyoracle.reference() if pyoracle.have_reference() else _nullctx()):
+        oray, oJ, ook = pyoracle.interpolate_ray(pair["X_a"], pair["valid_a"], 96, 128, p)
+    assert np.array_equal(ok, ook) and ok.sum() > 2000
+    np.testing.assert_allclose(ray[ok == 1], oray[ook == 1], rtol=0, atol=4e-16)
+    np.testing.assert_allclose(J[ok == 1], oJ[ook == 1], rtol=1e-12, atol=1e-14)
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
