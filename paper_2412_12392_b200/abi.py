@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libpmx_cuda.so")
+# PMX_LIB (dev only): load a variant build of the library instead (tools/variants.sh)
+LIB_PATH = os.environ.get("PMX_LIB") or os.path.join(_HERE, "csrc", "libpmx_cuda.so")
 
 PMX_OK = 0
 PMX_ERR_INVALID_ARGUMENT = 1
@@ -185,6 +186,8 @@ def load_library(path: str = LIB_PATH):
     lib.pmx_constrain_to_rays.argtypes = [C.c_void_p, C.c_int, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                           C.c_void_p]
     for name in PMX_SYMBOLS:
+        if os.environ.get("PMX_LIB") and not hasattr(lib, name):
+            continue  # dev variant builds of older sources may lack newer entries
         fn = getattr(lib, name)
         if name not in ("pmx_last_error", "pmx_get_stream", "pmx_kernel_launch_count",
                         "pmx_create") and not name.startswith("pmx_default") \

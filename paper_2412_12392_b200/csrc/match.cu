@@ -33,6 +33,17 @@
 
 #include "pmx_common.cuh"
 
+// Build-time variants (dev ablations; defaults are the product).
+#ifndef PMX_PRUNE
+#define PMX_PRUNE 0  // head-bound pruning of level-1 refinement candidates
+#endif
+#ifndef PMX_LD256
+#define PMX_LD256 1  // one 256-bit load per ray-map support
+#endif
+#ifndef PMX_RCP
+#define PMX_RCP 1  // LM quotients as products with reciprocals
+#endif
+
 namespace pmx {
 
 constexpr int kHist1 = 4096, kHist2 = 4096, kHist3 = 256;
@@ -82,11 +93,13 @@ struct PairDev {
   // descriptor pruning aux (dim == 24, 16-byte rows): planar 8-dim heads and
   // {||a||_2, ||a[8:24]||_2} upper bounds of every a-pixel (L2-resident)
   float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (standalone refine)
-  // int8 descriptors of every a-pixel, round(127 x) (batched refine), 32 B per
-  // pixel as two words: q8[2i] = {dims 0-3, dims 4-7, nt, 0} with nt =
-  // ceil(sqrt(sum of the squares of dims 8-23)) (the Cauchy-Schwarz bound of
-  // the tail), q8[2i+1] = dims 8-23
-  uint4* q8;
+  // int8 descriptors of every a-pixel, round(127 x) (batched refine), planar
+  // (a warp's 32 neighbouring candidates read contiguous bytes): q8h = dims
+  // 0-7, q8n = nt = ceil(sqrt(sum of squares of dims 8-23)) (the
+  // Cauchy-Schwarz bound of the tail), q8t = dims 8-23
+  uint2* q8h;
+  uint16_t* q8n;
+  uint4* q8t;
 };
 
 struct LMParams {
@@ -270,16 +283,17 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
     P.rays[i] = r;
     if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
-    if (P.q8) {
+    if (P.q8h) {
       const uint4* row = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)i;
       const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
-      P.q8[2 * (size_t)i] = make_uint4(q.a.x, q.a.y, (uint32_t)q.nt, 0u);
-      P.q8[2 * (size_t)i + 1] = make_uint4(q.a.z, q.a.w, q.b.x, q.b.y);
+      P.q8h[i] = make_uint2(q.a.x, q.a.y);
+      P.q8n[i] = (uint16_t)q.nt;
+      P.q8t[i] = make_uint4(q.a.z, q.a.w, q.b.x, q.b.y);
       a1max = max(a1max, q.l2);
       qbad |= q.bad;
     }
   }
-  if (P.q8) {
+  if (P.q8h) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a1max = max(a1max, __shfl_xor_sync(0xffffffffu, a1max, o));
@@ -498,14 +512,22 @@ __global__ void __launch_bounds__(256) k_sel_exact(const PairDev* __restrict__ p
 // One 256-bit load per support (LDG.E.ENL2.256 on sm_100: 32-byte aligned
 // double4 through the read-only path).
 __device__ __forceinline__ double4 ld_ray(const double4* __restrict__ rays, int i) {
+#if PMX_LD256
   double4 v;
   asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(rays + i));
   return v;
+#else
+  const double2* p = reinterpret_cast<const double2*>(rays + i);
+  const double2 a = __ldg(p), b = __ldg(p + 1);
+  return make_double4(a.x, a.y, b.x, b.y);
+#endif
 }
 
 // interpolate_ray, camera.cpp:58-100, split so the 3x2 Jacobian is only
 // formed for accepted points (the reference computes it for every trial;
 // the value is identical, it is just never used when a trial is rejected).
+// (An eager-Jacobian form that lets the supports die early measured ~1%
+// slower: the extra FP64 work of rejected trials outweighs the registers.)
 struct Interp {
   double r0, r1, r2;  // unit ray g / |g|
   double rs;          // 1 / |g|
@@ -590,15 +612,24 @@ __device__ __forceinline__ void ldlt2_solve(double h00, double h01, double h11, 
   }
   // the quotients of Eigen's LDLT as products with reciprocals (within 1-2
   // ulp of the IEEE quotients, like the rsqrt normalisation of interp_eval)
+#if PMX_RCP
   const double i00 = rcp64(m00);
   m10 *= i00;
+#else
+  m10 /= m00;
+#endif
   const double temp0 = m00 * m10;
   m11 -= m10 * temp0;
   double d0 = sw ? b1 : b0, d1 = sw ? b0 : b1;
   d1 -= m10 * d0;
   const double tiny = 2.2250738585072014e-308;
+#if PMX_RCP
   d0 = fabs(m00) > tiny ? d0 * i00 : 0.0;
   d1 = fabs(m11) > tiny ? d1 * rcp64(m11) : 0.0;
+#else
+  d0 = fabs(m00) > tiny ? d0 / m00 : 0.0;
+  d1 = fabs(m11) > tiny ? d1 / m11 : 0.0;
+#endif
   d0 -= m10 * d1;
   *x0 = sw ? d1 : d0;
   *x1 = sw ? d0 : d1;
@@ -625,8 +656,12 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     res.pv = cv;
     return res;
   }
+#if PMX_RCP
   const double ixn = rcp64(xn);
   const double t0 = x0 * ixn, t1 = x1 * ixn, t2 = x2 * ixn;
+#else
+  const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
+#endif
   double pu = cu, pv = cv;
   Interp I;
   if (!interp_eval(rays, W, H, pu, pv, I)) {
@@ -1122,7 +1157,7 @@ struct QB {  // register-resident int8 target descriptor
 };
 
 // Head (dims 0-7) and tail (dims 8-23) partial scores of one candidate.
-__device__ __forceinline__ int qdot_head(const uint4 h, const QB& B) {
+__device__ __forceinline__ int qdot_head(const uint2 h, const QB& B) {
   return __dp4a((int)h.y, (int)B.w[1], __dp4a((int)h.x, (int)B.w[0], 0));
 }
 __device__ __forceinline__ int qdot_tail(const uint4 t, const QB& B, int s) {
@@ -1150,11 +1185,14 @@ __device__ __forceinline__ void top2_add(Top2& T, int key) {
 // The int8 a-image read in place from the (L2-resident) chunk scratch
 // through the L1 cache: no staging, no block barriers.
 struct QGlob {
-  const uint4* __restrict__ q;  // 2 words per pixel (see PairDev::q8)
-  int bw;                       // row pitch (= W)
+  const uint2* __restrict__ h;     // dims 0-7 (see PairDev::q8h)
+  const uint16_t* __restrict__ n;  // tail bound
+  const uint4* __restrict__ t;     // dims 8-23
+  int bw;                          // row pitch (= W)
   __device__ __forceinline__ int at(int u, int v) const { return v * bw + u; }
-  __device__ __forceinline__ uint4 head(int i) const { return __ldg(q + 2 * i); }
-  __device__ __forceinline__ uint4 tail(int i) const { return __ldg(q + 2 * i + 1); }
+  __device__ __forceinline__ uint2 head(int i) const { return __ldg(h + i); }
+  __device__ __forceinline__ int nt(int i) const { return (int)__ldg(n + i); }
+  __device__ __forceinline__ uint4 tail(int i) const { return __ldg(t + i); }
   __device__ __forceinline__ int score(int i, const QB& B) const { return qdot_tail(tail(i), B, qdot_head(head(i), B)); }
 };
 
@@ -1178,9 +1216,8 @@ __device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int
     for (int du = 0; du < D; ++du) {
       if (dv * D + du == C) continue;
       const int i = base + dv * S * T.bw + du * S;
-      const uint4 h = T.head(i);
-      const int s8 = qdot_head(h, B);
-      if (s8 + (int)h.z * B.nt > thr) {
+      const int s8 = qdot_head(T.head(i), B);
+      if (!PMX_PRUNE || s8 + T.nt(i) * B.nt > thr) {
         top2_add(t, qkey(qdot_tail(T.tail(i), B, s8), dv * D + du));
         thr = t.score1() - tgap - 1;
       }
@@ -1313,7 +1350,10 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
 // the valid matches; the int8 a-image (L2-resident chunk scratch) is read
 // through L1, where a tile's windows overlap.  Fusing lets the FP64-bound LM
 // of some warps overlap the integer-bound refinement of others on every SM.
-__global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
+#ifndef PMX_MR_BLOCKS
+#define PMX_MR_BLOCKS 4  // resident CTAs per SM (64 registers)
+#endif
+__global__ void __launch_bounds__(256, PMX_MR_BLOCKS) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
                                                          RefineLevels L, unsigned long long* __restrict__ exact_px) {
   const PairDev& P = pairs[blockIdx.z];
   if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * 8 >= P.Hb) return;
@@ -1327,7 +1367,7 @@ __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restri
     pcv = r.w;
     if (r.y) n = m;
   }
-  const bool fast_pair = P.q8 != nullptr && P.sel->qbad == 0;
+  const bool fast_pair = P.q8h != nullptr && P.sel->qbad == 0;
   QB B;
   int tgap = 0;
   bool fast = n >= 0 && fast_pair;
@@ -1346,7 +1386,7 @@ __global__ void __launch_bounds__(256, 4) k_match_refine(const PairDev* __restri
   }
   QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
   if (__any_sync(0xffffffffu, fast)) {
-    const QGlob T{P.q8, P.Wa};
+    const QGlob T{P.q8h, P.q8n, P.q8t, P.Wa};
     q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
   }
   if (exact_px) {
@@ -1578,7 +1618,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   }
   // chunks of pairs sharing one scratch allocation: FP64 ray maps + int8
   // descriptors (56 B per a-pixel), see kChunkBytes
-  const size_t per_px = sizeof(double4) + 2 * sizeof(uint4);
+  const size_t per_px = sizeof(double4) + sizeof(uint2) + sizeof(uint16_t) + sizeof(uint4);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   int chunk = std::max(1, std::min(npairs, (int)((size_t(kChunkBytes)) / std::max<size_t>(pair_bytes, 1))));
   if (hooks) chunk = std::max(1, std::min(chunk, hooks->chunk_pairs));
@@ -1591,7 +1631,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   char* base = scratch.as<char>();
   const size_t nslot = (size_t)max_hwa * chunk;
   double4* rays = reinterpret_cast<double4*>(base);
-  uint4* q8 = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
+  uint4* q8t = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
+  uint2* q8h = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint16_t* q8n = reinterpret_cast<uint16_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(uint2)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
@@ -1601,7 +1643,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     hp[i].dnorm = nullptr;
     const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
     if (refine && hp[i].dim == 24 && aligned) {
-      hp[i].q8 = q8 + 2 * (size_t)slot * max_hwa;
+      hp[i].q8h = q8h + (size_t)slot * max_hwa;
+      hp[i].q8n = q8n + (size_t)slot * max_hwa;
+      hp[i].q8t = q8t + (size_t)slot * max_hwa;
     }
   }
   PMX_CUDA(cudaMemcpyAsync(dpairs.p, hp.data(), sizeof(PairDev) * npairs, cudaMemcpyHostToDevice, ctx.stream));
