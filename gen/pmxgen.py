@@ -368,3 +368,116 @@ def config2(seed: int = 2, height=H, width=W, n_kf: int = 32, edges=None):
         return pair_from_cameras(cam(a), cam(b), salt=2 * e)
 
     return sc, poses, edges, make_pair
+
+
+# ------------------------------------------------- device pair predictions
+_CU_PATH = os.path.join(_HERE, "libpmx_gen_cuda.so")
+_cu = None
+
+
+def _load_cuda():
+    global _cu
+    if _cu is None:
+        if not os.path.exists(_CU_PATH):
+            subprocess.check_call(["make", "-s", "-C", _HERE, "libpmx_gen_cuda.so"])
+        _cu = C.CDLL(_CU_PATH)
+        _cu.gen_cuda_express.restype = C.c_int
+        _cu.gen_cuda_pair_desc.restype = C.c_int
+    return _cu
+
+
+def _tp(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class DeviceCamera:
+    """A Camera's world points / validity / Q resident on the GPU (torch)."""
+
+    def __init__(self, cam: Camera, device):
+        import torch
+        self.cam = cam
+        self.P = torch.from_numpy(cam.P).to(device)
+        self.valid = torch.from_numpy(cam.valid).to(device)
+        self.Q = torch.from_numpy(cam.Q).to(device)
+
+
+def device_pair(ca: DeviceCamera, cb: DeviceCamera, salt: int, stream=None):
+    """Pair prediction of edge (a, b) in frame a generated on the GPU
+    (gen/pmx_gen_cuda.cu, the device twin of pair_from_cameras)."""
+    import torch
+    from paper_2412_12392_b200.abi import pmx_sim3
+    sc = ca.cam.scene
+    n = sc.height * sc.width
+    dev = ca.P.device
+    s = C.c_void_p(stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream)
+    Ta = ca.cam.T.to_struct(pmx_sim3)
+    Tb = cb.cam.T.to_struct(pmx_sim3)
+    X_a = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    X_b = torch.empty((n, 3), dtype=torch.float32, device=dev)
+    D_a = torch.empty((n, sc.dim), dtype=torch.int16, device=dev)
+    D_b = torch.empty((n, sc.dim), dtype=torch.int16, device=dev)
+    L = _load_cuda()
+    for rc in (L.gen_cuda_express(_p(sc.params), C.c_int64(ca.cam.image_id), C.byref(Ta), C.byref(Ta),
+                                  C.c_uint64(salt), _tp(ca.P), _tp(ca.valid), _tp(X_a), s),
+               L.gen_cuda_express(_p(sc.params), C.c_int64(cb.cam.image_id), C.byref(Tb), C.byref(Ta),
+                                  C.c_uint64(salt + 1), _tp(cb.P), _tp(cb.valid), _tp(X_b), s),
+               L.gen_cuda_pair_desc(_p(sc.params), C.c_int64(ca.cam.image_id), C.byref(Ta), _tp(ca.valid),
+                                    C.c_int64(cb.cam.image_id), _tp(cb.P), _tp(cb.valid), _tp(D_a), _tp(D_b), s)):
+        if rc != 0:
+            raise RuntimeError(f"gen_cuda: CUDA error {rc}")
+    return {"X_a": X_a, "valid_a": ca.valid, "Q_a": ca.Q, "D_a": D_a,
+            "X_b": X_b, "valid_b": cb.valid, "Q_b": cb.Q, "D_b": D_b, "height": sc.height, "width": sc.width}
+
+
+MATCHED_SALT = 1_000_000
+
+
+def backend_graph_matched(ctx, n_kf: int, reach: int, seed: int, height=H, width=W, loops: int = 1,
+                          radius: float = 5.0, rot_deg=2.0, trans=0.05, scale_frac=0.03, edge_range=None,
+                          chunk: int = 64, device=None, keep_host: bool = False):
+    """Configs 3/4 with matches "precomputed as in config 2" (BASELINE.json):
+    every edge's pair prediction (camera i's and camera j's points in frame
+    i + pair descriptors, generated on the GPU) is matched by the product's
+    batched matcher (LM lambda 1e-8, tol 1e-6 rad, refine {(1,3),(1,3)}), and
+    the resulting MatchSets (pixel_a in i, pixel_b = index in j, q, valid)
+    are the backend's frozen matches.  Canonicals, poses, edges and the
+    perturbed initial poses are those of backend_graph.  Returns the
+    backend_graph dict with "matches" as device MatchSets (and host numpy
+    copies under "matches_host" when keep_host)."""
+    import torch
+    from paper_2412_12392_b200 import FeatureMap, MatchSet, Pointmap, abi
+    device = device or torch.device("cuda", torch.cuda.current_device())
+    sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H, surface="heightfield")
+    gt = loop_trajectory(n_kf, radius, loops, seed)
+    cams = [Camera(sc, k, gt[k]) for k in range(n_kf)]
+    canon = [(c.express(c.T, 1000 + k), c.valid) for k, c in enumerate(cams)]
+    edges = loop_edges(n_kf, reach)
+    e0, e1 = edge_range if edge_range is not None else (0, len(edges))
+    need = sorted({k for e in range(e0, e1) for k in edges[e]})
+    dcams = {k: DeviceCamera(cams[k], device) for k in need}
+    mp = abi.default_match_params()
+    mp.projection.lambda_init = 1e-8
+    mp.projection.angle_tol = 1e-6
+    rp = abi.refine_params([(1, 3), (1, 3)])
+    n = height * width
+    empty = MatchSet(torch.empty(0, dtype=torch.int32, device=device), torch.empty(0, dtype=torch.float32, device=device),
+                     torch.empty(0, dtype=torch.uint8, device=device))
+    matches = [empty] * len(edges)
+    for c0 in range(e0, e1, chunk):
+        c1 = min(e1, c0 + chunk)
+        preds = [device_pair(dcams[edges[e][0]], dcams[edges[e][1]], MATCHED_SALT + 2 * e) for e in range(c0, c1)]
+        outs = [MatchSet.empty(n, device) for _ in range(c0, c1)]
+        ctx.match_batch([(Pointmap(p["X_a"], p["valid_a"], height, width), Pointmap(p["X_b"], p["valid_b"], height, width),
+                          FeatureMap(p["D_a"], p["Q_a"], height, width), FeatureMap(p["D_b"], p["Q_b"], height, width))
+                         for p in preds], params=mp, refine=rp, outs=outs)
+        for k, e in enumerate(range(c0, c1)):
+            matches[e] = outs[k]
+        del preds
+    torch.cuda.synchronize(device)
+    init = [gt[0]] + [perturb_pose(gt[k], seed, 5000 + 3 * k, rot_deg, trans, scale_frac) for k in range(1, n_kf)]
+    out = {"scene": sc, "gt": gt, "init": init, "canonicals": canon, "edges": edges, "matches": matches,
+           "height": height, "width": width, "matcher": "config-2 matcher (device pair predictions)"}
+    if keep_host:
+        out["matches_host"] = [{"pixel_a": m.pixel_a.cpu().numpy(), "confidence": m.confidence.cpu().numpy(),
+                                "valid": m.valid.cpu().numpy()} for m in matches]
+    return out

@@ -54,6 +54,9 @@ class ShardedResult:
     converged: bool = False
     cost_trace: List[float] = field(default_factory=list)
     poses: list = field(default_factory=list)
+    # poses after every iteration (the reverted ones for a rejected step), as
+    # pmx_global_optimize's pose_trace
+    pose_trace: list = field(default_factory=list)
 
 
 def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params: abi.pmx_backend_params,
@@ -71,7 +74,8 @@ def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params
     import torch
     import torch.distributed as dist
 
-    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    single = not (dist.is_available() and dist.is_initialized())  # one process: no collectives
+    rank, world = (0, 1) if single else (dist.get_rank(group), dist.get_world_size(group))
     n = len(poses)
     P = [abi.pmx_sim3.from_buffer_copy(T) for T in poses]
     res = ShardedResult(poses=P)
@@ -98,14 +102,16 @@ def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params
             local = terms_fn(e0, e1, P)
             full[e0:e1] = torch.as_tensor(local, dtype=torch.float64, device=dev)
         t0 = tick("accumulate", t0)
-        dist.reduce(full, dst=0, group=group)
+        if not single:
+            dist.reduce(full, dst=0, group=group)
         tick("communication", t0)
         return full
 
     def bcast(vec: np.ndarray) -> np.ndarray:
         t0 = _time.perf_counter()
         t = torch.as_tensor(vec, dtype=torch.float64, device=dev).clone()
-        dist.broadcast(t, src=0, group=group)
+        if not single:
+            dist.broadcast(t, src=0, group=group)
         out = t.cpu().numpy()
         tick("communication", t0)
         return out
@@ -138,7 +144,9 @@ def global_optimize_sharded(poses: Sequence, num_edges: int, anchor: int, params
         flag = bcast(flag)
         if flag[0] == 0.0:  # revert (backend.cpp:242-246)
             P = previous
+            res.pose_trace.append(list(P))
             break
+        res.pose_trace.append(list(P))
         cost = flag[1]
         terms = terms_new
         res.cost_trace.append(cost)

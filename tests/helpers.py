@@ -58,3 +58,42 @@ def compare_matches(gpu: MatchSet, orc, width: int):
         "worst_px": worst,
         "all_index_equal": bool((ga == oa).all()),
     }
+
+
+def numpy_solve(graph, params):
+    """Rank-0 solve from per-edge terms: adjoint sandwich (backend.cpp:114-141),
+    gauge (144-155), damping retries (208-230) with the oracle's LDL^T."""
+    import pyoracle  # test-only checker
+
+    def solve(terms, P):
+        t = np.asarray(terms)
+        n = len(P)
+        dim = 7 * n
+        Hm = np.zeros((dim, dim))
+        gv = np.zeros(dim)
+        iu = np.triu_indices(7)
+        adj = [pyoracle.sim3_adjoint(pyoracle.sim3_inverse(T)) for T in P]
+        for e, (i, j) in enumerate(graph.edges):
+            H1 = np.zeros((7, 7)); H1[iu] = t[e, :28]; H1 = H1 + np.triu(H1, 1).T
+            H2 = np.zeros((7, 7)); H2[iu] = t[e, 36:64]; H2 = H2 + np.triu(H2, 1).T
+            S = adj[i].T @ H1 @ adj[i] + adj[j].T @ H2 @ adj[j]
+            g = -adj[i].T @ t[e, 28:35] + adj[j].T @ t[e, 64:71]
+            for (a, b, sg) in ((i, i, 1), (i, j, -1), (j, i, -1), (j, j, 1)):
+                Hm[7 * a:7 * a + 7, 7 * b:7 * b + 7] += sg * S
+            gv[7 * i:7 * i + 7] += g
+            gv[7 * j:7 * j + 7] -= g
+        a = graph.anchor
+        Hm[7 * a:7 * a + 7, :] = 0
+        Hm[:, 7 * a:7 * a + 7] = 0
+        Hm[7 * a:7 * a + 7, 7 * a:7 * a + 7] = np.eye(7)
+        gv[7 * a:7 * a + 7] = 0
+        lam = 0.0
+        for _ in range(params.damping_retries + 1):
+            x, ok = pyoracle.ldlt_solve(Hm + lam * np.eye(dim), -gv)
+            if ok and np.isfinite(x).all() and np.abs(x).max() < 1e3:
+                return x, True
+            lam = params.damping_init if lam == 0.0 else lam * 10
+        return np.zeros(dim), False
+    return solve
+
+
