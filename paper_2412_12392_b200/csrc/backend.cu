@@ -50,7 +50,17 @@ struct GNState {
   int iterations;
   int trace_len;
   double trace[PMX_MAX_TRACE];
+  // Exact accept test (backend.cpp:241-246): the fp32-accumulated costs of
+  // the edge pass carry ~1e-7 relative error per term; when the trial cost
+  // lies within kCostBand of the accept threshold the decision is taken on
+  // FP64 costs of every directed residual (ray_cost64) at both poses.
+  int amb;          // this iteration's decision is ambiguous in fp32
+  int c64_valid;    // cost64 holds the FP64 cost of the current poses
+  double cost64, cost64_trial;
+  int amb_count;    // iterations decided in FP64 (reported)
 };
+
+constexpr double kCostBand = 1e-7;  // relative band of the fp32 cost around the accept threshold
 
 __device__ __forceinline__ bool gn_stopped(const GNState* st) { return st && st->stop; }
 
@@ -1201,6 +1211,17 @@ __global__ void k_gn_retract(const DSim3* __restrict__ P, DSim3* __restrict__ Pt
   if (k < N) Pt[k] = k == anchor ? P[k] : sim3_mul(sim3_exp(tau + 7 * k), P[k]);
 }
 
+// Is this iteration's accept decision within the fp32 cost's error band?
+__global__ void k_gn_check(const double* __restrict__ tbase, int64_t half, int E, GNState* st) {
+  if (st->stop) return;
+  const double c = terms_cost(tbase + (1 - st->cur) * half, E);
+  if (threadIdx.x == 0) {
+    const double thr = st->cost * (1.0 + 1e-12) + 1e-300;
+    st->amb = fabs(c - thr) <= kCostBand * fmax(fabs(c), fabs(st->cost)) ? 1 : 0;
+    if (st->amb) st->amb_count++;
+  }
+}
+
 // Accept / revert (backend.cpp:240-252) and the pose trace of the iteration.
 __global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int E, DSim3* __restrict__ P,
                             const DSim3* __restrict__ Pt, const double* __restrict__ tau, int N, double tol,
@@ -1212,7 +1233,8 @@ __global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int 
   for (int i = threadIdx.x; i < 7 * N; i += blockDim.x) t2 += tau[i] * tau[i];
   const double n2 = block_sum_fixed(t2);
   if (threadIdx.x == 0) {
-    accept = !(c > st->cost * (1.0 + 1e-12) + 1e-300);
+    accept = st->amb ? !(st->cost64_trial > st->cost64 * (1.0 + 1e-12) + 1e-300)  // FP64 costs
+                     : !(c > st->cost * (1.0 + 1e-12) + 1e-300);
     it = st->iterations - 1;
   }
   __syncthreads();
@@ -1227,7 +1249,9 @@ __global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int 
     } else {
       st->cost = c;
       st->cur = 1 - st->cur;
-      if (st->trace_len < PMX_MAX_TRACE) st->trace[st->trace_len++] = c;
+      if (st->trace_len < PMX_MAX_TRACE) st->trace[st->trace_len++] = st->amb ? st->cost64_trial : c;
+      st->c64_valid = st->amb;
+      if (st->amb) st->cost64 = st->cost64_trial;
       if (sqrt(n2) < tol) {
         st->stop = 1;
         st->converged = 1;
@@ -1412,9 +1436,71 @@ __global__ void k_rel_poses(const DSim3* __restrict__ P, const int2* __restrict_
   rel64[2 * e + 1] = make_pose<double>(b);
 }
 
+// FP64 cost of both directed constraints of every compacted match at the
+// relative poses rel64 (backend_cost, backend.cpp:175-190, through
+// block_cost, tracking.cpp:134-147, with ray_cost64): the exact side of an
+// ambiguous accept decision (GNState::amb).  which = 0: the current poses
+// (skipped when their FP64 cost is already known), 1: the trial poses.
+__device__ __forceinline__ bool cost64_needed(const GNState* st, int which) {
+  return !st->stop && st->amb && !(which == 0 && st->c64_valid);
+}
+
+__global__ void k_rel64_amb(const DSim3* __restrict__ P, const int2* __restrict__ edges, int N, int E,
+                            PoseR<double>* rel64, const GNState* st, int which) {
+  if (!cost64_needed(st, which)) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int2 ij = edges[e];
+  if (ij.x < 0 || ij.y < 0 || ij.x >= N || ij.y >= N) return;
+  rel64[2 * e] = make_pose<double>(sim3_mul(sim3_inv(P[ij.x]), P[ij.y]));      // ref = i, src = j
+  rel64[2 * e + 1] = make_pose<double>(sim3_mul(sim3_inv(P[ij.y]), P[ij.x]));  // ref = j, src = i
+}
+
+__global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<double>* __restrict__ rel64, int e0,
+                                                    double* __restrict__ part, const GNState* st, int which) {
+  if (!cost64_needed(st, which)) return;
+  const int e = e0 + blockIdx.y, b = blockIdx.x;
+  const int2 ij = A.edges[e];
+  double c = 0.0;
+  if (ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N) {
+    const float4* __restrict__ Ci = A.c4[ij.x];
+    const float4* __restrict__ Cj = A.c4[ij.y];
+    const int4* __restrict__ M = A.packed + (size_t)e * A.seg;
+    const int64_t cnt = A.pk_total[e];
+    const PoseR<double> T1 = rel64[2 * e], T2 = rel64[2 * e + 1];
+    const double s2 = A.wp.sigma2, ld = A.wp.distance_weight, delta = A.wp.huber_delta;
+    for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < cnt; k += (int64_t)A.bpe * blockDim.x) {
+      const int4 m = __ldg(M + k);
+      const float4 Pi = __ldg(Ci + m.x), Pj = __ldg(Cj + m.y);
+      const double info = 1.0 / (s2 / (double)__int_as_float(m.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
+      const double pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
+      if (Pi.w >= 1e-24f) c += ray_cost64(T1, pi, pj, info, ld, delta);  // ref = i, src = j (swapped)
+      if (Pj.w >= 1e-24f) c += ray_cost64(T2, pj, pi, info, ld, delta);  // ref = j, src = i
+    }
+  }
+  c = block_sum_fixed(c);
+  if (threadIdx.x == 0) part[(size_t)e * A.bpe + b] = c;
+}
+
+__global__ void k_cost64_sum(const double* __restrict__ part, int64_t n, GNState* st, int which) {
+  if (!cost64_needed(st, which)) return;
+  double c = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += part[i];
+  c = block_sum_fixed(c);
+  if (threadIdx.x == 0) {
+    if (which) {
+      st->cost64_trial = c;
+    } else {
+      st->cost64 = c;
+      st->c64_valid = 1;
+    }
+  }
+}
+
 // Buffers of one edge pass, allocated once per API call.
 struct EdgeWork {
   DevBuf rel, rel64, partials;
+  DevBuf rel64b, part64;  // FP64 cost pass of ambiguous accept decisions
   int bpe = 1;
   EdgeArgs A;
 };
@@ -1431,6 +1517,10 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   const bool ray = p.mode == PMX_TRACK_RAY;
   require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
   W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);
+  if (ray) {  // allocated here: cost64_pass may run inside a captured loop graph
+    W.rel64b = DevBuf(sizeof(PoseR<double>) * 2 * (size_t)E, ctx.stream);
+    W.part64 = DevBuf(sizeof(double) * (size_t)E * W.bpe, ctx.stream);
+  }
   EdgeArgs& A = W.A;
   A.st = nullptr;
   A.clouds = G.clouds.as<CloudDev>();
@@ -1453,6 +1543,23 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_edge_terms_ray, cudaFuncAttributeMaxDynamicSharedMemorySize, kEdgeSmem));
   A.inv_s2 = (float)(1.0 / A.wp.sigma2);
   A.rw = RayW{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta), (float)A.wp.distance_weight};
+}
+
+// FP64 cost of every directed residual at the device poses dP into
+// st->cost64 (which = 0) / st->cost64_trial (which = 1), enqueued always and
+// a no-op unless the iteration's decision is ambiguous (ray mode).
+static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim3* dP, GNState* S, int which) {
+  if (G.E == 0) return;
+  require(W.rel64b.p && W.part64.p, "cost64: buffers missing");
+  k_rel64_amb<<<(G.E + 127) / 128, 128, 0, ctx.stream>>>(dP, G.edges_dev.as<int2>(), G.N, G.E,
+                                                          W.rel64b.as<PoseR<double>>(), S, which);
+  for (int c0 = 0; c0 < G.E; c0 += 65535) {
+    const int cn = std::min(65535, G.E - c0);
+    k_cost64_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(W.A, W.rel64b.as<PoseR<double>>(), c0,
+                                                          W.part64.as<double>(), S, which);
+  }
+  k_cost64_sum<<<1, 1024, 0, ctx.stream>>>(W.part64.as<double>(), (int64_t)G.E * W.bpe, S, which);
+  launch_check(ctx, "k_cost64");
 }
 
 // Edge terms for edges [e0, e1) at the device poses dP -> terms (indexed by
@@ -2130,6 +2237,11 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
       k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP.as<DSim3>(), dPt.as<DSim3>(), dtau.as<double>(), n,
                                                             G.anchor, S);
       edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
+      if (p.mode == PMX_TRACK_RAY) {  // exact decision when the fp32 costs cannot resolve it
+        k_gn_check<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, S);
+        cost64_pass(ctx, G, W, dP.as<DSim3>(), S, 0);
+        cost64_pass(ctx, G, W, dPt.as<DSim3>(), S, 1);
+      }
       k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
                                               dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
       launch_check(ctx, "k_gn_iteration");
@@ -2172,6 +2284,7 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     result->iterations = hs.iterations;
     result->converged = hs.failed ? 0 : 1;  // backend.cpp:228-230 vs 244, 250, 254
+    ctx.counters["backend_fp64_decisions"] += hs.amb_count;
     result->cost_trace_len = hs.trace_len;
     for (int i = 0; i < hs.trace_len && i < PMX_MAX_TRACE; ++i) result->cost_trace[i] = hs.trace[i];
     for (int k = 0; k < n; ++k) g->poses[k] = to_pmx(P[k]);
