@@ -427,6 +427,28 @@ int pmx_graph_solve(pmx_context* ctx, pmx_prepared_graph* pg, const pmx_sim3* po
                     double* tau, double* cost, int32_t* solved);
 int pmx_graph_release(pmx_context* ctx, pmx_prepared_graph* pg);
 
+/* NCCL communicator of the context (one process per GPU).  Rank 0 creates
+ * the 128-byte unique id, the caller ships it to every rank (any side
+ * channel, e.g. torch.distributed), and every rank initialises with its
+ * rank / rank count.  NCCL is resolved at run time (libnccl.so.2, shared
+ * with a copy already loaded in the process). */
+int pmx_nccl_unique_id(pmx_context* ctx, uint8_t id[128]);
+int pmx_nccl_init(pmx_context* ctx, const uint8_t id[128], int32_t rank, int32_t nranks);
+
+/* global_optimize (backend.cpp:192-256) edge-sharded over the context's
+ * communicator, every iteration enqueued on the context stream with no host
+ * round trip: each rank's prepared edge range (pmx_graph_prepare) gives its
+ * per-edge terms, one ncclReduce(sum) of the E x 72 FP64 terms reaches rank
+ * 0, rank 0 assembles, solves (damping retries) and decides accept / revert
+ * (on FP64 costs when ambiguous), and broadcasts of the loop state and tau
+ * keep every rank's FP64 poses identical.  poses: host pmx_sim3[N], in/out
+ * (every rank).  pose_trace (nullable, rank 0): as pmx_global_optimize.
+ * timings (nullable): double[3] device ms of the call spent in
+ * accumulation / communication / rank-0 solve.  Without a communicator the
+ * loop runs on one process (rank 0, all edges prepared). */
+int pmx_graph_optimize_sharded(pmx_context* ctx, pmx_prepared_graph* pg, pmx_sim3* poses,
+                               pmx_optimize_result* result, pmx_sim3* pose_trace, double* timings);
+
 /* Dense symmetric LDL^T solve of A x = b (n x n, row-major, FP64) on the
  * device, no pivoting, fails (status field 0) on an exactly zero pivot —
  * the factorisation semantics of SimplicialLDLT (backend.cpp:216-218). */

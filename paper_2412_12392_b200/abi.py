@@ -153,7 +153,8 @@ PMX_SYMBOLS = [
     "pmx_ldlt_solve", "pmx_profile_enable", "pmx_profile_reset", "pmx_profile_get",
     "pmx_sim3_retract", "pmx_sim3_relative", "pmx_accept_loop_edges", "pmx_ingest_pair_record",
     "pmx_constrain_to_rays", "pmx_graph_prepare", "pmx_graph_edge_terms", "pmx_graph_solve",
-    "pmx_graph_release", "pmx_set_device_graphs",
+    "pmx_graph_release", "pmx_set_device_graphs", "pmx_nccl_unique_id", "pmx_nccl_init",
+    "pmx_graph_optimize_sharded",
 ]
 
 _lib = None

@@ -196,6 +196,17 @@ class Context:
     def profile_enable(self, on: bool = True):
         self._check(self.lib.pmx_profile_enable(self.h, int(on)))
 
+    def nccl_unique_id(self) -> bytes:
+        """128-byte NCCL unique id (rank 0) for nccl_init on every rank."""
+        buf = (C.c_uint8 * 128)()
+        self._check(self.lib.pmx_nccl_unique_id(self.h, buf))
+        return bytes(buf)
+
+    def nccl_init(self, uid: bytes, rank: int, nranks: int):
+        """The context's NCCL communicator (edge-sharded backend)."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        self._check(self.lib.pmx_nccl_init(self.h, buf, C.c_int32(rank), C.c_int32(nranks)))
+
     def set_device_graphs(self, on: bool = True):
         """Device loops as one CUDA graph with a conditional WHILE node (default)."""
         self._check(self.lib.pmx_set_device_graphs(self.h, int(on)))
@@ -648,6 +659,24 @@ class PreparedGraph:
         self.ctx._check(self.ctx.lib.pmx_graph_solve(self.ctx.h, self.h, self._poses(poses), ptr(terms), ptr(tau),
                                                      C.byref(cost), C.byref(solved)))
         return tau, cost.value, bool(solved.value)
+
+    def optimize_sharded(self, poses, params=None, trace: bool = False):
+        """pmx_graph_optimize_sharded: the whole GN loop of global_optimize
+        with this rank's edges, NCCL reduce / broadcast on the device.
+        Returns (OptimizeResult, poses, timings {accumulate, communication,
+        solve} in device ms)."""
+        P = self._poses(poses)
+        res = abi.pmx_optimize_result()
+        mi = (params or abi.default_backend_params()).max_iterations
+        tr = (abi.pmx_sim3 * max(1, mi * self.n))() if trace else None
+        tm = (C.c_double * 3)()
+        self.ctx._check(self.ctx.lib.pmx_graph_optimize_sharded(self.ctx.h, self.h, P, C.byref(res), tr, tm))
+        rows = res.iterations if res.converged else max(0, res.iterations - 1)
+        pt = [[abi.pmx_sim3.from_buffer_copy(tr[it * self.n + k]) for k in range(self.n)] for it in range(rows)] \
+            if trace else []
+        out = [abi.pmx_sim3.from_buffer_copy(P[k]) for k in range(self.n)]
+        return (OptimizeResult(res.iterations, bool(res.converged), list(res.cost_trace[:res.cost_trace_len]), pt),
+                out, {"accumulate": tm[0], "communication": tm[1], "solve": tm[2]})
 
     def release(self):
         if getattr(self, "h", None):

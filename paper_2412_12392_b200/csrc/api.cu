@@ -4,6 +4,7 @@
 #include <cstring>
 #include <string>
 
+#include "nccl_dl.cuh"
 #include "pmx_common.cuh"
 
 using pmx::Context;
@@ -27,6 +28,10 @@ int pmx_impl_normalize_rays(pmx_context*, pmx_memory, const pmx_pointmap*, doubl
 int pmx_impl_interpolate_ray(pmx_context*, pmx_memory, const pmx_pointmap*, int64_t, const double*, double*, double*,
                              uint8_t*);
 int pmx_impl_median_scene_distance(pmx_context*, pmx_memory, const pmx_pointmap*, double*);
+int pmx_impl_nccl_unique_id(pmx_context*, uint8_t*);
+int pmx_impl_nccl_init(pmx_context*, const uint8_t*, int32_t, int32_t);
+int pmx_impl_graph_optimize_sharded(pmx_context*, pmx_prepared_graph*, pmx_sim3*, pmx_optimize_result*, pmx_sim3*,
+                                    double*);
 int pmx_impl_iterative_project(pmx_context*, pmx_memory, const pmx_pointmap*, int64_t, const float*,
                                const double*, const pmx_iter_proj_params*, double*, uint8_t*, int32_t*);
 int pmx_impl_match_stats(pmx_context*, pmx_memory, const pmx_matchset*, int32_t, int64_t*, double*);
@@ -189,6 +194,12 @@ int pmx_destroy(pmx_context* c) {
       cudaStreamDestroy(s);
     }
   for (auto& kv : ctx->dev_counters) cudaFree(kv.second);
+  if (ctx->nccl_comm) {
+    try {
+      if (pmx::nccl_api().CommDestroy) pmx::nccl_api().CommDestroy((ncclComm_t)ctx->nccl_comm);
+    } catch (...) {
+    }
+  }
   delete ctx;
   return (int)PMX_OK;
 }
@@ -289,6 +300,19 @@ int pmx_normalize_rays(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, d
 int pmx_interpolate_ray(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, int64_t n, const double* p,
                         double* ray, double* jacobian, uint8_t* ok) {
   return guarded(c, [&] { return pmx_impl_interpolate_ray(c, mem, pm, n, p, ray, jacobian, ok); });
+}
+
+int pmx_nccl_unique_id(pmx_context* c, uint8_t id[128]) {
+  return guarded(c, [&] { return pmx_impl_nccl_unique_id(c, id); });
+}
+
+int pmx_nccl_init(pmx_context* c, const uint8_t id[128], int32_t rank, int32_t nranks) {
+  return guarded(c, [&] { return pmx_impl_nccl_init(c, id, rank, nranks); });
+}
+
+int pmx_graph_optimize_sharded(pmx_context* c, pmx_prepared_graph* pg, pmx_sim3* poses, pmx_optimize_result* result,
+                               pmx_sim3* pose_trace, double* timings) {
+  return guarded(c, [&] { return pmx_impl_graph_optimize_sharded(c, pg, poses, result, pose_trace, timings); });
 }
 
 int pmx_median_scene_distance(pmx_context* c, pmx_memory mem, const pmx_pointmap* pm, double* out) {

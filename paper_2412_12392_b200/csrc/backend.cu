@@ -30,6 +30,7 @@
 #include <map>
 #include <vector>
 
+#include "nccl_dl.cuh"
 #include "residual.cuh"
 #include "select.cuh"
 
@@ -58,6 +59,7 @@ struct GNState {
   int c64_valid;    // cost64 holds the FP64 cost of the current poses
   double cost64, cost64_trial;
   int amb_count;    // iterations decided in FP64 (reported)
+  int last_accept;  // this iteration's step was accepted (edge-sharded loop: applied on every rank)
 };
 
 constexpr double kCostBand = 1e-7;  // relative band of the fp32 cost around the accept threshold
@@ -1190,6 +1192,7 @@ __global__ void k_gn_init(const double* __restrict__ terms, int E, GNState* st) 
 
 // Start of an iteration: count it, clear the solve flag (backend.cpp:203-204).
 __global__ void k_gn_begin(GNState* st) {
+  st->last_accept = 0;
   if (st->stop) return;
   st->iterations++;
   st->solved = 0;
@@ -1222,13 +1225,15 @@ __global__ void k_gn_check(const double* __restrict__ tbase, int64_t half, int E
   }
 }
 
-// Accept / revert (backend.cpp:240-252) and the pose trace of the iteration.
-__global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int E, DSim3* __restrict__ P,
-                            const DSim3* __restrict__ Pt, const double* __restrict__ tau, int N, double tol,
-                            pmx_sim3* trace, GNState* st) {
+// Accept / revert (backend.cpp:240-252) and the pose trace of the iteration;
+// trial = the terms at the trial poses.  swap: the terms halves swap roles
+// on acceptance (single-process loop); otherwise the caller copies them.
+__device__ void gn_accept(const double* __restrict__ trial, int E, DSim3* __restrict__ P,
+                          const DSim3* __restrict__ Pt, const double* __restrict__ tau, int N, double tol,
+                          pmx_sim3* trace, GNState* st, bool swap) {
   __shared__ int accept, it;
   if (st->stop) return;  // uniform: st is only written below, after the barriers
-  const double c = terms_cost(tbase + (1 - st->cur) * half, E);
+  const double c = terms_cost(trial, E);
   double t2 = 0.0;
   for (int i = threadIdx.x; i < 7 * N; i += blockDim.x) t2 += tau[i] * tau[i];
   const double n2 = block_sum_fixed(t2);
@@ -1247,8 +1252,9 @@ __global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int 
       st->stop = 1;
       st->converged = 1;
     } else {
+      st->last_accept = 1;
       st->cost = c;
-      st->cur = 1 - st->cur;
+      if (swap) st->cur = 1 - st->cur;
       if (st->trace_len < PMX_MAX_TRACE) st->trace[st->trace_len++] = st->amb ? st->cost64_trial : c;
       st->c64_valid = st->amb;
       if (st->amb) st->cost64 = st->cost64_trial;
@@ -1258,6 +1264,40 @@ __global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int 
       }
     }
   }
+}
+
+__global__ void k_gn_accept(const double* __restrict__ tbase, int64_t half, int E, DSim3* __restrict__ P,
+                            const DSim3* __restrict__ Pt, const double* __restrict__ tau, int N, double tol,
+                            pmx_sim3* trace, GNState* st) {
+  gn_accept(tbase + (1 - st->cur) * half, E, P, Pt, tau, N, tol, trace, st, true);
+}
+
+// Fixed-half variants of the edge-sharded loop (current terms in `cur`,
+// trial terms in `trial`; k_terms_accept copies them on acceptance).
+__global__ void k_gn_accept_split(const double* __restrict__ cur, const double* __restrict__ trial, int E,
+                                  DSim3* __restrict__ P, const DSim3* __restrict__ Pt, const double* __restrict__ tau,
+                                  int N, double tol, pmx_sim3* trace, GNState* st) {
+  (void)cur;
+  gn_accept(trial, E, P, Pt, tau, N, tol, trace, st, false);
+}
+
+__global__ void k_gn_check_split(const double* __restrict__ cur, const double* __restrict__ trial, int E,
+                                 GNState* st) {
+  (void)cur;
+  if (st->stop) return;
+  const double c = terms_cost(trial, E);
+  if (threadIdx.x == 0) {
+    const double thr = st->cost * (1.0 + 1e-12) + 1e-300;
+    st->amb = fabs(c - thr) <= kCostBand * fmax(fabs(c), fabs(st->cost)) ? 1 : 0;
+    if (st->amb) st->amb_count++;
+  }
+}
+
+__global__ void k_terms_accept(const double* __restrict__ trial, double* __restrict__ cur, int64_t n,
+                               const GNState* st) {
+  if (!st->last_accept) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) cur[i] = trial[i];
 }
 
 // ------------------------------------------------------------------ host
@@ -1482,13 +1522,17 @@ __global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<doub
   if (threadIdx.x == 0) part[(size_t)e * A.bpe + b] = c;
 }
 
-__global__ void k_cost64_sum(const double* __restrict__ part, int64_t n, GNState* st, int which) {
+// out (nullable): the edge-sharded loop writes this rank's partial cost to
+// out[which] (summed over ranks by a reduce, then k_cost64_merge).
+__global__ void k_cost64_sum(const double* __restrict__ part, int64_t n, GNState* st, int which, double* out) {
   if (!cost64_needed(st, which)) return;
   double c = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += part[i];
   c = block_sum_fixed(c);
   if (threadIdx.x == 0) {
-    if (which) {
+    if (out) {
+      out[which] = c;
+    } else if (which) {
       st->cost64_trial = c;
     } else {
       st->cost64 = c;
@@ -1548,17 +1592,20 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
 // FP64 cost of every directed residual at the device poses dP into
 // st->cost64 (which = 0) / st->cost64_trial (which = 1), enqueued always and
 // a no-op unless the iteration's decision is ambiguous (ray mode).
-static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim3* dP, GNState* S, int which) {
+static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim3* dP, GNState* S, int which,
+                        int e0 = 0, int e1 = -1, double* out = nullptr) {
   if (G.E == 0) return;
+  if (e1 < 0) e1 = G.E;
   require(W.rel64b.p && W.part64.p, "cost64: buffers missing");
   k_rel64_amb<<<(G.E + 127) / 128, 128, 0, ctx.stream>>>(dP, G.edges_dev.as<int2>(), G.N, G.E,
                                                           W.rel64b.as<PoseR<double>>(), S, which);
-  for (int c0 = 0; c0 < G.E; c0 += 65535) {
-    const int cn = std::min(65535, G.E - c0);
+  for (int c0 = e0; c0 < e1; c0 += 65535) {
+    const int cn = std::min(65535, e1 - c0);
     k_cost64_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(W.A, W.rel64b.as<PoseR<double>>(), c0,
                                                           W.part64.as<double>(), S, which);
   }
-  k_cost64_sum<<<1, 1024, 0, ctx.stream>>>(W.part64.as<double>(), (int64_t)G.E * W.bpe, S, which);
+  k_cost64_sum<<<1, 1024, 0, ctx.stream>>>(W.part64.as<double>() + (size_t)e0 * W.bpe, (int64_t)(e1 - e0) * W.bpe, S,
+                                           which, out);
   launch_check(ctx, "k_cost64");
 }
 
@@ -1566,10 +1613,11 @@ static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim
 // absolute edge; with a loop state: the current / trial half of `terms`).
 static void edge_terms_dev(Context& ctx, const DevGraph& G, const pmx_backend_params& p, EdgeWork& W,
                            const DSim3* dP, int e0, int e1, double* terms, const GNState* st = nullptr,
-                           int which = 0) {
+                           int which = 0, bool fixed = false) {
   if (e1 <= e0) return;
   const bool ray = p.mode == PMX_TRACK_RAY;
-  const int64_t half = (int64_t)PMX_EDGE_TERMS * std::max(G.E, 1);
+  // fixed: `terms` is the output itself (the loop state only gates the kernels)
+  const int64_t half = fixed ? 0 : (int64_t)PMX_EDGE_TERMS * std::max(G.E, 1);
   k_rel_poses<<<(e1 - e0 + 127) / 128, 128, 0, ctx.stream>>>(dP, G.edges_dev.as<int2>(), G.N, e0, e1,
                                                                 W.rel.as<PoseR<float>>(), W.rel64.as<PoseR<double>>(),
                                                                 st);
@@ -2436,6 +2484,201 @@ extern "C" int pmx_impl_graph_release(pmx_context* c, pmx_prepared_graph* h) {
   if (h) {
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     delete reinterpret_cast<PreparedGraph*>(h);
+  }
+  return PMX_OK;
+}
+
+// ------------------------------------------------ edge-sharded device loop
+// Accept-apply of the edge-sharded loop: every rank holds the trial poses
+// (retracted from the broadcast tau), rank 0 decided (GNState broadcast).
+__global__ void k_gn_apply(DSim3* __restrict__ P, const DSim3* __restrict__ Pt, int N, const GNState* st) {
+  if (!st->last_accept) return;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) P[k] = Pt[k];
+}
+
+// The FP64 costs of an ambiguous decision, summed over ranks (in[0]: current
+// poses unless already known, in[1]: trial poses).
+__global__ void k_cost64_merge(const double* __restrict__ in, GNState* st) {
+  if (st->stop || !st->amb) return;
+  if (!st->c64_valid) {
+    st->cost64 = in[0];
+    st->c64_valid = 1;
+  }
+  st->cost64_trial = in[1];
+}
+
+extern "C" int pmx_impl_nccl_unique_id(pmx_context* c, uint8_t* id) {
+  require(c && id, "nccl_unique_id: null arguments");
+  ncclUniqueId u;
+  PMX_NCCL(nccl_api().GetUniqueId(&u));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, sizeof(u));
+  return PMX_OK;
+}
+
+extern "C" int pmx_impl_nccl_init(pmx_context* c, const uint8_t* id, int32_t rank, int32_t nranks) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(id && nranks >= 1 && rank >= 0 && rank < nranks, "nccl_init: bad arguments");
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  ncclComm_t comm = nullptr;
+  PMX_NCCL(nccl_api().CommInitRank(&comm, nranks, u, rank));
+  if (ctx.nccl_comm && nccl_api().CommDestroy) nccl_api().CommDestroy((ncclComm_t)ctx.nccl_comm);
+  ctx.nccl_comm = comm;
+  ctx.nccl_rank = rank;
+  ctx.nccl_nranks = nranks;
+  return PMX_OK;
+}
+
+// global_optimize (backend.cpp:192-256) with the per-edge accumulation
+// sharded by edge over the ranks of the context's NCCL communicator, every
+// iteration enqueued on the context stream (no host round trip):
+//   all ranks : edge terms of the rank's prepared edges at the trial poses
+//   reduce    : one ncclReduce(sum) of the E x 72 FP64 terms to rank 0
+//   rank 0    : ambiguity check, assembly + damped solve, accept / revert
+//   broadcast : GNState (+ tau after the solve); every rank retracts the
+//               replicated FP64 poses with the same kernel and applies the
+//               accepted step, so the replicas stay bit-identical.
+// Ambiguous decisions add a broadcast of the flag and a reduce of the two
+// FP64 partial costs.  Without a communicator (or one rank) the collectives
+// are skipped.  timings (nullable, host doubles): accumulate / communication
+// / solve device ms of the call (CUDA events, no per-iteration host sync).
+extern "C" int pmx_impl_graph_optimize_sharded(pmx_context* c, pmx_prepared_graph* h, pmx_sim3* poses,
+                                               pmx_optimize_result* result, pmx_sim3* pose_trace,
+                                               double* timings) {
+  Context& ctx = *reinterpret_cast<Context*>(c);
+  require(h && poses && result, "graph_optimize_sharded: null arguments");
+  PreparedGraph& pg = *reinterpret_cast<PreparedGraph*>(h);
+  std::memset(result, 0, sizeof(*result));
+  const int n = pg.G.N, E = pg.G.E;
+  if (n < 2 || E == 0) {  // backend.cpp:195-198
+    result->converged = 1;
+    return PMX_OK;
+  }
+  const bool coll = ctx.nccl_comm != nullptr;  // one rank with a communicator still runs the collectives
+  const bool root = ctx.nccl_rank == 0;
+  require(root || coll, "graph_optimize_sharded: rank > 0 without a communicator");
+  require(pg.As.sky_ok, "graph_optimize_sharded: system too large for the device solver");
+  const pmx_backend_params& p = pg.p;
+  ncclComm_t comm = (ncclComm_t)ctx.nccl_comm;
+  const int64_t half = (int64_t)PMX_EDGE_TERMS * E;
+  upload_poses(ctx, pg, poses);
+  DevBuf terms(sizeof(double) * 2 * half, ctx.stream), dPt(sizeof(DSim3) * n, ctx.stream),
+      dst(sizeof(GNState), ctx.stream), dtau(sizeof(double) * pg.As.dim, ctx.stream), c64(sizeof(double) * 2, ctx.stream);
+  DevBuf dtrace(pose_trace && root ? sizeof(pmx_sim3) * (size_t)std::max(p.max_iterations, 1) * n : 0, ctx.stream);
+  PMX_CUDA(cudaMemsetAsync(terms.p, 0, terms.bytes, ctx.stream));
+  PMX_CUDA(cudaMemsetAsync(dst.p, 0, sizeof(GNState), ctx.stream));
+  GNState* S = dst.as<GNState>();
+  DSim3* dP = pg.dP.as<DSim3>();
+  const bool ray = p.mode == PMX_TRACK_RAY;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> evs[3];  // accumulate, communication, solve
+  auto mark = [&](int phase, bool begin) {
+    if (!timings) return;
+    cudaEvent_t e;
+    PMX_CUDA(cudaEventCreate(&e));
+    PMX_CUDA(cudaEventRecord(e, ctx.stream));
+    if (begin)
+      evs[phase].push_back({e, nullptr});
+    else
+      evs[phase].back().second = e;
+  };
+  auto bcast_state = [&] {
+    if (!coll) return;
+    mark(1, true);
+    PMX_NCCL(nccl_api().Broadcast(S, S, sizeof(GNState), ncclUint8, 0, comm, ctx.stream));
+    mark(1, false);
+  };
+  // The single-process loop swaps the terms halves on acceptance (st->cur);
+  // here the host enqueues collectives on fixed buffers, so the current terms
+  // stay in half 0, the trial terms in half 1, and an accepted trial half is
+  // copied over the current one (k_terms_accept).
+  double* cur = terms.as<double>();
+  double* trial = terms.as<double>() + half;
+  // initial terms + cost at the initial poses (backend.cpp:200-201)
+  mark(0, true);
+  edge_terms_dev(ctx, pg.G, p, pg.W, dP, pg.e0, pg.e1, cur, S, 0, true);
+  mark(0, false);
+  if (coll) {
+    mark(1, true);
+    PMX_NCCL(nccl_api().Reduce(cur, cur, (size_t)half, ncclFloat64, ncclSum, 0, comm, ctx.stream));
+    mark(1, false);
+  }
+  if (root) k_gn_init<<<1, 1024, 0, ctx.stream>>>(cur, E, S);
+  bcast_state();
+  for (int iter = 0; iter < p.max_iterations; ++iter) {
+    k_gn_begin<<<1, 1, 0, ctx.stream>>>(S);
+    if (root) {
+      mark(2, true);
+      assemble_sky(ctx, pg.G, pg.As, dP, cur, 0, S);
+      solve_sky(ctx, p, pg.As, S, dtau.as<double>());
+      mark(2, false);
+    }
+    bcast_state();  // solved flag
+    if (coll) {
+      mark(1, true);
+      PMX_NCCL(nccl_api().Broadcast(dtau.p, dtau.p, (size_t)pg.As.dim, ncclFloat64, 0, comm, ctx.stream));
+      mark(1, false);
+    }
+    k_gn_retract<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP, dPt.as<DSim3>(), dtau.as<double>(), n, pg.G.anchor, S);
+    mark(0, true);
+    PMX_CUDA(cudaMemsetAsync(trial, 0, sizeof(double) * half, ctx.stream));
+    edge_terms_dev(ctx, pg.G, p, pg.W, dPt.as<DSim3>(), pg.e0, pg.e1, trial, S, 1, true);
+    mark(0, false);
+    if (coll) {
+      mark(1, true);
+      PMX_NCCL(nccl_api().Reduce(trial, trial, (size_t)half, ncclFloat64, ncclSum, 0, comm, ctx.stream));
+      mark(1, false);
+    }
+    if (ray) {  // exact decision when the fp32 costs cannot resolve it
+      if (root) k_gn_check_split<<<1, 1024, 0, ctx.stream>>>(cur, trial, E, S);
+      bcast_state();  // amb flag
+      PMX_CUDA(cudaMemsetAsync(c64.p, 0, c64.bytes, ctx.stream));
+      cost64_pass(ctx, pg.G, pg.W, dP, S, 0, pg.e0, pg.e1, c64.as<double>());
+      cost64_pass(ctx, pg.G, pg.W, dPt.as<DSim3>(), S, 1, pg.e0, pg.e1, c64.as<double>());
+      if (coll) {
+        mark(1, true);
+        PMX_NCCL(nccl_api().Reduce(c64.p, c64.p, 2, ncclFloat64, ncclSum, 0, comm, ctx.stream));
+        mark(1, false);
+      }
+      if (root) k_cost64_merge<<<1, 1, 0, ctx.stream>>>(c64.as<double>(), S);
+    }
+    if (root)
+      k_gn_accept_split<<<1, 1024, 0, ctx.stream>>>(cur, trial, E, dP, dPt.as<DSim3>(), dtau.as<double>(), n,
+                                                    p.update_tol, dtrace.as<pmx_sim3>(), S);
+    bcast_state();
+    if (!root) k_gn_apply<<<(n + 127) / 128, 128, 0, ctx.stream>>>(dP, dPt.as<DSim3>(), n, S);
+    // the accepted trial terms become the current ones (rank 0 holds the reduced sums)
+    k_terms_accept<<<(unsigned)((half + 255) / 256), 256, 0, ctx.stream>>>(trial, cur, half, S);
+    launch_check(ctx, "graph_optimize_sharded");
+  }
+  GNState hs;
+  std::vector<DSim3> P(n);
+  PMX_CUDA(cudaMemcpyAsync(&hs, S, sizeof(GNState), cudaMemcpyDeviceToHost, ctx.stream));
+  PMX_CUDA(cudaMemcpyAsync(P.data(), dP, sizeof(DSim3) * n, cudaMemcpyDeviceToHost, ctx.stream));
+  PMX_CUDA(cudaStreamSynchronize(ctx.stream));
+  if (pose_trace && root) {
+    const int rec = hs.failed ? hs.iterations - 1 : hs.iterations;
+    if (rec > 0) PMX_CUDA(cudaMemcpy(pose_trace, dtrace.p, sizeof(pmx_sim3) * (size_t)rec * n, cudaMemcpyDeviceToHost));
+  }
+  result->iterations = hs.iterations;
+  result->converged = hs.failed ? 0 : 1;
+  result->cost_trace_len = hs.trace_len;
+  for (int i = 0; i < hs.trace_len && i < PMX_MAX_TRACE; ++i) result->cost_trace[i] = hs.trace[i];
+  for (int k = 0; k < n; ++k) poses[k] = to_pmx(P[k]);
+  ctx.counters["backend_fp64_decisions"] += hs.amb_count;
+  if (timings) {
+    for (int ph = 0; ph < 3; ++ph) {
+      double t = 0.0;
+      for (auto& ab : evs[ph]) {
+        float ms = 0.0f;
+        PMX_CUDA(cudaEventElapsedTime(&ms, ab.first, ab.second));
+        t += ms;
+        cudaEventDestroy(ab.first);
+        cudaEventDestroy(ab.second);
+      }
+      timings[ph] = t;
+    }
   }
   return PMX_OK;
 }

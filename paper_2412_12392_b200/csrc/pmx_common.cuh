@@ -58,6 +58,9 @@ struct Context {
   std::vector<ProfEvent> prof;  // unresolved event pairs (pmx_profile_*)
   std::map<std::string, int64_t> counters;  // profiling counters (pmx_profile_get, total_ms = 0)
   std::map<std::string, unsigned long long*> dev_counters;  // device-side counters, read at pmx_profile_get
+  // NCCL communicator of the edge-sharded backend (pmx_nccl_init; ncclComm_t)
+  void* nccl_comm = nullptr;
+  int nccl_rank = 0, nccl_nranks = 1;
 };
 
 // Device-side profiling counter `name` (allocated on first use, zeroed).

@@ -202,3 +202,22 @@ def gpu_prepared_callbacks(ctx, graph, params, begin: int, end: int, rank: int =
         return float(np.sum(t[:, 35]) + np.sum(t[:, 71])) if t.size else 0.0
 
     return terms_fn, solve_fn, cost_fn, pg
+
+
+def device_sharded_optimize(ctx, graph, params, rank: int, world: int, trace: bool = False):
+    """The edge-sharded backend as one device-resident loop per rank
+    (pmx_graph_optimize_sharded): the context's NCCL communicator is created
+    from a unique id broadcast over torch.distributed, each rank prepares
+    its contiguous edge shard, and every GN iteration runs on the device
+    (reduce of the terms to rank 0, solve on rank 0, broadcasts of state and
+    tau) with no host round trip.  Returns (OptimizeResult, poses, timings,
+    prepared graph)."""
+    import torch.distributed as dist
+    if world > 1:
+        uid = [ctx.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.nccl_init(uid[0], rank, world)
+    e0, e1 = shard_range(len(graph.edges), rank, world)
+    pg = ctx.prepare_graph(graph, params, e0, e1)
+    res, poses, timings = pg.optimize_sharded(list(graph.poses), params, trace=trace)
+    return res, poses, timings, pg

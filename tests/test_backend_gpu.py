@@ -282,3 +282,32 @@ def test_zero_iterations_leaves_poses(ctx, graphs):
         assert len(r.cost_trace) == 1 and r.cost_trace[0] > 0
     finally:
         ctx.set_device_graphs(True)
+
+
+@pytest.mark.parametrize("with_nccl", [False, True])
+def test_device_sharded_loop_single_rank(with_nccl):
+    """pmx_graph_optimize_sharded (the device-resident edge-sharded GN loop)
+    on one rank, with and without an NCCL communicator (reduce / broadcast
+    on one rank), equals global_optimize: same iterations, cost trace and
+    bit-identical poses."""
+    from paper_2412_12392_b200 import Context
+    from paper_2412_12392_b200.distributed import device_sharded_optimize
+    c = Context(0)
+    try:
+        if with_nccl:
+            c.nccl_init(c.nccl_unique_id(), 0, 1)
+        g, G, O = _graph(n_kf=20, reach=4)
+        p = _params()
+        p.max_iterations = 10
+        ref = Graph(G.canonicals, list(G.poses), G.edges, G.matches, anchor=0)
+        rr = c.global_optimize(ref, p, trace=True)
+        rs, poses, tm, pg = device_sharded_optimize(c, G, p, 0, 1, trace=True)
+        pg.release()
+        assert rs.iterations == rr.iterations and rs.converged == rr.converged
+        np.testing.assert_array_equal(rs.cost_trace, rr.cost_trace)
+        for a, b in zip(poses, ref.poses):
+            assert list(a.R) == list(b.R) and list(a.t) == list(b.t) and a.s == b.s
+        assert len(rs.pose_trace) == len(rr.pose_trace)
+        assert tm["accumulate"] > 0 and tm["solve"] > 0 and (tm["communication"] > 0) == with_nccl
+    finally:
+        c.close()
