@@ -62,7 +62,10 @@ struct GNState {
   int last_accept;  // this iteration's step was accepted (edge-sharded loop: applied on every rank)
 };
 
-constexpr double kCostBand = 1e-7;  // relative band of the fp32 cost around the accept threshold
+// Relative band of the fp32-accumulated cost around the accept threshold:
+// measured errors of the fp32 cost against the FP64 oracle at the config-3
+// size are 7e-9 .. 9e-8 (tools/probe_costs.py), so 2e-7 keeps a margin.
+constexpr double kCostBand = 2e-7;
 
 __device__ __forceinline__ bool gn_stopped(const GNState* st) { return st && st->stop; }
 
@@ -1485,58 +1488,108 @@ __device__ __forceinline__ bool cost64_needed(const GNState* st, int which) {
   return !st->stop && st->amb && !(which == 0 && st->c64_valid);
 }
 
-__global__ void k_rel64_amb(const DSim3* __restrict__ P, const int2* __restrict__ edges, int N, int E,
-                            PoseR<double>* rel64, const GNState* st, int which) {
-  if (!cost64_needed(st, which)) return;
+// Relative poses of the current (rel64[0 .. 2E)) and trial (rel64[2E .. 4E))
+// poses, for an ambiguous decision.
+__global__ void k_rel64_amb(const DSim3* __restrict__ P, const DSim3* __restrict__ Pt, const int2* __restrict__ edges,
+                            int N, int E, PoseR<double>* rel64, const GNState* st) {
+  if (!cost64_needed(st, 1)) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int2 ij = edges[e];
   if (ij.x < 0 || ij.y < 0 || ij.x >= N || ij.y >= N) return;
-  rel64[2 * e] = make_pose<double>(sim3_mul(sim3_inv(P[ij.x]), P[ij.y]));      // ref = i, src = j
-  rel64[2 * e + 1] = make_pose<double>(sim3_mul(sim3_inv(P[ij.y]), P[ij.x]));  // ref = j, src = i
+  for (int w = 0; w < 2; ++w) {
+    const DSim3* Q = w ? Pt : P;
+    rel64[(size_t)2 * E * w + 2 * e] = make_pose<double>(sim3_mul(sim3_inv(Q[ij.x]), Q[ij.y]));      // ref = i, src = j
+    rel64[(size_t)2 * E * w + 2 * e + 1] = make_pose<double>(sim3_mul(sim3_inv(Q[ij.y]), Q[ij.x]));  // ref = j, src = i
+  }
 }
 
-__global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<double>* __restrict__ rel64, int e0,
-                                                    double* __restrict__ part, const GNState* st, int which) {
-  if (!cost64_needed(st, which)) return;
+// One read of every compacted match, the FP64 costs of both directed
+// constraints at the trial poses and (unless already known) the current ones.
+__global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<double>* __restrict__ rel64, int E, int e0,
+                                                    double* __restrict__ part, const GNState* st) {
+  if (!cost64_needed(st, 1)) return;
+  const bool cur = !st->c64_valid;
   const int e = e0 + blockIdx.y, b = blockIdx.x;
   const int2 ij = A.edges[e];
-  double c = 0.0;
+  // the edge's relative poses are block-uniform: shared memory, not registers
+  __shared__ PoseR<double> T[4];  // current dir 1, dir 2, trial dir 1, dir 2
+  constexpr int kPD = (int)(sizeof(PoseR<double>) / sizeof(double));
+  if (threadIdx.x < 4 * kPD) {
+    const int w = threadIdx.x / (2 * kPD), r = threadIdx.x % (2 * kPD);
+    reinterpret_cast<double*>(T)[threadIdx.x] =
+        reinterpret_cast<const double*>(rel64 + (size_t)2 * E * w + 2 * e)[r];
+  }
+  __syncthreads();
+  double cc = 0.0, ct = 0.0;
   if (ij.x >= 0 && ij.y >= 0 && ij.x < A.N && ij.y < A.N) {
     const float4* __restrict__ Ci = A.c4[ij.x];
     const float4* __restrict__ Cj = A.c4[ij.y];
     const int4* __restrict__ M = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
-    const PoseR<double> T1 = rel64[2 * e], T2 = rel64[2 * e + 1];
     const double s2 = A.wp.sigma2, ld = A.wp.distance_weight, delta = A.wp.huber_delta;
-    for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < cnt; k += (int64_t)A.bpe * blockDim.x) {
-      const int4 m = __ldg(M + k);
-      const float4 Pi = __ldg(Ci + m.x), Pj = __ldg(Cj + m.y);
-      const double info = 1.0 / (s2 / (double)__int_as_float(m.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
-      const double pi[3] = {Pi.x, Pi.y, Pi.z}, pj[3] = {Pj.x, Pj.y, Pj.z};
-      if (Pi.w >= 1e-24f) c += ray_cost64(T1, pi, pj, info, ld, delta);  // ref = i, src = j (swapped)
-      if (Pj.w >= 1e-24f) c += ray_cost64(T2, pj, pi, info, ld, delta);  // ref = j, src = i
+    const int64_t stride = (int64_t)A.bpe * blockDim.x;
+    int64_t k = (int64_t)b * blockDim.x + threadIdx.x;
+    // two-deep register pipeline: the record of match k + stride and the
+    // points of match k are in flight while match k - stride is evaluated
+    int4 m = k < cnt ? __ldg(M + k) : make_int4(0, 0, 0, 0);
+    float4 Pi = make_float4(0.f, 0.f, 0.f, 0.f), Pj = Pi;
+    if (k < cnt) {
+      Pi = __ldg(Ci + m.x);
+      Pj = __ldg(Cj + m.y);
+    }
+    int4 mn = k + stride < cnt ? __ldg(M + k + stride) : make_int4(0, 0, 0, 0);
+    for (; k < cnt; k += stride) {
+      const int4 mc = m;
+      const float4 Pic = Pi, Pjc = Pj;
+      m = mn;
+      if (k + stride < cnt) {
+        Pi = __ldg(Ci + m.x);
+        Pj = __ldg(Cj + m.y);
+      }
+      if (k + 2 * stride < cnt) mn = __ldg(M + k + 2 * stride);
+      const double info = 1.0 / (s2 / (double)__int_as_float(mc.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
+      const double pi[3] = {Pic.x, Pic.y, Pic.z}, pj[3] = {Pjc.x, Pjc.y, Pjc.z};
+      if (Pic.w >= 1e-24f) {  // ref = i, src = j (swapped)
+        ct += ray_cost64(T[2], pi, pj, info, ld, delta);
+        if (cur) cc += ray_cost64(T[0], pi, pj, info, ld, delta);
+      }
+      if (Pjc.w >= 1e-24f) {  // ref = j, src = i
+        ct += ray_cost64(T[3], pj, pi, info, ld, delta);
+        if (cur) cc += ray_cost64(T[1], pj, pi, info, ld, delta);
+      }
     }
   }
-  c = block_sum_fixed(c);
-  if (threadIdx.x == 0) part[(size_t)e * A.bpe + b] = c;
+  ct = block_sum_fixed(ct);
+  cc = block_sum_fixed(cc);
+  if (threadIdx.x == 0) {
+    part[2 * ((size_t)e * A.bpe + b)] = cc;
+    part[2 * ((size_t)e * A.bpe + b) + 1] = ct;
+  }
 }
 
-// out (nullable): the edge-sharded loop writes this rank's partial cost to
-// out[which] (summed over ranks by a reduce, then k_cost64_merge).
-__global__ void k_cost64_sum(const double* __restrict__ part, int64_t n, GNState* st, int which, double* out) {
-  if (!cost64_needed(st, which)) return;
-  double c = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) c += part[i];
-  c = block_sum_fixed(c);
+// out (nullable): the edge-sharded loop writes this rank's partial costs to
+// out[0] (current) / out[1] (trial), summed over ranks by a reduce, then
+// k_cost64_merge; else they land in the loop state directly.
+__global__ void k_cost64_sum(const double* __restrict__ part, int64_t n, GNState* st, double* out) {
+  if (!cost64_needed(st, 1)) return;
+  double c0 = 0.0, c1 = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    c0 += part[2 * i];
+    c1 += part[2 * i + 1];
+  }
+  c0 = block_sum_fixed(c0);
+  c1 = block_sum_fixed(c1);
   if (threadIdx.x == 0) {
     if (out) {
-      out[which] = c;
-    } else if (which) {
-      st->cost64_trial = c;
+      out[0] = c0;
+      out[1] = c1;
     } else {
-      st->cost64 = c;
-      st->c64_valid = 1;
+      if (!st->c64_valid) {
+        st->cost64 = c0;
+        st->c64_valid = 1;
+      }
+      st->cost64_trial = c1;
     }
   }
 }
@@ -1562,8 +1615,8 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
   W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);
   if (ray) {  // allocated here: cost64_pass may run inside a captured loop graph
-    W.rel64b = DevBuf(sizeof(PoseR<double>) * 2 * (size_t)E, ctx.stream);
-    W.part64 = DevBuf(sizeof(double) * (size_t)E * W.bpe, ctx.stream);
+    W.rel64b = DevBuf(sizeof(PoseR<double>) * 4 * (size_t)E, ctx.stream);
+    W.part64 = DevBuf(sizeof(double) * 2 * (size_t)E * W.bpe, ctx.stream);
   }
   EdgeArgs& A = W.A;
   A.st = nullptr;
@@ -1589,23 +1642,25 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   A.rw = RayW{(float)A.wp.huber_delta, (float)(A.wp.huber_delta * A.wp.huber_delta), (float)A.wp.distance_weight};
 }
 
-// FP64 cost of every directed residual at the device poses dP into
-// st->cost64 (which = 0) / st->cost64_trial (which = 1), enqueued always and
-// a no-op unless the iteration's decision is ambiguous (ray mode).
-static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim3* dP, GNState* S, int which,
+// FP64 costs of every directed residual at the current poses dP (unless
+// already known) and the trial poses dPt into st->cost64 / st->cost64_trial
+// (or `out` for the edge-sharded loop), enqueued always and a no-op unless
+// the iteration's decision is ambiguous (ray mode).
+static void cost64_pass(Context& ctx, const DevGraph& G, EdgeWork& W, const DSim3* dP, const DSim3* dPt, GNState* S,
                         int e0 = 0, int e1 = -1, double* out = nullptr) {
   if (G.E == 0) return;
   if (e1 < 0) e1 = G.E;
   require(W.rel64b.p && W.part64.p, "cost64: buffers missing");
-  k_rel64_amb<<<(G.E + 127) / 128, 128, 0, ctx.stream>>>(dP, G.edges_dev.as<int2>(), G.N, G.E,
-                                                          W.rel64b.as<PoseR<double>>(), S, which);
+  k_rel64_amb<<<(G.E + 127) / 128, 128, 0, ctx.stream>>>(dP, dPt, G.edges_dev.as<int2>(), G.N, G.E,
+                                                          W.rel64b.as<PoseR<double>>(), S);
+  ProfScope ps(ctx, "k_cost64");
   for (int c0 = e0; c0 < e1; c0 += 65535) {
     const int cn = std::min(65535, e1 - c0);
-    k_cost64_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(W.A, W.rel64b.as<PoseR<double>>(), c0,
-                                                          W.part64.as<double>(), S, which);
+    k_cost64_ray<<<dim3(W.bpe, cn), 256, 0, ctx.stream>>>(W.A, W.rel64b.as<PoseR<double>>(), G.E, c0,
+                                                          W.part64.as<double>(), S);
   }
-  k_cost64_sum<<<1, 1024, 0, ctx.stream>>>(W.part64.as<double>() + (size_t)e0 * W.bpe, (int64_t)(e1 - e0) * W.bpe, S,
-                                           which, out);
+  k_cost64_sum<<<1, 1024, 0, ctx.stream>>>(W.part64.as<double>() + 2 * (size_t)e0 * W.bpe,
+                                           (int64_t)(e1 - e0) * W.bpe, S, out);
   launch_check(ctx, "k_cost64");
 }
 
@@ -2287,8 +2342,7 @@ extern "C" int pmx_impl_global_optimize(pmx_context* c, pmx_memory mem, pmx_grap
       edge_terms_dev(ctx, G, p, W, dPt.as<DSim3>(), 0, G.E, terms.as<double>(), S, 1);
       if (p.mode == PMX_TRACK_RAY) {  // exact decision when the fp32 costs cannot resolve it
         k_gn_check<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, S);
-        cost64_pass(ctx, G, W, dP.as<DSim3>(), S, 0);
-        cost64_pass(ctx, G, W, dPt.as<DSim3>(), S, 1);
+        cost64_pass(ctx, G, W, dP.as<DSim3>(), dPt.as<DSim3>(), S);
       }
       k_gn_accept<<<1, 1024, 0, ctx.stream>>>(terms.as<double>(), half, G.E, dP.as<DSim3>(), dPt.as<DSim3>(),
                                               dtau.as<double>(), n, p.update_tol, dtrace.as<pmx_sim3>(), S);
@@ -2634,8 +2688,7 @@ extern "C" int pmx_impl_graph_optimize_sharded(pmx_context* c, pmx_prepared_grap
       if (root) k_gn_check_split<<<1, 1024, 0, ctx.stream>>>(cur, trial, E, S);
       bcast_state();  // amb flag
       PMX_CUDA(cudaMemsetAsync(c64.p, 0, c64.bytes, ctx.stream));
-      cost64_pass(ctx, pg.G, pg.W, dP, S, 0, pg.e0, pg.e1, c64.as<double>());
-      cost64_pass(ctx, pg.G, pg.W, dPt.as<DSim3>(), S, 1, pg.e0, pg.e1, c64.as<double>());
+      cost64_pass(ctx, pg.G, pg.W, dP, dPt.as<DSim3>(), S, pg.e0, pg.e1, c64.as<double>());
       if (coll) {
         mark(1, true);
         PMX_NCCL(nccl_api().Reduce(c64.p, c64.p, 2, ncclFloat64, ncclSum, 0, comm, ctx.stream));
