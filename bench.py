@@ -47,7 +47,7 @@ ALG_BYTES_PER_PX = 133  # X_b 12 + X_a 12 + Q_a 4 + Q_b 4 + D_
 #  k_match_refine  X_b 12 + valid_b 1 + X_a (one ray per pixel) 12 + D_b 48 + Q_a 4 + Q_b 4
 #                  + pa/valid/q out 9                                  = 90
 KERNEL_BYTES_PER_PX = {"k_select": 12, "k_prep": 61, "k_match_refine": 90}
-TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r01_dram_traffic.json")
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "r02_dram_traffic.json")  # tools/ncu_all.sh + ncu_summary_r02.py
 
 
 def _dist():
@@ -250,6 +250,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _edge_traffic(nmatch):
+    """ncu DRAM bytes (read + write) of one k_edge_terms_ray pass, from the
+    per-valid-match figure of the committed capture (profiles/r02_*), scaled
+    to this run's valid matches."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            return json.load(f)["k_edge_terms_ray"]["dram_bytes_per_unit"] * nmatch
+    except Exception:
+        return None
+
+
 def cpu_backend_baseline(ctx, g, G, p, init, cans, ms, k=20):
     """The reference's backend per GN iteration on one pinned core
     (BASELINE.md section 3): assemble_system at the current poses +
@@ -387,7 +398,7 @@ def bench_backend(ctx, dev, cpu: bool, n_kf=100, reach=4, loops=1, iters=10, con
                    "(breakdown from the same call enqueued kernel by kernel: "
                    f"{eager_loop_ms / max(1, r_e.iterations):.3f} ms per iteration)",
            "roofline": {"bound": "hbm", "kernel": "k_edge_terms", "achieved": achieved, "peak": peaks["hbm_gbs"],
-                        "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                        "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": _edge_traffic(nmatch),
                         "alg_bytes_per_match": 32, "matches_per_launch": nmatch, "peak_kind": peak_kind}}
     if cpu:
         out["cpu_baseline"] = cpu_backend_baseline(ctx, g, G, p, init, cans, ms)
