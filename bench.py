@@ -119,8 +119,11 @@ class ClockSampler:
 
 
 def edge_shard(rank, world):
-    per = (N_EDGES + world - 1) // world
-    return list(range(rank * per, min(N_EDGES, (rank + 1) * per)))
+    """This rank's contiguous block of the 64 config-2 edges (distributed.shard_range,
+    covered by tests/test_distributed.py::test_matching_shards_cover_every_edge_once)."""
+    from paper_2412_12392_b200.distributed import shard_range
+    e0, e1 = shard_range(N_EDGES, rank, world)
+    return list(range(e0, e1))
 
 
 def match_params():

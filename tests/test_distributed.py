@@ -87,3 +87,49 @@ def test_sharded_backend_equals_single_process_oracle():
         np.testing.assert_allclose(R, list(T.R), atol=1e-9)
         np.testing.assert_allclose(t, list(T.t), atol=1e-9)
         assert abs(s - T.s) < 1e-9
+
+
+def _match_worker(rank, world, port, q):
+    """One rank of the edge-sharded batched matcher (bench.py's config-2
+    path): its contiguous edge shard, matched by the CPU oracle here (the
+    checker; the GPU runs the same shard through libpmx_cuda.so), gathered
+    to rank 0 with the edge ids."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from helpers import BASELINE_REFINE, baseline_match_params
+    n_edges = 7
+    pairs = [pmxgen.config0(seed=40 + e, height=24, width=32) for e in range(n_edges)]
+    e0, e1 = shard_range(n_edges, rank, world)
+    mine = pyoracle.match_batch(pairs[e0:e1], baseline_match_params(), abi.refine_params(BASELINE_REFINE))
+    payload = [(e0 + k, m.pixel_a.tolist(), m.valid.tolist()) for k, m in enumerate(mine)]
+    out = [None] * world
+    dist.all_gather_object(out, payload)
+    if rank == 0:
+        q.put(out)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_matching_shards_cover_every_edge_once(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_match_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    got = sorted(e for shard in out for e, _, _ in shard)
+    assert got == list(range(7))  # every edge exactly once
+    from helpers import BASELINE_REFINE, baseline_match_params
+    pairs = [pmxgen.config0(seed=40 + e, height=24, width=32) for e in range(7)]
+    ref = pyoracle.match_batch(pairs, baseline_match_params(), abi.refine_params(BASELINE_REFINE))
+    for shard in out:
+        for e, pa, v in shard:  # reassembled in edge order = the single-process batch
+            assert np.array_equal(np.array(pa, np.int32), ref[e].pixel_a) and np.array_equal(np.array(v), ref[e].valid)
