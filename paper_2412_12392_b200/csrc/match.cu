@@ -35,19 +35,13 @@
 
 // Build-time variants (dev ablations; defaults are the product).
 #ifndef PMX_PRUNE
-#define PMX_PRUNE 0  // two-pass head-bound pruning of level-1 refinement candidates (measured slower: off)
+#define PMX_PRUNE 0  // head-bound pruning of level-1 refinement candidates
 #endif
 #ifndef PMX_LD256
 #define PMX_LD256 1  // one 256-bit load per ray-map support
 #endif
 #ifndef PMX_RCP
 #define PMX_RCP 1  // LM quotients as products with reciprocals
-#endif
-#ifndef PMX_SPLIT
-#define PMX_SPLIT 0  // LM and refinement as two kernels (k_match + k_refine_q8)
-#endif
-#ifndef PMX_LM_BLOCKS
-#define PMX_LM_BLOCKS 3
 #endif
 
 namespace pmx {
@@ -65,7 +59,6 @@ struct SelState {
   uint32_t krem;    // rank within the current bucket
   double threshold; // invalidation_median_fraction * median
   int a1max;        // max over a-pixels of sum q8(D_a)^2 (int8 refinement error bound)
-  int ntmax;        // max over a-pixels of ceil(sqrt(sum of squares of q8 dims 16-23)) (tail bound)
   int qbad;         // some |D_a component| * 127 >= 127.5: no int8 fast path for this pair
   // exact FP64 median: the fp32 key of the rank-k element, how many norms
   // share that key, and their FP64 values (the rank-krem one is the median)
@@ -102,10 +95,11 @@ struct PairDev {
   float4* dnorm;  // {||a||, ||a[16:24]||, ||a[8:24]||} upper bounds, .w = qa (standalone refine)
   // int8 descriptors of every a-pixel, round(127 x) (batched refine), planar
   // (a warp's 32 neighbouring candidates read contiguous bytes): q8h = dims
-  // 0-15 (the head), q8t = dims 16-23 (the tail); the pair's largest tail
-  // norm bound is SelState::ntmax
-  uint4* q8h;
-  uint2* q8t;
+  // 0-7, q8n = nt = ceil(sqrt(sum of squares of dims 8-23)) (the
+  // Cauchy-Schwarz bound of the tail), q8t = dims 8-23
+  uint2* q8h;
+  uint16_t* q8n;
+  uint4* q8t;
 };
 
 struct LMParams {
@@ -192,7 +186,7 @@ struct Q8 {
   uint4 a;  // dims 0-15
   uint2 b;  // dims 16-23
   int l2;   // sum of squares, all dims
-  int nt;   // ceil(sqrt(sum of squares of dims 16-23)) (Cauchy-Schwarz bound of the tail)
+  int nt;   // ceil(sqrt(sum of squares of dims 8-23))
   int bad;
 };
 __device__ __forceinline__ uint32_t q8_word(uint32_t w0, uint32_t w1, __half2& amax) {
@@ -219,10 +213,11 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
   q.b.y = q8_word(d2.z, d2.w, amax);
   const float2 m = __half22float2(amax);
   q.bad = !(m.x <= 1.00390625f && m.y <= 1.00390625f);  // also NaN / inf
-  int l2h = __dp4a((int)q.a.y, (int)q.a.y, __dp4a((int)q.a.x, (int)q.a.x, 0));
-  l2h = __dp4a((int)q.a.z, (int)q.a.z, l2h);
-  l2h = __dp4a((int)q.a.w, (int)q.a.w, l2h);
-  const int l2t = __dp4a((int)q.b.y, (int)q.b.y, __dp4a((int)q.b.x, (int)q.b.x, 0));
+  const int l2h = __dp4a((int)q.a.y, (int)q.a.y, __dp4a((int)q.a.x, (int)q.a.x, 0));
+  int l2t = __dp4a((int)q.a.z, (int)q.a.z, 0);
+  l2t = __dp4a((int)q.a.w, (int)q.a.w, l2t);
+  l2t = __dp4a((int)q.b.x, (int)q.b.x, l2t);
+  l2t = __dp4a((int)q.b.y, (int)q.b.y, l2t);
   q.l2 = l2h + l2t;
   int nt = (int)ceilf(sqrtf((float)l2t));  // exact integer ceil(sqrt): l2t < 2^24
   if (nt * nt < l2t) ++nt;
@@ -273,7 +268,7 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     for (int i = threadIdx.x; i < kHist1; i += blockDim.x) sh[i] = 0;
     __syncthreads();
   }
-  int a1max = 0, qbad = 0, ntmax = 0;
+  int a1max = 0, qbad = 0;
   for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
     const double x = P.xa[3 * i], y = P.xa[3 * i + 1], z = P.xa[3 * i + 2];
     const bool v = P.va ? P.va[i] != 0 : true;
@@ -291,10 +286,10 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
     if (P.q8h) {
       const uint4* row = reinterpret_cast<const uint4*>(P.da) + 3 * (size_t)i;
       const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
-      P.q8h[i] = q.a;
-      P.q8t[i] = q.b;
+      P.q8h[i] = make_uint2(q.a.x, q.a.y);
+      if (PMX_PRUNE) P.q8n[i] = (uint16_t)q.nt;  // the tail bound only feeds the pruned form
+      P.q8t[i] = make_uint4(q.a.z, q.a.w, q.b.x, q.b.y);
       a1max = max(a1max, q.l2);
-      ntmax = max(ntmax, q.nt);
       qbad |= q.bad;
     }
   }
@@ -302,12 +297,10 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       a1max = max(a1max, __shfl_xor_sync(0xffffffffu, a1max, o));
-      ntmax = max(ntmax, __shfl_xor_sync(0xffffffffu, ntmax, o));
       qbad |= __shfl_xor_sync(0xffffffffu, qbad, o);
     }
     if ((threadIdx.x & 31) == 0) {
       if (a1max) atomicMax(&P.sel->a1max, a1max);
-      if (ntmax) atomicMax(&P.sel->ntmax, ntmax);
       if (qbad) atomicOr(&P.sel->qbad, qbad);
     }
   }
@@ -1130,7 +1123,7 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
 }
 
 // One thread per b-pixel, 32x8 pixel tiles, blockIdx.y = pair (no refinement).
-__global__ void __launch_bounds__(256, PMX_LM_BLOCKS) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
+__global__ void __launch_bounds__(256, 3) k_match(const PairDev* __restrict__ pairs, LMParams lp) {
   const PairDev& P = pairs[blockIdx.z];
   const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
   if (u >= P.Wb || v >= P.Hb) return;
@@ -1159,20 +1152,19 @@ __global__ void __launch_bounds__(256, PMX_LM_BLOCKS) k_match(const PairDev* __r
 // previous window (those were all strictly below the moved-to centre); a level
 // whose window is unchanged is skipped (camera.cpp semantics, strict '>').
 struct QB {  // register-resident int8 target descriptor
-  uint32_t w[6];  // dims 0-3, 4-7, 8-11, 12-15 (head), 16-19, 20-23 (tail)
+  uint32_t w[6];  // dims 0-3, 4-7 (head), 8-11, 12-15, 16-19, 20-23 (tail)
   int nt;         // ceil(sqrt(sum of squares of the tail))
 };
 
-// Head (dims 0-15) and tail (dims 16-23) partial scores of one candidate.
-__device__ __forceinline__ int qdot_head(const uint4 h, const QB& B) {
-  int s = __dp4a((int)h.x, (int)B.w[0], 0);
-  s = __dp4a((int)h.y, (int)B.w[1], s);
-  s = __dp4a((int)h.z, (int)B.w[2], s);
-  return __dp4a((int)h.w, (int)B.w[3], s);
+// Head (dims 0-7) and tail (dims 8-23) partial scores of one candidate.
+__device__ __forceinline__ int qdot_head(const uint2 h, const QB& B) {
+  return __dp4a((int)h.y, (int)B.w[1], __dp4a((int)h.x, (int)B.w[0], 0));
 }
-__device__ __forceinline__ int qdot_tail(const uint2 t, const QB& B, int s) {
-  s = __dp4a((int)t.x, (int)B.w[4], s);
-  return __dp4a((int)t.y, (int)B.w[5], s);
+__device__ __forceinline__ int qdot_tail(const uint4 t, const QB& B, int s) {
+  s = __dp4a((int)t.x, (int)B.w[2], s);
+  s = __dp4a((int)t.y, (int)B.w[3], s);
+  s = __dp4a((int)t.z, (int)B.w[4], s);
+  return __dp4a((int)t.w, (int)B.w[5], s);
 }
 
 // Best and second-best candidate of a scan as packed keys score * 256 + rank
@@ -1193,61 +1185,45 @@ __device__ __forceinline__ void top2_add(Top2& T, int key) {
 // The int8 a-image read in place from the (L2-resident) chunk scratch
 // through the L1 cache: no staging, no block barriers.
 struct QGlob {
-  const uint4* __restrict__ h;  // dims 0-15 (see PairDev::q8h)
-  const uint2* __restrict__ t;  // dims 16-23
-  int bw;                       // row pitch (= W)
+  const uint2* __restrict__ h;     // dims 0-7 (see PairDev::q8h)
+  const uint16_t* __restrict__ n;  // tail bound
+  const uint4* __restrict__ t;     // dims 8-23
+  int bw;                          // row pitch (= W)
   __device__ __forceinline__ int at(int u, int v) const { return v * bw + u; }
-  __device__ __forceinline__ uint4 head(int i) const { return __ldg(h + i); }
-  __device__ __forceinline__ uint2 tail(int i) const { return __ldg(t + i); }
+  __device__ __forceinline__ uint2 head(int i) const { return __ldg(h + i); }
+  __device__ __forceinline__ int nt(int i) const { return (int)__ldg(n + i); }
+  __device__ __forceinline__ uint4 tail(int i) const { return __ldg(t + i); }
   __device__ __forceinline__ int score(int i, const QB& B) const { return qdot_tail(tail(i), B, qdot_head(head(i), B)); }
 };
 
 // First level, compile-time radius / stride, window inside the image,
-// unrolled (immediate load offsets).
-//
-// PMX_PRUNE = 0: every candidate gets its full score (6 DP4A, 24 bytes).
-// PMX_PRUNE = 1 (two passes): the centre is scored first; pass 1 gives every
-// other candidate its 16-dim head score plus the Cauchy-Schwarz bound of its
-// 8-dim tail, |tail . b_tail| <= ntmax nt_b (ntmax: the pair's largest tail
-// norm bound), and marks it in a bit mask only if even that upper bound
-// exceeds centre - tgap - 1 (else it can neither be the argmax nor come
-// within the uniqueness gap of the final best, which is >= the centre);
-// pass 2 scores the lane's marked candidates in full.  Pass 1 is branch
-// free (16 bytes, 4 DP4A per candidate), so the warp never pays for another
-// lane's survivors position by position.
+// unrolled (immediate load offsets).  The centre is scored first; every other
+// candidate costs its 8-dim head score plus the Cauchy-Schwarz bound of its
+// tail, |tail . b_tail| <= nt_a nt_b, and is skipped when even that upper
+// bound stays at or below best - tgap - 1: it can then neither become the
+// argmax nor come within the uniqueness gap of the final best (which is >=
+// the running best), so skipping it leaves the decision exact.  Survivors
+// (the true peak, near ties) get the full score (4 more DP4A).
 template <int R, int S, class Tile>
-__device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int cv, int tgap, int kbound) {
+__device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int cv, int tgap) {
   constexpr int D = 2 * R + 1, C = R * D + R;
   const int base = T.at(cu - R * S, cv - R * S);
-#if PMX_PRUNE
   Top2 t{qkey(T.score(base + R * S * T.bw + R * S, B), C), INT_MIN};
-  const int thr = t.score1() - tgap - 1 - kbound;  // head score above thr -> may matter
-  unsigned long long mask = 0ull;
+  int thr = t.score1() - tgap - 1;
 #pragma unroll
   for (int dv = 0; dv < D; ++dv) {
 #pragma unroll
     for (int du = 0; du < D; ++du) {
       if (dv * D + du == C) continue;
-      const int s16 = qdot_head(T.head(base + dv * S * T.bw + du * S), B);
-      mask |= (unsigned long long)(s16 > thr) << (dv * D + du);
+      const int i = base + dv * S * T.bw + du * S;
+      const int s8 = qdot_head(T.head(i), B);
+      if (!PMX_PRUNE || s8 + T.nt(i) * B.nt > thr) {
+        top2_add(t, qkey(qdot_tail(T.tail(i), B, s8), dv * D + du));
+        thr = t.score1() - tgap - 1;
+      }
     }
   }
-  while (mask) {
-    const int k = __ffsll((long long)mask) - 1;
-    mask &= mask - 1;
-    top2_add(t, qkey(T.score(base + (k / D) * S * T.bw + (k % D) * S, B), k));
-  }
   return t;
-#else
-  (void)kbound;
-  Top2 t{INT_MIN, INT_MIN};
-#pragma unroll
-  for (int dv = 0; dv < D; ++dv) {
-#pragma unroll
-    for (int du = 0; du < D; ++du) top2_add(t, qkey(T.score(base + dv * S * T.bw + du * S, B), dv * D + du));
-  }
-  return t;
-#endif
 }
 
 // One level at run-time radius / stride for one lane (border windows and
@@ -1304,7 +1280,7 @@ __device__ __forceinline__ void q_advance(QState& q, const Top2& t, int tgap, in
 // need (their centre moved: BASELINE's second level) is evaluated by the whole
 // warp, one such pixel at a time, lanes spread over its window.
 template <class Tile>
-__device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tgap, int kbound, int Wa, int Ha,
+__device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tgap, int Wa, int Ha,
                                               const RefineLevels& L, QState& q) {
   const int lane = threadIdx.x & 31;
   for (int l = 0; l < L.n; ++l) {
@@ -1319,9 +1295,9 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
                               q.cv + r * s < Ha;
         if (interior && s == 1 && r == 3) {
-          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap, kbound);
+          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
         } else if (interior && s == 2 && r == 2) {
-          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap, kbound);
+          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap);
         } else {
           if (q.best == INT_MIN) q.best = T.score(T.at(q.cu, q.cv), B);
           t = q_level_lane(T, B, q.cu, q.cv, s, r, Wa, Ha, q.best, q.pcu, q.pcv, q.ps, q.pr);
@@ -1369,46 +1345,6 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
   return refine_dispatch(P, pa, n, L);
 }
 
-// The refinement half of one b-pixel (n = its index when its match is
-// valid else -1, pa / (pcu, pcv): the LM's pixel).  Warp-collective.
-__device__ __forceinline__ void refine_tail(const PairDev& P, const RefineLevels& L, int n, int pa, int pcu, int pcv,
-                                            unsigned long long* __restrict__ exact_px) {
-  const bool fast_pair = P.q8h != nullptr && P.sel->qbad == 0;
-  QB B;
-  int tgap = 0, kbound = 0;
-  bool fast = n >= 0 && fast_pair;
-  if (fast) {
-    const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
-    const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
-    B.w[0] = q.a.x;
-    B.w[1] = q.a.y;
-    B.w[2] = q.a.z;
-    B.w[3] = q.a.w;
-    B.w[4] = q.b.x;
-    B.w[5] = q.b.y;
-    B.nt = q.nt;
-    kbound = P.sel->ntmax * q.nt;  // tail bound of every candidate of this pixel
-    tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
-    fast = !q.bad;
-  }
-  QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
-  if (__any_sync(0xffffffffu, fast)) {
-    const QGlob T{P.q8h, P.q8t, P.Wa};
-    q_refine_warp(T, B, tgap, kbound, P.Wa, P.Ha, L, q);
-  }
-  if (exact_px) {
-    const unsigned c = __popc(__ballot_sync(0xffffffffu, q.st == 1));
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(exact_px, (unsigned long long)c);
-  }
-  if (q.st != 2) {
-    const int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
-    if (out != pa) {
-      P.out_pa[n] = out;
-      P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
-    }
-  }
-}
-
 // K3 + K4 fused: one thread per b-pixel of a 32x8 tile (blockIdx.x = tile,
 // blockIdx.y = pair) runs the LM, then (warp-collectively) the refinement of
 // the valid matches; the int8 a-image (L2-resident chunk scratch) is read
@@ -1431,26 +1367,39 @@ __global__ void __launch_bounds__(256, PMX_MR_BLOCKS) k_match_refine(const PairD
     pcv = r.w;
     if (r.y) n = m;
   }
-  refine_tail(P, L, n, pa, pcu, pcv, exact_px);
-}
-
-// K4 alone (the split form, PMX_SPLIT): the refinement of the matches k_match
-// wrote, one thread per b-pixel, at its own (lower) register budget.
-#ifndef PMX_REF_BLOCKS
-#define PMX_REF_BLOCKS 6
-#endif
-__global__ void __launch_bounds__(256, PMX_REF_BLOCKS) k_refine_q8(const PairDev* __restrict__ pairs, RefineLevels L,
-                                                                   unsigned long long* __restrict__ exact_px) {
-  const PairDev& P = pairs[blockIdx.z];
-  if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * 8 >= P.Hb) return;
-  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
-  const int m = v * P.Wb + u;
-  int n = -1, pa = 0;
-  if (u < P.Wb && v < P.Hb && P.out_valid[m]) {
-    n = m;
-    pa = P.out_pa[m];
+  const bool fast_pair = P.q8h != nullptr && P.sel->qbad == 0;
+  QB B;
+  int tgap = 0;
+  bool fast = n >= 0 && fast_pair;
+  if (fast) {
+    const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
+    const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
+    B.w[0] = q.a.x;
+    B.w[1] = q.a.y;
+    B.w[2] = q.a.z;
+    B.w[3] = q.a.w;
+    B.w[4] = q.b.x;
+    B.w[5] = q.b.y;
+    B.nt = q.nt;
+    tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
+    fast = !q.bad;
   }
-  refine_tail(P, L, n, pa, pa % P.Wa, pa / P.Wa, exact_px);
+  QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
+  if (__any_sync(0xffffffffu, fast)) {
+    const QGlob T{P.q8h, P.q8n, P.q8t, P.Wa};
+    q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
+  }
+  if (exact_px) {
+    const unsigned c = __popc(__ballot_sync(0xffffffffu, q.st == 1));
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(exact_px, (unsigned long long)c);
+  }
+  if (q.st != 2) {
+    const int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
+    if (out != pa) {
+      P.out_pa[n] = out;
+      P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
+    }
+  }
 }
 
 // Standalone feature_refine over an arbitrary MatchSet (camera.cpp:239-271).
@@ -1669,7 +1618,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   }
   // chunks of pairs sharing one scratch allocation: FP64 ray maps + int8
   // descriptors (56 B per a-pixel), see kChunkBytes
-  const size_t per_px = sizeof(double4) + sizeof(uint4) + sizeof(uint2);
+  const size_t per_px = sizeof(double4) + sizeof(uint2) + sizeof(uint16_t) + sizeof(uint4);
   const size_t pair_bytes = per_px * (size_t)max_hwa;
   int chunk = std::max(1, std::min(npairs, (int)((size_t(kChunkBytes)) / std::max<size_t>(pair_bytes, 1))));
   if (hooks) chunk = std::max(1, std::min(chunk, hooks->chunk_pairs));
@@ -1682,8 +1631,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
   char* base = scratch.as<char>();
   const size_t nslot = (size_t)max_hwa * chunk;
   double4* rays = reinterpret_cast<double4*>(base);
-  uint4* q8h = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
-  uint2* q8t = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint4* q8t = reinterpret_cast<uint4*>(base + sizeof(double4) * nslot);
+  uint2* q8h = reinterpret_cast<uint2*>(base + (sizeof(double4) + sizeof(uint4)) * nslot);
+  uint16_t* q8n = reinterpret_cast<uint16_t*>(base + (sizeof(double4) + sizeof(uint4) + sizeof(uint2)) * nslot);
   for (int i = 0; i < npairs; ++i) {
     const int slot = i % chunk;
     hp[i].rays = rays + (size_t)slot * max_hwa;
@@ -1694,6 +1644,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     const bool aligned = ((uintptr_t)hp[i].da % 16 == 0) && ((uintptr_t)hp[i].db % 16 == 0);
     if (refine && hp[i].dim == 24 && aligned) {
       hp[i].q8h = q8h + (size_t)slot * max_hwa;
+      hp[i].q8n = q8n + (size_t)slot * max_hwa;
       hp[i].q8t = q8t + (size_t)slot * max_hwa;
     }
   }
@@ -1718,14 +1669,7 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
       max_tx = std::max(max_tx, (hp[i].Wb + 31) / 32);
       max_ty = std::max(max_ty, (hp[i].Hb + 7) / 8);
     }
-    if (refine && L.n > 0 && PMX_SPLIT) {  // LM and refinement as two kernels
-      ProfScope ps(ctx, "k_match_refine");
-      unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
-      k_match<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp);
-      launch_check(ctx, "k_match");
-      k_refine_q8<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, L, exact_px);
-      launch_check(ctx, "k_refine_q8");
-    } else if (refine && L.n > 0) {
+    if (refine && L.n > 0) {
       ProfScope ps(ctx, "k_match_refine");
       unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
       k_match_refine<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp, L, exact_px);
