@@ -263,6 +263,9 @@ int pmx_profile_reset(pmx_context* c) {
   });
 }
 
+unsigned long long pmx_checked_violations_match();
+unsigned long long pmx_checked_violations_backend();
+
 int pmx_profile_get(pmx_context* c, const char* kernel, double* total_ms, int64_t* launches) {
   return guarded(c, [&] {
     pmx::require(kernel && total_ms && launches, "profile_get: null arguments");
@@ -279,6 +282,10 @@ int pmx_profile_get(pmx_context* c, const char* kernel, double* total_ms, int64_
     }
     auto it = ctx.counters.find(kernel);
     if (it != ctx.counters.end()) n = it->second;  // counters report through `launches`
+    if (std::strcmp(kernel, "checked_violations") == 0) {  // range violations of a -DPMX_CHECKED build
+      PMX_CUDA(cudaDeviceSynchronize());
+      n = (int64_t)(pmx_checked_violations_match() + pmx_checked_violations_backend());
+    }
     auto dc = ctx.dev_counters.find(kernel);
     if (dc != ctx.dev_counters.end()) {
       unsigned long long v = 0;

@@ -351,6 +351,16 @@ __global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
     const float4* __restrict__ Cj = A.c4[ij.y];
     const int4* __restrict__ P = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
+#ifdef PMX_CHECKED
+    const int hwi = A.clouds[ij.x].H * A.clouds[ij.x].W, hwj = A.clouds[ij.y].H * A.clouds[ij.y].W;
+    for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < cnt; k += (int64_t)A.bpe * blockDim.x) {
+      int x = P[k].x, y = P[k].y;  // every compacted record indexes inside both clouds
+      PMX_CHECK_INDEX(x, hwi);
+      PMX_CHECK_INDEX(y, hwj);
+    }
+    int segc = (int)cnt;
+    PMX_CHECK_INDEX(segc, A.seg + 1);
+#endif
     const PoseR<double> T1 = A.rel64[2 * e], T2 = A.rel64[2 * e + 1];
     const float inv_s2 = A.inv_s2;
     const RayW c = A.rw;
@@ -2760,3 +2770,5 @@ extern "C" int pmx_impl_ldlt_solve(pmx_context* c, pmx_memory mem, int32_t n, co
   *ok = h;
   return PMX_OK;
 }
+
+PMX_DEFINE_VIOLATION_READER(pmx_checked_violations_backend)

@@ -548,7 +548,9 @@ __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, in
   u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
   v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
   const int du = min(u0 + 1, W - 1) - u0, dv = (min(v0 + 1, H - 1) - v0) * W;
-  const double4* p = rays + (v0 * W + u0);
+  int base = v0 * W + u0;
+  PMX_CHECK_INDEX(base, W * H - dv - du);  // all four supports inside the map
+  const double4* p = rays + base;
   I.fu = u - u0;
   I.fv = v - v0;
   I.c00 = ld_ray(p, 0);
@@ -1108,6 +1110,7 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
     cu = min(max((int)round(pr.pu), 0), P.Wa - 1);  // std::lround: half away from zero
     cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
     int pa = cv * P.Wa + cu;
+    PMX_CHECK_INDEX(pa, P.Wa * P.Ha);
     bool valid = pr.converged && (P.va ? P.va[pa] != 0 : true);
     if (valid) {
       const double a0 = P.xa[3 * pa], a1 = P.xa[3 * pa + 1], a2 = P.xa[3 * pa + 2];
@@ -1192,10 +1195,20 @@ struct QGlob {
   const uint16_t* __restrict__ n;  // tail bound
   const uint4* __restrict__ t;     // dims 8-23
   int bw;                          // row pitch (= W)
+  int hw;                          // pixels of the a-image (checked builds)
   __device__ __forceinline__ int at(int u, int v) const { return v * bw + u; }
-  __device__ __forceinline__ uint2 head(int i) const { return __ldg(h + i); }
-  __device__ __forceinline__ int nt(int i) const { return (int)__ldg(n + i); }
-  __device__ __forceinline__ uint4 tail(int i) const { return __ldg(t + i); }
+  __device__ __forceinline__ uint2 head(int i) const {
+    PMX_CHECK_INDEX(i, hw);
+    return __ldg(h + i);
+  }
+  __device__ __forceinline__ int nt(int i) const {
+    PMX_CHECK_INDEX(i, hw);
+    return (int)__ldg(n + i);
+  }
+  __device__ __forceinline__ uint4 tail(int i) const {
+    PMX_CHECK_INDEX(i, hw);
+    return __ldg(t + i);
+  }
   __device__ __forceinline__ int score(int i, const QB& B) const { return qdot_tail(tail(i), B, qdot_head(head(i), B)); }
 };
 
@@ -1389,7 +1402,7 @@ __global__ void __launch_bounds__(256, PMX_MR_BLOCKS) k_match_refine(const PairD
   }
   QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
   if (__any_sync(0xffffffffu, fast)) {
-    const QGlob T{P.q8h, P.q8n, P.q8t, P.Wa};
+    const QGlob T{P.q8h, P.q8n, P.q8t, P.Wa, P.Wa * P.Ha};
     q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
   }
   if (exact_px) {
@@ -1397,7 +1410,8 @@ __global__ void __launch_bounds__(256, PMX_MR_BLOCKS) k_match_refine(const PairD
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(exact_px, (unsigned long long)c);
   }
   if (q.st != 2) {
-    const int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
+    int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
+    PMX_CHECK_INDEX(out, P.Wa * P.Ha);
     if (out != pa) {
       P.out_pa[n] = out;
       P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
@@ -2146,3 +2160,5 @@ extern "C" int pmx_impl_iterative_project(pmx_context* c, pmx_memory mem, const 
   if (mem == PMX_MEM_HOST) PMX_CUDA(cudaStreamSynchronize(ctx.stream));
   return PMX_OK;
 }
+
+PMX_DEFINE_VIOLATION_READER(pmx_checked_violations_match)

@@ -360,6 +360,35 @@ __host__ __device__ inline void ldlt_pivoted_solve(int n, const double* A_in, co
 // the same bin (keys of one image cluster in a few bins: plain atomics would
 // serialise on them).  Call from every lane of the converged warp; `take` =
 // this lane has a key.
+// Checked builds (-DPMX_CHECKED, tools/gpu_checked.sh): every gather index
+// of the hot kernels is range-checked on the device; a violation is counted
+// (per translation unit, read by pmx_checked_violations) and the access is
+// redirected to element 0, so a bad index shows up as a non-zero count
+// instead of a fault.  Substitutes for compute-sanitizer, which this pool
+// does not offer.  Release builds compile the checks away.
+#ifdef PMX_CHECKED
+static __device__ unsigned long long g_pmx_violations;
+#define PMX_CHECK_INDEX(i, n)                                                        \
+  do {                                                                              \
+    if ((unsigned long long)(long long)(i) >= (unsigned long long)(long long)(n)) { \
+      atomicAdd(&g_pmx_violations, 1ull);                                           \
+      (i) = 0;                                                                      \
+    }                                                                               \
+  } while (0)
+#define PMX_DEFINE_VIOLATION_READER(fn)                                                 \
+  extern "C" unsigned long long fn() {                                                  \
+    unsigned long long v = 0;                                                           \
+    cudaMemcpyFromSymbol(&v, g_pmx_violations, sizeof(v));                              \
+    return v;                                                                           \
+  }
+#else
+#define PMX_CHECK_INDEX(i, n) \
+  do {                        \
+  } while (0)
+#define PMX_DEFINE_VIOLATION_READER(fn) \
+  extern "C" unsigned long long fn() { return 0; }
+#endif
+
 // FP64 reciprocal from the MUFU seed + two Newton steps (within 1 ulp of the
 // correctly rounded 1/d; zero, non-finite and extreme inputs take the IEEE
 // division).
