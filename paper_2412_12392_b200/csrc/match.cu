@@ -1367,13 +1367,16 @@ __device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, c
 // through L1, where a tile's windows overlap.  Fusing lets the FP64-bound LM
 // of some warps overlap the integer-bound refinement of others on every SM.
 #ifndef PMX_MR_BLOCKS
-#define PMX_MR_BLOCKS 4  // resident CTAs per SM (64 registers)
+#define PMX_MR_BLOCKS 4  // resident CTAs per SM (64 registers at 256 threads)
 #endif
-__global__ void __launch_bounds__(256, PMX_MR_BLOCKS) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
+#ifndef PMX_MR_TY
+#define PMX_MR_TY 8  // tile rows: 32 x PMX_MR_TY b-pixels per CTA
+#endif
+__global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(const PairDev* __restrict__ pairs, LMParams lp,
                                                          RefineLevels L, unsigned long long* __restrict__ exact_px) {
   const PairDev& P = pairs[blockIdx.z];
-  if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * 8 >= P.Hb) return;
-  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * 8 + (threadIdx.x >> 5);
+  if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * PMX_MR_TY >= P.Hb) return;
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * PMX_MR_TY + (threadIdx.x >> 5);
   const int m = v * P.Wb + u;
   int n = -1, pa = 0, pcu = 0, pcv = 0;
   if (u < P.Wb && v < P.Hb) {
@@ -1727,7 +1730,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     if (refine && L.n > 0) {
       ProfScope ps(ctx, "k_match_refine");
       unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
-      k_match_refine<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp, L, exact_px);
+      int ty = 0;
+      for (int i = c0; i < c0 + cn; ++i) ty = std::max(ty, (hp[i].Hb + PMX_MR_TY - 1) / PMX_MR_TY);
+      k_match_refine<<<dim3(max_tx, ty, cn), 32 * PMX_MR_TY, 0, ctx.stream>>>(dp, lp, L, exact_px);
       launch_check(ctx, "k_match_refine");
     } else {
       ProfScope ps(ctx, "k_match");
