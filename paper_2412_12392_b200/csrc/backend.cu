@@ -1494,6 +1494,10 @@ __global__ void k_rel_poses(const DSim3* __restrict__ P, const int2* __restrict_
 // block_cost, tracking.cpp:134-147, with ray_cost64): the exact side of an
 // ambiguous accept decision (GNState::amb).  which = 0: the current poses
 // (skipped when their FP64 cost is already known), 1: the trial poses.
+#ifndef PMX_COST64
+#define PMX_COST64 ray_cost64_direct  // ray_cost64: the cancellation-free form (~2x the FP64 work)
+#endif
+
 __device__ __forceinline__ bool cost64_needed(const GNState* st, int which) {
   return !st->stop && st->amb && !(which == 0 && st->c64_valid);
 }
@@ -1561,12 +1565,12 @@ __global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<doub
       const double info = 1.0 / (s2 / (double)__int_as_float(mc.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
       const double pi[3] = {Pic.x, Pic.y, Pic.z}, pj[3] = {Pjc.x, Pjc.y, Pjc.z};
       if (Pic.w >= 1e-24f) {  // ref = i, src = j (swapped)
-        ct += ray_cost64(T[2], pi, pj, info, ld, delta);
-        if (cur) cc += ray_cost64(T[0], pi, pj, info, ld, delta);
+        ct += PMX_COST64(T[2], pi, pj, info, ld, delta);
+        if (cur) cc += PMX_COST64(T[0], pi, pj, info, ld, delta);
       }
       if (Pjc.w >= 1e-24f) {  // ref = j, src = i
-        ct += ray_cost64(T[3], pj, pi, info, ld, delta);
-        if (cur) cc += ray_cost64(T[1], pj, pi, info, ld, delta);
+        ct += PMX_COST64(T[3], pj, pi, info, ld, delta);
+        if (cur) cc += PMX_COST64(T[1], pj, pi, info, ld, delta);
       }
     }
   }
