@@ -1520,7 +1520,10 @@ __global__ void k_rel64_amb(const DSim3* __restrict__ P, const DSim3* __restrict
 
 // One read of every compacted match, the FP64 costs of both directed
 // constraints at the trial poses and (unless already known) the current ones.
-__global__ void __launch_bounds__(256) k_cost64_ray(EdgeArgs A, const PoseR<double>* __restrict__ rel64, int E, int e0,
+#ifndef PMX_C64_BLOCKS
+#define PMX_C64_BLOCKS 4  // 64 registers: 4 CTAs per SM (3 and 5 measured 6-12% slower)
+#endif
+__global__ void __launch_bounds__(256, PMX_C64_BLOCKS) k_cost64_ray(EdgeArgs A, const PoseR<double>* __restrict__ rel64, int E, int e0,
                                                     double* __restrict__ part, const GNState* st) {
   if (!cost64_needed(st, 1)) return;
   const bool cur = !st->c64_valid;
