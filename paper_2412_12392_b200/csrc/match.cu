@@ -43,6 +43,9 @@
 #ifndef PMX_RCP
 #define PMX_RCP 1  // LM quotients as products with reciprocals
 #endif
+#ifndef PMX_LM_F32
+#define PMX_LM_F32 1  // LM step direction (Jacobian, normal equations, 2x2 solve) in fp32
+#endif
 #ifndef PMX_OVERLAP
 #define PMX_OVERLAP 0  // pairs per chunk of the overlapped device path (0: one chunk; 8 / 16 / 32 measured 7-17% slower)
 #endif
@@ -603,6 +606,53 @@ __device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int
   return true;
 }
 
+// PMX_LM_F32: the LM's step direction in fp32.  Only the decisions need
+// FP64 - the ray, r = ray - t (a difference of nearly equal unit vectors),
+// the cost |r|^2 and the convergence dot are kept FP64; the Jacobian, J^T J,
+// J^T r and the 2x2 damped solve only steer the step, and a ~1e-7 relative
+// change of a step moves the next iterate by ~1e-7 of the step (the same
+// class of perturbation as the rsqrt normalisation), far from the decision
+// boundaries except in the rare stalled-LM end game.
+__device__ __forceinline__ void interp_jac_f(const Interp& I, float J[6]) {
+  const float fu = (float)I.fu, fv = (float)I.fv;
+  const float a0 = (float)(I.c10.x - I.c00.x), a1 = (float)(I.c10.y - I.c00.y), a2 = (float)(I.c10.z - I.c00.z);
+  const float b0 = (float)(I.c11.x - I.c01.x), b1 = (float)(I.c11.y - I.c01.y), b2 = (float)(I.c11.z - I.c01.z);
+  const float c0 = (float)(I.c01.x - I.c00.x), c1 = (float)(I.c01.y - I.c00.y), c2 = (float)(I.c01.z - I.c00.z);
+  const float e0 = (float)(I.c11.x - I.c10.x), e1 = (float)(I.c11.y - I.c10.y), e2 = (float)(I.c11.z - I.c10.z);
+  const float du0 = fmaf(fv, b0 - a0, a0), du1 = fmaf(fv, b1 - a1, a1), du2 = fmaf(fv, b2 - a2, a2);
+  const float dv0 = fmaf(fu, e0 - c0, c0), dv1 = fmaf(fu, e1 - c1, c1), dv2 = fmaf(fu, e2 - c2, c2);
+  const float r0 = (float)I.r0, r1 = (float)I.r1, r2 = (float)I.r2, rs = (float)I.rs;
+  const float rdu = fmaf(r0, du0, fmaf(r1, du1, r2 * du2)), rdv = fmaf(r0, dv0, fmaf(r1, dv1, r2 * dv2));
+  J[0] = fmaf(-r0, rdu, du0) * rs;
+  J[1] = fmaf(-r1, rdu, du1) * rs;
+  J[2] = fmaf(-r2, rdu, du2) * rs;
+  J[3] = fmaf(-r0, rdv, dv0) * rs;
+  J[4] = fmaf(-r1, rdv, dv1) * rs;
+  J[5] = fmaf(-r2, rdv, dv2) * rs;
+}
+
+__device__ __forceinline__ void ldlt2_solve_f(float h00, float h01, float h11, float b0, float b1, float* x0,
+                                              float* x1) {
+  const bool sw = fabsf(h11) > fabsf(h00);
+  const float m00 = sw ? h11 : h00;
+  float m11 = sw ? h00 : h11;
+  if (!(fabsf(m00) > 0.0f)) {
+    *x0 = 0.0f;
+    *x1 = 0.0f;
+    return;
+  }
+  const float i00 = 1.0f / m00;
+  const float m10 = h01 * i00;
+  m11 -= m10 * (m00 * m10);
+  float d0 = sw ? b1 : b0, d1 = sw ? b0 : b1;
+  d1 -= m10 * d0;
+  d0 = d0 * i00;
+  d1 = fabsf(m11) > 1.17549435e-38f ? d1 / m11 : 0.0f;
+  d0 -= m10 * d1;
+  *x0 = sw ? d1 : d0;
+  *x1 = sw ? d0 : d1;
+}
+
 // 2x2 instance of Eigen's pivoted LDLT solve (camera.cpp:147), same ops as
 // ldlt_pivoted_solve(2, ...).
 __device__ __forceinline__ void ldlt2_solve(double h00, double h01, double h11, double b0, double b1,
@@ -683,14 +733,33 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     res.converged = true;
     return res;
   }
+#if PMX_LM_F32
+  float J[6];
+  interp_jac_f(I, J);
+#else
   double J[6];
   interp_jac(I, J);
+#endif
   double lambda = lp.lambda_init;
   for (int it = 0; it < lp.max_iterations; ++it) {
     ++res.iterations;
     r0 = ray0 - t0;
     r1 = ray1 - t1;
     r2 = ray2 - t2;
+#if PMX_LM_F32
+    const float fr0 = (float)r0, fr1 = (float)r1, fr2 = (float)r2;
+    const float a00 = fmaf(J[0], J[0], fmaf(J[1], J[1], J[2] * J[2]));
+    const float a01 = fmaf(J[0], J[3], fmaf(J[1], J[4], J[2] * J[5]));
+    const float a11 = fmaf(J[3], J[3], fmaf(J[4], J[4], J[5] * J[5]));
+    const float g0 = fmaf(J[0], fr0, fmaf(J[1], fr1, J[2] * fr2));
+    const float g1 = fmaf(J[3], fr0, fmaf(J[4], fr1, J[5] * fr2));
+    const float fl = (float)lambda;
+    const float h00 = fmaf(fl, fmaxf(a00, 1e-12f), a00);
+    const float h11 = fmaf(fl, fmaxf(a11, 1e-12f), a11);
+    float fs0, fs1;
+    ldlt2_solve_f(h00, a01, h11, g0, g1, &fs0, &fs1);
+    const double d0 = -(double)fs0, d1 = -(double)fs1;
+#else
     const double a00 = J[0] * J[0] + J[1] * J[1] + J[2] * J[2];
     const double a01 = J[0] * J[3] + J[1] * J[4] + J[2] * J[5];
     const double a11 = J[3] * J[3] + J[4] * J[4] + J[5] * J[5];
@@ -701,6 +770,7 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     double s0, s1;
     ldlt2_solve(h00, a01, h11, g0, g1, &s0, &s1);
     const double d0 = -s0, d1 = -s1;
+#endif
     if (!isfinite(d0) || !isfinite(d1)) break;
     // clamp_to_image (camera.cpp:104-107); pu + d0 is finite here
     const double xu = pu + d0, xv = pv + d1;
@@ -723,7 +793,11 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
           res.converged = true;
           return res;
         }
+#if PMX_LM_F32
+        interp_jac_f(I, J);
+#else
         interp_jac(I, J);
+#endif
         continue;
       }
     }
