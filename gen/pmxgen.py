@@ -449,11 +449,14 @@ def backend_graph_matched(ctx, n_kf: int, reach: int, seed: int, height=H, width
     device = device or torch.device("cuda", torch.cuda.current_device())
     sc = Scene(seed, height, width, f=F * width / W, cx=CX * width / W, cy=CY * height / H, surface="heightfield")
     gt = loop_trajectory(n_kf, radius, loops, seed)
-    cams = [Camera(sc, k, gt[k]) for k in range(n_kf)]
-    canon = [(c.express(c.T, 1000 + k), c.valid) for k, c in enumerate(cams)]
     edges = loop_edges(n_kf, reach)
     e0, e1 = edge_range if edge_range is not None else (0, len(edges))
     need = sorted({k for e in range(e0, e1) for k in edges[e]})
+    # an edge shard only ray-casts its own keyframes; the others get empty
+    # (all-invalid) canonicals, which no edge of the shard reads
+    cams = {k: Camera(sc, k, gt[k]) for k in need}
+    blank = (np.zeros((height * width, 3), np.float32), np.zeros(height * width, np.uint8))
+    canon = [(cams[k].express(cams[k].T, 1000 + k), cams[k].valid) if k in cams else blank for k in range(n_kf)]
     dcams = {k: DeviceCamera(cams[k], device) for k in need}
     mp = abi.default_match_params()
     mp.projection.lambda_init = 1e-8
