@@ -1802,8 +1802,9 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
       max_ty = std::max(max_ty, (hp[i].Hb + 7) / 8);
     }
     if (refine && L.n > 0) {
-      ProfScope ps(ctx, "k_match_refine");
+      // counter first: its first allocation must stay outside the timed scope
       unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
+      ProfScope ps(ctx, "k_match_refine");
       int ty = 0;
       for (int i = c0; i < c0 + cn; ++i) ty = std::max(ty, (hp[i].Hb + PMX_MR_TY - 1) / PMX_MR_TY);
       k_match_refine<<<dim3(max_tx, ty, cn), 32 * PMX_MR_TY, 0, ctx.stream>>>(dp, lp, L, exact_px);

@@ -9,5 +9,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
   --log-file gpurun_out/launches_r02.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-secondary \
   > gpurun_out/ncu_launches.log 2>&1; echo "launches rc=$?"
 timeout 300 python tools/ncu_target.py match 5 > gpurun_out/plain_match.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_match_refine' -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k 'regex:k_match_refine' -s 1 -c 1 \
   -o gpurun_out/prof_match_r02b -f python tools/ncu_target.py match 5 > gpurun_out/ncu_match.log 2>&1; echo "full rc=$?"
