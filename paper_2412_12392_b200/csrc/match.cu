@@ -23,6 +23,8 @@
 //                    ties) take the exact path, so the argmax equals the
 //                    reference's exact-arithmetic argmax (strict '>' scan,
 //                    ties keep the centre / first raster).
+#include <math_constants.h>
+
 #include <cfloat>
 #include <climits>
 #include <cmath>
@@ -45,6 +47,18 @@
 #endif
 #ifndef PMX_LM_F32
 #define PMX_LM_F32 1  // LM step direction (Jacobian, normal equations, 2x2 solve) in fp32
+#endif
+#ifndef PMX_PAIRLD
+#define PMX_PAIRLD 0  // level-1 window rows as aligned pixel pairs (16-B heads, 32-B tails): identical outputs, 1.50 -> 1.61 ms
+#endif
+#ifndef PMX_PREFETCH
+#define PMX_PREFETCH 1  // the target descriptor row is prefetched into L2 before the LM
+#endif
+#ifndef PMX_EAGER_F32
+#define PMX_EAGER_F32 0  // fp32 LM: Jacobian support differences formed in interp_eval (corners die early; same spills, 1.500 -> 1.517 ms)
+#endif
+#ifndef PMX_RAY24
+#define PMX_RAY24 0  // LM gathers 24 B (x, y, z: 16 + 8 B loads) per support, NaN-marked invalid rays: 1.500 -> 1.551 ms
 #endif
 #ifndef PMX_OVERLAP
 #define PMX_OVERLAP 0  // pairs per chunk of the overlapped device path (0: one chunk; 8 / 16 / 32 measured 7-17% slower)
@@ -285,7 +299,9 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       hist_add(sh, key >> 20, key != kNoKey);
       P.keys[i] = key;
     }
-    double4 r = make_double4(0.0, 0.0, 1.0, 0.0);
+    // invalid: w = 0, and (PMX_RAY24) NaN components, so the LM's 24-byte
+    // gathers see an invalid support through the NaN its weighted sum takes
+    double4 r = PMX_RAY24 ? make_double4(CUDART_NAN, CUDART_NAN, CUDART_NAN, 0.0) : make_double4(0.0, 0.0, 1.0, 0.0);
     if (v && !(nrm < 1e-12) && isfinite(nrm)) r = make_double4(x / nrm, y / nrm, z / nrm, 1.0);
     P.rays[i] = r;
     if (P.dnorm) desc_aux(P.da + (size_t)i * 24, P.qa[i], P.dnorm + i);
@@ -575,6 +591,54 @@ __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, in
   return true;
 }
 
+// The LM's form of interp_eval (PMX_RAY24): 24-byte supports (x, y, z: one
+// 16-byte + one 8-byte load), validity from the NaN an invalid support puts
+// into the weighted sum (weights are finite, 0 x NaN = NaN).  8 fewer
+// registers per live support set and 25% fewer L1 wavefronts than the
+// 256-bit form; same values.
+struct Interp3 {
+  double r0, r1, r2;
+  double rs;
+  double fu, fv;
+  double3 c00, c10, c01, c11;
+};
+
+__device__ __forceinline__ double3 ld_ray3(const double4* __restrict__ rays, int i) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(rays + i));
+  const double c = __ldg(reinterpret_cast<const double*>(rays + i) + 2);
+  return make_double3(a.x, a.y, c);
+}
+
+__device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, int W, int H, double u, double v,
+                                            Interp3& I) {
+  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+  int u0 = (int)floor(u);
+  int v0 = (int)floor(v);
+  u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
+  v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
+  const int du = min(u0 + 1, W - 1) - u0, dv = (min(v0 + 1, H - 1) - v0) * W;
+  int base = v0 * W + u0;
+  PMX_CHECK_INDEX(base, W * H - dv - du);
+  I.fu = u - u0;
+  I.fv = v - v0;
+  I.c00 = ld_ray3(rays, base);
+  I.c10 = ld_ray3(rays, base + du);
+  I.c01 = ld_ray3(rays, base + dv);
+  I.c11 = ld_ray3(rays, base + dv + du);
+  const double fu = I.fu, fv = I.fv;
+  const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
+  const double g0 = w00 * I.c00.x + w10 * I.c10.x + w01 * I.c01.x + w11 * I.c11.x;
+  const double g1 = w00 * I.c00.y + w10 * I.c10.y + w01 * I.c01.y + w11 * I.c11.y;
+  const double g2 = w00 * I.c00.z + w10 * I.c10.z + w01 * I.c01.z + w11 * I.c11.z;
+  const double gg = g0 * g0 + g1 * g1 + g2 * g2;
+  if (!(gg >= 1e-24)) return false;  // an invalid support (NaN) / |g| < 1e-12
+  I.rs = rsqrt(gg);
+  I.r0 = g0 * I.rs;
+  I.r1 = g1 * I.rs;
+  I.r2 = g2 * I.rs;
+  return true;
+}
+
 // J = (I - r r^T) / |g| [dg/du, dg/dv]  (camera.cpp:92-98)
 __device__ __forceinline__ void interp_jac(const Interp& I, double J[6]) {
   const double fu = I.fu, fv = I.fv;
@@ -613,7 +677,8 @@ __device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int
 // change of a step moves the next iterate by ~1e-7 of the step (the same
 // class of perturbation as the rsqrt normalisation), far from the decision
 // boundaries except in the rare stalled-LM end game.
-__device__ __forceinline__ void interp_jac_f(const Interp& I, float J[6]) {
+template <class IP>
+__device__ __forceinline__ void interp_jac_f(const IP& I, float J[6]) {
   const float fu = (float)I.fu, fv = (float)I.fv;
   const float a0 = (float)(I.c10.x - I.c00.x), a1 = (float)(I.c10.y - I.c00.y), a2 = (float)(I.c10.z - I.c00.z);
   const float b0 = (float)(I.c11.x - I.c01.x), b1 = (float)(I.c11.y - I.c01.y), b2 = (float)(I.c11.z - I.c01.z);
@@ -629,6 +694,69 @@ __device__ __forceinline__ void interp_jac_f(const Interp& I, float J[6]) {
   J[3] = fmaf(-r0, rdv, dv0) * rs;
   J[4] = fmaf(-r1, rdv, dv1) * rs;
   J[5] = fmaf(-r2, rdv, dv2) * rs;
+}
+
+// Eager form of the fp32 path: interp_eval_f keeps only what the step needs
+// - the FP64 unit ray, and the fp32 dg/du, dg/dv and 1/|g| - so the four
+// FP64 supports (32 registers) die inside the interpolation instead of
+// living until the accept test.  Same operations as interp_jac_f on the
+// same values (identical Jacobian); the differences are also formed for
+// trials that end up rejected (rare at lambda = 1e-8).
+struct InterpF {
+  double r0, r1, r2;  // unit ray g / |g|
+  float rs;           // 1 / |g|
+  float du[3], dv[3];
+};
+
+__device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, int W, int H, double u, double v,
+                                              InterpF& I) {
+  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+  int u0 = (int)floor(u);
+  int v0 = (int)floor(v);
+  u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
+  v0 = min(v0, H - 2 >= 0 ? H - 2 : 0);
+  const int du = min(u0 + 1, W - 1) - u0, dv = (min(v0 + 1, H - 1) - v0) * W;
+  int base = v0 * W + u0;
+  PMX_CHECK_INDEX(base, W * H - dv - du);
+  const double4* p = rays + base;
+  const double fu = u - u0, fv = v - v0;
+  const double4 c00 = ld_ray(p, 0), c10 = ld_ray(p, du), c01 = ld_ray(p, dv), c11 = ld_ray(p, dv + du);
+  const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
+  const double g0 = w00 * c00.x + w10 * c10.x + w01 * c01.x + w11 * c11.x;
+  const double g1 = w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y;
+  const double g2 = w00 * c00.z + w10 * c10.z + w01 * c01.z + w11 * c11.z;
+  const double gg = g0 * g0 + g1 * g1 + g2 * g2;
+  const bool valid = c00.w != 0.0 && c10.w != 0.0 && c01.w != 0.0 && c11.w != 0.0;
+  if (!valid || gg < 1e-24) return false;
+  const double rs = rsqrt(gg);
+  I.r0 = g0 * rs;
+  I.r1 = g1 * rs;
+  I.r2 = g2 * rs;
+  I.rs = (float)rs;
+  const float ffu = (float)fu, ffv = (float)fv;
+  const float a0 = (float)(c10.x - c00.x), a1 = (float)(c10.y - c00.y), a2 = (float)(c10.z - c00.z);
+  const float b0 = (float)(c11.x - c01.x), b1 = (float)(c11.y - c01.y), b2 = (float)(c11.z - c01.z);
+  const float d0 = (float)(c01.x - c00.x), d1 = (float)(c01.y - c00.y), d2 = (float)(c01.z - c00.z);
+  const float e0 = (float)(c11.x - c10.x), e1 = (float)(c11.y - c10.y), e2 = (float)(c11.z - c10.z);
+  I.du[0] = fmaf(ffv, b0 - a0, a0);
+  I.du[1] = fmaf(ffv, b1 - a1, a1);
+  I.du[2] = fmaf(ffv, b2 - a2, a2);
+  I.dv[0] = fmaf(ffu, e0 - d0, d0);
+  I.dv[1] = fmaf(ffu, e1 - d1, d1);
+  I.dv[2] = fmaf(ffu, e2 - d2, d2);
+  return true;
+}
+
+__device__ __forceinline__ void interp_jac_f(const InterpF& I, float J[6]) {
+  const float r0 = (float)I.r0, r1 = (float)I.r1, r2 = (float)I.r2, rs = I.rs;
+  const float rdu = fmaf(r0, I.du[0], fmaf(r1, I.du[1], r2 * I.du[2]));
+  const float rdv = fmaf(r0, I.dv[0], fmaf(r1, I.dv[1], r2 * I.dv[2]));
+  J[0] = fmaf(-r0, rdu, I.du[0]) * rs;
+  J[1] = fmaf(-r1, rdu, I.du[1]) * rs;
+  J[2] = fmaf(-r2, rdu, I.du[2]) * rs;
+  J[3] = fmaf(-r0, rdv, I.dv[0]) * rs;
+  J[4] = fmaf(-r1, rdv, I.dv[1]) * rs;
+  J[5] = fmaf(-r2, rdv, I.dv[2]) * rs;
 }
 
 __device__ __forceinline__ void ldlt2_solve_f(float h00, float h01, float h11, float b0, float b1, float* x0,
@@ -718,8 +846,17 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
   const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
 #endif
   double pu = cu, pv = cv;
+#if PMX_LM_F32 && PMX_EAGER_F32
+  InterpF I;
+#define PMX_INTERP_EVAL interp_eval_f
+#elif PMX_RAY24
+  Interp3 I;
+#define PMX_INTERP_EVAL interp_eval
+#else
   Interp I;
-  if (!interp_eval(rays, W, H, pu, pv, I)) {
+#define PMX_INTERP_EVAL interp_eval
+#endif
+  if (!PMX_INTERP_EVAL(rays, W, H, pu, pv, I)) {
     res.pu = pu;
     res.pv = pv;
     return res;
@@ -776,7 +913,7 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     const double xu = pu + d0, xv = pv + d1;
     const double tu = xu < 0.0 ? 0.0 : (xu > (double)(W - 1) ? (double)(W - 1) : xu);
     const double tv = xv < 0.0 ? 0.0 : (xv > (double)(H - 1) ? (double)(H - 1) : xv);
-    if (interp_eval(rays, W, H, tu, tv, I)) {
+    if (PMX_INTERP_EVAL(rays, W, H, tu, tv, I)) {
       const double e0 = I.r0 - t0, e1 = I.r1 - t1, e2 = I.r2 - t2;
       const double ct = e0 * e0 + e1 * e1 + e2 * e2;
       if (ct < cost) {
@@ -807,6 +944,7 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
   res.pv = pv;
   res.converged = ray0 * t0 + ray1 * t1 + ray2 * t2 >= lp.cos_tol;
   return res;
+#undef PMX_INTERP_EVAL
 }
 
 // ------------------------------------------------------------ refine (K4)
@@ -1316,6 +1454,53 @@ __device__ __forceinline__ Top2 q_level1(const Tile& T, const QB& B, int cu, int
   return t;
 }
 
+// 256-bit read-only load of two consecutive tails (dims 8-23 of pixels i, i+1; 32-B aligned).
+__device__ __forceinline__ void ld_tail2(const uint4* p, uint4& a, uint4& b) {
+  unsigned long long x, y, z, w;
+  asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(x), "=l"(y), "=l"(z), "=l"(w) : "l"(p));
+  a = make_uint4((uint32_t)x, (uint32_t)(x >> 32), (uint32_t)y, (uint32_t)(y >> 32));
+  b = make_uint4((uint32_t)z, (uint32_t)(z >> 32), (uint32_t)w, (uint32_t)(w >> 32));
+}
+
+// First level, stride 1, as q_level1<R, 1> but each window row is read as
+// the R + 1 aligned pixel pairs (e, e + 1), e = row start & ~1, that cover
+// it: one 16-byte head load and one 32-byte tail load per two candidates.
+// Neighbouring lanes' windows start one pixel apart, so two lanes share
+// every pair and the warp moves ~half the L1 bytes of per-candidate loads.
+// The slot outside the window (first or last of the 2R + 2) is masked; the
+// centre is scored in its row.  Same top-2 as q_level1 (keys are
+// order-independent).  Needs 16-B aligned heads and 32-B aligned tails; the
+// last pair may reach one pixel past the image (the chunk scratch continues
+// there: q8t is followed by q8h, q8h by q8n).
+template <int R, class Tile>
+__device__ __forceinline__ Top2 q_level1_pairs(const Tile& T, const QB& B, int cu, int cv) {
+  constexpr int D = 2 * R + 1;
+  const int s0 = T.at(cu - R, cv - R);
+  Top2 t{INT_MIN, INT_MIN};
+#pragma unroll
+  for (int dv = 0; dv < D; ++dv) {
+    const int rs = s0 + dv * T.bw;  // window row start
+    const int e = rs & ~1;
+    const int sh = rs - e;  // 0 or 1: slot k of the row is window column k - sh
+    PMX_CHECK_INDEX(e, T.hw);
+    PMX_CHECK_INDEX(e + 2 * R + 1, T.hw + 1);
+    const uint4* hp = reinterpret_cast<const uint4*>(T.h + e);
+    const uint4* tp = T.t + e;
+#pragma unroll
+    for (int j = 0; j <= R; ++j) {
+      const uint4 h2 = __ldg(hp + j);
+      uint4 ta, tb;
+      ld_tail2(tp + 2 * j, ta, tb);
+      const int sa = qdot_tail(ta, B, qdot_head(make_uint2(h2.x, h2.y), B));
+      const int sb = qdot_tail(tb, B, qdot_head(make_uint2(h2.z, h2.w), B));
+      const int ka = 2 * j - sh, kb = 2 * j + 1 - sh;
+      top2_add(t, ka >= 0 ? qkey(sa, dv * D + ka) : INT_MIN);
+      top2_add(t, kb < D ? qkey(sb, dv * D + kb) : INT_MIN);
+    }
+  }
+  return t;
+}
+
 // One level at run-time radius / stride for one lane (border windows and
 // uncommon level shapes).  Candidates of the previous window (pr >= 0) are
 // skipped; the centre enters with score `centre` (its rank r*D+r).
@@ -1360,8 +1545,15 @@ __device__ __forceinline__ void q_advance(QState& q, const Top2& t, int tgap, in
   q.pcv = q.cv;
   q.ps = s;
   q.pr = r;
-  q.cu += (k % D - r) * s;
-  q.cv += (k / D - r) * s;
+  if (r == 3) {  // BASELINE's window: division by a constant
+    const int kv = k / 7;
+    q.cu += (k - 7 * kv - 3) * s;
+    q.cv += (kv - 3) * s;
+  } else {
+    const int kv = k / D;
+    q.cu += (k - D * kv - r) * s;
+    q.cv += (kv - r) * s;
+  }
   q.best = t.score1();
 }
 
@@ -1373,6 +1565,7 @@ template <class Tile>
 __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tgap, int Wa, int Ha,
                                               const RefineLevels& L, QState& q) {
   const int lane = threadIdx.x & 31;
+  const bool pair_aligned = ((uintptr_t)T.h & 15) == 0 && ((uintptr_t)T.t & 31) == 0;
   for (int l = 0; l < L.n; ++l) {
     const int s = L.stride[l], r = L.radius[l];
     const bool same = q.pr >= 0 && s == q.ps && r == q.pr && q.cu == q.pcu && q.cv == q.pcv;  // identical window
@@ -1385,7 +1578,12 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
                               q.cv + r * s < Ha;
         if (interior && s == 1 && r == 3) {
-          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
+#if PMX_PAIRLD
+          if (pair_aligned)
+            t = q_level1_pairs<3, Tile>(T, B, q.cu, q.cv);
+          else
+#endif
+            t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
         } else if (interior && s == 2 && r == 2) {
           t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap);
         } else {
@@ -1453,6 +1651,11 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
   const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * PMX_MR_TY + (threadIdx.x >> 5);
   const int m = v * P.Wb + u;
   int n = -1, pa = 0, pcu = 0, pcv = 0;
+#if PMX_PREFETCH
+  // the descriptor row quantized after the LM: its HBM latency overlaps the LM
+  if (u < P.Wb && v < P.Hb && P.q8h != nullptr)
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(P.db) + 48 * (size_t)m));
+#endif
   if (u < P.Wb && v < P.Hb) {
     const int4 r = match_pixel(P, lp, m, u, v);
     pa = r.x;
@@ -1545,7 +1748,8 @@ __global__ void k_rays_out(const double4* __restrict__ rays, int HW, double* out
                            uint8_t* out_valid, const float* __restrict__ xyz) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= HW) return;
-  const double4 r = rays[i];
+  double4 r = rays[i];
+  if (r.w == 0.0) r = make_double4(0.0, 0.0, 1.0, 0.0);  // camera.cpp: invalid pixels keep (0, 0, 1)
   out_rays[3 * i] = r.x;
   out_rays[3 * i + 1] = r.y;
   out_rays[3 * i + 2] = r.z;
