@@ -188,7 +188,7 @@ int pmx_destroy(pmx_context* c) {
     cudaStreamSynchronize(ctx->own_stream);
     cudaStreamDestroy(ctx->own_stream);
   }
-  for (cudaStream_t s : {ctx->copy_in, ctx->copy_out, ctx->aux})
+  for (cudaStream_t s : {ctx->copy_in, ctx->copy_in2, ctx->copy_out, ctx->aux})
     if (s) {
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);

@@ -60,6 +60,12 @@
 #ifndef PMX_RAY24
 #define PMX_RAY24 0  // LM gathers 24 B (x, y, z: 16 + 8 B loads) per support, NaN-marked invalid rays: 1.500 -> 1.551 ms
 #endif
+#ifndef PMX_H2D_QUEUES
+#define PMX_H2D_QUEUES 2  // host path: input copies alternate over this many copy streams
+#endif
+#ifndef PMX_HOST_CHUNK
+#define PMX_HOST_CHUNK 4  // host path: pairs per full chunk (~95 MB of inputs: ~1.8 ms of H2D against ~0.2 ms of compute)
+#endif
 #ifndef PMX_OVERLAP
 #define PMX_OVERLAP 0  // pairs per chunk of the overlapped device path (0: one chunk; 8 / 16 / 32 measured 7-17% slower)
 #endif
@@ -1973,8 +1979,14 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
     PMX_CUDA(cudaEventRecord(ev_prep[nchunks], main_stream));  // scratch allocated, state zeroed
     PMX_CUDA(cudaStreamWaitEvent(ctx.aux, ev_prep[nchunks], 0));
   }
-  for (int c0 = 0; c0 < npairs; c0 += chunk) {
-    const int cn = std::min(chunk, npairs - c0);
+  // Host path: the last chunks halve (4, 2, 1, 1 after full ones), so the
+  // compute and output copies left after the final input copy are one pair's.
+  auto chunk_at = [&](int c0) {
+    const int rest = npairs - c0;
+    return hooks && rest <= chunk ? std::max(1, (rest + 1) / 2) : std::min(chunk, rest);
+  };
+  for (int c0 = 0, cn = 0; c0 < npairs; c0 += cn) {
+    cn = chunk_at(c0);
     const int ci = c0 / chunk;
     PairDev* dp = dpairs.as<PairDev>() + c0;
     if (hooks) hooks->before_chunk(c0, cn);
@@ -2103,7 +2115,7 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     hp[i].out_valid = st.out(outs[i].valid, hwb);
   }
   MatchHooks hooks;
-  hooks.chunk_pairs = 8;  // ~190 MB of inputs per chunk: ~3.5 ms of H2D against ~0.3 ms of compute
+  hooks.chunk_pairs = PMX_HOST_CHUNK;
   cudaEvent_t ev_a = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_out;
   if (pipelined) {  // device mirrors of every array (one allocation), copies issued by the hooks
@@ -2111,6 +2123,8 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
       PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_in, cudaStreamNonBlocking));
       PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_out, cudaStreamNonBlocking));
     }
+    if (PMX_H2D_QUEUES > 1 && !ctx.copy_in2)
+      PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_in2, cudaStreamNonBlocking));
     size_t total = 0;
     auto room = [&](size_t bytes) { total += (bytes + 255) & ~size_t(255); };
     for (int i = 0; i < num_pairs; ++i) {
@@ -2146,8 +2160,23 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     PMX_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
     PMX_CUDA(cudaEventRecord(ev_a, ctx.stream));  // device buffers allocated (stream-ordered)
     PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in, ev_a, 0));
+    if (PMX_H2D_QUEUES > 1) PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in2, ev_a, 0));
+    // Input copies alternate over the H2D queues: one queue leaves the link
+    // idle between consecutive small copies (valid masks, confidences).
+    int h2d_turn = 0;
     auto h2d = [&](const void* d, const void* h, size_t bytes) {
-      if (bytes) PMX_CUDA(cudaMemcpyAsync(const_cast<void*>(d), h, bytes, cudaMemcpyHostToDevice, ctx.copy_in));
+      if (!bytes) return;
+      cudaStream_t q = (PMX_H2D_QUEUES > 1 && (h2d_turn++ & 1)) ? ctx.copy_in2 : ctx.copy_in;
+      PMX_CUDA(cudaMemcpyAsync(const_cast<void*>(d), h, bytes, cudaMemcpyHostToDevice, q));
+    };
+    // the compute stream waits for every queue's copies so far
+    auto join_h2d = [&](cudaEvent_t e, cudaEvent_t e2) {
+      PMX_CUDA(cudaEventRecord(e, ctx.copy_in));
+      PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
+      if (PMX_H2D_QUEUES > 1) {
+        PMX_CUDA(cudaEventRecord(e2, ctx.copy_in2));
+        PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e2, 0));
+      }
     };
     auto d2h = [&](void* h, const void* d, size_t bytes) {
       if (bytes && h) PMX_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, ctx.copy_out));
@@ -2158,8 +2187,10 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
         h2d(hp[i].xa, pairs[i].X_a.xyz, 12 * hwa);
         if (pairs[i].X_a.valid) h2d(hp[i].va, pairs[i].X_a.valid, hwa);
       }
-      PMX_CUDA(cudaEventRecord(ev_a, ctx.copy_in));
-      PMX_CUDA(cudaStreamWaitEvent(ctx.stream, ev_a, 0));
+      cudaEvent_t e2;
+      PMX_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+      ev_in.push_back(e2);
+      join_h2d(ev_a, e2);
     };
     hooks.before_chunk = [&](int c0, int cn) {
       for (int i = c0; i < c0 + cn; ++i) {
@@ -2172,11 +2203,12 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
         h2d(hp[i].qa, p.F_a.match_confidence, 4 * hwa);
         h2d(hp[i].qb, p.F_b.match_confidence, 4 * hwb);
       }
-      cudaEvent_t e;
+      cudaEvent_t e, e2;
       PMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      PMX_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
       ev_in.push_back(e);
-      PMX_CUDA(cudaEventRecord(e, ctx.copy_in));
-      PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
+      ev_in.push_back(e2);
+      join_h2d(e, e2);
     };
     hooks.after_chunk = [&](int c0, int cn) {
       if (gate_counts) return;  // the gate still rewrites valid: copied back at the end
@@ -2219,6 +2251,7 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     }
     PMX_CUDA(cudaStreamSynchronize(ctx.copy_out));
     PMX_CUDA(cudaStreamSynchronize(ctx.copy_in));
+    if (ctx.copy_in2) PMX_CUDA(cudaStreamSynchronize(ctx.copy_in2));
     PMX_CUDA(cudaStreamSynchronize(ctx.stream));
     cudaEventDestroy(ev_a);
     for (auto e : ev_in) cudaEventDestroy(e);
