@@ -60,8 +60,11 @@
 #ifndef PMX_RAY24
 #define PMX_RAY24 0  // LM gathers 24 B (x, y, z: 16 + 8 B loads) per support, NaN-marked invalid rays: 1.500 -> 1.551 ms
 #endif
-#ifndef PMX_H2D_QUEUES
-#define PMX_H2D_QUEUES 2  // host path: input copies alternate over this many copy streams
+#ifndef PMX_SM_COPY_MAX_KB
+#define PMX_SM_COPY_MAX_KB 1024  // inputs below this size qualify for the SM copy
+#endif
+#ifndef PMX_SM_SMALL_COPIES
+#define PMX_SM_SMALL_COPIES 1  // host path: small pinned inputs copied by one SM kernel instead of DMA
 #endif
 #ifndef PMX_HOST_CHUNK
 #define PMX_HOST_CHUNK 4  // host path: pairs per full chunk (~95 MB of inputs: ~1.8 ms of H2D against ~0.2 ms of compute)
@@ -1791,6 +1794,39 @@ __global__ void __launch_bounds__(256) k_loop_gate(const PairDev* __restrict__ p
   if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(valid_count + blockIdx.y, (unsigned long long)cnt);
 }
 
+// Host path: copies of the small per-pair inputs (valid masks, confidences)
+// from pinned, device-mapped host memory, done by SM loads over PCIe in one
+// launch per chunk.  Each DMA transfer costs the copy engine a fixed ~5 us
+// on top of its bytes; these arrays are half of the transfers and 8% of the
+// bytes (tools/probes/zerocopy.cu: 512 DMA copies of the config-2 mix 21.6
+// ms per GiB, large ones by DMA + small ones by this kernel 20.8 ms).
+struct CopySeg {
+  const uint8_t* src;  // device-mapped host pointer
+  uint8_t* dst;
+  unsigned long long bytes;
+};
+constexpr int kMaxCopySegs = 96;
+struct CopySegs {
+  int n;
+  CopySeg s[kMaxCopySegs];
+};
+__global__ void __launch_bounds__(256) k_copy_segs(const CopySegs segs) {
+  for (int g = blockIdx.y; g < segs.n; g += gridDim.y) {
+    const CopySeg sg = segs.s[g];
+    const unsigned long long step = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long t0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long done = 0;
+    if ((((uintptr_t)sg.src | (uintptr_t)sg.dst) & 15) == 0) {  // 16-byte body
+      const unsigned long long n16 = sg.bytes >> 4;
+      const uint4* src = reinterpret_cast<const uint4*>(sg.src);
+      uint4* dst = reinterpret_cast<uint4*>(sg.dst);
+      for (unsigned long long i = t0; i < n16; i += step) dst[i] = src[i];
+      done = n16 << 4;
+    }
+    for (unsigned long long i = done + t0; i < sg.bytes; i += step) sg.dst[i] = sg.src[i];
+  }
+}
+
 // ------------------------------------------------------------------ host
 // Largest double d with acos(clamp(d, -1, 1)) >= tol, found on the host with
 // the same libm acos the reference uses; the device tests d >= cos_tol.
@@ -2123,8 +2159,11 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
       PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_in, cudaStreamNonBlocking));
       PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_out, cudaStreamNonBlocking));
     }
-    if (PMX_H2D_QUEUES > 1 && !ctx.copy_in2)
-      PMX_CUDA(cudaStreamCreateWithFlags(&ctx.copy_in2, cudaStreamNonBlocking));
+    if (PMX_SM_SMALL_COPIES && !ctx.copy_in2) {  // high priority: its blocks slot in as matcher CTAs retire
+      int lo = 0, hi = 0;
+      PMX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      PMX_CUDA(cudaStreamCreateWithPriority(&ctx.copy_in2, cudaStreamNonBlocking, hi));
+    }
     size_t total = 0;
     auto room = [&](size_t bytes) { total += (bytes + 255) & ~size_t(255); };
     for (int i = 0; i < num_pairs; ++i) {
@@ -2160,20 +2199,42 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
     PMX_CUDA(cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming));
     PMX_CUDA(cudaEventRecord(ev_a, ctx.stream));  // device buffers allocated (stream-ordered)
     PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in, ev_a, 0));
-    if (PMX_H2D_QUEUES > 1) PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in2, ev_a, 0));
-    // Input copies alternate over the H2D queues: one queue leaves the link
-    // idle between consecutive small copies (valid masks, confidences).
-    int h2d_turn = 0;
+    if (PMX_SM_SMALL_COPIES) PMX_CUDA(cudaStreamWaitEvent(ctx.copy_in2, ev_a, 0));
     auto h2d = [&](const void* d, const void* h, size_t bytes) {
-      if (!bytes) return;
-      cudaStream_t q = (PMX_H2D_QUEUES > 1 && (h2d_turn++ & 1)) ? ctx.copy_in2 : ctx.copy_in;
-      PMX_CUDA(cudaMemcpyAsync(const_cast<void*>(d), h, bytes, cudaMemcpyHostToDevice, q));
+      if (bytes) PMX_CUDA(cudaMemcpyAsync(const_cast<void*>(d), h, bytes, cudaMemcpyHostToDevice, ctx.copy_in));
     };
-    // the compute stream waits for every queue's copies so far
+    // Small inputs in pinned (device-mapped) host memory: gathered into one
+    // k_copy_segs launch per chunk on copy_in2; anything else goes by DMA.
+    CopySegs pending;
+    pending.n = 0;
+    auto flush_small = [&]() {
+      if (!pending.n) return;
+      k_copy_segs<<<dim3(4, pending.n), 256, 0, ctx.copy_in2>>>(pending);
+      launch_check(ctx, "k_copy_segs");
+      pending.n = 0;
+    };
+    auto h2d_small = [&](const void* d, const void* h, size_t bytes) {
+      if (!bytes) return;
+      const void* mapped = nullptr;
+      if (PMX_SM_SMALL_COPIES && bytes < (size_t(PMX_SM_COPY_MAX_KB) << 10)) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, h) == cudaSuccess) {
+          if (a.type == cudaMemoryTypeHost && a.devicePointer) mapped = a.devicePointer;
+        } else {
+          cudaGetLastError();  // not a CUDA-known pointer: plain DMA
+        }
+      }
+      if (!mapped) return h2d(d, h, bytes);
+      if (pending.n == kMaxCopySegs) flush_small();
+      pending.s[pending.n++] = CopySeg{static_cast<const uint8_t*>(mapped), static_cast<uint8_t*>(const_cast<void*>(d)),
+                                       (unsigned long long)bytes};
+    };
+    // the compute stream waits for both input queues' copies so far
     auto join_h2d = [&](cudaEvent_t e, cudaEvent_t e2) {
+      flush_small();
       PMX_CUDA(cudaEventRecord(e, ctx.copy_in));
       PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e, 0));
-      if (PMX_H2D_QUEUES > 1) {
+      if (PMX_SM_SMALL_COPIES) {
         PMX_CUDA(cudaEventRecord(e2, ctx.copy_in2));
         PMX_CUDA(cudaStreamWaitEvent(ctx.stream, e2, 0));
       }
@@ -2185,7 +2246,7 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
       for (int i = 0; i < num_pairs; ++i) {
         const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa;
         h2d(hp[i].xa, pairs[i].X_a.xyz, 12 * hwa);
-        if (pairs[i].X_a.valid) h2d(hp[i].va, pairs[i].X_a.valid, hwa);
+        if (pairs[i].X_a.valid) h2d_small(hp[i].va, pairs[i].X_a.valid, hwa);
       }
       cudaEvent_t e2;
       PMX_CUDA(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
@@ -2197,11 +2258,11 @@ static void run_match_batch(Context& ctx, pmx_memory mem, int32_t num_pairs, con
         const pmx_pair& p = pairs[i];
         const size_t hwa = (size_t)hp[i].Ha * hp[i].Wa, hwb = (size_t)hp[i].Hb * hp[i].Wb;
         h2d(hp[i].xb, p.X_b_in_a.xyz, 12 * hwb);
-        if (p.X_b_in_a.valid) h2d(hp[i].vb, p.X_b_in_a.valid, hwb);
+        if (p.X_b_in_a.valid) h2d_small(hp[i].vb, p.X_b_in_a.valid, hwb);
         h2d(hp[i].da, p.F_a.descriptors, 2 * hwa * hp[i].dim);
         h2d(hp[i].db, p.F_b.descriptors, 2 * hwb * hp[i].dim);
-        h2d(hp[i].qa, p.F_a.match_confidence, 4 * hwa);
-        h2d(hp[i].qb, p.F_b.match_confidence, 4 * hwb);
+        h2d_small(hp[i].qa, p.F_a.match_confidence, 4 * hwa);
+        h2d_small(hp[i].qb, p.F_b.match_confidence, 4 * hwb);
       }
       cudaEvent_t e, e2;
       PMX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

@@ -49,7 +49,7 @@ struct Context {
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // pipelined host staging (created on first use)
-  cudaStream_t copy_in2 = nullptr;                      // second H2D queue (PMX_H2D_QUEUES = 2)
+  cudaStream_t copy_in2 = nullptr;                      // small pinned inputs by SM copy (PMX_SM_SMALL_COPIES)
   cudaStream_t aux = nullptr;  // high-priority side stream of the overlapped matcher (created on first use)
   std::string err;
   int64_t launches = 0;
