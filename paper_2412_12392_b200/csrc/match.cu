@@ -69,6 +69,9 @@
 #ifndef PMX_HOST_CHUNK
 #define PMX_HOST_CHUNK 4  // host path: pairs per full chunk (~95 MB of inputs: ~1.8 ms of H2D against ~0.2 ms of compute)
 #endif
+#ifndef PMX_J_SMEM
+#define PMX_J_SMEM 0  // LM fp32 Jacobian in shared memory instead of registers (spills 180 -> 172 B; neutral: 1.502 vs 1.495 ms)
+#endif
 #ifndef PMX_OVERLAP
 #define PMX_OVERLAP 0  // pairs per chunk of the overlapped device path (0: one chunk; 8 / 16 / 32 measured 7-17% slower)
 #endif
@@ -686,8 +689,21 @@ __device__ __forceinline__ bool interp_ray(const double4* __restrict__ rays, int
 // change of a step moves the next iterate by ~1e-7 of the step (the same
 // class of perturbation as the rsqrt normalisation), far from the decision
 // boundaries except in the rare stalled-LM end game.
-template <class IP>
-__device__ __forceinline__ void interp_jac_f(const IP& I, float J[6]) {
+// Jacobian storage of the fp32 LM: registers, or (JSm) a thread's column
+// of a shared-memory array - the loop-carried J otherwise spills to local
+// memory at 64 registers.
+struct JReg {
+  float v[6];
+  __device__ __forceinline__ float& operator[](int k) { return v[k]; }
+};
+template <int STRIDE>
+struct JSm {
+  float* p;
+  __device__ __forceinline__ float& operator[](int k) { return p[k * STRIDE]; }
+};
+
+template <class IP, class JT>
+__device__ __forceinline__ void interp_jac_f(const IP& I, JT& J) {
   const float fu = (float)I.fu, fv = (float)I.fv;
   const float a0 = (float)(I.c10.x - I.c00.x), a1 = (float)(I.c10.y - I.c00.y), a2 = (float)(I.c10.z - I.c00.z);
   const float b0 = (float)(I.c11.x - I.c01.x), b1 = (float)(I.c11.y - I.c01.y), b2 = (float)(I.c11.z - I.c01.z);
@@ -756,7 +772,8 @@ __device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, 
   return true;
 }
 
-__device__ __forceinline__ void interp_jac_f(const InterpF& I, float J[6]) {
+template <class JT>
+__device__ __forceinline__ void interp_jac_f(const InterpF& I, JT& J) {
   const float r0 = (float)I.r0, r1 = (float)I.r1, r2 = (float)I.r2, rs = I.rs;
   const float rdu = fmaf(r0, I.du[0], fmaf(r1, I.du[1], r2 * I.du[2]));
   const float rdv = fmaf(r0, I.dv[0], fmaf(r1, I.dv[1], r2 * I.dv[2]));
@@ -834,9 +851,10 @@ struct ProjOut {
 };
 
 // iterative_project, camera.cpp:115-174
-__device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W, int H, double x0,
-                                         double x1, double x2, double pu0, double pv0,
-                                         const LMParams& lp) {
+template <class JT = JReg>
+__device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W, int H, double x0,
+                                                         double x1, double x2, double pu0, double pv0,
+                                                         const LMParams& lp, JT J = JT()) {
   ProjOut res;
   res.converged = false;
   res.iterations = 0;
@@ -880,7 +898,6 @@ __device__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W
     return res;
   }
 #if PMX_LM_F32
-  float J[6];
   interp_jac_f(I, J);
 #else
   double J[6];
@@ -1300,7 +1317,8 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 // lround + clamp, validity, q.  Writes the outputs; returns (pa, valid).
 // (u, v): the b-pixel's column / row (n = v W_b + u).  Returns {pixel_a,
 // valid, column, row of pixel_a} (pixel_a = -1: skipped pixel).
-__device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp, int n, int u, int v) {
+template <class JT = JReg>
+__device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp, int n, int u, int v, JT J = JT()) {
   if (P.out_pb) P.out_pb[n] = n;
   int32_t pa_out = -1;
   float q_out = 0.0f;
@@ -1327,7 +1345,7 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
         }
       }
     }
-    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp);
+    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp, J);
     cu = min(max((int)round(pr.pu), 0), P.Wa - 1);  // std::lround: half away from zero
     cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
     int pa = cv * P.Wa + cu;
@@ -1666,7 +1684,12 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
     asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(P.db) + 48 * (size_t)m));
 #endif
   if (u < P.Wb && v < P.Hb) {
+#if PMX_J_SMEM && PMX_LM_F32
+    __shared__ float sJ[6 * 32 * PMX_MR_TY];
+    const int4 r = match_pixel(P, lp, m, u, v, JSm<32 * PMX_MR_TY>{sJ + threadIdx.x});
+#else
     const int4 r = match_pixel(P, lp, m, u, v);
+#endif
     pa = r.x;
     pcu = r.z;
     pcv = r.w;
