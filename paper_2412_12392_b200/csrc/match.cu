@@ -90,7 +90,7 @@ struct SelState {
   uint32_t prefix;  // resolved high bits so far
   uint32_t krem;    // rank within the current bucket
   double threshold; // invalidation_median_fraction * median
-  int a1max;        // max over a-pixels of sum q8(D_a)^2 (int8 refinement error bound)
+  int a1max;        // max over a-pixels of sum |q8(D_a)| (int8 refinement error bound)
   int qbad;         // some |D_a component| * 127 >= 127.5: no int8 fast path for this pair
   // exact FP64 median: the fp32 key of the rank-k element, how many norms
   // share that key, and their FP64 values (the rank-krem one is the median)
@@ -213,11 +213,11 @@ __device__ __forceinline__ void desc_aux(const __half* row, float q, float4* nrm
 // exactly in fp16 as the low byte of fma(x, 127, 1536) (the product is exact
 // in the FMA, and 1536 + q is representable with ulp 1 for |q| <= 511).
 // Valid (|127 x| <= 127.49, so q fits int8) iff max |x_k| <= 1 + 2^-8.
-// l2 = sum q_k^2 (exact, DP4A), which bounds sum |q_k| <= sqrt(24 l2).
+// l1 = sum |q_k| (exact: per-byte |q| summed by DP4A).
 struct Q8 {
   uint4 a;  // dims 0-15
   uint2 b;  // dims 16-23
-  int l2;   // sum of squares, all dims
+  int l1;   // sum of |q_k|, all dims
   int nt;   // ceil(sqrt(sum of squares of dims 8-23))
   int bad;
 };
@@ -245,19 +245,22 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
   q.b.y = q8_word(d2.z, d2.w, amax);
   const float2 m = __half22float2(amax);
   q.bad = !(m.x <= 1.00390625f && m.y <= 1.00390625f);  // also NaN / inf
-  const int l2h = __dp4a((int)q.a.y, (int)q.a.y, __dp4a((int)q.a.x, (int)q.a.x, 0));
+  constexpr int kOnes = 0x01010101;  // |q| <= 127 for a valid row, so the bytes stay positive as int8
+  int l1 = __dp4a((int)__vabsss4(q.a.x), kOnes, 0);
+  l1 = __dp4a((int)__vabsss4(q.a.y), kOnes, l1);
+  l1 = __dp4a((int)__vabsss4(q.a.z), kOnes, l1);
+  l1 = __dp4a((int)__vabsss4(q.a.w), kOnes, l1);
+  l1 = __dp4a((int)__vabsss4(q.b.x), kOnes, l1);
+  q.l1 = __dp4a((int)__vabsss4(q.b.y), kOnes, l1);
   int l2t = __dp4a((int)q.a.z, (int)q.a.z, 0);
   l2t = __dp4a((int)q.a.w, (int)q.a.w, l2t);
   l2t = __dp4a((int)q.b.x, (int)q.b.x, l2t);
   l2t = __dp4a((int)q.b.y, (int)q.b.y, l2t);
-  q.l2 = l2h + l2t;
   int nt = (int)ceilf(sqrtf((float)l2t));  // exact integer ceil(sqrt): l2t < 2^24
   if (nt * nt < l2t) ++nt;
   q.nt = nt;
   return q;
 }
-// Upper bound of sum |q_k| from sum q_k^2 (Cauchy-Schwarz over 24 dims).
-__device__ __forceinline__ float q8_l1_bound(int l2) { return sqrtf(24.0f * (float)l2) * 1.0001f + 1.0f; }
 
 // ---------------------------------------------------------------- K1
 // Norm keys of median_scene_distance (camera.cpp:181-186: valid pixels with
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(256) k_prep(const PairDev* __restrict__ pairs,
       P.q8h[i] = make_uint2(q.a.x, q.a.y);
       if (PMX_PRUNE) P.q8n[i] = (uint16_t)q.nt;  // the tail bound only feeds the pruned form
       P.q8t[i] = make_uint4(q.a.z, q.a.w, q.b.x, q.b.y);
-      a1max = max(a1max, q.l2);
+      a1max = max(a1max, q.l1);
       qbad |= q.bad;
     }
   }
@@ -1634,7 +1637,8 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         Top2 t{lane == 0 ? qkey(centre, lim0) : INT_MIN, INT_MIN};
         const int lim = pr * ps;
         for (int k = lane; k < nc; k += 32) {
-          const int dv = k / D - r, du = k % D - r;
+          const int kv = r == 3 ? k / 7 : k / D;  // BASELINE's window: a constant divisor
+          const int dv = kv - r, du = k - D * kv - r;
           const int u = cu + du * s, v = cv + dv * s;
           if (u < 0 || u >= Wa || v < 0 || v >= Ha || (du == 0 && dv == 0)) continue;
           const int eu = u - pcu, ev = v - pcv;
@@ -1709,7 +1713,7 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
     B.w[4] = q.b.x;
     B.w[5] = q.b.y;
     B.nt = q.nt;
-    tgap = (int)ceilf(2.0f * (0.5f * (q8_l1_bound(P.sel->a1max) + q8_l1_bound(q.l2)) + 6.0f)) + 1;
+    tgap = P.sel->a1max + q.l1 + 12;  // 2E, E = (sum|q8(a)| + sum|q8(b)|) / 2 + 6
     fast = !q.bad;
   }
   QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};

@@ -52,6 +52,7 @@ for _ in range(10):
     ctx.match_batch(batch, params=mp, refine=rp, outs=outs)
 torch.cuda.synchronize()
 k = {name: round(ctx.profile_get(name)[0] / 10, 4) for name in ("k_select", "k_prep", "k_match_refine")}
+k["exact_path_px_per_step"] = ctx.profile_get("refine_exact_px")[1] / 10
 pa = np.concatenate([o.pixel_a.cpu().numpy() for o in outs])
 va = np.concatenate([o.valid.cpu().numpy() for o in outs])
 if os.environ.get("PMX_SAVE"):  # outputs for a variant-vs-default comparison
