@@ -1587,10 +1587,12 @@ __device__ __forceinline__ void q_advance(QState& q, const Top2& t, int tgap, in
   q.best = t.score1();
 }
 
-// All levels of the warp's 32 pixels.  Level 0 runs per
-// lane (unrolled for the common shapes); a later level that only some lanes
-// need (their centre moved: BASELINE's second level) is evaluated by the whole
-// warp, one such pixel at a time, lanes spread over its window.
+// All levels of the warp's 32 pixels.  Interior first-level windows of the
+// common shapes run per lane, unrolled; every other window (border windows,
+// a later level that only some lanes need because their centre moved:
+// BASELINE's second level) is evaluated by the whole warp, one such pixel at
+// a time, lanes spread over its window - or per lane when more than 8 lanes
+// need one.
 template <class Tile>
 __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tgap, int Wa, int Ha,
                                               const RefineLevels& L, QState& q) {
@@ -1600,26 +1602,35 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
     const int s = L.stride[l], r = L.radius[l];
     const bool same = q.pr >= 0 && s == q.ps && r == q.pr && q.cu == q.pcu && q.cv == q.pcv;  // identical window
     const bool need = q.st == 0 && !same;
-    const unsigned m = __ballot_sync(0xffffffffu, need);
-    if (!m) continue;
-    if (l == 0 || __popc(m) > 8) {  // per lane
-      if (need) {
-        Top2 t;
-        const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
-                              q.cv + r * s < Ha;
-        if (interior && s == 1 && r == 3) {
+    if (!__any_sync(0xffffffffu, need)) continue;
+    // Interior first-level windows of the common shapes: unrolled, per lane.
+    const bool interior = q.pr < 0 && q.cu - r * s >= 0 && q.cu + r * s < Wa && q.cv - r * s >= 0 &&
+                          q.cv + r * s < Ha;
+    const bool fixed = need && interior && ((s == 1 && r == 3) || (s == 2 && r == 2));
+    if (__any_sync(0xffffffffu, fixed) && fixed) {
+      Top2 t;
+      if (s == 1) {
 #if PMX_PAIRLD
-          if (pair_aligned)
-            t = q_level1_pairs<3, Tile>(T, B, q.cu, q.cv);
-          else
+        if (pair_aligned)
+          t = q_level1_pairs<3, Tile>(T, B, q.cu, q.cv);
+        else
 #endif
-            t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
-        } else if (interior && s == 2 && r == 2) {
-          t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap);
-        } else {
-          if (q.best == INT_MIN) q.best = T.score(T.at(q.cu, q.cv), B);
-          t = q_level_lane(T, B, q.cu, q.cv, s, r, Wa, Ha, q.best, q.pcu, q.pcv, q.ps, q.pr);
-        }
+          t = q_level1<3, 1, Tile>(T, B, q.cu, q.cv, tgap);
+      } else {
+        t = q_level1<2, 2, Tile>(T, B, q.cu, q.cv, tgap);
+      }
+      q_advance(q, t, tgap, s, r);
+    }
+    // The rest - border windows, moved centres of later levels, uncommon
+    // shapes: per lane when many, else by the whole warp one pixel at a time
+    // (a warp with one border lane no longer runs the generic window loop
+    // for it while 31 lanes wait).
+    const unsigned m = __ballot_sync(0xffffffffu, need && !fixed);
+    if (!m) continue;
+    if (__popc(m) > 8) {  // per lane
+      if (need && !fixed) {
+        if (q.best == INT_MIN) q.best = T.score(T.at(q.cu, q.cv), B);
+        const Top2 t = q_level_lane(T, B, q.cu, q.cv, s, r, Wa, Ha, q.best, q.pcu, q.pcv, q.ps, q.pr);
         q_advance(q, t, tgap, s, r);
       }
     } else {  // warp-cooperative, one pending pixel at a time
@@ -1630,17 +1641,18 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         const int pcu = __shfl_sync(0xffffffffu, q.pcu, src), pcv = __shfl_sync(0xffffffffu, q.pcv, src);
         const int ps = __shfl_sync(0xffffffffu, q.ps, src), pr = __shfl_sync(0xffffffffu, q.pr, src);
         const int centre = __shfl_sync(0xffffffffu, q.best, src);
+        const bool have_centre = centre != INT_MIN;  // not yet scored on a first-level border window
         QB Bs;
 #pragma unroll
         for (int w = 0; w < 6; ++w) Bs.w[w] = __shfl_sync(0xffffffffu, B.w[w], src);
         Bs.nt = __shfl_sync(0xffffffffu, B.nt, src);
-        Top2 t{lane == 0 ? qkey(centre, lim0) : INT_MIN, INT_MIN};
+        Top2 t{lane == 0 && have_centre ? qkey(centre, lim0) : INT_MIN, INT_MIN};
         const int lim = pr * ps;
         for (int k = lane; k < nc; k += 32) {
           const int kv = r == 3 ? k / 7 : k / D;  // BASELINE's window: a constant divisor
           const int dv = kv - r, du = k - D * kv - r;
           const int u = cu + du * s, v = cv + dv * s;
-          if (u < 0 || u >= Wa || v < 0 || v >= Ha || (du == 0 && dv == 0)) continue;
+          if (u < 0 || u >= Wa || v < 0 || v >= Ha || (du == 0 && dv == 0 && have_centre)) continue;
           const int eu = u - pcu, ev = v - pcv;
           if (pr >= 0 && abs(eu) <= lim && abs(ev) <= lim && (ps == 1 || (eu % ps == 0 && ev % ps == 0))) continue;
           top2_add(t, qkey(T.score(T.at(u, v), Bs), k));
