@@ -1494,6 +1494,9 @@ __global__ void k_rel_poses(const DSim3* __restrict__ P, const int2* __restrict_
 // block_cost, tracking.cpp:134-147, with ray_cost64): the exact side of an
 // ambiguous accept decision (GNState::amb).  which = 0: the current poses
 // (skipped when their FP64 cost is already known), 1: the trial poses.
+#ifndef PMX_COST64_FAST
+#define PMX_COST64_FAST 1  // ray_cost64_fast (1-ulp rsqrt, shared reference norms); 0: PMX_COST64 below
+#endif
 #ifndef PMX_COST64
 #define PMX_COST64 ray_cost64_direct  // ray_cost64: the cancellation-free form (~2x the FP64 work)
 #endif
@@ -1545,6 +1548,8 @@ __global__ void __launch_bounds__(256, PMX_C64_BLOCKS) k_cost64_ray(EdgeArgs A, 
     const int4* __restrict__ M = A.packed + (size_t)e * A.seg;
     const int64_t cnt = A.pk_total[e];
     const double s2 = A.wp.sigma2, ld = A.wp.distance_weight, delta = A.wp.huber_delta;
+    const double inv_s2 = 1.0 / s2;
+    (void)inv_s2;
     const int64_t stride = (int64_t)A.bpe * blockDim.x;
     int64_t k = (int64_t)b * blockDim.x + threadIdx.x;
     // two-deep register pipeline: the record of match k + stride and the
@@ -1565,8 +1570,21 @@ __global__ void __launch_bounds__(256, PMX_C64_BLOCKS) k_cost64_ray(EdgeArgs A, 
         Pj = __ldg(Cj + m.y);
       }
       if (k + 2 * stride < cnt) mn = __ldg(M + k + 2 * stride);
-      const double info = 1.0 / (s2 / (double)__int_as_float(mc.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
       const double pi[3] = {Pic.x, Pic.y, Pic.z}, pj[3] = {Pjc.x, Pjc.y, Pjc.z};
+#if PMX_COST64_FAST
+      const double info = (double)__int_as_float(mc.z) * inv_s2;  // 1 / robust_weight (tracking.cpp:11, 64-66), ~1 ulp
+      if (Pic.w >= 1e-24f) {  // ref = i, src = j (swapped)
+        const Ref64 R = ref64(Pic.x, Pic.y, Pic.z);
+        ct += ray_cost64_fast(T[2], R, pj, info, ld, delta);
+        if (cur) cc += ray_cost64_fast(T[0], R, pj, info, ld, delta);
+      }
+      if (Pjc.w >= 1e-24f) {  // ref = j, src = i
+        const Ref64 R = ref64(Pjc.x, Pjc.y, Pjc.z);
+        ct += ray_cost64_fast(T[3], R, pi, info, ld, delta);
+        if (cur) cc += ray_cost64_fast(T[1], R, pi, info, ld, delta);
+      }
+#else
+      const double info = 1.0 / (s2 / (double)__int_as_float(mc.z));  // 1 / robust_weight (tracking.cpp:11, 64-66)
       if (Pic.w >= 1e-24f) {  // ref = i, src = j (swapped)
         ct += PMX_COST64(T[2], pi, pj, info, ld, delta);
         if (cur) cc += PMX_COST64(T[0], pi, pj, info, ld, delta);
@@ -1575,6 +1593,7 @@ __global__ void __launch_bounds__(256, PMX_C64_BLOCKS) k_cost64_ray(EdgeArgs A, 
         ct += PMX_COST64(T[3], pj, pi, info, ld, delta);
         if (cur) cc += PMX_COST64(T[1], pj, pi, info, ld, delta);
       }
+#endif
     }
   }
   ct = block_sum_fixed(ct);
