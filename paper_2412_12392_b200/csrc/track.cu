@@ -11,8 +11,9 @@
 //                   (its H/g are reused when the step is accepted, exactly as
 //                   the reference reuses blocks_new), a deterministic FP64
 //                   block/grid reduction, and the 7x7 pivoted LDL^T solve +
-//                   retract + accept test on block 0.  Nothing per-match is
-//                   written to HBM.
+//                   retract + accept test replicated in every block (one grid
+//                   barrier per iteration).  Nothing per-match is written to
+//                   HBM.
 //   K6 k_fuse       one thread per pixel, in place.
 #include <cooperative_groups.h>
 
@@ -153,7 +154,7 @@ struct TrackArgs {
 
 __device__ void load_sums(const double* __restrict__ partials, int nblocks, bool ray, double* H, double* g,
                           double* cost) {
-  // block 0, all threads: fixed-order sum (deterministic), columns x 8 row
+  // one block, all threads: fixed-order sum (deterministic), columns x 8 row
   // groups in parallel, then the groups in order; results into shared
   __shared__ double s[kAcc];
   __shared__ double grp[8][kAcc];
@@ -281,13 +282,23 @@ __device__ void ldlt7_solve_warp(const double* H, const double* mg, double* tau,
   __syncwarp();
 }
 
+// The loop state is replicated in every block (shared memory): after the
+// one grid barrier of an iteration every block sums the partials in the same
+// fixed order, solves the same 7x7 system and takes the same accept
+// decision, so the replicas stay bit-identical and the next residual pass
+// starts without a second barrier.  The partials alternate between two
+// buffers: a block can be at most one pass ahead of the slowest reader.
+// Block 0 publishes the state (pose, iterations, cost trace) to A.st.
 template <bool RAY>
 __global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double s_Hd[49], s_mg[7], s_tau[7], s_M[49], s_tmp[7];  // block 0's 7x7 solve
+  __shared__ double s_Hd[49], s_mg[7], s_tau[7], s_M[49], s_tmp[7];  // the 7x7 solve (warp 0)
   __shared__ int s_tr[7];
-  GNState* st = A.st;
+  __shared__ GNState L;  // this block's replica of the loop state
   const int nb = gridDim.x;
+  const size_t half = (size_t)nb * kAcc;
+  const bool pub = blockIdx.x == 0 && threadIdx.x == 0;  // publishes to A.st
+  if (threadIdx.x == 0) L = *A.st;  // initial pose (host-written)
   // valid_count (camera.cpp:10-14) for the lost test (tracking.cpp:165-168)
   {
     float acc[kAcc];
@@ -300,106 +311,110 @@ __global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
     block_reduce_to(acc, A.partials + (size_t)blockIdx.x * kAcc);
   }
   grid.sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (threadIdx.x == 0) {
     double c = 0.0;
     for (int b = 0; b < nb; ++b) c += A.partials[(size_t)b * kAcc + 36];
-    st->valid_count = (int64_t)c;
-    st->lost = c < (double)A.min_valid ? 1 : 0;
-    st->stop = st->lost;
-    st->q_min = A.q_min_fraction * (*A.median_dev);
-    st->lambda = 1e-8;
-    st->iterations = 0;
-    st->trace_len = 0;
+    L.valid_count = (int64_t)c;
+    L.lost = c < (double)A.min_valid ? 1 : 0;
+    L.stop = L.lost;
+    L.q_min = A.q_min_fraction * (*A.median_dev);
+    L.lambda = 1e-8;
+    L.iterations = 0;
+    L.trace_len = 0;
   }
-  grid.sync();
-  if (st->stop) return;
-  WeightsDev wp = A.wp;
-  wp.q_min = st->q_min;
-  constexpr bool ray = RAY;  // ray mode gets its own instance (register budget)
-  if (ray) {
-    eval_pass_ray(make_pose<double>(st->T), A.M, A.Xref, A.Xsrc, wp, A.partials);
-  } else {
-    const PoseR<float> T = make_pose<float>(st->T);
-    eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, A.partials);
-  }
-  grid.sync();
-  if (blockIdx.x == 0) {
-    double H[49], g[7], c;
-    load_sums(A.partials, nb, ray, H, g, &c);
-    if (threadIdx.x == 0) {
-      for (int i = 0; i < 49; ++i) st->H[i] = H[i];
-      for (int i = 0; i < 7; ++i) st->g[i] = g[i];
-      st->cost = c;
-      st->trace[st->trace_len++] = c;
-    }
-  }
-  grid.sync();
-  for (int it = 0; it < A.max_iterations; ++it) {
-    if (blockIdx.x == 0 && threadIdx.x < 32) {
-      // tracking.cpp:200-206 (the 7x7 pivoted LDLT on warp 0, bit-identical)
-      for (int i = threadIdx.x; i < 49; i += 32) s_Hd[i] = st->H[i];
-      __syncwarp();
-      if (threadIdx.x < 7) {
-        s_Hd[threadIdx.x * 8] += st->lambda * fmax(st->H[threadIdx.x * 8], 1e-12);
-        s_mg[threadIdx.x] = -st->g[threadIdx.x];
-      }
-      __syncwarp();
-      ldlt7_solve_warp(s_Hd, s_mg, s_tau, s_M, s_tmp, s_tr);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      st->iterations++;
-      double tau[7];
-      for (int k = 0; k < 7; ++k) tau[k] = s_tau[k];
-      bool fin = true;
-      double inf = 0.0;
-      for (int k = 0; k < 7; ++k) {
-        fin = fin && isfinite(tau[k]);
-        inf = fmax(inf, fabs(tau[k]));
-        st->tau[k] = tau[k];
-      }
-      if (fin && inf < 1e3) {
-        st->Ttrial = sim3_mul(sim3_exp(tau), st->T);  // left-plus retract, lie.hpp:54
-        st->trial_ok = 1;
-      } else {
-        st->trial_ok = 0;
-        st->lambda *= 10.0;
-        if (st->lambda > 1e8) st->stop = 1;
-      }
-    }
-    grid.sync();
-    if (st->stop) break;
-    if (!st->trial_ok) continue;
+  __syncthreads();
+  int buf = 1;  // the count above used buffer 0
+  if (!L.stop) {
+    WeightsDev wp = A.wp;
+    wp.q_min = L.q_min;
+    constexpr bool ray = RAY;  // ray mode gets its own instance (register budget)
+    double* part = A.partials + buf * half;
     if (ray) {
-      eval_pass_ray(make_pose<double>(st->Ttrial), A.M, A.Xref, A.Xsrc, wp, A.partials);
+      eval_pass_ray(make_pose<double>(L.T), A.M, A.Xref, A.Xsrc, wp, part);
     } else {
-      const PoseR<float> T = make_pose<float>(st->Ttrial);
-      eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, A.partials);
+      const PoseR<float> T = make_pose<float>(L.T);
+      eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part);
     }
     grid.sync();
-    if (blockIdx.x == 0) {
+    {
       double H[49], g[7], c;
-      load_sums(A.partials, nb, ray, H, g, &c);
+      load_sums(part, nb, ray, H, g, &c);
       if (threadIdx.x == 0) {
-        // tracking.cpp:210-223
-        if (c <= st->cost * (1.0 + 1e-12) + 1e-300) {
-          st->T = st->Ttrial;
-          for (int i = 0; i < 49; ++i) st->H[i] = H[i];
-          for (int i = 0; i < 7; ++i) st->g[i] = g[i];
-          st->cost = c;
-          if (st->trace_len < PMX_MAX_TRACE) st->trace[st->trace_len++] = c;
-          st->lambda = fmax(st->lambda * 0.3, 1e-10);
-          double n2 = 0.0;
-          for (int k = 0; k < 7; ++k) n2 += st->tau[k] * st->tau[k];
-          if (sqrt(n2) < A.update_tol) st->stop = 1;
+        for (int i = 0; i < 49; ++i) L.H[i] = H[i];
+        for (int i = 0; i < 7; ++i) L.g[i] = g[i];
+        L.cost = c;
+        L.trace[L.trace_len++] = c;
+      }
+      __syncthreads();
+    }
+    for (int it = 0; it < A.max_iterations; ++it) {
+      if (threadIdx.x < 32) {
+        // tracking.cpp:200-206 (the 7x7 pivoted LDLT on warp 0, bit-identical)
+        for (int i = threadIdx.x; i < 49; i += 32) s_Hd[i] = L.H[i];
+        __syncwarp();
+        if (threadIdx.x < 7) {
+          s_Hd[threadIdx.x * 8] += L.lambda * fmax(L.H[threadIdx.x * 8], 1e-12);
+          s_mg[threadIdx.x] = -L.g[threadIdx.x];
+        }
+        __syncwarp();
+        ldlt7_solve_warp(s_Hd, s_mg, s_tau, s_M, s_tmp, s_tr);
+      }
+      if (threadIdx.x == 0) {
+        L.iterations++;
+        double tau[7];
+        for (int k = 0; k < 7; ++k) tau[k] = s_tau[k];
+        bool fin = true;
+        double inf = 0.0;
+        for (int k = 0; k < 7; ++k) {
+          fin = fin && isfinite(tau[k]);
+          inf = fmax(inf, fabs(tau[k]));
+          L.tau[k] = tau[k];
+        }
+        if (fin && inf < 1e3) {
+          L.Ttrial = sim3_mul(sim3_exp(tau), L.T);  // left-plus retract, lie.hpp:54
+          L.trial_ok = 1;
         } else {
-          st->lambda *= 10.0;
-          if (st->lambda > 1e8) st->stop = 1;
+          L.trial_ok = 0;
+          L.lambda *= 10.0;
+          if (L.lambda > 1e8) L.stop = 1;
         }
       }
+      __syncthreads();
+      if (L.stop) break;
+      if (!L.trial_ok) continue;
+      buf ^= 1;
+      part = A.partials + buf * half;
+      if (ray) {
+        eval_pass_ray(make_pose<double>(L.Ttrial), A.M, A.Xref, A.Xsrc, wp, part);
+      } else {
+        const PoseR<float> T = make_pose<float>(L.Ttrial);
+        eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part);
+      }
+      grid.sync();
+      double H[49], g[7], c;
+      load_sums(part, nb, ray, H, g, &c);
+      if (threadIdx.x == 0) {
+        // tracking.cpp:210-223
+        if (c <= L.cost * (1.0 + 1e-12) + 1e-300) {
+          L.T = L.Ttrial;
+          for (int i = 0; i < 49; ++i) L.H[i] = H[i];
+          for (int i = 0; i < 7; ++i) L.g[i] = g[i];
+          L.cost = c;
+          if (L.trace_len < PMX_MAX_TRACE) L.trace[L.trace_len++] = c;
+          L.lambda = fmax(L.lambda * 0.3, 1e-10);
+          double n2 = 0.0;
+          for (int k = 0; k < 7; ++k) n2 += L.tau[k] * L.tau[k];
+          if (sqrt(n2) < A.update_tol) L.stop = 1;
+        } else {
+          L.lambda *= 10.0;
+          if (L.lambda > 1e8) L.stop = 1;
+        }
+      }
+      __syncthreads();
+      if (L.stop) break;
     }
-    grid.sync();
-    if (st->stop) break;
   }
+  if (pub) *A.st = L;
 }
 
 // ----------------------------------------------------------------- fusion
@@ -609,7 +624,7 @@ extern "C" int pmx_impl_track_given_matches(pmx_context* c, pmx_memory mem, cons
   A.median_dev = median.as<double>();
   const void* kern = mode == PMX_TRACK_RAY ? (const void*)k_track_gn<true> : (const void*)k_track_gn<false>;
   const int nb = grid_for(ctx, kern, 256);
-  DevBuf partials(sizeof(double) * kAcc * nb, ctx.stream), state(sizeof(GNState), ctx.stream);
+  DevBuf partials(2 * sizeof(double) * kAcc * nb, ctx.stream), state(sizeof(GNState), ctx.stream);  // two buffers
   GNState init_state;
   std::memset(&init_state, 0, sizeof(init_state));
   init_state.T = T0;
