@@ -448,11 +448,24 @@ __global__ void __launch_bounds__(256) k_sel_hist(const PairDev* __restrict__ pa
   const uint32_t prefix = P.sel->prefix;
   const int begin = blockIdx.x * px_per_block;
   const int end = min(HW, begin + px_per_block);
-  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
-    const uint32_t key = P.keys[i];
+  auto add = [&](uint32_t key) {
     const bool take = key != kNoKey && (PASS == 2 ? (key >> 20) == prefix : (key >> 8) == prefix);
     hist_add(sh, PASS == 2 ? (key >> 8) & 0xfff : key & 0xff, take);
+  };
+  int i0 = begin;
+  if ((reinterpret_cast<uintptr_t>(P.keys + begin) & 15) == 0) {  // 16-byte body
+    const int nv = (end - begin) >> 2;
+    const uint4* v = reinterpret_cast<const uint4*>(P.keys + begin);
+    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+      const uint4 k4 = v[j];
+      add(k4.x);
+      add(k4.y);
+      add(k4.z);
+      add(k4.w);
+    }
+    i0 = begin + 4 * nv;
   }
+  for (int i = i0 + threadIdx.x; i < end; i += blockDim.x) add(P.keys[i]);
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += blockDim.x)
     if (sh[i]) atomicAdd(&h[i], sh[i]);
@@ -475,11 +488,26 @@ __global__ void __launch_bounds__(256) k_sel_collect(const PairDev* __restrict__
   const int HW = P.Ha * P.Wa;
   const int begin = blockIdx.x * px_per_block;
   const int end = min(HW, begin + px_per_block);
-  for (int i = begin + threadIdx.x; i < end; i += blockDim.x) {
-    if (P.keys[i] != key) continue;
+  auto take = [&](uint32_t k, int i) {
+    if (k != key) return;
     const uint32_t slot = atomicAdd(&st->cnt, 1u);
     if (slot < (uint32_t)kSelCap) st->cand[slot] = norm64(P.xa, i);
+  };
+  int i0 = begin;
+  if ((reinterpret_cast<uintptr_t>(P.keys + begin) & 15) == 0) {  // 16-byte body
+    const int nv = (end - begin) >> 2;
+    const uint4* v = reinterpret_cast<const uint4*>(P.keys + begin);
+    for (int j = threadIdx.x; j < nv; j += blockDim.x) {
+      const uint4 k4 = v[j];
+      const int i = begin + 4 * j;
+      take(k4.x, i);
+      take(k4.y, i + 1);
+      take(k4.z, i + 2);
+      take(k4.w, i + 3);
+    }
+    i0 = begin + 4 * nv;
   }
+  for (int i = i0 + threadIdx.x; i < end; i += blockDim.x) take(P.keys[i], i);
 }
 
 // Exact median, step 2 (one block per pair): the krem-th smallest of the
@@ -1929,8 +1957,11 @@ static void check_pointmap(const pmx_pointmap& p) {
 // (keys / hist / sel set), enqueued on ctx.stream: one key pass and three
 // radix-select rounds over all pairs at once.
 // The three radix rounds after the keys and the first histogram level.
+#ifndef PMX_SEL_PPB
+#define PMX_SEL_PPB 16384  // keys per block of the histogram / collect passes (4096 measured slower)
+#endif
 static void select_rounds(Context& ctx, PairDev* dev_pairs, int n, int max_hwa, double fraction) {
-  const int ppb = 4096;
+  const int ppb = PMX_SEL_PPB;
   dim3 g1((max_hwa + ppb - 1) / ppb, n);
   k_sel_scan<1><<<n, 1024, 0, ctx.stream>>>(dev_pairs, fraction);
   launch_check(ctx, "k_sel_scan1");
