@@ -826,13 +826,14 @@ __device__ __forceinline__ void ldlt2_solve_f(float h00, float h01, float h11, f
     *x1 = 0.0f;
     return;
   }
-  const float i00 = 1.0f / m00;
+  // approximate reciprocals (MUFU, ~1 ulp): the step only steers the LM
+  const float i00 = __fdividef(1.0f, m00);
   const float m10 = h01 * i00;
   m11 -= m10 * (m00 * m10);
   float d0 = sw ? b1 : b0, d1 = sw ? b0 : b1;
   d1 -= m10 * d0;
   d0 = d0 * i00;
-  d1 = fabsf(m11) > 1.17549435e-38f ? d1 / m11 : 0.0f;
+  d1 = fabsf(m11) > 1.17549435e-38f ? __fdividef(d1, m11) : 0.0f;
   d0 -= m10 * d1;
   *x0 = sw ? d1 : d0;
   *x1 = sw ? d0 : d1;
