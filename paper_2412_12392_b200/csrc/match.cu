@@ -574,6 +574,24 @@ __global__ void __launch_bounds__(256) k_sel_exact(const PairDev* __restrict__ p
 }
 
 // ---------------------------------------------------------------- LM
+#ifndef PMX_LM_RSQRT
+#define PMX_LM_RSQRT 1  // the LM's ray normalisation: MUFU estimate + two Newton steps (~1 ulp) instead of rsqrt()
+#endif
+__device__ __forceinline__ double lm_rsqrt(double x) {
+#if PMX_LM_RSQRT
+  // x = |g|^2 of an interpolated unit-ray combination: within [1e-24, 1],
+  // far from the subnormal range ftz touches
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  return fma(0.5 * y, e, y);
+#else
+  return rsqrt(x);
+#endif
+}
+
 // One 256-bit load per support (LDG.E.ENL2.256 on sm_100: 32-byte aligned
 // double4 through the read-only path).
 __device__ __forceinline__ double4 ld_ray(const double4* __restrict__ rays, int i) {
@@ -627,7 +645,7 @@ __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, in
   const double gg = g0 * g0 + g1 * g1 + g2 * g2;
   const bool valid = I.c00.w != 0.0 && I.c10.w != 0.0 && I.c01.w != 0.0 && I.c11.w != 0.0;
   if (!valid || gg < 1e-24) return false;  // an invalid support / |g| < 1e-12
-  I.rs = rsqrt(gg);
+  I.rs = lm_rsqrt(gg);
   I.r0 = g0 * I.rs;
   I.r1 = g1 * I.rs;
   I.r2 = g2 * I.rs;
@@ -675,7 +693,7 @@ __device__ __forceinline__ bool interp_eval(const double4* __restrict__ rays, in
   const double g2 = w00 * I.c00.z + w10 * I.c10.z + w01 * I.c01.z + w11 * I.c11.z;
   const double gg = g0 * g0 + g1 * g1 + g2 * g2;
   if (!(gg >= 1e-24)) return false;  // an invalid support (NaN) / |g| < 1e-12
-  I.rs = rsqrt(gg);
+  I.rs = lm_rsqrt(gg);
   I.r0 = g0 * I.rs;
   I.r1 = g1 * I.rs;
   I.r2 = g2 * I.rs;
