@@ -910,6 +910,17 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
   res.iterations = 0;
   const double cu = fmin(fmax(pu0, 0.0), (double)(W - 1));
   const double cv = fmin(fmax(pv0, 0.0), (double)(H - 1));
+#if PMX_LM_RSQRT
+  // |x| < 1e-12 as |x|^2 < 1e-24, and x / |x| as x * rsqrt(|x|^2) (~1 ulp)
+  const double xx = x0 * x0 + x1 * x1 + x2 * x2;
+  if (xx < 1e-24 || !(isfinite(x0) && isfinite(x1) && isfinite(x2))) {
+    res.pu = cu;
+    res.pv = cv;
+    return res;
+  }
+  const double ixn = lm_rsqrt(xx);
+  const double t0 = x0 * ixn, t1 = x1 * ixn, t2 = x2 * ixn;
+#else
   const double xn = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
   if (xn < 1e-12 || !(isfinite(x0) && isfinite(x1) && isfinite(x2))) {
     res.pu = cu;
@@ -921,6 +932,7 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
   const double t0 = x0 * ixn, t1 = x1 * ixn, t2 = x2 * ixn;
 #else
   const double t0 = x0 / xn, t1 = x1 / xn, t2 = x2 / xn;
+#endif
 #endif
   double pu = cu, pv = cv;
 #if PMX_LM_F32 && PMX_EAGER_F32
@@ -1376,9 +1388,9 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
   int cu = 0, cv = 0;
   const bool vb = P.vb ? P.vb[n] != 0 : true;
   const double x0 = P.xb[3 * n], x1 = P.xb[3 * n + 1], x2 = P.xb[3 * n + 2];
-  // camera.cpp:217-219 (norm < 1e-12 skips; a NaN norm does not)
-  const double xnorm = sqrt(x0 * x0 + x1 * x1 + x2 * x2);
-  if (vb && !(xnorm < 1e-12)) {
+  // camera.cpp:217-219 (norm < 1e-12 skips; a NaN norm does not), as |x|^2 < 1e-24
+  const double xx = x0 * x0 + x1 * x1 + x2 * x2;
+  if (vb && !(xx < 1e-24)) {
     // seed = pixel n of the a-grid (camera.cpp:221), or the init match
     int su = u, sv = v;
     if (P.Wa != P.Wb) {
