@@ -10,5 +10,6 @@ import numpy as np
 a=np.load('/tmp/out_default.npz'); b=np.load('/tmp/out_$n.npz')
 both=(a['valid']==1)&(b['valid']==1); d=(a['pa']!=b['pa'])&both
 W=512; du=np.abs(a['pa'][d]%W-b['pa'][d]%W); dv=np.abs(a['pa'][d]//W-b['pa'][d]//W)
-print('$n vs default: valid mismatch', int((a['valid']!=b['valid']).sum()), 'index mismatch', int(d.sum()), 'of', int(both.sum()), 'worst px', int(max(du.max(initial=0), dv.max(initial=0))))"
+qd = (a['q'] != b['q']) & both & (a['pa'] == b['pa']) if 'q' in a and 'q' in b else np.zeros(1, bool)
+print('$n vs default: valid mismatch', int((a['valid']!=b['valid']).sum()), 'index mismatch', int(d.sum()), 'of', int(both.sum()), 'worst px', int(max(du.max(initial=0), dv.max(initial=0))), 'q differing', int(qd.sum()))"
 done

@@ -55,8 +55,9 @@ k = {name: round(ctx.profile_get(name)[0] / 10, 4) for name in ("k_select", "k_p
 k["exact_path_px_per_step"] = ctx.profile_get("refine_exact_px")[1] / 10
 pa = np.concatenate([o.pixel_a.cpu().numpy() for o in outs])
 va = np.concatenate([o.valid.cpu().numpy() for o in outs])
+qa = np.concatenate([o.confidence.cpu().numpy() for o in outs])
 if os.environ.get("PMX_SAVE"):  # outputs for a variant-vs-default comparison
-    np.savez(os.environ["PMX_SAVE"], pa=pa, valid=va)
+    np.savez(os.environ["PMX_SAVE"], pa=pa, valid=va, q=qa)
 print(json.dumps({"lib": os.environ.get("PMX_LIB", "default"), "ms_per_step": round(step, 4),
                   "gpx_s": round(n * H * W / step / 1e6, 3), "kernels": k,
                   "checksum": int(pa.astype(np.int64).sum())}), flush=True)
