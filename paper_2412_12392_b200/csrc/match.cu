@@ -72,6 +72,9 @@
 #ifndef PMX_J_SMEM
 #define PMX_J_SMEM 0  // LM fp32 Jacobian in shared memory instead of registers (spills 180 -> 172 B; neutral: 1.502 vs 1.495 ms)
 #endif
+#ifndef PMX_LM_NE_STATE
+#define PMX_LM_NE_STATE 1  // fp32 LM: carry J^T J, J^T r across iterations instead of J and the FP64 ray
+#endif
 #ifndef PMX_OVERLAP
 #define PMX_OVERLAP 0  // pairs per chunk of the overlapped device path (0: one chunk; 8 / 16 / 32 measured 7-17% slower)
 #endif
@@ -959,6 +962,66 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
     res.converged = true;
     return res;
   }
+#if PMX_LM_F32 && PMX_LM_NE_STATE
+  // Loop state: the iterate, its FP64 cost, lambda and the fp32 normal
+  // equations J^T J, J^T r of the current point - they only change when a
+  // step is accepted, so they are formed there once (same fp32 operations on
+  // the same values as forming them every iteration).  The FP64 ray is not
+  // kept: every decision on it is taken at acceptance.
+  (void)J;
+  float a00, a01, a11, g0, g1;
+  auto normal_eqs = [&](double e0, double e1, double e2) {
+    float Jf[6];
+    interp_jac_f(I, Jf);
+    const float fr0 = (float)e0, fr1 = (float)e1, fr2 = (float)e2;
+    a00 = fmaf(Jf[0], Jf[0], fmaf(Jf[1], Jf[1], Jf[2] * Jf[2]));
+    a01 = fmaf(Jf[0], Jf[3], fmaf(Jf[1], Jf[4], Jf[2] * Jf[5]));
+    a11 = fmaf(Jf[3], Jf[3], fmaf(Jf[4], Jf[4], Jf[5] * Jf[5]));
+    g0 = fmaf(Jf[0], fr0, fmaf(Jf[1], fr1, Jf[2] * fr2));
+    g1 = fmaf(Jf[3], fr0, fmaf(Jf[4], fr1, Jf[5] * fr2));
+  };
+  normal_eqs(r0, r1, r2);
+  double lambda = lp.lambda_init;
+  for (int it = 0; it < lp.max_iterations; ++it) {
+    ++res.iterations;
+    const float fl = (float)lambda;
+    const float h00 = fmaf(fl, fmaxf(a00, 1e-12f), a00);
+    const float h11 = fmaf(fl, fmaxf(a11, 1e-12f), a11);
+    float fs0, fs1;
+    ldlt2_solve_f(h00, a01, h11, g0, g1, &fs0, &fs1);
+    if (!isfinite(fs0) || !isfinite(fs1)) break;
+    const double d0 = -(double)fs0, d1 = -(double)fs1;
+    // clamp_to_image (camera.cpp:104-107); pu + d0 is finite here
+    const double xu = pu + d0, xv = pv + d1;
+    const double tu = xu < 0.0 ? 0.0 : (xu > (double)(W - 1) ? (double)(W - 1) : xu);
+    const double tv = xv < 0.0 ? 0.0 : (xv > (double)(H - 1) ? (double)(H - 1) : xv);
+    if (PMX_INTERP_EVAL(rays, W, H, tu, tv, I)) {
+      const double e0 = I.r0 - t0, e1 = I.r1 - t1, e2 = I.r2 - t2;
+      const double ct = e0 * e0 + e1 * e1 + e2 * e2;
+      if (ct < cost) {
+        pu = tu;
+        pv = tv;
+        cost = ct;
+        lambda *= lp.lambda_down;
+        if (I.r0 * t0 + I.r1 * t1 + I.r2 * t2 >= lp.cos_tol) {
+          res.pu = pu;
+          res.pv = pv;
+          res.converged = true;
+          return res;
+        }
+        normal_eqs(e0, e1, e2);
+        continue;
+      }
+    }
+    lambda *= lp.lambda_up;
+  }
+  res.pu = pu;
+  res.pv = pv;
+  // the current point failed the convergence test when it was accepted (or
+  // at the start): the reference's final test is false here
+  res.converged = false;
+  return res;
+#else
 #if PMX_LM_F32
   interp_jac_f(I, J);
 #else
@@ -1032,6 +1095,7 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
   res.pv = pv;
   res.converged = ray0 * t0 + ray1 * t1 + ray2 * t2 >= lp.cos_tol;
   return res;
+#endif
 #undef PMX_INTERP_EVAL
 }
 
