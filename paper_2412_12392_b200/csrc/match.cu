@@ -55,7 +55,7 @@
 #define PMX_PREFETCH 1  // the target descriptor row is prefetched into L2 before the LM
 #endif
 #ifndef PMX_EAGER_F32
-#define PMX_EAGER_F32 0  // fp32 LM: Jacobian support differences formed in interp_eval (corners die early; same spills, 1.500 -> 1.517 ms)
+#define PMX_EAGER_F32 1  // fp32 LM: Jacobian support differences formed in interp_eval, so the FP64 supports die there (with the normal-equation loop state: spills 156 -> 116 B, 1.425 -> 1.422 ms)
 #endif
 #ifndef PMX_RAY24
 #define PMX_RAY24 0  // LM gathers 24 B (x, y, z: 16 + 8 B loads) per support, NaN-marked invalid rays: 1.500 -> 1.551 ms
