@@ -63,6 +63,24 @@ if os.path.exists(rep):
     summ = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep, "k_match_refine"],
                           capture_output=True, text=True).stdout
     regions = os.path.join(ROOT, "tools", "match_regions.json")
+    # source regions of match.cu from its section markers (line numbers move)
+    src = open(os.path.join(ROOT, "paper_2412_12392_b200", "csrc", "match.cu")).read().splitlines()
+
+    def at(marker):
+        return next(i + 1 for i, l in enumerate(src) if l.startswith(marker))
+
+    lm0, rf0 = at("// ---------------------------------------------------------------- LM"), at("// ------------------------------------------------------------ refine (K4)")
+    mp0, qb0 = at("// ---------------------------------------------------------------- K3 + K4"), at("struct QB {")
+    ex0, kr0 = at("__device__ __noinline__ int refine_exact_path"), at("// K3 + K4 fused")
+    sa0 = at("// Standalone feature_refine")
+    q80, k10 = at("struct Q8 {"), at("// ---------------------------------------------------------------- K1")
+    json.dump({"LM (interpolation, step, accept)": [["match.cu", lm0, rf0 - 1], ["pmx_common.cuh", 1, 5000]],
+               "match_pixel (seed, lround, validity, outputs)": [["match.cu", mp0, qb0 - 1]],
+               "refinement: int8 window search": [["match.cu", qb0, ex0 - 1], ["sm_61_intrinsics.hpp", 1, 5000],
+                                                  ["sm_32_intrinsics.hpp", 1, 5000]],
+               "refinement: exact fallback path": [["match.cu", rf0, mp0 - 1], ["match.cu", ex0, kr0 - 1]],
+               "int8 quantisation of the target": [["match.cu", q80, k10 - 1]],
+               "kernel body": [["match.cu", kr0, sa0 - 1]]}, open(regions, "w"), indent=1)
     attrib = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_attrib.py"), rep, "k_match_refine",
                              regions], capture_output=True, text=True).stdout
     with open(os.path.join(PROF, "r02_ncu_match_full.txt"), "w") as f:
