@@ -357,3 +357,18 @@ class _nullctx:
 
     def __exit__(self, *a):
         return False
+
+
+@pytest.mark.parametrize("shapes", [[(37, 53)], [(9, 7), (2, 33), (1, 40)], [(37, 53), (31, 33), (9, 7)]])
+def test_odd_sizes_match_and_refine(ctx, shapes):
+    """Odd and tiny images (widths not multiples of the 32-pixel tile, odd
+    pixel counts so the int8 image slots sit at odd offsets, windows that
+    cross every border, a one-row image) through the fused batch kernel, in
+    one batch: same indices / validity as the reference restatement."""
+    pairs = [pmxgen.config0(seed=41 + i, height=h, width=w) for i, (h, w) in enumerate(shapes)]
+    params, rp = baseline_match_params(), abi.refine_params(BASELINE_REFINE)
+    gpu = ctx.match_batch([pmx_pair(p) for p in pairs], params=params, refine=rp)
+    for g, p in zip(gpu, pairs):
+        orc = pyoracle.feature_refine(pyoracle.match_pointmaps(p, params), p, rp)
+        st = compare_matches(g, orc, p["width"])
+        assert st["all_index_equal"] and st["valid_mismatch"] == 0, (p["height"], p["width"], st)
