@@ -1722,7 +1722,15 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
   const int lane = threadIdx.x & 31;
   const bool pair_aligned = ((uintptr_t)T.h & 15) == 0 && ((uintptr_t)T.t & 31) == 0;
   for (int l = 0; l < L.n; ++l) {
-    const int s = L.stride[l], r = L.radius[l];
+    // compile-time indices: the levels stay in the kernel's parameter bank
+    // (a dynamic index would copy them to local memory in every thread)
+    int s = L.stride[0], r = L.radius[0];
+#pragma unroll
+    for (int k = 1; k < PMX_MAX_REFINE_LEVELS; ++k)
+      if (l == k) {
+        s = L.stride[k];
+        r = L.radius[k];
+      }
     const bool same = q.pr >= 0 && s == q.ps && r == q.pr && q.cu == q.pcu && q.cv == q.pcv;  // identical window
     const bool need = q.st == 0 && !same;
     if (!__any_sync(0xffffffffu, need)) continue;
@@ -1795,7 +1803,7 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
 
 // Undecided pixels (near ties, unstageable tiles, no int8 image): the
 // per-thread exact refinement, kept out of line (rare).
-__device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, const RefineLevels& L) {
+__device__ __noinline__ int refine_exact_path(const PairDev& P, int pa, int n, const RefineLevels L) {
   return refine_dispatch(P, pa, n, L);
 }
 
