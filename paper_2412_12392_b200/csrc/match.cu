@@ -51,6 +51,9 @@
 #ifndef PMX_PAIRLD
 #define PMX_PAIRLD 0  // level-1 window rows as aligned pixel pairs (16-B heads, 32-B tails): identical outputs, 1.50 -> 1.61 ms
 #endif
+#ifndef PMX_SEL_DIRECT_ATOMICS
+#define PMX_SEL_DIRECT_ATOMICS 1  // median select passes 2-3: plain shared atomics instead of warp-aggregated ones
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 1  // the target descriptor row is prefetched into L2 before the LM
 #endif
@@ -453,7 +456,13 @@ __global__ void __launch_bounds__(256) k_sel_hist(const PairDev* __restrict__ pa
   const int end = min(HW, begin + px_per_block);
   auto add = [&](uint32_t key) {
     const bool take = key != kNoKey && (PASS == 2 ? (key >> 20) == prefix : (key >> 8) == prefix);
+#if PMX_SEL_DIRECT_ATOMICS
+    // the low bits of keys inside one bucket spread over the bins: plain
+    // shared-memory atomics (rarely conflicting) beat warp aggregation
+    if (take) atomicAdd(&sh[PASS == 2 ? (key >> 8) & 0xfff : key & 0xff], 1u);
+#else
     hist_add(sh, PASS == 2 ? (key >> 8) & 0xfff : key & 0xff, take);
+#endif
   };
   int i0 = begin;
   if ((reinterpret_cast<uintptr_t>(P.keys + begin) & 15) == 0) {  // 16-byte body
