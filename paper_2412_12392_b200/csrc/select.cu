@@ -42,7 +42,10 @@ __global__ void __launch_bounds__(256) k_hist(const SelSeg* __restrict__ segs, u
     const uint32_t k = fkey(v);
     const bool take = ok && v == v &&
                       (PASS == 1 || (PASS == 2 ? (k >> 20) == prefix : (k >> 8) == prefix));
-    hist_add(sh, PASS == 1 ? k >> 20 : PASS == 2 ? (k >> 8) & 0xfff : k & 0xff, take);
+    if (PASS == 1)  // the top bits of neighbouring values collide: warp-aggregated
+      hist_add(sh, k >> 20, take);
+    else if (take)  // the low bits inside one bucket spread: plain shared atomics
+      atomicAdd(&sh[PASS == 2 ? (k >> 8) & 0xfff : k & 0xff], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NB; i += blockDim.x)
