@@ -1485,15 +1485,19 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
     cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
     int pa = cv * P.Wa + cu;
     PMX_CHECK_INDEX(pa, P.Wa * P.Ha);
-    bool valid = pr.converged && (P.va ? P.va[pa] != 0 : true);
+    // every gather of pa issued at once (one round trip, not one per test)
+    const uint8_t vpa = P.va ? __ldg(P.va + pa) : (uint8_t)1;
+    const float a0f = __ldg(P.xa + 3 * pa), a1f = __ldg(P.xa + 3 * pa + 1), a2f = __ldg(P.xa + 3 * pa + 2);
+    const float qpa = __ldg(P.qa + pa), qn = __ldg(P.qb + n);
+    const double thr = P.sel->threshold;
+    bool valid = pr.converged && vpa != 0;
     if (valid) {
-      const double a0 = P.xa[3 * pa], a1 = P.xa[3 * pa + 1], a2 = P.xa[3 * pa + 2];
-      const double e0 = a0 - x0, e1 = a1 - x1, e2 = a2 - x2;
+      const double e0 = (double)a0f - x0, e1 = (double)a1f - x1, e2 = (double)a2f - x2;
       const double dist = sqrt(e0 * e0 + e1 * e1 + e2 * e2);
-      if (dist > P.sel->threshold) valid = false;
+      if (dist > thr) valid = false;
     }
     pa_out = pa;
-    q_out = (float)sqrt((double)P.qa[pa] * (double)P.qb[n]);
+    q_out = (float)sqrt((double)qpa * (double)qn);
     valid_out = valid ? 1 : 0;
   }
   P.out_pa[n] = pa_out;
