@@ -54,6 +54,9 @@
 #ifndef PMX_SEL_DIRECT_ATOMICS
 #define PMX_SEL_DIRECT_ATOMICS 1  // median select passes 2-3: plain shared atomics instead of warp-aggregated ones
 #endif
+#ifndef PMX_ROW_WITH_GATHERS
+#define PMX_ROW_WITH_GATHERS 1  // the refinement's target row loaded with the LM result's gathers
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 1  // the target descriptor row is prefetched into L2 before the LM
 #endif
@@ -1452,8 +1455,17 @@ __device__ __forceinline__ int refine_dispatch(const PairDev& P, int pa, int pb,
 // lround + clamp, validity, q.  Writes the outputs; returns (pa, valid).
 // (u, v): the b-pixel's column / row (n = v W_b + u).  Returns {pixel_a,
 // valid, column, row of pixel_a} (pixel_a = -1: skipped pixel).
-template <class JT = JReg>
-__device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp, int n, int u, int v, JT J = JT()) {
+// Post-LM loads of the refinement (PMX_ROW_WITH_GATHERS): the target
+// descriptor row and the pair's int8 statistics, fetched with the pixel_a
+// gathers (one round trip).
+struct RowLoads {
+  uint4 d0, d1, d2;
+  int qbad, a1max;
+};
+
+template <class JT = JReg, bool ROW = false>
+__device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp, int n, int u, int v, JT J = JT(),
+                                            RowLoads* rl = nullptr) {
   if (P.out_pb) P.out_pb[n] = n;
   int32_t pa_out = -1;
   float q_out = 0.0f;
@@ -1490,6 +1502,14 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
     const float a0f = __ldg(P.xa + 3 * pa), a1f = __ldg(P.xa + 3 * pa + 1), a2f = __ldg(P.xa + 3 * pa + 2);
     const float qpa = __ldg(P.qa + pa), qn = __ldg(P.qb + n);
     const double thr = P.sel->threshold;
+    if (ROW) {
+      const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
+      rl->d0 = __ldg(row);
+      rl->d1 = __ldg(row + 1);
+      rl->d2 = __ldg(row + 2);
+      rl->qbad = __ldg(&P.sel->qbad);
+      rl->a1max = __ldg(&P.sel->a1max);
+    }
     bool valid = pr.converged && vpa != 0;
     if (valid) {
       const double e0 = (double)a0f - x0, e1 = (double)a1f - x1, e2 = (double)a2f - x2;
@@ -1838,6 +1858,10 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
   const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * PMX_MR_TY + (threadIdx.x >> 5);
   const int m = v * P.Wb + u;
   int n = -1, pa = 0, pcu = 0, pcv = 0;
+#if PMX_ROW_WITH_GATHERS
+  RowLoads rl{};
+  rl.qbad = 1;  // pixels outside the image: no fast path
+#endif
 #if PMX_PREFETCH
   // the descriptor row quantized after the LM: its HBM latency overlaps the LM
   if (u < P.Wb && v < P.Hb && P.q8h != nullptr)
@@ -1847,6 +1871,8 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
 #if PMX_J_SMEM && PMX_LM_F32
     __shared__ float sJ[6 * 32 * PMX_MR_TY];
     const int4 r = match_pixel(P, lp, m, u, v, JSm<32 * PMX_MR_TY>{sJ + threadIdx.x});
+#elif PMX_ROW_WITH_GATHERS
+    const int4 r = match_pixel<JReg, true>(P, lp, m, u, v, JReg(), &rl);
 #else
     const int4 r = match_pixel(P, lp, m, u, v);
 #endif
@@ -1855,13 +1881,21 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
     pcv = r.w;
     if (r.y) n = m;
   }
+#if PMX_ROW_WITH_GATHERS
+  const bool fast_pair = P.q8h != nullptr && rl.qbad == 0;
+#else
   const bool fast_pair = P.q8h != nullptr && P.sel->qbad == 0;
+#endif
   QB B;
   int tgap = 0;
   bool fast = n >= 0 && fast_pair;
   if (fast) {
+#if PMX_ROW_WITH_GATHERS
+    const Q8 q = quantize24(rl.d0, rl.d1, rl.d2);
+#else
     const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
     const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
+#endif
     B.w[0] = q.a.x;
     B.w[1] = q.a.y;
     B.w[2] = q.a.z;
@@ -1869,7 +1903,11 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
     B.w[4] = q.b.x;
     B.w[5] = q.b.y;
     B.nt = q.nt;
+#if PMX_ROW_WITH_GATHERS
+    tgap = rl.a1max + q.l1 + 12;  // 2E, E = (sum|q8(a)| + sum|q8(b)|) / 2 + 6
+#else
     tgap = P.sel->a1max + q.l1 + 12;  // 2E, E = (sum|q8(a)| + sum|q8(b)|) / 2 + 6
+#endif
     fast = !q.bad;
   }
   QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
