@@ -58,7 +58,7 @@
 #define PMX_ROW_WITH_GATHERS 1  // the refinement's target row loaded with the LM result's gathers
 #endif
 #ifndef PMX_PREFETCH
-#define PMX_PREFETCH 1  // the target descriptor row is prefetched into L2 before the LM
+#define PMX_PREFETCH 0  // L2 prefetch of the target descriptor row before the LM (neutral at first; with the row loaded among the post-LM gathers, 1.296 -> 1.306 ms)
 #endif
 #ifndef PMX_EAGER_F32
 #define PMX_EAGER_F32 1  // fp32 LM: Jacobian support differences formed in interp_eval, so the FP64 supports die there (with the normal-equation loop state: spills 156 -> 116 B, 1.425 -> 1.422 ms)
