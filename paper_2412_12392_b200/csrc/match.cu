@@ -57,6 +57,9 @@
 #ifndef PMX_ROW_WITH_GATHERS
 #define PMX_ROW_WITH_GATHERS 1  // the refinement's target row loaded with the LM result's gathers
 #endif
+#ifndef PMX_PRELOAD_SEED
+#define PMX_PRELOAD_SEED 0  // the identity seed's supports loaded together with X_b (spills 112 -> 128 B: 1.297 -> 1.377 ms)
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 0  // L2 prefetch of the target descriptor row before the LM (neutral at first; with the row loaded among the post-LM gathers, 1.296 -> 1.306 ms)
 #endif
@@ -797,9 +800,14 @@ struct InterpF {
   float du[3], dv[3];
 };
 
-__device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, int W, int H, double u, double v,
-                                              InterpF& I) {
-  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+// The four supports of an interpolation and the fractional offsets.
+struct Corners {
+  double4 c00, c10, c01, c11;
+  double fu, fv;
+};
+
+__device__ __forceinline__ void corners_load(const double4* __restrict__ rays, int W, int H, double u, double v,
+                                             Corners& C) {
   int u0 = (int)floor(u);
   int v0 = (int)floor(v);
   u0 = min(u0, W - 2 >= 0 ? W - 2 : 0);
@@ -808,8 +816,17 @@ __device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, 
   int base = v0 * W + u0;
   PMX_CHECK_INDEX(base, W * H - dv - du);
   const double4* p = rays + base;
-  const double fu = u - u0, fv = v - v0;
-  const double4 c00 = ld_ray(p, 0), c10 = ld_ray(p, du), c01 = ld_ray(p, dv), c11 = ld_ray(p, dv + du);
+  C.fu = u - u0;
+  C.fv = v - v0;
+  C.c00 = ld_ray(p, 0);
+  C.c10 = ld_ray(p, du);
+  C.c01 = ld_ray(p, dv);
+  C.c11 = ld_ray(p, dv + du);
+}
+
+__device__ __forceinline__ bool interp_math_f(const Corners& C, InterpF& I) {
+  const double4 &c00 = C.c00, &c10 = C.c10, &c01 = C.c01, &c11 = C.c11;
+  const double fu = C.fu, fv = C.fv;
   const double w00 = (1 - fu) * (1 - fv), w10 = fu * (1 - fv), w01 = (1 - fu) * fv, w11 = fu * fv;
   const double g0 = w00 * c00.x + w10 * c10.x + w01 * c01.x + w11 * c11.x;
   const double g1 = w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y;
@@ -834,6 +851,14 @@ __device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, 
   I.dv[1] = fmaf(ffu, e1 - d1, d1);
   I.dv[2] = fmaf(ffu, e2 - d2, d2);
   return true;
+}
+
+__device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, int W, int H, double u, double v,
+                                              InterpF& I) {
+  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+  Corners C;
+  corners_load(rays, W, H, u, v, C);
+  return interp_math_f(C, I);
 }
 
 template <class JT>
@@ -919,7 +944,8 @@ struct ProjOut {
 template <class JT = JReg>
 __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W, int H, double x0,
                                                          double x1, double x2, double pu0, double pv0,
-                                                         const LMParams& lp, JT J = JT()) {
+                                                         const LMParams& lp, JT J = JT(),
+                                                         const Corners* pre = nullptr) {
   ProjOut res;
   res.converged = false;
   res.iterations = 0;
@@ -960,7 +986,14 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
   Interp I;
 #define PMX_INTERP_EVAL interp_eval
 #endif
-  if (!PMX_INTERP_EVAL(rays, W, H, pu, pv, I)) {
+#if PMX_LM_F32 && PMX_EAGER_F32
+  // pre: the seed's supports, loaded by the caller with its own inputs
+  const bool first_ok = pre ? interp_math_f(*pre, I) : PMX_INTERP_EVAL(rays, W, H, pu, pv, I);
+#else
+  (void)pre;
+  const bool first_ok = PMX_INTERP_EVAL(rays, W, H, pu, pv, I);
+#endif
+  if (!first_ok) {
     res.pu = pu;
     res.pv = pv;
     return res;
@@ -1471,6 +1504,13 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
   float q_out = 0.0f;
   uint8_t valid_out = 0;
   int cu = 0, cv = 0;
+#if PMX_PRELOAD_SEED && PMX_LM_F32 && PMX_EAGER_F32
+  // identity seed (camera.cpp:221): its ray-map supports are loaded together
+  // with X_b instead of after it (same indices / values as the LM's own load)
+  Corners pre;
+  const bool have_pre = !P.seed_last && P.Wa == P.Wb && P.Ha >= 1;
+  if (have_pre) corners_load(P.rays, P.Wa, P.Ha, (double)u, (double)min(v, P.Ha - 1), pre);
+#endif
   const bool vb = P.vb ? P.vb[n] != 0 : true;
   const double x0 = P.xb[3 * n], x1 = P.xb[3 * n + 1], x2 = P.xb[3 * n + 2];
   // camera.cpp:217-219 (norm < 1e-12 skips; a NaN norm does not), as |x|^2 < 1e-24
@@ -1492,7 +1532,12 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
         }
       }
     }
+#if PMX_PRELOAD_SEED && PMX_LM_F32 && PMX_EAGER_F32
+    const ProjOut pr =
+        iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp, J, have_pre ? &pre : nullptr);
+#else
     const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp, J);
+#endif
     cu = min(max((int)round(pr.pu), 0), P.Wa - 1);  // std::lround: half away from zero
     cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
     int pa = cv * P.Wa + cu;
