@@ -855,7 +855,9 @@ __device__ __forceinline__ bool interp_math_f(const Corners& C, InterpF& I) {
 
 __device__ __forceinline__ bool interp_eval_f(const double4* __restrict__ rays, int W, int H, double u, double v,
                                               InterpF& I) {
-  if (u < 0.0 || v < 0.0 || u > (double)(W - 1) || v > (double)(H - 1)) return false;
+  // the LM only evaluates clamped points (the seed and clamp_to_image's
+  // trials, camera.cpp:104-107, 124-125): the range test of interpolate_ray
+  // always passes there and is not repeated (the API entry keeps it)
   Corners C;
   corners_load(rays, W, H, u, v, C);
   return interp_math_f(C, I);
