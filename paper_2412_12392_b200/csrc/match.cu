@@ -834,7 +834,7 @@ __device__ __forceinline__ bool interp_math_f(const Corners& C, InterpF& I) {
   const double gg = g0 * g0 + g1 * g1 + g2 * g2;
   const bool valid = c00.w != 0.0 && c10.w != 0.0 && c01.w != 0.0 && c11.w != 0.0;
   if (!valid || gg < 1e-24) return false;
-  const double rs = rsqrt(gg);
+  const double rs = lm_rsqrt(gg);
   I.r0 = g0 * rs;
   I.r1 = g1 * rs;
   I.r2 = g2 * rs;
