@@ -942,8 +942,10 @@ struct ProjOut {
   int iterations;
 };
 
-// iterative_project, camera.cpp:115-174
-template <class JT = JReg>
+// iterative_project, camera.cpp:115-174.  SEED_CLAMPED: the caller passes an
+// integer seed already clamped into the image (the matcher's pixel seeds), so
+// the FP64 clamp of camera.cpp:124-125 is the identity and is skipped.
+template <class JT = JReg, bool SEED_CLAMPED = false>
 __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restrict__ rays, int W, int H, double x0,
                                                          double x1, double x2, double pu0, double pv0,
                                                          const LMParams& lp, JT J = JT(),
@@ -951,8 +953,8 @@ __device__ __forceinline__ ProjOut iterative_project_dev(const double4* __restri
   ProjOut res;
   res.converged = false;
   res.iterations = 0;
-  const double cu = fmin(fmax(pu0, 0.0), (double)(W - 1));
-  const double cv = fmin(fmax(pv0, 0.0), (double)(H - 1));
+  const double cu = SEED_CLAMPED ? pu0 : fmin(fmax(pu0, 0.0), (double)(W - 1));
+  const double cv = SEED_CLAMPED ? pv0 : fmin(fmax(pv0, 0.0), (double)(H - 1));
 #if PMX_LM_RSQRT
   // |x| < 1e-12 as |x|^2 < 1e-24, and x / |x| as x * rsqrt(|x|^2) (~1 ulp)
   const double xx = x0 * x0 + x1 * x1 + x2 * x2;
@@ -1538,7 +1540,10 @@ __device__ __forceinline__ int4 match_pixel(const PairDev& P, const LMParams& lp
     const ProjOut pr =
         iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp, J, have_pre ? &pre : nullptr);
 #else
-    const ProjOut pr = iterative_project_dev(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)su, (double)sv, lp, J);
+    // the seed clamped in integers (camera.cpp:124-125 on an integer seed)
+    const int csu = min(max(su, 0), P.Wa - 1), csv = min(max(sv, 0), P.Ha - 1);
+    const ProjOut pr =
+        iterative_project_dev<JT, true>(P.rays, P.Wa, P.Ha, x0, x1, x2, (double)csu, (double)csv, lp, J);
 #endif
     cu = min(max((int)round(pr.pu), 0), P.Wa - 1);  // std::lround: half away from zero
     cv = min(max((int)round(pr.pv), 0), P.Ha - 1);
