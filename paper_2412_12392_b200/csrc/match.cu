@@ -264,6 +264,7 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
   l1 = __dp4a((int)__vabsss4(q.a.w), kOnes, l1);
   l1 = __dp4a((int)__vabsss4(q.b.x), kOnes, l1);
   q.l1 = __dp4a((int)__vabsss4(q.b.y), kOnes, l1);
+#if PMX_PRUNE  // the tail bound only feeds the pruned form
   int l2t = __dp4a((int)q.a.z, (int)q.a.z, 0);
   l2t = __dp4a((int)q.a.w, (int)q.a.w, l2t);
   l2t = __dp4a((int)q.b.x, (int)q.b.x, l2t);
@@ -271,6 +272,9 @@ __device__ __forceinline__ Q8 quantize24(const uint4 d0, const uint4 d1, const u
   int nt = (int)ceilf(sqrtf((float)l2t));  // exact integer ceil(sqrt): l2t < 2^24
   if (nt * nt < l2t) ++nt;
   q.nt = nt;
+#else
+  q.nt = 0;
+#endif
   return q;
 }
 
@@ -1861,7 +1865,11 @@ __device__ __forceinline__ void q_refine_warp(const Tile& T, const QB& B, int tg
         QB Bs;
 #pragma unroll
         for (int w = 0; w < 6; ++w) Bs.w[w] = __shfl_sync(0xffffffffu, B.w[w], src);
+#if PMX_PRUNE
         Bs.nt = __shfl_sync(0xffffffffu, B.nt, src);
+#else
+        Bs.nt = 0;
+#endif
         Top2 t{lane == 0 && have_centre ? qkey(centre, lim0) : INT_MIN, INT_MIN};
         const int lim = pr * ps;
         for (int k = lane; k < nc; k += 32) {
