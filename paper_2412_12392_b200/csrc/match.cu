@@ -60,6 +60,9 @@
 #ifndef PMX_PRELOAD_SEED
 #define PMX_PRELOAD_SEED 0  // the identity seed's supports loaded together with X_b (spills 112 -> 128 B: 1.297 -> 1.377 ms)
 #endif
+#ifndef PMX_VALID_BITS
+#define PMX_VALID_BITS 1  // support validity from the high words of the ray map's w (1.0 / 0.0)
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 0  // L2 prefetch of the target descriptor row before the LM (neutral at first; with the row loaded among the post-LM gathers, 1.296 -> 1.306 ms)
 #endif
@@ -836,7 +839,13 @@ __device__ __forceinline__ bool interp_math_f(const Corners& C, InterpF& I) {
   const double g1 = w00 * c00.y + w10 * c10.y + w01 * c01.y + w11 * c11.y;
   const double g2 = w00 * c00.z + w10 * c10.z + w01 * c01.z + w11 * c11.z;
   const double gg = g0 * g0 + g1 * g1 + g2 * g2;
+#if PMX_VALID_BITS
+  // w is exactly 1.0 (valid) or 0.0 (k_prep): all four valid iff the AND of
+  // their high words (0x3ff00000 or 0) is non-zero - integer ops, not DSETPs
+  const bool valid = (__double2hiint(c00.w) & __double2hiint(c10.w) & __double2hiint(c01.w) & __double2hiint(c11.w)) != 0;
+#else
   const bool valid = c00.w != 0.0 && c10.w != 0.0 && c01.w != 0.0 && c11.w != 0.0;
+#endif
   if (!valid || gg < 1e-24) return false;
   const double rs = lm_rsqrt(gg);
   I.r0 = g0 * rs;
