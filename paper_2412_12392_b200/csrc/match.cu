@@ -63,6 +63,9 @@
 #ifndef PMX_VALID_BITS
 #define PMX_VALID_BITS 1  // support validity from the high words of the ray map's w (1.0 / 0.0)
 #endif
+#ifndef PMX_JDIFF_F32
+#define PMX_JDIFF_F32 0  // Jacobian support differences from fp32-rounded supports (1.252 -> 1.245 ms; valid matches identical, a few invalid pixels' pixel_a differ)
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 0  // L2 prefetch of the target descriptor row before the LM (neutral at first; with the row loaded among the post-LM gathers, 1.296 -> 1.306 ms)
 #endif
@@ -853,10 +856,22 @@ __device__ __forceinline__ bool interp_math_f(const Corners& C, InterpF& I) {
   I.r2 = g2 * rs;
   I.rs = (float)rs;
   const float ffu = (float)fu, ffv = (float)fv;
+#if PMX_JDIFF_F32
+  // differences of the fp32-rounded supports (steering only; ~2e-5 relative)
+  const float x00 = (float)c00.x, y00 = (float)c00.y, z00 = (float)c00.z;
+  const float x10 = (float)c10.x, y10 = (float)c10.y, z10 = (float)c10.z;
+  const float x01 = (float)c01.x, y01 = (float)c01.y, z01 = (float)c01.z;
+  const float x11 = (float)c11.x, y11 = (float)c11.y, z11 = (float)c11.z;
+  const float a0 = x10 - x00, a1 = y10 - y00, a2 = z10 - z00;
+  const float b0 = x11 - x01, b1 = y11 - y01, b2 = z11 - z01;
+  const float d0 = x01 - x00, d1 = y01 - y00, d2 = z01 - z00;
+  const float e0 = x11 - x10, e1 = y11 - y10, e2 = z11 - z10;
+#else
   const float a0 = (float)(c10.x - c00.x), a1 = (float)(c10.y - c00.y), a2 = (float)(c10.z - c00.z);
   const float b0 = (float)(c11.x - c01.x), b1 = (float)(c11.y - c01.y), b2 = (float)(c11.z - c01.z);
   const float d0 = (float)(c01.x - c00.x), d1 = (float)(c01.y - c00.y), d2 = (float)(c01.z - c00.z);
   const float e0 = (float)(c11.x - c10.x), e1 = (float)(c11.y - c10.y), e2 = (float)(c11.z - c10.z);
+#endif
   I.du[0] = fmaf(ffv, b0 - a0, a0);
   I.du[1] = fmaf(ffv, b1 - a1, a1);
   I.du[2] = fmaf(ffv, b2 - a2, a2);
