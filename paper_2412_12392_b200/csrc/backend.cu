@@ -337,7 +337,10 @@ constexpr int kEdgeSmem = (6 * 256 + 8 * 256) * 16;  // cp.async stages of k_edg
 static_assert(kEdgeSmem >= block_reduce_scratch_bytes<2 * kRayAcc>(), "reduction scratch aliases the stages");
 
 // Both directed constraints of an edge from one read of its compacted matches.
-__global__ void __launch_bounds__(256, 2) k_edge_terms_ray(EdgeArgs A, int e0) {
+#ifndef PMX_EDGE_BLOCKS
+#define PMX_EDGE_BLOCKS 2  // resident CTAs per SM of the edge pass (128 registers; 3 at 80 registers spills 544 B: 10.7 -> 19.2 ms per config-4 pass)
+#endif
+__global__ void __launch_bounds__(256, PMX_EDGE_BLOCKS) k_edge_terms_ray(EdgeArgs A, int e0) {
   if (gn_stopped(A.st)) return;
   extern __shared__ int4 edge_sm[];
   const int e = e0 + blockIdx.y;
