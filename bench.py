@@ -522,6 +522,58 @@ def bench_tracking(ctx, dev):
                                 "alg_bytes_per_px": 48}}
 
 
+def bench_single_pair(ctx, dev, cpu: bool):
+    """BASELINE config 0: one 512x384 pair, match + refine (what the CPU
+    reference runs per edge): device-resident ms, host-buffer ms through the
+    C ABI, and the reference build on one pinned core."""
+    import torch
+    import pmxgen
+    from paper_2412_12392_b200 import FeatureMap, MatchSet, Pointmap
+    pair = pmxgen.config0(seed=0)
+    mp, rp = match_params()
+    Tt = lambda x: torch.from_numpy(np.ascontiguousarray(x.view(np.int16) if x.dtype == np.uint16 else x)).to(dev)
+    dp = (Pointmap(Tt(pair["X_a"]), Tt(pair["valid_a"]), H, W), Pointmap(Tt(pair["X_b"]), Tt(pair["valid_b"]), H, W),
+          FeatureMap(Tt(pair["D_a"]), Tt(pair["Q_a"]), H, W), FeatureMap(Tt(pair["D_b"]), Tt(pair["Q_b"]), H, W))
+    outs = [MatchSet.empty(H * W, dev)]
+    batch = ctx.prepare_match_batch([dp], outs)
+    for _ in range(5):
+        ctx.match_batch(batch, params=mp, refine=rp)
+    stream = torch.cuda.current_stream()
+    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    for _ in range(20):
+        ctx.match_batch(batch, params=mp, refine=rp)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    dev_ms = ev[0].elapsed_time(ev[1]) / 20
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()  # noqa: E731
+    hp = (Pointmap(pin(pair["X_a"]), pin(pair["valid_a"]), H, W), Pointmap(pin(pair["X_b"]), pin(pair["valid_b"]), H, W),
+          FeatureMap(pin(pair["D_a"]), pin(pair["Q_a"]), H, W), FeatureMap(pin(pair["D_b"]), pin(pair["Q_b"]), H, W))
+    houts = [MatchSet(pin(np.zeros(H * W, np.int32)), pin(np.zeros(H * W, np.float32)), pin(np.zeros(H * W, np.uint8)))]
+    hbatch = ctx.prepare_match_batch([hp], houts)
+    ctx.match_batch(hbatch, params=mp, refine=rp)
+    e2e = []
+    for _ in range(10):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.match_batch(hbatch, params=mp, refine=rp)
+        e2e.append((time.perf_counter() - t0) * 1e3)
+    line = {"metric": "single-pair match + refine ms (config 0)", "value": dev_ms, "unit": "ms",
+            "higher_is_better": False,
+            "config": {"workload": "config0: one 512x384 pair, 24-d fp16, LM 10 it, refine {(1,3),(1,3)}",
+                       "valid_fraction": float(outs[0].valid.float().mean().item())},
+            "e2e_ms": min(e2e),
+            "context": "the paper's own CUDA matcher: 2 ms per frame on an RTX 4090 (BASELINE.md, context only)"}
+    if cpu:
+        ctxm, kind = _ref_ctx()
+        with pinned_core():
+            s = min(cpu_sample([pair], threads=1) for _ in range(2))
+        line["cpu_baseline"] = {"value": s * 1e3, "unit": "ms", "cores": 1, "kind": kind,
+                                "sample": "the same pair, match_pointmaps + feature_refine, one pinned core"}
+    return line
+
+
 def run_pmx(args):
     import torch
     import pmxgen
@@ -732,7 +784,8 @@ def run_pmx(args):
             line["secondary"] = [sharded]
         if world == 1 and not args.no_secondary:
             line["secondary"] = ([sharded] if sharded is not None else []) + \
-                [bench_backend(ctx, dev, cpu=not args.no_cpu), bench_tracking(ctx, dev)]
+                [bench_single_pair(ctx, dev, cpu=not args.no_cpu), bench_backend(ctx, dev, cpu=not args.no_cpu),
+                 bench_tracking(ctx, dev)]
             torch.cuda.empty_cache()
             line["secondary"].append(bench_backend(ctx, dev, cpu=not args.no_cpu, n_kf=1000, reach=5, loops=3,
                                                    iters=5, config="config4"))
