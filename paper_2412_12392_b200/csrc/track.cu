@@ -47,18 +47,23 @@ __device__ void eval_pass(const PoseR<float>& T, const MatchesDev& M, const Clou
 // Ray mode (the tracking configuration): closed-form sums with the cancelling
 // parts of the residual in FP64 (residual.cuh ray_accumulate) -> kRayAcc
 // partials per block (stride kAcc).  Same skips as eval_match.
+// with_count: the pass also counts the valid flags of all matches (the lost
+// test's valid_count, camera.cpp:10-14) into slot kAcc - 1 of the partials.
 __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const CloudDev& Xref,
-                              const CloudDev& Xsrc, const WeightsDev& wp, double* __restrict__ partials) {
+                              const CloudDev& Xsrc, const WeightsDev& wp, double* __restrict__ partials,
+                              bool with_count = false) {
   float acc[kRayAcc];
 #pragma unroll
   for (int i = 0; i < kRayAcc; ++i) acc[i] = 0.0f;
   const RayW c{(float)wp.huber_delta, (float)(wp.huber_delta * wp.huber_delta), (float)wp.distance_weight};
   double cost64 = 0.0;
+  int nvalid = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M.count; k += stride) {
     const int pa = M.pa ? __ldg(M.pa + k) : (int)k;
     const int pb = M.pb ? __ldg(M.pb + k) : (int)k;
     const bool mv = M.valid ? __ldg(M.valid + k) != 0 : true;
+    nvalid += mv ? 1 : 0;
     if (!mv || pa < 0 || pb < 0 || pb >= Xref.H * Xref.W || pa >= Xsrc.H * Xsrc.W) continue;
     float rf[3], sf[3];
     if (!load_point(Xref, pb, rf) || !load_point(Xsrc, pa, sf)) continue;
@@ -75,13 +80,23 @@ __device__ void eval_pass_ray(const PoseR<double>& T, const MatchesDev& M, const
   block_reduce_n<kRayAcc>(acc, partials + (size_t)blockIdx.x * kAcc);
   // the cost slot takes the FP64 sum (deterministic: warp sums in lane order, warps in order)
   __shared__ double wc[32];
+  __shared__ int wn[32];
   cost64 = warp_sum(cost64);
-  if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = cost64;
+  for (int o = 16; o > 0; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+  if ((threadIdx.x & 31) == 0) {
+    wc[threadIdx.x >> 5] = cost64;
+    wn[threadIdx.x >> 5] = nvalid;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wc[w];
+    int nv = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += wc[w];
+      nv += wn[w];
+    }
     partials[(size_t)blockIdx.x * kAcc + kRayAcc - 1] = t;
+    if (with_count) partials[(size_t)blockIdx.x * kAcc + kAcc - 1] = (double)nv;
   }
   __syncthreads();
 }
@@ -299,43 +314,47 @@ __global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
   const size_t half = (size_t)nb * kAcc;
   const bool pub = blockIdx.x == 0 && threadIdx.x == 0;  // publishes to A.st
   if (threadIdx.x == 0) L = *A.st;  // initial pose (host-written)
-  // valid_count (camera.cpp:10-14) for the lost test (tracking.cpp:165-168)
-  {
+  __syncthreads();
+  constexpr bool ray = RAY;  // ray mode gets its own instance (register budget)
+  WeightsDev wp = A.wp;
+  wp.q_min = A.q_min_fraction * (*A.median_dev);  // tracking.cpp:170-171
+  int buf = 1;
+  double* part = A.partials + buf * half;
+  if (ray) {
+    // the first residual pass at the initial pose also counts the valid
+    // matches; the lost test (tracking.cpp:165-168) then discards it if needed
+    eval_pass_ray(make_pose<double>(L.T), A.M, A.Xref, A.Xsrc, wp, part, true);
+  } else {
+    // valid_count (camera.cpp:10-14) for the lost test (tracking.cpp:165-168)
     float acc[kAcc];
     for (int i = 0; i < kAcc; ++i) acc[i] = 0.0f;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int cnt = 0;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < A.M.count; k += stride)
       cnt += (A.M.valid ? A.M.valid[k] != 0 : 1);
-    acc[36] = (float)cnt;
-    block_reduce_to(acc, A.partials + (size_t)blockIdx.x * kAcc);
+    acc[kAcc - 1] = (float)cnt;
+    block_reduce_to(acc, A.partials + (size_t)blockIdx.x * kAcc);  // buffer 0
   }
   grid.sync();
   if (threadIdx.x == 0) {
+    const double* cp = ray ? part : A.partials;
     double c = 0.0;
-    for (int b = 0; b < nb; ++b) c += A.partials[(size_t)b * kAcc + 36];
+    for (int b = 0; b < nb; ++b) c += cp[(size_t)b * kAcc + kAcc - 1];
     L.valid_count = (int64_t)c;
     L.lost = c < (double)A.min_valid ? 1 : 0;
     L.stop = L.lost;
-    L.q_min = A.q_min_fraction * (*A.median_dev);
+    L.q_min = wp.q_min;
     L.lambda = 1e-8;
     L.iterations = 0;
     L.trace_len = 0;
   }
   __syncthreads();
-  int buf = 1;  // the count above used buffer 0
   if (!L.stop) {
-    WeightsDev wp = A.wp;
-    wp.q_min = L.q_min;
-    constexpr bool ray = RAY;  // ray mode gets its own instance (register budget)
-    double* part = A.partials + buf * half;
-    if (ray) {
-      eval_pass_ray(make_pose<double>(L.T), A.M, A.Xref, A.Xsrc, wp, part);
-    } else {
+    if (!ray) {
       const PoseR<float> T = make_pose<float>(L.T);
       eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part);
+      grid.sync();
     }
-    grid.sync();
     {
       double H[49], g[7], c;
       load_sums(part, nb, ray, H, g, &c);
