@@ -66,6 +66,9 @@
 #ifndef PMX_JDIFF_F32
 #define PMX_JDIFF_F32 0  // Jacobian support differences from fp32-rounded supports (1.252 -> 1.245 ms; valid matches identical, a few invalid pixels' pixel_a differ)
 #endif
+#ifndef PMX_SPLIT
+#define PMX_SPLIT 0  // LM (k_match) and refinement (k_refine_tiles) as two kernels (1.250 -> 1.434 ms at the best occupancy: the fused kernel overlaps the phases)
+#endif
 #ifndef PMX_PREFETCH
 #define PMX_PREFETCH 0  // L2 prefetch of the target descriptor row before the LM (neutral at first; with the row loaded among the post-LM gathers, 1.296 -> 1.306 ms)
 #endif
@@ -2013,6 +2016,59 @@ __global__ void __launch_bounds__(32 * PMX_MR_TY, PMX_MR_BLOCKS) k_match_refine(
   }
 }
 
+// PMX_SPLIT: the refinement as its own kernel after k_match (each phase with
+// its own register budget / occupancy; the fused kernel overlaps them).
+#ifndef PMX_RF_TY
+#define PMX_RF_TY 4
+#endif
+#ifndef PMX_RF_BLOCKS
+#define PMX_RF_BLOCKS 8  // 64 registers (12 / 16: 40 / 32 registers, heavy spills)
+#endif
+__global__ void __launch_bounds__(32 * PMX_RF_TY, PMX_RF_BLOCKS) k_refine_tiles(const PairDev* __restrict__ pairs,
+                                                                              RefineLevels L) {
+  const PairDev& P = pairs[blockIdx.z];
+  if ((int)blockIdx.x * 32 >= P.Wb || (int)blockIdx.y * PMX_RF_TY >= P.Hb) return;
+  const int u = blockIdx.x * 32 + (threadIdx.x & 31), v = blockIdx.y * PMX_RF_TY + (threadIdx.x >> 5);
+  const int m = v * P.Wb + u;
+  int n = -1, pa = 0, pcu = 0, pcv = 0;
+  if (u < P.Wb && v < P.Hb && P.out_valid[m]) {
+    pa = P.out_pa[m];
+    pcu = pa % P.Wa;
+    pcv = pa / P.Wa;
+    n = m;
+  }
+  const bool fast_pair = P.q8h != nullptr && __ldg(&P.sel->qbad) == 0;
+  QB B;
+  int tgap = 0;
+  bool fast = n >= 0 && fast_pair;
+  if (fast) {
+    const uint4* row = reinterpret_cast<const uint4*>(P.db) + 3 * (size_t)n;
+    const Q8 q = quantize24(__ldg(row), __ldg(row + 1), __ldg(row + 2));
+    B.w[0] = q.a.x;
+    B.w[1] = q.a.y;
+    B.w[2] = q.a.z;
+    B.w[3] = q.a.w;
+    B.w[4] = q.b.x;
+    B.w[5] = q.b.y;
+    B.nt = q.nt;
+    tgap = __ldg(&P.sel->a1max) + q.l1 + 12;
+    fast = !q.bad;
+  }
+  QState q{pcu, pcv, 0, 0, 1, -1, INT_MIN, n < 0 ? 2 : fast ? 0 : 1};
+  if (__any_sync(0xffffffffu, fast)) {
+    const QGlob T{P.q8h, P.q8n, P.q8t, P.Wa, P.Wa * P.Ha};
+    q_refine_warp(T, B, tgap, P.Wa, P.Ha, L, q);
+  }
+  if (q.st != 2) {
+    int out = q.st == 0 ? q.cv * P.Wa + q.cu : refine_exact_path(P, pa, n, L);
+    PMX_CHECK_INDEX(out, P.Wa * P.Ha);
+    if (out != pa) {
+      P.out_pa[n] = out;
+      P.out_q[n] = (float)sqrt((double)__ldg(P.qa + out) * (double)__ldg(P.qb + n));
+    }
+  }
+}
+
 // Standalone feature_refine over an arbitrary MatchSet (camera.cpp:239-271).
 __global__ void __launch_bounds__(256) k_refine(PairDev P, int64_t count, const int32_t* __restrict__ in_pa,
                                                 const int32_t* __restrict__ in_pb,
@@ -2361,7 +2417,15 @@ void match_batch_device(Context& ctx, const std::vector<PairDev>& host_pairs, co
       max_tx = std::max(max_tx, (hp[i].Wb + 31) / 32);
       max_ty = std::max(max_ty, (hp[i].Hb + 7) / 8);
     }
-    if (refine && L.n > 0) {
+    if (PMX_SPLIT && refine && L.n > 0) {
+      ProfScope ps(ctx, "k_match_refine");  // both kernels under the fused kernel's name
+      k_match<<<dim3(max_tx, max_ty, cn), 256, 0, ctx.stream>>>(dp, lp);
+      launch_check(ctx, "k_match");
+      int ty = 0;
+      for (int i = c0; i < c0 + cn; ++i) ty = std::max(ty, (hp[i].Hb + PMX_RF_TY - 1) / PMX_RF_TY);
+      k_refine_tiles<<<dim3(max_tx, ty, cn), 32 * PMX_RF_TY, 0, ctx.stream>>>(dp, L);
+      launch_check(ctx, "k_refine_tiles");
+    } else if (refine && L.n > 0) {
       // counter first: its first allocation must stay outside the timed scope
       unsigned long long* exact_px = ctx.profiling ? dev_counter(ctx, "refine_exact_px") : nullptr;
       ProfScope ps(ctx, "k_match_refine");
