@@ -372,3 +372,15 @@ def test_odd_sizes_match_and_refine(ctx, shapes):
         orc = pyoracle.feature_refine(pyoracle.match_pointmaps(p, params), p, rp)
         st = compare_matches(g, orc, p["width"])
         assert st["all_index_equal"] and st["valid_mismatch"] == 0, (p["height"], p["width"], st)
+
+
+@pytest.mark.parametrize("shape", [(96, 128), (384, 512)])
+def test_reference_default_parameters_parity(ctx, shape):
+    """The reference's own defaults (LM lambda 1e-4, angle tol 1e-5 rad,
+    refine levels {(2,2),(1,2)}; inc/camera.hpp:103-107, 142) rather than the
+    BASELINE schedule: same indices / validity as the restatement."""
+    pair = pmxgen.config0(seed=17, height=shape[0], width=shape[1])
+    params, rp = abi.default_match_params(), abi.default_refine_params()
+    orc = pyoracle.feature_refine(pyoracle.match_pointmaps(pair, params), pair, rp)
+    gpu = ctx.match_batch([pmx_pair(pair)], params=params, refine=rp)[0]
+    _check(compare_matches(gpu, orc, shape[1]))
