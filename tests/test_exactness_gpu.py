@@ -117,7 +117,7 @@ def _graph(n_kf=12, reach=3, h=48, w=64, seed=5, low_q=0.0):
     return g, G, O
 
 
-@pytest.mark.parametrize("mode", [abi.PMX_TRACK_RAY, abi.PMX_TRACK_PIXEL])
+@pytest.mark.parametrize("mode", [abi.PMX_TRACK_RAY, abi.PMX_TRACK_POINT, abi.PMX_TRACK_PIXEL])
 def test_backend_with_exclusions(ctx, mode):
     """Per-edge q_min = 0.1 x median (backend.cpp:37-46, 62-63) with 15% of
     every edge's valid matches below it: edge terms and the GN loop."""
