@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
     float acc[kAcc];
 #pragma unroll
     for (int i = 0; i < kAcc; ++i) acc[i] = 0.0f;
+    double cost64 = 0.0;  // the cost slot in FP64 (exact accept / revert, backend.cpp:241-246)
     if (ok) {
       // dir 0: ref = i, src = j, swapped matches (backend.cpp:65)
       // dir 1: ref = j, src = i, original matches (backend.cpp:66)
@@ -116,14 +117,31 @@ __global__ void __launch_bounds__(256) k_edge_terms(EdgeArgs A, int e0) {
       const CloudDev Xref = A.clouds[dir == 0 ? ij.x : ij.y];
       const CloudDev Xsrc = A.clouds[dir == 0 ? ij.y : ij.x];
       const PoseR<float> T = A.rel[2 * e + dir];
+      const PoseR<double> Td = A.rel64[2 * e + dir];
       const int64_t stride = (int64_t)A.bpe * blockDim.x;
+      (void)T;
       for (int64_t k = (int64_t)b * blockDim.x + threadIdx.x; k < Md.count; k += stride) {
-        MatchEval<float> m;
-        eval_match<float>(T, Md, Xref, Xsrc, A.mode, wp, A.K, k, m);
-        accumulate<float>(m, A.mode, wp, acc);
+        // residuals in FP64: in point / pixel mode r = ref - T src cancels
+        // (|r| << |x|), so an fp32 evaluation would steer the end game with
+        // ~|x|/|r| x 1e-7 relative error; the products are accumulated in fp32
+        MatchEval<double> md;
+        eval_match<double>(Td, Md, Xref, Xsrc, A.mode, wp, A.K, k, md);
+        accumulate<double>(md, A.mode, wp, acc);
+        if (md.used) cost64 += block_cost_one<double>(md, A.mode, wp);
       }
     }
-    block_reduce_to(acc, A.partials + (((size_t)e * A.bpe + b) * 2 + dir) * kAcc);
+    double* row = A.partials + (((size_t)e * A.bpe + b) * 2 + dir) * kAcc;
+    block_reduce_to(acc, row);
+    __shared__ double wc[32];
+    cost64 = warp_sum(cost64);
+    if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = cost64;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // warps in order: deterministic
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wc[w];
+      row[35] = t;
+    }
+    __syncthreads();
   }
 }
 

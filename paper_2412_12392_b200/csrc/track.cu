@@ -30,18 +30,43 @@ namespace cg = cooperative_groups;
 namespace pmx {
 
 // Fused residual pass over all matches at pose T -> per-block partials.
+// Td (the GN loop): the cost slot (35) takes the FP64 block_cost of the
+// FP64-evaluated residuals instead of the fp32 sum, so the accept / stop
+// decisions (tracking.cpp:210-223) are taken on the reference's arithmetic
+// (as ray mode's ray_cost64 does).
 __device__ void eval_pass(const PoseR<float>& T, const MatchesDev& M, const CloudDev& Xref, const CloudDev& Xsrc,
-                          int mode, const WeightsDev& wp, const IntrDev& K, double* __restrict__ partials) {
+                          int mode, const WeightsDev& wp, const IntrDev& K, double* __restrict__ partials,
+                          const PoseR<double>* Td = nullptr) {
   float acc[kAcc];
 #pragma unroll
   for (int i = 0; i < kAcc; ++i) acc[i] = 0.0f;
+  double cost64 = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < M.count; k += stride) {
-    MatchEval<float> m;
-    eval_match<float>(T, M, Xref, Xsrc, mode, wp, K, k, m);
-    accumulate<float>(m, mode, wp, acc);
+    if (Td) {  // residuals in FP64 (they cancel in point / pixel mode), products accumulated in fp32
+      MatchEval<double> md;
+      eval_match<double>(*Td, M, Xref, Xsrc, mode, wp, K, k, md);
+      accumulate<double>(md, mode, wp, acc);
+      if (md.used) cost64 += block_cost_one<double>(md, mode, wp);
+    } else {
+      MatchEval<float> m;
+      eval_match<float>(T, M, Xref, Xsrc, mode, wp, K, k, m);
+      accumulate<float>(m, mode, wp, acc);
+    }
   }
   block_reduce_to(acc, partials + (size_t)blockIdx.x * kAcc);
+  if (Td) {  // deterministic: warp sums in lane order, warps in order
+    __shared__ double wc[32];
+    cost64 = warp_sum(cost64);
+    if ((threadIdx.x & 31) == 0) wc[threadIdx.x >> 5] = cost64;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += wc[w];
+      partials[(size_t)blockIdx.x * kAcc + 35] = t;
+    }
+    __syncthreads();
+  }
 }
 
 // Ray mode (the tracking configuration): closed-form sums with the cancelling
@@ -352,7 +377,8 @@ __global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
   if (!L.stop) {
     if (!ray) {
       const PoseR<float> T = make_pose<float>(L.T);
-      eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part);
+      const PoseR<double> Td = make_pose<double>(L.T);
+      eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part, &Td);
       grid.sync();
     }
     {
@@ -407,7 +433,8 @@ __global__ void __launch_bounds__(256, 2) k_track_gn(TrackArgs A) {
         eval_pass_ray(make_pose<double>(L.Ttrial), A.M, A.Xref, A.Xsrc, wp, part);
       } else {
         const PoseR<float> T = make_pose<float>(L.Ttrial);
-        eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part);
+        const PoseR<double> Td = make_pose<double>(L.Ttrial);
+        eval_pass(T, A.M, A.Xref, A.Xsrc, A.mode, wp, A.K, part, &Td);
       }
       grid.sync();
       double H[49], g[7], c;

@@ -77,7 +77,7 @@ def test_normal_equations_with_exclusions(ctx, mode):
     assert _rel(Hg, Ho) < 1e-4 and _rel(gg, go) < 1e-4 and abs(cg - co) <= 1e-5 * abs(co)
 
 
-@pytest.mark.parametrize("mode", [abi.PMX_TRACK_RAY, abi.PMX_TRACK_PIXEL])
+@pytest.mark.parametrize("mode", [abi.PMX_TRACK_RAY, abi.PMX_TRACK_POINT, abi.PMX_TRACK_PIXEL])
 def test_track_given_matches_with_exclusions(ctx, mode):
     """q_min = 0.1 x median of the valid matches' q (tracking.cpp:170-171),
     with 15% of them below it."""
@@ -166,3 +166,54 @@ def test_backend_end_game_decisions_exact(ctx):
     for a, b in zip(G.poses, O.poses):
         et, er, es = _pose_err(a, b)
         assert et < 1e-6 and er < 1e-6 and es < 1e-6, (et, er, es)
+
+
+@pytest.mark.parametrize("mode", [abi.PMX_TRACK_POINT, abi.PMX_TRACK_PIXEL])
+def test_backend_end_game_decisions_exact_point_pixel(ctx, mode):
+    """update_tol = 0 in point and pixel mode: the generic edge pass carries
+    the FP64 cost (FP64-evaluated residuals, block_cost) in its cost slot, so
+    the accept / revert end game (backend.cpp:241-246) follows the oracle's
+    iterations and cost trace."""
+    h, w = 48, 64
+    g, G, O = _graph(n_kf=10, reach=3, h=h, w=w)
+    p = abi.default_backend_params()
+    p.weights.distance_weight = 0.1
+    p.update_tol = 0.0
+    p.max_iterations = 30
+    p.mode = mode
+    if mode == abi.PMX_TRACK_PIXEL:
+        p.has_intrinsics = 1
+        p.intrinsics = _K(h, w)
+    rg = ctx.global_optimize(G, p)
+    ro, _ = pyoracle.global_optimize(O, p)
+    assert rg.iterations == ro.iterations, (rg.iterations, ro.iterations)
+    assert rg.converged == bool(ro.converged)
+    np.testing.assert_allclose(rg.cost_trace, list(ro.cost_trace[:ro.cost_trace_len]), rtol=1e-7)
+    for a, b in zip(G.poses, O.poses):
+        et, er, es = _pose_err(a, b)
+        assert et < 1e-6 and er < 1e-6 and es < 1e-6, (et, er, es)
+
+
+@pytest.mark.parametrize("mode", [abi.PMX_TRACK_POINT, abi.PMX_TRACK_PIXEL])
+def test_track_end_game_decisions_exact_point_pixel(ctx, mode):
+    """Tracking's accept / stop decisions in point and pixel mode on FP64
+    costs (update_tol = 0, 20 iterations): same iterations and cost trace as
+    the oracle."""
+    h, w = 96, 128
+    c, pa, v, q = _frame(21, h, w)
+    p = abi.default_solve_pose_params()
+    p.max_iterations = 20
+    p.update_tol = 0.0
+    p.weights.distance_weight = 0.1
+    if mode == abi.PMX_TRACK_PIXEL:
+        p.has_intrinsics = 1
+        p.intrinsics = _K(h, w)
+    m = MatchSet(pa, q, v)
+    can = Pointmap(c["canonical"], c["canonical_valid"], h, w)
+    src = Pointmap(c["X_f_f"], c["valid_f"], h, w)
+    rg = ctx.track_given_matches(can, src, m, sim3(), mode=mode, params=p)
+    om = pyoracle.MatchSet(pa, np.arange(h * w), q.astype(np.float64), v)
+    ro = pyoracle.track_given_matches(c["canonical"], c["canonical_valid"], c["X_f_f"], c["valid_f"], h, w, om,
+                                      sim3(), mode=mode, params=p)
+    assert rg.iterations == ro.iterations, (rg.iterations, ro.iterations)
+    np.testing.assert_allclose(list(rg.cost_trace), list(ro.cost_trace[:ro.cost_trace_len]), rtol=1e-9)
