@@ -305,6 +305,36 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Bulk copies on the TMA engine (cp.async.bulk, global -> shared) completing
+// on an mbarrier's transaction count, and the mbarrier primitives around them.
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {  // arrive (count 1) + expect bytes
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
 // Both directed constraints of one compacted match, packed as a float2 pair
 // (.x: ref = i, src = j, swapped; .y: ref = j, src = i).  The FP64 offsets
 // delta = T src - ref are per direction; everything after them runs as packed
@@ -351,7 +381,22 @@ __device__ __forceinline__ void ray_match(const PoseR<double>& T1, const PoseR<d
   ray_match_scalar(T1, T2, __ldg(Ci + m.x), __ldg(Cj + m.y), info, c, reinterpret_cast<float*>(acc));
 }
 
-constexpr int kEdgeSmem = (6 * 256 + 8 * 256) * 16;  // cp.async stages of k_edge_terms_ray (56 KB)
+#ifndef PMX_EDGE_TMA
+// Record stream of the edge pass by TMA bulk copies + mbarriers (1) instead of
+// per-thread cp.async (0).  Measured slower on config 4 (53.6 -> 61.2 ms per
+// 6 passes, the same with 4/6/8 stages and 2/4 tiles ahead): the CTA-wide
+// stage ring couples the warps that the per-thread pipeline keeps
+// independent.  Kept as an off option.
+#define PMX_EDGE_TMA 0
+#endif
+#ifndef PMX_REC_STAGES
+#define PMX_REC_STAGES 4
+#endif
+#ifndef PMX_REC_AHEAD
+#define PMX_REC_AHEAD 2  // tiles of records in flight ahead of the one being evaluated (TMA form)
+#endif
+constexpr int kRecStages = PMX_EDGE_TMA ? PMX_REC_STAGES : 3;  // record tiles in shared memory
+constexpr int kEdgeSmem = (2 * kRecStages * 256 + 8 * 256) * 16;  // stages of k_edge_terms_ray (56 / 64 KB)
 static_assert(kEdgeSmem >= block_reduce_scratch_bytes<2 * kRayAcc>(), "reduction scratch aliases the stages");
 
 // Both directed constraints of an edge from one read of its compacted matches.
@@ -361,6 +406,17 @@ static_assert(kEdgeSmem >= block_reduce_scratch_bytes<2 * kRayAcc>(), "reduction
 __global__ void __launch_bounds__(256, PMX_EDGE_BLOCKS) k_edge_terms_ray(EdgeArgs A, int e0) {
   if (gn_stopped(A.st)) return;
   extern __shared__ int4 edge_sm[];
+#if PMX_EDGE_TMA
+  __shared__ uint64_t edge_full[kRecStages], edge_empty[kRecStages];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRecStages; ++s) {
+      mbar_init(&edge_full[s], 1);
+      mbar_init(&edge_empty[s], blockDim.x / 32);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+#endif
   const int e = e0 + blockIdx.y;
   const int b = blockIdx.x;
   const int2 ij = A.edges[e];
@@ -391,10 +447,10 @@ __global__ void __launch_bounds__(256, PMX_EDGE_BLOCKS) k_edge_terms_ray(EdgeArg
     // only what it copied): while tile t (this thread's matches 2t, 2t+1) is
     // evaluated, the records of tile t+2 and the two points of each match of
     // tile t+1 travel into shared memory, holding no registers.
-    int4* R = edge_sm;                                        // [3 stages][2][256] records
-    float4* PT = reinterpret_cast<float4*>(edge_sm + 6 * 256);  // [2 stages][2][2 (Pi, Pj)][256]
+    int4* R = edge_sm;                                                       // [kRecStages][2][256] records
+    float4* PT = reinterpret_cast<float4*>(edge_sm + 2 * kRecStages * 256);  // [2 stages][2][2 (Pi, Pj)][256]
     const int tid = threadIdx.x;
-    auto rslot = [&](int t, int j) { return R + ((t % 3) * 2 + j) * 256 + tid; };
+    auto rslot = [&](int t, int j) { return R + ((t % kRecStages) * 2 + j) * 256 + tid; };
     auto pslot = [&](int t, int j, int side) { return PT + (((t & 1) * 2 + j) * 2 + side) * 256 + tid; };
     const int64_t nmine = k0 < cnt ? (cnt - k0 + stride - 1) / stride : 0;
     const int ntile = (int)((nmine + 1) / 2);
@@ -413,6 +469,59 @@ __global__ void __launch_bounds__(256, PMX_EDGE_BLOCKS) k_edge_terms_ray(EdgeArg
           cp_async_n<16>(pslot(t, j, 1), Cj + m.y);
         }
     };
+#if PMX_EDGE_TMA
+    // The records of tile t are two contiguous runs of 256 (j = 0, 1) for the
+    // whole CTA: thread 0 moves them with two bulk copies on the TMA engine
+    // that complete on full[t % 4]; every thread arrives on empty[t % 4] once
+    // it has read its records of tile t, and thread 0 waits for that before
+    // refilling the stage with tile t + 4 (issued two tiles ahead, so the
+    // wait is for consumers two tiles behind).  The point gathers stay
+    // per-thread cp.async.  Thread 0 has the most tiles (per-thread counts
+    // differ by at most one match), so it issues every tile.
+    const int64_t nmine0 = (int64_t)b * blockDim.x < cnt ? (cnt - (int64_t)b * blockDim.x + stride - 1) / stride : 0;
+    const int ntile0 = (int)((nmine0 + 1) / 2);
+    auto issue_rec_tma = [&](int t) {  // thread 0
+      if (t >= ntile0) return;
+      const int s = t % kRecStages;
+      if (t >= kRecStages) mbar_wait(&edge_empty[s], ((t - kRecStages) / kRecStages) & 1);
+      unsigned n[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int64_t base = (int64_t)b * blockDim.x + (int64_t)(2 * t + j) * stride;
+        n[j] = base < cnt ? (unsigned)(cnt - base < 256 ? cnt - base : 256) : 0u;
+      }
+      mbar_expect_tx(&edge_full[s], 16u * (n[0] + n[1]));
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (n[j]) bulk_g2s(R + (s * 2 + j) * 256, P + (int64_t)b * blockDim.x + (int64_t)(2 * t + j) * stride,
+                           16u * n[j], &edge_full[s]);
+    };
+    auto rec_ready = [&](int t) { mbar_wait(&edge_full[t % kRecStages], (t / kRecStages) & 1); };
+    if (tid == 0)
+      for (int t = 0; t < PMX_REC_AHEAD; ++t) issue_rec_tma(t);
+    if (ntile > 0) {
+      rec_ready(0);
+      issue_pts(0);
+      cp_async_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+      if (tid == 0) issue_rec_tma(t + PMX_REC_AHEAD);
+      cp_async_wait_all();  // points of tile t
+      if (t + 1 < ntile) {
+        rec_ready(t + 1);
+        issue_pts(t + 1);
+        cp_async_commit();
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        if (2 * t + j < nmine)
+          ray_match(T1, T2, *rslot(t, j), Ci, Cj, *pslot(t, j, 0), *pslot(t, j, 1), inv_s2, c, acc);
+      // one arrival per warp (the empty barriers count warps): every lane of
+      // a warp is in the loop except possibly in the CTA's last tile, whose
+      // stage is never refilled
+      if ((tid & 31) == __ffs(__activemask()) - 1) mbar_arrive(&edge_empty[t % kRecStages]);
+    }
+#else
     if (ntile > 0) {
       issue_rec(0);
       issue_rec(1);
@@ -431,6 +540,7 @@ __global__ void __launch_bounds__(256, PMX_EDGE_BLOCKS) k_edge_terms_ray(EdgeArg
         if (2 * t + j < nmine)
           ray_match(T1, T2, *rslot(t, j), Ci, Cj, *pslot(t, j, 0), *pslot(t, j, 1), inv_s2, c, acc);
     }
+#endif
   }
   cp_async_wait_all();
   __syncthreads();  // the pipeline's shared memory becomes the reduction scratch
