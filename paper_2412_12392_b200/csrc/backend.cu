@@ -870,6 +870,7 @@ static_assert(kSkyThreads >= kFront * kPW, "backward pass holds one L entry per 
 struct SkyArgs {
   const double* H;          // assembled skyline (undamped)
   const int4* trip;         // entering triples {slot a, slot b, skyline index or -1, diag}
+  const double2* ent;       // the same in panel order with their values: {meta a | b << 8 | diag << 16, H[z] or 0}
   const int4* pinfo;        // [npanel] {trip begin, trip end, live-row begin, live-row end}
   const int2* pextra;       // [npanel] {live rows that are the next panel's pivots (lead), pivot-block triples (lead)}
   const int2* rinfo;        // live non-pivot rows of each panel {index, slot}
@@ -919,7 +920,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   double* sW = sL + kFront * kPW;                        // [kFront][kPW]
   __shared__ double sD[2][kPW][kPW + 1], sIv[2][kPW];    // pivot block of the current / next panel
   __shared__ int2 rows[2][kFront];
-  __shared__ int psl[2][kPW];
+  __shared__ int psl[3][kPW];  // pivot slots of panels k, k + 1, k + 2 (index k % 3)
   __shared__ int ok;
   const int n = P.n, tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5;
   for (int i = tid; i < n; i += nth) y[i] = -P.grad[i];
@@ -930,47 +931,37 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   }
   if (tid == 0) ok = 1;
   __syncthreads();
-  // Prefetch pipeline (cp.async, one item per thread): entering triples two
-  // panels ahead, their values and pivot slots one panel ahead, live rows one
-  // panel ahead; every panel ends with all copies landed.
-  __shared__ int4 stri[2][kSkyThreads];   // entering triples of a panel (slot of panel k: k & 1)
-  __shared__ double sval[2][kSkyThreads];  // their skyline values
+  // Prefetch pipeline (cp.async, one item per thread): entering entries
+  // (triple + value, gathered into panel order by k_sky_entries: one
+  // coalesced 16-byte copy each) and pivot slots two panels ahead, live rows
+  // one panel ahead; every panel ends with all copies landed, so nothing in a
+  // panel waits for global memory.
+  __shared__ double2 sent[2][kSkyThreads];  // entering entries of a panel (slot of panel k: k & 1)
   // Copy roles: warps 1.. (ti = tid - 32) issue every copy and land every
   // triple, so warp 0 - the look-ahead's critical path - issues none; the
   // pivot-block triples (first in the list) and the next pivot slots belong to
   // warp 1, which hands them to warp 0 through named barrier 2.
   const int ti = tid - 32, ntc = nth - 32;
-  auto issue_struct = [&](int k) {
+  auto issue_ent = [&](int k) {  // entries and pivot slots of panel k
     const int4 pi = pin[k];
-    if (ti >= 0 && pi.x + ti < pi.y) cp_async_n<16>(&stri[k & 1][ti], P.trip + pi.x + ti);
+    if (ti >= 0 && pi.x + ti < pi.y) cp_async_n<16>(&sent[k & 1][ti], P.ent + pi.x + ti);
+    if (ti >= 0 && ti < min(kPW, n - kPW * k)) cp_async_n<4>(&psl[k % 3][ti], P.slot + kPW * k + ti);
   };
   auto issue_rows = [&](int k) {
     const int4 pi = pin[k];
     if (ti >= 0 && pi.z + ti < pi.w) cp_async_n<8>(&rows[k & 1][ti], P.rinfo + pi.z + ti);
   };
-  auto issue_vals = [&](int k) {  // needs panel k's triples landed
-    const int4 pi = pin[k];
-    if (ti >= 0 && pi.x + ti < pi.y) {
-      const int z = stri[k & 1][ti].z;
-      if (z >= 0) cp_async_n<8>(&sval[k & 1][ti], P.H + z);
-    }
-    if (ti >= 0 && ti < min(kPW, n - kPW * k)) cp_async_n<4>(&psl[k & 1][ti], P.slot + kPW * k + ti);
-  };
   auto land = [&](int k) {  // this thread's entering triple of panel k (+ the rare overflow) into the front
     const int4 pi = pin[k];
-    if (ti >= 0 && pi.x + ti < pi.y) {
-      const int4 t = stri[k & 1][ti];
-      const double v = (t.z >= 0 ? sval[k & 1][ti] : 0.0) + (t.w ? lambda : 0.0);  // backend.cpp:210-213
-      F[t.x * kFS + t.y] = v;
-      F[t.y * kFS + t.x] = v;
-    }
+    auto put = [&](const double2 q) {
+      const int m = (int)__double_as_longlong(q.x), a = m & 255, b = (m >> 8) & 255;
+      const double v = q.y + ((m >> 16) ? lambda : 0.0);  // backend.cpp:210-213
+      F[a * kFS + b] = v;
+      F[b * kFS + a] = v;
+    };
+    if (ti >= 0 && pi.x + ti < pi.y) put(sent[k & 1][ti]);
     if (ti >= 0)
-      for (int t = pi.x + ntc + ti; t < pi.y; t += ntc) {  // rare: more triples than threads (never pivot ones)
-        const int4 q = P.trip[t];
-        const double v = (q.z >= 0 ? P.H[q.z] : 0.0) + (q.w ? lambda : 0.0);
-        F[q.x * kFS + q.y] = v;
-        F[q.y * kFS + q.x] = v;
-      }
+      for (int t = pi.x + ntc + ti; t < pi.y; t += ntc) put(P.ent[t]);  // rare: more entries than threads (never pivot ones)
   };
   // Warp 0: the 7x7 pivot block of panel k from the front, in registers
   // (lane r holds row r) -> sD/sIv[fb], the block's unit L and D, and the
@@ -980,9 +971,10 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
     const int ns = pin[k].w - pin[k].z;
     double* Lp = P.Lst + plofs[k];
     double a[kPW];
-    const int sr = lane < nb ? psl[fb][lane] : 0;
+    const int* ps = psl[k % 3];
+    const int sr = lane < nb ? ps[lane] : 0;
 #pragma unroll
-    for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFS + psl[fb][c]] : 0.0;
+    for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFS + ps[c]] : 0.0;
 #pragma unroll
     for (int p = 0; p < kPW; ++p) {
       if (p < nb) {
@@ -1034,12 +1026,9 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
     F[si * kFS + sj] = v;
     F[sj * kFS + si] = v;
   };
-  issue_struct(0);
-  cp_async_commit();
-  cp_async_wait_all();
-  issue_vals(0);
+  issue_ent(0);
   issue_rows(0);
-  if (npanel > 1) issue_struct(1);
+  if (npanel > 1) issue_ent(1);
   cp_async_commit();
   cp_async_wait_all();
   land(0);
@@ -1065,9 +1054,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
     double* Lp = P.Lst + plofs[k];
     const bool next = k + 1 < npanel;
     if (next) {
-      issue_vals(k + 1);  // group A: what the look-ahead needs
-      cp_async_commit();
-      if (k + 2 < npanel) issue_struct(k + 2);  // group B
+      if (k + 2 < npanel) issue_ent(k + 2);
       issue_rows(k + 1);
       cp_async_commit();
     }
@@ -1076,7 +1063,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
       const int2 ri = rows[buf][q];
       double w[kPW];
 #pragma unroll
-      for (int t = 0; t < kPW; ++t) w[t] = t < nb ? F[ri.y * kFS + psl[buf][t]] : 0.0;
+      for (int t = 0; t < kPW; ++t) w[t] = t < nb ? F[ri.y * kFS + psl[k % 3][t]] : 0.0;
 #pragma unroll
       for (int t = 1; t < kPW; ++t)
 #pragma unroll
@@ -1109,8 +1096,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
         factor(k + 1, buf ^ 1);
       }
     } else {
-      if (warp == 1 && next) {
-        cp_async_wait_group<1>();  // group A of this thread
+      if (warp == 1 && next) {  // panel k + 1's entries landed before this panel began
         land(k + 1);
         __threadfence_block();
         asm volatile("bar.arrive 2, 64;" ::: "memory");
@@ -1118,10 +1104,7 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
       asm volatile("bar.sync 1, %0;" ::"r"(nth) : "memory");  // every row of (b) is in
       SKY_T(1)
       for (int t = nlead + tid - 32; t < npair; t += nth - 32) schur(t, buf);
-      if (next && warp != 1) {
-        cp_async_wait_group<1>();
-        land(k + 1);
-      }
+      if (next && warp != 1) land(k + 1);
     }
     cp_async_wait_all();  // the next panel's rows / pivot slots, visible after the barrier
     SKY_T(2)
@@ -1199,6 +1182,20 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
   }
   __syncthreads();
   if (tid == 0 && good) P.st->solved = 1;
+}
+
+// The frontal plan's entering triples in panel order with their values from
+// the freshly assembled skyline: one coalesced 16-byte entry per triple for
+// k_ldlt_sky (instead of a scattered 8-byte gather per triple inside the
+// serial panel loop).
+__global__ void k_sky_entries(const int4* __restrict__ trip, const double* __restrict__ H, int ntrip,
+                              double2* __restrict__ ent, const GNState* st) {
+  if (st && (st->stop || st->solved)) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntrip) return;
+  const int4 q = trip[t];
+  const long long m = (long long)(q.x | (q.y << 8) | ((q.w ? 1 : 0) << 16));
+  ent[t] = make_double2(__longlong_as_double(m), q.z >= 0 ? H[q.z] : 0.0);
 }
 
 // All damping attempts in one launch: attempt a runs only while no earlier one
@@ -1886,6 +1883,8 @@ struct Assembly {
   long long nnz = 0;
   DevBuf first, rowptr, rp_ptr, rp_rows, skyH;
   DevBuf trip, pinfo, pextra, rinfo, slot, lofs, Lst, Dst;  // frontal factorisation plan
+  DevBuf ent;  // entering triples with their values, panel order (k_sky_entries)
+  int ntrip = 0;
   // band plan (preferred when the RCM bandwidth is small): block cyclic reduction
   bool band_ok = false;
   int band_m = 0, band_w = 0, band_S = 0, band_npad = 0;
@@ -2113,6 +2112,8 @@ static void build_assembly(Context& ctx, const DevGraph& G, Assembly& As) {
       As.pextra = DevBuf(sizeof(int2) * npanel, ctx.stream);
       PMX_CUDA(cudaMemcpyAsync(As.pextra.p, pext.data(), sizeof(int2) * npanel, cudaMemcpyHostToDevice, ctx.stream));
       As.trip = DevBuf(sizeof(int4) * std::max<size_t>(trip.size(), 1), ctx.stream);
+      As.ent = DevBuf(sizeof(double2) * std::max<size_t>(trip.size(), 1), ctx.stream);
+      As.ntrip = (int)trip.size();
       if (!trip.empty())
         PMX_CUDA(cudaMemcpyAsync(As.trip.p, trip.data(), sizeof(int4) * trip.size(), cudaMemcpyHostToDevice, ctx.stream));
       As.skyH = DevBuf(sizeof(double) * nnz, ctx.stream);
@@ -2290,11 +2291,14 @@ static void solve_sky(Context& ctx, const pmx_backend_params& p, Assembly& As, G
   const size_t smem = sizeof(double) * ((size_t)kFront * kFS + n + 2 * kFront * kPW) +
                       (sizeof(int4) + sizeof(int2)) * (size_t)npanel + sizeof(double) * (size_t)((npanel + 1) / 2);
   PMX_CUDA(cudaFuncSetAttribute((const void*)k_ldlt_sky, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.pinfo.as<int4>(), As.pextra.as<int2>(), As.rinfo.as<int2>(),
+  SkyArgs a{As.skyH.as<double>(), As.trip.as<int4>(), As.ent.as<double2>(), As.pinfo.as<int4>(), As.pextra.as<int2>(), As.rinfo.as<int2>(),
             As.slot.as<int>(), As.lofs.as<int>(), As.Lst.as<double>(), As.Dst.as<double>(), As.grad.as<double>(), tau,
             n, std::max(p.damping_retries, 0), p.damping_init, st};
   {
     ProfScope ps(ctx, "k_ldlt");
+    if (As.ntrip > 0)
+      k_sky_entries<<<(As.ntrip + 255) / 256, 256, 0, ctx.stream>>>(As.trip.as<int4>(), As.skyH.as<double>(),
+                                                                    As.ntrip, As.ent.as<double2>(), st);
     k_ldlt_sky<<<1, kSkyThreads, smem, ctx.stream>>>(a);
   }
   launch_check(ctx, "k_ldlt_sky");

@@ -97,6 +97,7 @@ elif mode == "match":
     print("valid", float(np.mean([o.valid.float().mean().item() for o in outs])))
 else:
     kf = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+    ctx.set_device_graphs(False)  # kernels enqueued one by one (the conditional-graph loop hides them from -k)
     g = pmxgen.backend_graph(kf, 4, 3)
     cans = [Pointmap(T(x), T(v), H, W) for x, v in g["canonicals"]]
     ms = [MatchSet(T(m["pixel_a"]), T(m["confidence"]), T(m["valid"])) for m in g["matches"]]
