@@ -661,7 +661,11 @@ def run_pmx(args):
     if (args.backend_sharded or world > 1) and dist:  # every rank takes part (collectives)
         del dev_pairs, batch
         torch.cuda.empty_cache()
-        sharded = bench_backend_sharded(ctx, dev, rank, world)
+        try:
+            sharded = bench_backend_sharded(ctx, dev, rank, world)
+        except Exception as ex:  # keep the headline line if the secondary fails on every rank
+            sharded = {"metric": "global GN iteration ms at N=1000 (edge-sharded)", "value": None,
+                       "error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # e2e through the public API with host (pinned) buffers: H2D inputs, D2H results
     host_structs = [structs(p, lambda a: to_dev(a, pinned=True)) for p in host_pairs]
