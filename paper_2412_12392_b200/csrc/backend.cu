@@ -975,6 +975,10 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
     const int sr = lane < nb ? ps[lane] : 0;
 #pragma unroll
     for (int c = 0; c < kPW; ++c) a[c] = (lane < nb && c <= lane) ? F[sr * kFS + ps[c]] : 0.0;
+    // L y = b inside the panel rides along the elimination (y_p is final
+    // once step p - 1 ran; same products and order as a separate sweep), so
+    // it adds no step to warp 0's chain
+    double yv = lane < nb ? y[c0 + lane] : 0.0;
 #pragma unroll
     for (int p = 0; p < kPW; ++p) {
       if (p < nb) {
@@ -984,13 +988,18 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
         double wc[kPW];
 #pragma unroll
         for (int c = p; c < kPW; ++c) wc[c] = __shfl_sync(0xffffffffu, w, c);
+        const double yp = __shfl_sync(0xffffffffu, yv, p);
         const double D = wc[p];
         if (lane == 0 && D == 0.0) ok = 0;  // SimplicialLDLT: exact zero pivot fails
         const double iD = fast_rcp(D);
 #pragma unroll
         for (int c = p + 1; c < kPW; ++c)
           if (lane >= c) a[c] -= w * (wc[c] * iD);
-        if (lane > p) a[p] = w * iD;
+        const double l = w * iD;
+        if (lane > p) {
+          a[p] = l;
+          if (lane < nb) yv -= l * yp;
+        }
         if (lane == p) sIv[fb][p] = iD;
       }
     }
@@ -1003,12 +1012,6 @@ __device__ __forceinline__ void sky_attempt(const SkyArgs& P, double lambda) {
         Lp[ns * kPW + lane * kPW + c] = c < lane ? a[c] : 0.0;  // unit L of the pivot block
       }
       P.Dst[c0 + lane] = dl;
-    }
-    double yv = lane < nb ? y[c0 + lane] : 0.0;  // L y = b inside the panel
-#pragma unroll
-    for (int p = 0; p < kPW; ++p) {
-      const double yp = __shfl_sync(0xffffffffu, yv, p);
-      if (lane > p && lane < nb) yv -= a[p] * yp;
     }
     if (lane < nb) y[c0 + lane] = yv;
   };
