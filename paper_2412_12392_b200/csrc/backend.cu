@@ -1769,6 +1769,9 @@ struct EdgeWork {
   EdgeArgs A;
 };
 
+#ifndef PMX_EDGE_PER_BLOCK
+#define PMX_EDGE_PER_BLOCK 16384  // matches per edge-pass block when edges are few (config 3: 8192 / 12288 / 32768 measured 1.519 / 1.490 / 1.496 ms per iteration against 1.477)
+#endif
 static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& p, EdgeWork& W) {
   const int E = std::max(G.E, 1);
   W.rel = DevBuf(sizeof(PoseR<float>) * 2 * (size_t)E, ctx.stream);
@@ -1777,7 +1780,9 @@ static void make_edge_work(Context& ctx, DevGraph& G, const pmx_backend_params& 
   // resident blocks cover a few edges at a time (their keyframes' clouds stay
   // L2-resident) and the last wave is short; many edges: one block per edge.
   const int64_t resident = 2LL * ctx.num_sms;
-  W.bpe = G.E < 4 * resident ? (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + 16383) / 16384)) : 1;
+  W.bpe = G.E < 4 * resident
+              ? (int)std::max<int64_t>(1, std::min<int64_t>(64, (G.max_count + PMX_EDGE_PER_BLOCK - 1) / PMX_EDGE_PER_BLOCK))
+              : 1;
   const bool ray = p.mode == PMX_TRACK_RAY;
   require(!ray || G.packed, "edge_terms: ray mode needs the packed graph");
   W.partials = DevBuf(sizeof(double) * (size_t)E * W.bpe * 2 * (ray ? kRayAcc : kAcc), ctx.stream);
